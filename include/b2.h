@@ -1,0 +1,151 @@
+/*
+ * b2.h — C ABI of the B200 map-execution backend (libb2.so).
+ *
+ * The reference executor is pure Python (pkg/src/sdfgkit/interp.py); this
+ * ABI is what its executor contract binds to through ctypes (see
+ * INTEGRATION.md).  Every entry point is `extern "C"`, takes plain pointers,
+ * sizes and opaque handles (no torch types), returns 0 on success or a
+ * nonzero B2_ERR_* code, and leaves a thread-local message readable through
+ * b2_last_error().  Streams are CUDA stream handles passed as void* (NULL =
+ * legacy default stream); device pointers are plain device addresses.
+ *
+ * Reference interfaces each group replaces:
+ *   runtime / memory .......... Machine.prepare/outputs, interp.py:180-236
+ *   JIT + launch .............. Machine.exec_map / exec_tasklet, interp.py:400-441
+ *                               (tasklet bodies: texpr.evaluate, texpr.py:89-133)
+ *   copy_view ................. Machine.exec_copy + TRANSPOSE, interp.py:383-398, 474-480
+ *   gemm ...................... exec_library MATMUL 2D@2D, interp.py:450-460 (np.matmul)
+ *   reduce .................... exec_library REDUCE, interp.py:461-473 (ufunc.reduce)
+ *   graph capture ............. Machine.run state loop, interp.py:240-263
+ */
+#ifndef B2_H
+#define B2_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define B2_API __attribute__((visibility("default")))
+#else
+#define B2_API
+#endif
+
+#define B2_OK 0
+#define B2_ERR_CUDA 1
+#define B2_ERR_NVRTC 2
+#define B2_ERR_ARG 3
+#define B2_ERR_UNSUPPORTED 4
+
+/* dtype codes shared with the Python host side */
+#define B2_F64 0
+#define B2_I64 1
+#define B2_I32 2
+#define B2_BOOL 3
+#define B2_F32 4
+
+/* write-conflict resolution (ir.py:72-91) */
+#define B2_WCR_NONE 0
+#define B2_WCR_ADD 1
+#define B2_WCR_MUL 2
+#define B2_WCR_MIN 3
+#define B2_WCR_MAX 4
+
+#define B2_MAX_DIMS 8
+
+typedef struct {
+  char name[128];
+  int major, minor;
+  int sm_count;
+  int l2_bytes;
+  int max_smem_optin;
+  size_t total_mem;
+} b2_device_info_t;
+
+/* A strided N-d view of a container: element (i0..i{n-1}) lives at
+ * base + elem_size * (offset + sum_d i_d * strides[d]). */
+typedef struct {
+  void *base;
+  int64_t offset;
+  int32_t dtype;
+  int32_t ndim;
+  int64_t shape[B2_MAX_DIMS];
+  int64_t strides[B2_MAX_DIMS];
+} b2_view_t;
+
+/* ---- runtime ------------------------------------------------------------ */
+B2_API int b2_version(void);
+B2_API const char *b2_last_error(void);
+B2_API int b2_init(int device);
+B2_API int b2_device_count(int *n);
+B2_API int b2_device_info(int device, b2_device_info_t *out);
+B2_API int b2_malloc(void **p, size_t bytes);
+B2_API int b2_free(void *p);
+B2_API int b2_memcpy_h2d(void *dst, const void *src, size_t bytes, void *stream);
+B2_API int b2_memcpy_d2h(void *dst, const void *src, size_t bytes, void *stream);
+B2_API int b2_memcpy_d2d(void *dst, const void *src, size_t bytes, void *stream);
+B2_API int b2_memset(void *dst, int value, size_t bytes, void *stream);
+B2_API int b2_stream_create(void **stream);
+B2_API int b2_stream_destroy(void *stream);
+B2_API int b2_stream_sync(void *stream);
+B2_API int b2_device_sync(void);
+B2_API int b2_event_create(void **ev);
+B2_API int b2_event_destroy(void *ev);
+B2_API int b2_event_record(void *ev, void *stream);
+B2_API int b2_event_elapsed_ms(void *start, void *end, float *ms);
+B2_API int b2_host_register(void *p, size_t bytes);
+B2_API int b2_host_unregister(void *p);
+
+/* ---- JIT of kernel families with inlined tasklet functors (NVRTC) ------ */
+/* Compile CUDA C++ `src` for sm_100a.  On success *cubin_size is the image
+ * size; call again with a buffer of that size to fetch it (cubin != NULL).
+ * `log` (may be NULL) receives the NVRTC log, truncated to log_len. */
+B2_API int b2_jit_compile(const char *src, const char *name, const char *const *opts, int nopts,
+                   void *cubin, size_t *cubin_size, char *log, size_t log_len);
+B2_API int b2_module_load(const void *image, void **module);
+B2_API int b2_module_unload(void *module);
+B2_API int b2_module_function(void *module, const char *kernel, void **fn);
+B2_API int b2_func_set_max_smem(void *fn, int bytes);
+/* Launch `fn` whose single by-value parameter is the byte blob `args`. */
+B2_API int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by,
+              unsigned bz, unsigned smem, void *stream, const void *args, size_t args_bytes);
+/* Number of kernel launches issued through this library so far. */
+B2_API int64_t b2_launch_count(void);
+
+/* ---- CUDA-graph capture of a whole state-machine trace ------------------ */
+B2_API int b2_capture_begin(void *stream);
+B2_API int b2_capture_end(void *stream, void **graph_exec);
+B2_API int b2_graph_launch(void *graph_exec, void *stream);
+B2_API int b2_graph_destroy(void *graph_exec);
+
+/* ---- ahead-of-time library kernels ------------------------------------- */
+/* dst[flat] (wcr)= convert(src[flat]) over the row-major flattening of both
+ * views (equal element counts).  Implements access->access copies with
+ * reshape (interp.py:383-398) and TRANSPOSE (interp.py:474-480). */
+B2_API int b2_copy_view(const b2_view_t *dst, const b2_view_t *src, int wcr, void *stream);
+/* Fill a view with a scalar (given as double). */
+B2_API int b2_fill_view(const b2_view_t *dst, double value, void *stream);
+/* C[i*rsc + j*csc] (wcr)= sum_k A[i*rsa+k*csa] B[k*rsb+j*csb]  (f64 2D@2D) */
+B2_API int b2_gemm_f64(int64_t M, int64_t N, int64_t K, const double *A, int64_t rsa, int64_t csa,
+                const double *B, int64_t rsb, int64_t csb, double *C, int64_t rsc,
+                int64_t csc, int wcr, void *stream);
+/* f32 GEMM with f32 accumulation (SUMMA f32 config). */
+B2_API int b2_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa, int64_t csa,
+                const float *B, int64_t rsb, int64_t csb, float *C, int64_t rsc,
+                int64_t csc, int wcr, void *stream);
+/* out (wcr)= op-reduce of `in` over the dims flagged in axes_mask (bit d),
+ * output enumerated row-major over the kept dims (ufunc.reduce semantics). */
+B2_API int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axes_mask, int op, int wcr,
+              void *stream);
+
+/* Matrix-vector products (np.matmul 2D@1D / 1D@2D) and their fusions
+ * (gemver / atax / bicg) are JIT "rowpass" family kernels: see
+ * paper_2107_00555_b200/csrc/families/rowpass.cuh. */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2_H */

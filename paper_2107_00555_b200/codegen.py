@@ -1,0 +1,540 @@
+"""CUDA C generation for map groups (the generic map-scope kernel family).
+
+A (fused) map group becomes one ``__global__`` kernel whose per-point body is
+the scope's tasklet chain in the reference's execution order
+(``Machine.exec_map`` runs children in topological order per point,
+interp.py:420-441; ``exec_tasklet`` interp.py:400-418).  Memlet reads/writes
+(interp.py:300-324) become loads/stores at row-major offsets; WCR writes
+(ir.py:72-91) become plain read-modify-writes on thread-private locations and
+atomics on shared ones; nested maps become in-thread loops; transients placed
+in registers or per-thread scratch by the planner never touch HBM.
+
+Thread mappings (chosen at plan time):
+  scalar - one thread (top-level tasklets, fused in program order)
+  seq    - one thread running the map lexicographically (SEQUENTIAL schedule)
+  flat   - 1-D grid-stride over the flattened iteration space
+  tile2  - 32x8 thread tiles over the two innermost parameters (coalesced
+           along the last one), outer parameters flattened into the block
+           index; virtual blocks are walked in order so concurrently resident
+           CTAs touch neighbouring planes (L2 reuse for stencils)
+"""
+
+from __future__ import annotations
+
+import struct
+
+from . import plan as P
+from . import scalar, sdfg, symexpr
+
+CT = {"f64": "double", "i64": "b2_ll", "i32": "int", "bool": "bool"}
+TC = {"f64": "f", "i64": "i", "i32": "i", "bool": "b"}
+
+MAX_BLOCKS = 148 * 16
+
+
+class KernelSpec:
+    """Generated kernel + host-side launch recipe."""
+
+    def __init__(self):
+        self.name = ""
+        self.source = ""
+        self.mode = "flat"
+        self.block = (256, 1, 1)
+        self.args: list[tuple] = []  # arg descriptors, in blob order
+        self.syms: list[str] = []
+        self.containers: list[str] = []
+        self.private: dict[str, int] = {}  # container -> elements per thread
+        self.checks: list[tuple] = []  # (container, subset, rename) depth-0 memory accesses
+        self.sites: list[str] = []  # device OOB guard site descriptions
+        self.uses_flag = False
+        self.params: list[str] = []
+        self.kernel = None  # runtime.Kernel
+
+    def arg_index(self, desc) -> int:
+        try:
+            return self.args.index(desc)
+        except ValueError:
+            self.args.append(desc)
+            return len(self.args) - 1
+
+
+class _Gen:
+    def __init__(self, planner: P.Planner, group: P.MapGroup, shapes: dict, name: str):
+        self.pl = planner
+        self.g = planner.g
+        self.group = group
+        self.shapes = shapes
+        self.spec = KernelSpec()
+        self.spec.name = name
+        self.lines: list[str] = []
+        self.uid = 0
+        self.regs: list[str] = []
+        self.ind = 2
+
+    # -- helpers ---------------------------------------------------------------
+
+    def emit(self, s: str):
+        self.lines.append(" " * self.ind + s)
+
+    def fresh(self, base: str) -> str:
+        self.uid += 1
+        return f"{base}_{self.uid}"
+
+    def arg(self, desc) -> str:
+        i = self.spec.arg_index(desc)
+        return f"a.w[{i}]"
+
+    def sym(self, name: str) -> str:
+        if name not in self.spec.syms:
+            self.spec.syms.append(name)
+        return f"s_{name}"
+
+    def name_of(self, env):
+        def f(n):
+            if n in env:
+                return env[n]
+            if n in self.g.containers:
+                raise P.PlanError(f"container '{n}' used as an index symbol")
+            return self.sym(n)
+        return f
+
+    def cont(self, name: str):
+        if name not in self.spec.containers:
+            self.spec.containers.append(name)
+        return self.g.containers[name]
+
+    def place(self, name: str) -> str:
+        return self.pl.placement.get(name, "memory")
+
+    def offset(self, name: str, idx_codes: list[str]) -> str:
+        c = self.cont(name)
+        if not idx_codes:
+            return "0LL"
+        terms = []
+        for d, ic in enumerate(idx_codes):
+            terms.append(f"({ic}) * st_{name}_{d}")
+        return " + ".join(terms)
+
+    def ptr(self, name: str) -> str:
+        pl = self.place(name)
+        return f"pv_{name}" if pl == "private" else f"c_{name}"
+
+    # -- reads / writes ---------------------------------------------------------
+
+    def read(self, m: sdfg.Memlet, env: dict, depth: int) -> tuple[str, str]:
+        c = self.cont(m.container)
+        t = TC[c.dtype]
+        pl = self.place(m.container)
+        if pl == "reg":
+            return f"r_{m.container}", t
+        idx = [symexpr.to_c(b, self.name_of(env)) for b, _, _ in m.subset]
+        off = self.offset(m.container, idx)
+        p = self.ptr(m.container)
+        if depth > 0 or pl == "private":
+            v = self.fresh("ld")
+            o = self.fresh("off")
+            size = f"sz_{m.container}"
+            site = self._site(f"read {m.text}")
+            self.emit(f"const b2_ll {o} = {off};")
+            self.emit(f"const {CT[c.dtype]} {v} = b2_oob({o}, {size}, {site}, flag) ? "
+                      f"({CT[c.dtype]})0 : {p}[{o}];")
+            return v, t
+        if depth == 0:
+            self.spec.checks.append((m.container, m.subset, env))
+        return f"{p}[{off}]", t
+
+    def _site(self, desc: str) -> int:
+        self.spec.uses_flag = True
+        self.spec.sites.append(desc)
+        return len(self.spec.sites) - 1
+
+    def write(self, m: sdfg.Memlet, code: str, vt: str, env: dict, depth: int):
+        c = self.cont(m.container)
+        ct = CT[c.dtype]
+        want = TC[c.dtype]
+        pl = self.place(m.container)
+        val = scalar.cast(code, vt, want)
+        if c.dtype == "i32":
+            val = f"(int)({val})"
+        if pl == "reg":
+            tgt = f"r_{m.container}"
+            if m.wcr is None:
+                self.emit(f"{tgt} = {val};")
+            else:
+                self.emit(f"b2_wcr_{m.wcr}(&{tgt}, ({ct})({val}));")
+            return
+        # subset may cover several elements: broadcast assignment
+        loops = []
+        idx = []
+        for d, (b, e, s) in enumerate(m.subset):
+            if b == e:
+                idx.append(symexpr.to_c(b, self.name_of(env)))
+            else:
+                v = self.fresh("w")
+                bb = symexpr.to_c(b, self.name_of(env))
+                ee = symexpr.to_c(e, self.name_of(env))
+                ss = symexpr.to_c(s, self.name_of(env))
+                loops.append(f"for (b2_ll {v} = {bb}; {v} <= {ee}; {v} += {ss})")
+                idx.append(v)
+        for lp in loops:
+            self.emit(lp + " {")
+            self.ind += 2
+        off = self.offset(m.container, idx)
+        p = self.ptr(m.container)
+        guarded = depth > 0 or loops or pl == "private"
+        shared = (self.group.schedule == "parallel" and bool(self.group.params)
+                  and pl == "memory")
+        if guarded:
+            o = self.fresh("off")
+            site = self._site(f"write {m.text}")
+            self.emit(f"const b2_ll {o} = {off};")
+            self.emit(f"if (!b2_oob({o}, sz_{m.container}, {site}, flag)) {{")
+            target = f"{p}[{o}]"
+            self.ind += 2
+        else:
+            self.spec.checks.append((m.container, m.subset, env))
+            target = f"{p}[{off}]"
+        if m.wcr is None:
+            self.emit(f"{target} = ({ct})({val});")
+        elif shared:
+            self.emit(f"b2_atomic_{m.wcr}(&{target}, ({ct})({val}));")
+        else:
+            self.emit(f"b2_wcr_{m.wcr}(&{target}, ({ct})({val}));")
+        if guarded:
+            self.ind -= 2
+            self.emit("}")
+        for _ in loops:
+            self.ind -= 2
+            self.emit("}")
+
+    # -- body -------------------------------------------------------------------
+
+    def tasklet(self, st: sdfg.State, t: sdfg.Tasklet, env: dict, depth: int):
+        types: dict[str, str] = {}
+        cname: dict[str, str] = {}
+        self.emit(f"{{  // tasklet {t.name} (node {t.id})")
+        self.ind += 2
+        for e in st.in_edges(t):
+            if e.memlet is None:
+                continue
+            code, ty = self.read(e.memlet, env, depth)
+            v = self.fresh("in")
+            cdt = CT[self.g.containers[e.memlet.container].dtype]
+            self.emit(f"const {cdt} {v} = {code};")
+            types[e.dst_conn] = ty
+            cname[e.dst_conn] = v
+        for _, code in t.code:
+            for n in scalar.free_names(code):
+                if n in types:
+                    continue
+                if n in env:
+                    types[n] = "i"
+                    cname[n] = env[n]
+                elif n in self.g.containers:
+                    raise P.PlanError(f"tasklet {t.name} reads container '{n}' without a memlet")
+                else:
+                    types[n] = "i"
+                    cname[n] = self.sym(n)
+        results: dict[str, tuple[str, str]] = {}
+        for conn, code in t.code:
+            c, ty = scalar.emit(code, types, lambda n: cname[n])
+            v = self.fresh("o")
+            self.emit(f"const {scalar.ctype(ty)} {v} = {c};")
+            results[conn] = (v, ty)
+        for e in st.out_edges(t):
+            if e.memlet is None:
+                continue
+            key = e.src_conn if e.src_conn in results else t.outs[0]
+            v, ty = results[key]
+            self.write(e.memlet, v, ty, env, depth)
+        self.ind -= 2
+        self.emit("}")
+
+    def scope(self, st: sdfg.State, entry: sdfg.MapEntry, env: dict, depth: int):
+        for c in P._scope_children(st, entry):
+            if isinstance(c, sdfg.Tasklet):
+                self.tasklet(st, c, env, depth)
+            elif isinstance(c, sdfg.MapEntry):
+                inner = dict(env)
+                heads = []
+                for p, (b, e, s) in c.params:
+                    v = self.fresh(f"p_{p}")
+                    bb = symexpr.to_c(b, self.name_of(inner))
+                    ee = symexpr.to_c(e, self.name_of(inner))
+                    ss = symexpr.to_c(s, self.name_of(inner))
+                    heads.append(f"for (b2_ll {v} = {bb}; {v} <= {ee}; {v} += {ss})")
+                    inner[p] = v
+                for h in heads:
+                    self.emit(h + " {")
+                    self.ind += 2
+                self.scope(st, c, inner, depth + 1)
+                for _ in heads:
+                    self.ind -= 2
+                    self.emit("}")
+            elif isinstance(c, sdfg.Library):
+                self.library_in_scope(st, c, env, depth + 1)
+            elif isinstance(c, (sdfg.Access, sdfg.MapExit)):
+                pass
+            else:
+                raise P.PlanError(f"unsupported node {type(c).__name__} inside a map scope")
+
+    def library_in_scope(self, st, n: sdfg.Library, env, depth):
+        """REDUCE inside a map scope (doitgen): sequential in-thread loop with
+        np.<op>.reduce semantics over the input subset (interp.py:461-473)."""
+        if n.kind != "reduce" or n.attrs.get("axes") is not None:
+            raise P.PlanError(f"library node '{n.kind}' inside a map scope is not supported")
+        ins = [e for e in st.in_edges(n) if e.memlet is not None]
+        outs = [e for e in st.out_edges(n) if e.memlet is not None]
+        op = n.attrs.get("op", "add")
+        m = ins[0].memlet
+        c = self.cont(m.container)
+        acc = self.fresh("acc")
+        first = self.fresh("first")
+        self.emit("{")
+        self.ind += 2
+        ident = {"add": "0.0", "mul": "1.0", "min": "b2_inf()", "max": "(-b2_inf())"}[op]
+        self.emit(f"double {acc} = {ident}; bool {first} = true;")
+        loops, idx = [], []
+        for (b, e, s) in m.subset:
+            v = self.fresh("r")
+            loops.append(f"for (b2_ll {v} = {symexpr.to_c(b, self.name_of(env))}; "
+                         f"{v} <= {symexpr.to_c(e, self.name_of(env))}; "
+                         f"{v} += {symexpr.to_c(s, self.name_of(env))})")
+            idx.append(v)
+        for lp in loops:
+            self.emit(lp + " {")
+            self.ind += 2
+        if self.place(m.container) == "reg":
+            val = f"r_{m.container}"
+        else:
+            o = self.fresh("off")
+            site = self._site(f"reduce read {m.text}")
+            self.emit(f"const b2_ll {o} = {self.offset(m.container, idx)};")
+            val = self.fresh("v")
+            self.emit(f"const double {val} = b2_oob({o}, sz_{m.container}, {site}, flag) ? 0.0 : "
+                      f"(double){self.ptr(m.container)}[{o}];")
+        comb = {"add": f"{acc} + {val}", "mul": f"{acc} * {val}",
+                "min": f"b2_npmin({acc}, {val})", "max": f"b2_npmax({acc}, {val})"}[op]
+        self.emit(f"{acc} = {first} ? {val} : ({comb}); {first} = false;")
+        for _ in loops:
+            self.ind -= 2
+            self.emit("}")
+        for e in outs:
+            self.write(e.memlet, acc, "f", env, depth)
+        self.ind -= 2
+        self.emit("}")
+        _ = c
+
+    # -- kernel -----------------------------------------------------------------
+
+    def build(self) -> KernelSpec:
+        grp = self.group
+        spec = self.spec
+        k = len(grp.params)
+        if grp.schedule == "scalar":
+            mode = "scalar"
+        elif grp.schedule == "sequential":
+            mode = "seq"
+        else:
+            mode = "flat"
+            if k >= 2:
+                last = _const_len(self.pl, grp.ranges[-1])
+                prev = _const_len(self.pl, grp.ranges[-2])
+                if last is not None and prev is not None and last >= 16 and prev >= 4:
+                    mode = "tile2"
+        spec.mode = mode
+        spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
+                      "tile2": (32, 8, 1)}[mode]
+
+        # body first (collects containers/symbols), then the prologue
+        env = {p: f"p_{p}" for p in grp.params}
+        body_lines_start = len(self.lines)
+        self.ind = 6
+        # registers for placed transients touched by this group
+        for mem in grp.members:
+            menv = {mp: env[gp] for mp, gp in mem.rename.items()}
+            if mem.tasklet is not None:
+                self.tasklet(mem.state, mem.tasklet, menv, 0)
+            else:
+                self.scope(mem.state, mem.entry, menv, 0)
+        body = self.lines[body_lines_start:]
+        self.lines = self.lines[:body_lines_start]
+
+        pro: list[str] = []
+        pro.append(f'extern "C" __global__ void __launch_bounds__(256) '
+                   f"{spec.name}(const __grid_constant__ B2Args a) {{")
+        for name in spec.containers:
+            c = self.g.containers[name]
+            pl = self.place(name)
+            if pl == "reg":
+                continue
+            base = self.arg(("ptr", name))
+            pro.append(f"  {CT[c.dtype]} *__restrict__ c_{name} = ({CT[c.dtype]} *){base};")
+            for d in range(len(c.shape)):
+                pro.append(f"  const b2_ll st_{name}_{d} = {self.arg(('stride', name, d))};")
+            pro.append(f"  const b2_ll sz_{name} = {self.arg(('size', name))};")
+        for s in spec.syms:
+            pro.append(f"  const b2_ll s_{s} = {self.arg(('sym', s))};")
+        if spec.uses_flag or True:
+            pro.append(f"  int *flag = (int *){self.arg(('flag',))};")
+        for i in range(k):
+            pro.append(f"  const b2_ll rb{i} = {self.arg(('rb', i))};")
+            pro.append(f"  const b2_ll rs{i} = {self.arg(('rs', i))};")
+            pro.append(f"  const b2_ll rl{i} = {self.arg(('rl', i))};")
+        privates = [n for n in spec.containers if self.place(n) == "private"]
+        if privates:
+            pro.append("  const b2_ll tflat = ((b2_ll)blockIdx.x * blockDim.y + threadIdx.y) * "
+                       "blockDim.x + threadIdx.x;")
+            for n in privates:
+                pro.append(f"  {CT[self.g.containers[n].dtype]} *__restrict__ pv_{n} = c_{n} + "
+                           f"tflat * sz_{n};")
+                spec.private[n] = 1
+        regs = [n for n in spec.containers if self.place(n) == "reg"]
+
+        def reg_decls(indent):
+            return [" " * indent + f"{CT[self.g.containers[n].dtype]} r_{n} = 0;" for n in regs]
+
+        loop: list[str] = []
+        if mode == "scalar":
+            loop.append("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
+            loop += reg_decls(4)
+            loop += [ln[2:] for ln in body]
+            loop.append("  }")
+        elif mode == "seq":
+            loop.append("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
+            for i, p in enumerate(grp.params):
+                loop.append(f"  for (b2_ll i{i} = 0; i{i} < rl{i}; ++i{i}) {{")
+                loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
+            loop += reg_decls(4)
+            loop += body
+            for _ in grp.params:
+                loop.append("  }")
+            loop.append("  }")
+        elif mode == "flat":
+            tot = " * ".join(f"rl{i}" for i in range(k))
+            loop.append(f"  const b2_ll total = {tot};")
+            loop.append("  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < total; "
+                        "f += (b2_ll)gridDim.x * blockDim.x) {")
+            loop.append("    b2_ll rem = f;")
+            for i in reversed(range(k)):
+                p = grp.params[i]
+                if i > 0:
+                    loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
+                else:
+                    loop.append(f"    const b2_ll i{i} = rem;")
+                loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
+            loop += reg_decls(4)
+            loop += [ln[2:] for ln in body]
+            loop.append("  }")
+        else:  # tile2
+            x, y = k - 1, k - 2
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + 31) / 32;")
+            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
+            outer = " * ".join(f"rl{i}" for i in range(k - 2)) or "1"
+            loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({outer});")
+            loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
+            loop.append("    const b2_ll tx = vb % tiles_x; b2_ll rem = vb / tiles_x;")
+            loop.append("    const b2_ll ty = rem % tiles_y; rem /= tiles_y;")
+            for i in reversed(range(k - 2)):
+                if i > 0:
+                    loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
+                else:
+                    loop.append(f"    const b2_ll i{i} = rem;")
+            loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
+            loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
+            loop.append(f"    if (i{x} >= rl{x} || i{y} >= rl{y}) continue;")
+            for i, p in enumerate(grp.params):
+                loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
+            loop += reg_decls(4)
+            loop += [ln[2:] for ln in body]
+            loop.append("  }")
+        src = [f"// generated by paper_2107_00555_b200.codegen for state "
+               f"'{grp.state.label}', group of {len(grp.members)} scope(s)",
+               "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
+        spec.source = "\n".join(src + pro + loop + ["}"]) + "\n"
+        return spec
+
+
+def _const_len(planner: P.Planner, rng) -> int | None:
+    b, e, s = rng
+    try:
+        env = dict(planner.fixed)
+        bv, ev, sv = (symexpr.evaluate(x, env) for x in (b, e, s))
+    except KeyError:
+        return None
+    return max(0, (ev - bv) // sv + 1)
+
+
+def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str) -> KernelSpec:
+    gen = _Gen(planner, group, shapes, name)
+    spec = gen.build()
+    spec.params = list(group.params)
+    # args block decoded positionally; fix the struct size after all args known
+    spec.source = spec.source.replace(
+        spec.source.splitlines()[1], "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)))
+    return spec
+
+
+# ---------------------------------------------------------------------------
+# host-side launch recipe
+
+
+def range_values(group: P.MapGroup, env: dict) -> list[tuple[int, int, int]]:
+    out = []
+    for b, e, s in group.ranges:
+        bv = symexpr.evaluate(b, env)
+        ev = symexpr.evaluate(e, env)
+        sv = symexpr.evaluate(s, env)
+        if sv < 1:
+            raise ValueError(f"stride {sv} < 1 in map range")
+        out.append((bv, sv, max(0, (ev - bv) // sv + 1)))
+    return out
+
+
+def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
+    if spec.mode in ("scalar", "seq"):
+        return (1, 1, 1), (1, 1, 1)
+    if spec.mode == "flat":
+        total = 1
+        for v in rl:
+            total *= v
+        blocks = max(1, min((total + 255) // 256, MAX_BLOCKS * 8))
+        if spec.private:
+            blocks = max(1, min(blocks, MAX_BLOCKS))
+        return (blocks, 1, 1), (256, 1, 1)
+    k = len(rl)
+    tiles = ((rl[k - 1] + 31) // 32) * ((rl[k - 2] + 7) // 8)
+    for v in rl[: k - 2]:
+        tiles *= v
+    blocks = max(1, min(tiles, MAX_BLOCKS * 8))
+    if spec.private:
+        blocks = max(1, min(blocks, MAX_BLOCKS))
+    return (blocks, 1, 1), (32, 8, 1)
+
+
+def pack_args(spec: KernelSpec, env: dict, rvals, ptrs: dict, strides: dict, sizes: dict,
+              scratch: dict, flag_ptr: int) -> bytes:
+    vals = []
+    for d in spec.args:
+        k = d[0]
+        if k == "ptr":
+            vals.append(scratch[d[1]] if d[1] in scratch else ptrs[d[1]])
+        elif k == "stride":
+            vals.append(strides[d[1]][d[2]])
+        elif k == "size":
+            vals.append(sizes[d[1]])
+        elif k == "sym":
+            vals.append(int(env[d[1]]))
+        elif k == "flag":
+            vals.append(flag_ptr)
+        elif k == "rb":
+            vals.append(rvals[d[1]][0])
+        elif k == "rs":
+            vals.append(rvals[d[1]][1])
+        elif k == "rl":
+            vals.append(rvals[d[1]][2])
+        else:
+            raise AssertionError(d)
+    if not vals:
+        vals = [0]
+    return struct.pack(f"<{len(vals)}q", *[v if v < (1 << 63) else v - (1 << 64) for v in vals])

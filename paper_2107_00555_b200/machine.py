@@ -1,0 +1,803 @@
+"""B200 drop-in for the reference executor ``sdfgkit.interp.interpret``.
+
+Contract mirrored from pkg/src/sdfgkit/interp.py:
+  * ``interpret(g, ctx, options=None) -> dict[str, np.ndarray]`` (139-150):
+    inputs in ``ctx.store`` are copied (caller arrays never mutated), the
+    returned arrays are executor-owned host copies of every non-transient
+    container, counters accumulate in ``ctx.counters``.
+  * ``ExecContext`` / ``Counters`` / ``InterpOptions`` (73-115) — the
+    reference's own objects are accepted too (duck-typed).
+  * errors: ``InterpreterError`` (RuntimeError) for invalid graphs, missing
+    symbols/inputs, shape mismatches, communication nodes, no transition,
+    transition budget; ``OutOfBoundsError`` for out-of-range memlets
+    (26-31, 185-213, 259-263, 284-298).
+
+Where it differs by design: all containers live in HBM for the whole run
+(no host round trips between states), the state machine is traced once on
+the host and replayed as a single CUDA graph when its transitions depend
+only on symbols, and map scopes are device kernels (plan.py / codegen.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import itertools
+import json
+from dataclasses import dataclass, field
+from typing import Mapping
+
+import numpy as np
+
+from . import codegen, plan as P, runtime as rt, scalar, sdfg, symexpr
+
+_NP = {"f64": np.float64, "i64": np.int64, "i32": np.int32, "bool": np.bool_}
+
+
+class InterpreterError(RuntimeError):
+    pass
+
+
+class OutOfBoundsError(InterpreterError):
+    pass
+
+
+@dataclass
+class Counters:
+    wcr_commits: int = 0
+    map_iterations: int = 0
+    bytes_moved: int = 0
+    messages_posted: int = 0
+    messages_delivered: int = 0
+    collective_calls: int = 0
+    comm_bytes: int = 0
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+@dataclass
+class ExecContext:
+    bindings: dict = field(default_factory=dict)
+    store: dict = field(default_factory=dict)
+    persistent: dict = field(default_factory=dict)
+    counters: Counters = field(default_factory=Counters)
+    rank: int = 0
+
+    def bind_inputs(self, inputs: Mapping) -> "ExecContext":
+        for k, v in inputs.items():
+            self.store[k] = np.asarray(v)
+        return self
+
+
+@dataclass
+class InterpOptions:
+    reverse_maps: bool = False  # order-insensitive on the device; accepted for parity
+    max_transitions: int = 10_000_000
+    skip_validation: bool = False
+
+
+# ---------------------------------------------------------------------------
+
+
+class _Buffers:
+    """HBM placement of one executor's containers."""
+
+    def __init__(self):
+        self.ptr: dict[str, int] = {}
+        self.nbytes: dict[str, int] = {}
+        self.shape: dict[str, tuple] = {}
+        self.strides: dict[str, list[int]] = {}
+        self.size: dict[str, int] = {}
+        self._owned: list[int] = []
+
+    def alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        rt.check(rt.lib().b2_malloc(ctypes.byref(p), max(8, nbytes)), "alloc")
+        self._owned.append(p.value)
+        return p.value
+
+    def free(self):
+        L = rt.lib()
+        for p in self._owned:
+            L.b2_free(p)
+        self._owned.clear()
+
+
+def _row_major(shape) -> list[int]:
+    st = [1] * len(shape)
+    acc = 1
+    for d in range(len(shape) - 1, -1, -1):
+        st[d] = acc
+        acc *= shape[d]
+    return st
+
+
+class GpuExecutor:
+    """Plan + HBM buffers + compiled kernels for one graph and one set of
+    symbol bindings.  Reusable across calls (buffers and the captured graph
+    persist; inputs are re-uploaded each call)."""
+
+    def __init__(self, g: sdfg.Graph, bindings: dict, device: int = 0, stream=None,
+                 options: InterpOptions | None = None, external: dict | None = None):
+        rt.device(device)
+        self.g = g
+        self.bindings = {k: int(v) for k, v in bindings.items()}
+        self.opt = options or InterpOptions()
+        self.planner = P.Planner(g, self.bindings).build()
+        self.buf = _Buffers()
+        self.flag = self.buf.alloc(8)
+        if stream is None:
+            s = ctypes.c_void_p()
+            rt.check(rt.lib().b2_stream_create(ctypes.byref(s)), "stream")
+            stream = s.value
+        self.stream = stream
+        self.graph_exec = None
+        self.capturable = self._capturable()
+        self.scratch: dict[str, int] = {}
+        self.launches = 0
+        self.children: dict[int, "GpuExecutor"] = {}
+        self._allocate(external or {})
+        self._compile()
+
+    # -- setup ------------------------------------------------------------------
+
+    def _capturable(self) -> bool:
+        for t in self.g.transitions:
+            if t.condition is not None and any(
+                    n in self.g.containers for n in scalar.free_names(t.condition)):
+                return False
+        return True
+
+    def _allocate(self, external: dict):
+        env = dict(self.bindings)
+        for name, c in self.g.containers.items():
+            try:
+                shape = tuple(symexpr.evaluate(d, env) for d in c.shape)
+            except KeyError as ex:
+                raise InterpreterError(f"missing symbol bindings: {ex}") from None
+            self.buf.shape[name] = shape
+            self.buf.strides[name] = _row_major(shape)
+            n = 1
+            for s in shape:
+                n *= s
+            self.buf.size[name] = n
+            nbytes = n * sdfg.DTYPE_BYTES[c.dtype]
+            self.buf.nbytes[name] = nbytes
+            if self.planner.placement.get(name) in ("reg", "private"):
+                continue
+            if name in external:
+                self.buf.ptr[name] = external[name]
+            else:
+                self.buf.ptr[name] = self.buf.alloc(nbytes)
+
+    def _compile(self):
+        self.specs: dict[int, codegen.KernelSpec] = {}
+        for op in self.planner.all_ops:
+            if isinstance(op, P.MapGroup):
+                name = f"b2_map_{self.g.name}_{op.idx}"
+                spec = codegen.generate(self.planner, op, self.buf.shape, name)
+                src = rt.family_source("prelude.cuh") + "\n" + spec.source
+                spec.kernel = rt.get_kernel(src, name)
+                self.specs[op.idx] = spec
+            elif isinstance(op, P.LibOp) and op.rowpass is not None:
+                op.rowpass.compile(self)
+        # private scratch sized for the largest grid of the owning kernel
+        for idx, spec in self.specs.items():
+            for n in spec.private:
+                per = self.buf.size[n] * sdfg.DTYPE_BYTES[self.g.containers[n].dtype]
+                threads = codegen.MAX_BLOCKS * 256
+                self.scratch[n] = self.buf.alloc(per * threads)
+                self.buf.nbytes[n + "#scratch"] = per * threads
+
+    def close(self):
+        if self.graph_exec is not None:
+            rt.lib().b2_graph_destroy(self.graph_exec)
+            self.graph_exec = None
+        for ch in self.children.values():
+            ch.close()
+        self.buf.free()
+
+    # -- data movement ---------------------------------------------------------
+
+    def upload(self, name: str, arr: np.ndarray):
+        c = self.g.containers[name]
+        a = np.ascontiguousarray(arr, dtype=_NP[c.dtype])
+        rt.check(rt.lib().b2_memcpy_h2d(self.buf.ptr[name], a.ctypes.data, a.nbytes, self.stream),
+                 "h2d")
+        return a  # keep alive until the stream is synchronised
+
+    def download(self, name: str) -> np.ndarray:
+        c = self.g.containers[name]
+        shape = self.buf.shape[name] if c.kind != "scalar" else ()
+        out = np.empty(shape, dtype=_NP[c.dtype])
+        rt.check(rt.lib().b2_memcpy_d2h(out.ctypes.data, self.buf.ptr[name], out.nbytes,
+                                        self.stream), "d2h")
+        return out
+
+    def zero(self, name: str):
+        if name in self.buf.ptr:
+            rt.check(rt.lib().b2_memset(self.buf.ptr[name], 0, self.buf.nbytes[name], self.stream),
+                     "memset")
+
+    def sync(self):
+        rt.check(rt.lib().b2_stream_sync(self.stream), "sync")
+
+    def prepare_inputs(self, store: Mapping, persistent_fresh: set | None = None) -> list:
+        """Upload non-transient inputs (copied, interp.py:208-215) and zero
+        scope transients (np.zeros each call, interp.py:220-221)."""
+        keep = []
+        for name, c in self.g.containers.items():
+            if c.transient:
+                continue
+            if name not in store:
+                raise InterpreterError(f"missing input container '{name}'")
+            arr = np.asarray(store[name], dtype=_NP[c.dtype])
+            if c.kind == "scalar":
+                arr = arr.reshape(())
+            elif arr.shape != self.buf.shape[name]:
+                raise InterpreterError(
+                    f"input '{name}' has shape {arr.shape}, descriptor says {self.buf.shape[name]}")
+            keep.append(self.upload(name, arr))
+        return keep
+
+    def zero_transients(self, first_call: bool):
+        for name, c in self.g.containers.items():
+            if not c.transient or name not in self.buf.ptr:
+                continue
+            if c.lifetime == "persistent" and not first_call:
+                continue  # persistent transients keep their contents (interp.py:216-219)
+            self.zero(name)
+        for n, p in self.scratch.items():
+            rt.check(rt.lib().b2_memset(p, 0, self.buf.nbytes[n + "#scratch"], self.stream), "memset")
+
+    # -- execution ---------------------------------------------------------------
+
+    def run_device(self, first_call: bool = True, counters=None):
+        """Execute the whole state machine on the device (inputs already
+        resident).  Returns after enqueueing; call ``sync()`` to wait."""
+        rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
+        self.zero_transients(first_call)
+        if self.capturable:
+            if self.graph_exec is None:
+                self._capture(counters)
+            rt.check(rt.lib().b2_graph_launch(self.graph_exec, self.stream), "graph launch")
+            if counters is not None and self._trace_counters is not None:
+                _add_counters(counters, self._trace_counters)
+        else:
+            self._run_states(counters, eager=True)
+
+    def _capture(self, counters):
+        L = rt.lib()
+        rt.check(L.b2_capture_begin(self.stream), "capture")
+        tc = Counters()
+        try:
+            self._run_states(tc, eager=False)
+        except BaseException:
+            ge = ctypes.c_void_p()
+            L.b2_capture_end(self.stream, ctypes.byref(ge))
+            if ge.value:
+                L.b2_graph_destroy(ge)
+            raise
+        ge = ctypes.c_void_p()
+        rt.check(L.b2_capture_end(self.stream, ctypes.byref(ge)), "capture end")
+        self.graph_exec = ge.value
+        self._trace_counters = tc
+
+    _trace_counters = None
+
+    def _run_states(self, counters, eager: bool):
+        g = self.g
+        sym = dict(self.bindings)
+        cur = g.start
+        steps = 0
+        while cur is not None:
+            for op in self.planner.ops[cur]:
+                self._exec_op(op, sym, counters)
+            cur = self.planner.chain_end[cur]
+            trs = g.out_transitions(cur)
+            if not trs:
+                break
+            nxt = None
+            for t in trs:
+                if t.condition is None or self._eval_cond(t.condition, sym):
+                    for k, v in t.assignments.items():
+                        sym[k] = symexpr.evaluate(v, sym)
+                    nxt = t.dst
+                    break
+            if nxt is None:
+                raise InterpreterError(f"no transition taken out of state '{cur}'")
+            cur = nxt
+            steps += 1
+            if steps > self.opt.max_transitions:
+                raise InterpreterError("transition budget exceeded (infinite loop?)")
+
+    def _eval_cond(self, cond, sym):
+        env = {}
+        for n in scalar.free_names(cond):
+            if n in sym:
+                env[n] = sym[n]
+            elif n in self.g.containers:
+                self.sync()
+                env[n] = self.download(n)[()]
+            else:
+                raise InterpreterError(f"condition references unknown name '{n}'")
+        return bool(scalar.evaluate(cond, env))
+
+    # -- ops -----------------------------------------------------------------------
+
+    def _exec_op(self, op, sym, counters):
+        if isinstance(op, P.MapGroup):
+            self._exec_map(op, sym, counters)
+        elif isinstance(op, P.CopyOp):
+            self._exec_copy(op, sym, counters)
+        elif isinstance(op, P.LibOp):
+            if op.kind == "comm":
+                raise InterpreterError(
+                    f"communication node '{op.node.kind}' requires the rank simulator")
+            if op.rowpass is not None:
+                op.rowpass.run(self, sym, counters)
+            elif op.kind == "matmul":
+                self._exec_matmul(op, sym, counters)
+            elif op.kind == "reduce":
+                self._exec_reduce(op, sym, counters)
+            elif op.kind == "transpose":
+                self._exec_transpose(op, sym, counters)
+        elif isinstance(op, P.NestedOp):
+            self._exec_nested(op, sym, counters)
+
+    def _check_bounds(self, spec, rvals, env, state, node_desc):
+        box_g = {}
+        for i, p in enumerate(spec_params(spec)):
+            b, s, n = rvals[i]
+            if n == 0:
+                return False
+            lo, hi = b, b + s * (n - 1)
+            box_g[p] = (min(lo, hi), max(lo, hi))
+        for cont, subset, cenv in spec.checks:
+            shape = self.buf.shape[cont]
+            box = {mp: box_g[cv[2:]] for mp, cv in cenv.items() if cv.startswith("p_") and cv[2:] in box_g}
+            if len(subset) != len(shape):
+                raise OutOfBoundsError(f"rank mismatch on '{cont}' in state '{state}'")
+            for d, (b, e, s) in enumerate(subset):
+                lo, _ = symexpr.interval(b, box, env)
+                _, hi = symexpr.interval(e, box, env)
+                if lo < 0 or hi >= shape[d]:
+                    raise OutOfBoundsError(
+                        f"out-of-bounds access {cont}[dim {d}: {lo}..{hi}] (extent {shape[d]}) "
+                        f"at {node_desc} in state '{state}'")
+        return True
+
+    def _exec_map(self, op: P.MapGroup, sym, counters):
+        spec = self.specs[op.idx]
+        env = sym
+        try:
+            rvals = codegen.range_values(op, env)
+        except KeyError as ex:
+            raise InterpreterError(f"missing symbol bindings: {ex}") from None
+        npts = 1
+        for _, _, n in rvals:
+            npts *= n
+        if op.params and npts == 0:
+            return
+        if not self._check_bounds(spec, rvals, env, op.state.label, f"map group {op.idx}"):
+            return
+        grid, block = codegen.launch_geometry(spec, [n for _, _, n in rvals])
+        blob = codegen.pack_args(spec, env, rvals, self.buf.ptr, self.buf.strides, self.buf.size,
+                                 self.scratch, self.flag)
+        rt.launch(spec.kernel, grid, block, blob, self.stream)
+        self.launches += 1
+        if counters is not None:
+            _count_map(self, op, rvals, counters, env)
+
+    def view(self, m: sdfg.Memlet, env, kept=None):
+        """Strided view of a memlet subset (+ optional squeeze of unkept dims,
+        interp.py:326-330)."""
+        name = m.container
+        if name not in self.buf.ptr:
+            raise InterpreterError(f"container '{name}' has no HBM buffer")
+        ranges = symexpr.eval_subset(m.subset, env)
+        shape = self.buf.shape[name]
+        if len(ranges) != len(shape):
+            raise OutOfBoundsError(f"rank mismatch on '{name}'")
+        for d, r in enumerate(ranges):
+            if len(r) and (r.start < 0 or r[-1] >= shape[d]):
+                raise OutOfBoundsError(
+                    f"out-of-bounds access {name}[dim {d}: {r.start}..{r[-1]}] "
+                    f"(extent {shape[d]})")
+        st = self.buf.strides[name]
+        off = sum(r.start * st[d] for d, r in enumerate(ranges))
+        dims = [(len(r), st[d] * r.step) for d, r in enumerate(ranges)]
+        if kept is not None:
+            dims = [dd for dd, k in zip(dims, kept) if k]
+        return self.buf.ptr[name], off, self.g.containers[name].dtype, dims
+
+    def _exec_copy(self, op: P.CopyOp, sym, counters):
+        e = op.edge
+        src, dst, m = e.src, e.dst, e.memlet
+        if m.container == src.container:
+            base, off, dt, dims = self.view(m, sym)
+            dshape = self.buf.shape[dst.container]
+            dv = rt.make_view(self.buf.ptr[dst.container], 0, self.g.containers[dst.container].dtype,
+                              dshape, self.buf.strides[dst.container])
+            sv = rt.make_view(base, off, dt, [d[0] for d in dims], [d[1] for d in dims])
+            wcr = m.wcr
+        else:
+            sshape = self.buf.shape[src.container]
+            sv = rt.make_view(self.buf.ptr[src.container], 0, self.g.containers[src.container].dtype,
+                              sshape, self.buf.strides[src.container])
+            base, off, dt, dims = self.view(m, sym)
+            dv = rt.make_view(base, off, dt, [d[0] for d in dims], [d[1] for d in dims])
+            wcr = m.wcr
+        n_src = int(np.prod([sv.shape[i] for i in range(sv.ndim)])) if sv.ndim else 1
+        n_dst = int(np.prod([dv.shape[i] for i in range(dv.ndim)])) if dv.ndim else 1
+        if n_src != n_dst:
+            raise InterpreterError(f"copy size mismatch {n_src} vs {n_dst}")
+        rt.check(rt.lib().b2_copy_view(ctypes.byref(dv), ctypes.byref(sv), rt.WCR_CODE[wcr],
+                                       self.stream), "copy")
+        self.launches += 1
+        if counters is not None:
+            counters.bytes_moved += n_src * sdfg.DTYPE_BYTES[self.g.containers[src.container].dtype]
+            counters.bytes_moved += n_dst * sdfg.DTYPE_BYTES[self.g.containers[dst.container].dtype]
+            if wcr is not None:
+                counters.wcr_commits += n_dst
+
+    def _io(self, op):
+        ins = {e.dst_conn: e for e in op.state.in_edges(op.node) if e.memlet is not None}
+        outs = [e for e in op.state.out_edges(op.node) if e.memlet is not None]
+        return ins, outs
+
+    def _exec_matmul(self, op: P.LibOp, sym, counters):
+        ins, outs = self._io(op)
+        n = op.node
+        ab, ao, adt, ad = self.view(ins["a"].memlet, sym, n.attrs.get("a_kept"))
+        bb, bo, bdt, bd = self.view(ins["b"].memlet, sym, n.attrs.get("b_kept"))
+        om = outs[0].memlet
+        cb, co, cdt, cd = self.view(om, sym)
+        if adt != "f64" or bdt != "f64" or cdt != "f64":
+            raise P.PlanError("MATMUL is implemented for f64 containers")
+        # np.matmul shapes: (M,K)@(K,N), (M,K)@(K,), (K,)@(K,N), (K,)@(K,)
+        if len(ad) == 2:
+            M, K = ad[0][0], ad[1][0]
+            rsa, csa = ad[0][1], ad[1][1]
+        elif len(ad) == 1:
+            M, K = 1, ad[0][0]
+            rsa, csa = 0, ad[0][1]
+        else:
+            raise InterpreterError("matmul operand a must be 1-D or 2-D")
+        if len(bd) == 2:
+            K2, N = bd[0][0], bd[1][0]
+            rsb, csb = bd[0][1], bd[1][1]
+        elif len(bd) == 1:
+            K2, N = bd[0][0], 1
+            rsb, csb = bd[0][1], 0
+        else:
+            raise InterpreterError("matmul operand b must be 1-D or 2-D")
+        if K != K2:
+            raise InterpreterError(f"matmul inner dimensions differ ({K} vs {K2})")
+        rsc, csc = _out_strides(cd, M, N)
+        if rsc is None:
+            raise P.PlanError("matmul output view is not an affine image of the result")
+        rt.check(rt.lib().b2_gemm_f64(M, N, K, ab + 8 * ao, rsa, csa, bb + 8 * bo, rsb, csb,
+                                      cb + 8 * co, rsc, csc, rt.WCR_CODE[om.wcr], self.stream),
+                 "gemm")
+        self.launches += 1
+        if counters is not None:
+            counters.bytes_moved += 8 * (M * K + K * N + M * N)
+            if om.wcr is not None:
+                counters.wcr_commits += M * N
+
+    def _exec_reduce(self, op: P.LibOp, sym, counters):
+        ins, outs = self._io(op)
+        n = op.node
+        ab, ao, adt, ad = self.view(ins["a"].memlet, sym, n.attrs.get("a_kept"))
+        om = outs[0].memlet
+        cb, co, cdt, cd = self.view(om, sym)
+        axes = n.attrs.get("axes")
+        mask = 0
+        for d in (range(len(ad)) if axes is None else axes):
+            mask |= 1 << (d % max(1, len(ad)))
+        iv = rt.make_view(ab, ao, adt, [d[0] for d in ad], [d[1] for d in ad])
+        ov = rt.make_view(cb, co, cdt, [d[0] for d in cd], [d[1] for d in cd])
+        opc = rt.WCR_CODE[n.attrs.get("op", "add")]
+        rt.check(rt.lib().b2_reduce(ctypes.byref(ov), ctypes.byref(iv), mask, opc,
+                                    rt.WCR_CODE[om.wcr], self.stream), "reduce")
+        self.launches += 1
+        if counters is not None:
+            nin = int(np.prod([d[0] for d in ad])) if ad else 1
+            nout = int(np.prod([d[0] for d in cd])) if cd else 1
+            counters.bytes_moved += nin * 8 + nout * 8
+            if om.wcr is not None:
+                counters.wcr_commits += nout
+
+    def _exec_transpose(self, op: P.LibOp, sym, counters):
+        ins, outs = self._io(op)
+        ab, ao, adt, ad = self.view(ins["a"].memlet, sym)
+        om = outs[0].memlet
+        cb, co, cdt, cd = self.view(om, sym)
+        ad = list(reversed(ad))  # a.T
+        iv = rt.make_view(ab, ao, adt, [d[0] for d in ad], [d[1] for d in ad])
+        ov = rt.make_view(cb, co, cdt, [d[0] for d in cd], [d[1] for d in cd])
+        rt.check(rt.lib().b2_copy_view(ctypes.byref(ov), ctypes.byref(iv), rt.WCR_CODE[om.wcr],
+                                       self.stream), "transpose")
+        self.launches += 1
+        if counters is not None:
+            nin = int(np.prod([d[0] for d in ad])) if ad else 1
+            counters.bytes_moved += 2 * nin * sdfg.DTYPE_BYTES[adt]
+            if om.wcr is not None:
+                counters.wcr_commits += nin
+
+    def _exec_nested(self, op: P.NestedOp, sym, counters):
+        """Nested graph (interp.py:491-517): inner containers alias the outer
+        memlet views when those are whole contiguous containers, else they
+        are copied in/out through b2_copy_view."""
+        n = op.node
+        inner = n.sdfg
+        binds = {}
+        for s in inner.free_symbols():
+            expr = n.symbol_map.get(s, ("s", s))
+            binds[s] = symexpr.evaluate(expr, sym)
+        key = (op.idx, tuple(sorted(binds.items())))
+        child = self.children.get(key)
+        ins = [e for e in op.state.in_edges(n) if e.memlet is not None]
+        outs = [e for e in op.state.out_edges(n) if e.memlet is not None]
+        if child is None:
+            external = {}
+            for e in ins + outs:
+                conn = e.dst_conn if e in ins else e.src_conn
+                name = e.memlet.container
+                ic = inner.containers[conn]
+                try:
+                    ishape = tuple(symexpr.evaluate(d, binds) for d in ic.shape)
+                except KeyError:
+                    ishape = None
+                if (_is_full(self, e.memlet, sym) and ishape == self.buf.shape[name]
+                        and self.g.containers[name].dtype == ic.dtype and name in self.buf.ptr):
+                    external[conn] = self.buf.ptr[name]
+            child = GpuExecutor(inner, binds, stream=self.stream, options=self.opt,
+                                external=external)
+            child._external = external
+            self.children[key] = child
+        for e in ins:
+            conn = e.dst_conn
+            if conn in child._external:
+                continue
+            self._copy_between(child, conn, e.memlet, sym, into_child=True)
+        rt.check(rt.lib().b2_memset(child.flag, 0, 8, self.stream), "memset")
+        child.zero_transients(first_call=True)
+        child._run_states(counters, eager=not self.capturable)
+        self.launches += child.launches
+        child.launches = 0
+        for e in outs:
+            conn = e.src_conn
+            if conn in child._external:
+                continue
+            self._copy_between(child, conn, e.memlet, sym, into_child=False)
+
+    def _copy_between(self, child, conn, m, sym, into_child):
+        base, off, dt, dims = self.view(m, sym)
+        ov = rt.make_view(base, off, dt, [d[0] for d in dims], [d[1] for d in dims])
+        cv = rt.make_view(child.buf.ptr[conn], 0, child.g.containers[conn].dtype,
+                          child.buf.shape[conn], child.buf.strides[conn])
+        src, dst = (ov, cv) if into_child else (cv, ov)
+        wcr = None if into_child else m.wcr
+        rt.check(rt.lib().b2_copy_view(ctypes.byref(dst), ctypes.byref(src), rt.WCR_CODE[wcr],
+                                       self.stream), "nested copy")
+        self.launches += 1
+
+    # -- results --------------------------------------------------------------
+
+    def check_flag(self):
+        v = np.zeros(2, dtype=np.int32)
+        rt.check(rt.lib().b2_memcpy_d2h(v.ctypes.data, self.flag, 8, self.stream), "d2h")
+        self.sync()
+        if v[0]:
+            site = int(v[0]) - 1
+            desc = "?"
+            for spec in self.specs.values():
+                if site < len(spec.sites):
+                    desc = spec.sites[site]
+                    break
+            raise OutOfBoundsError(f"out-of-bounds access detected on the device ({desc})")
+        for ch in self.children.values():
+            ch.check_flag()
+
+    def outputs(self) -> dict[str, np.ndarray]:
+        out = {n: self.download(n) for n, c in self.g.containers.items() if not c.transient}
+        self.sync()
+        return out
+
+
+def spec_params(spec):
+    return spec.params
+
+
+def _is_full(ex: GpuExecutor, m: sdfg.Memlet, sym) -> bool:
+    try:
+        ranges = symexpr.eval_subset(m.subset, sym)
+    except KeyError:
+        return False
+    shape = ex.buf.shape[m.container]
+    if len(ranges) != len(shape):
+        return False
+    return all(r.start == 0 and r.step == 1 and len(r) == s for r, s in zip(ranges, shape))
+
+
+def _out_strides(cd, M, N):
+    """Row/col strides placing the row-major (M, N) matmul result into the
+    output view ``cd`` (reshape semantics of interp.py:457-459)."""
+    dims = [d for d in cd if d[0] != 1]
+    if M * N == 1:
+        return 0, 0
+    if M == 1:
+        if len(dims) == 1 and dims[0][0] == N:
+            return 0, dims[0][1]
+    if N == 1:
+        if len(dims) == 1 and dims[0][0] == M:
+            return dims[0][1], 0
+    if len(dims) == 2 and dims[0][0] == M and dims[1][0] == N:
+        return dims[0][1], dims[1][1]
+    if len(dims) == 1 and dims[0][0] == M * N:
+        return N * dims[0][1], dims[0][1]
+    return None, None
+
+
+def _add_counters(dst, src):
+    for k in ("wcr_commits", "map_iterations", "bytes_moved"):
+        setattr(dst, k, getattr(dst, k) + getattr(src, k))
+
+
+def _count_map(ex: GpuExecutor, op: P.MapGroup, rvals, counters, env):
+    """Analytic restatement of the interpreter's counters (interp.py:73-92):
+    one map_iteration per point of every member map, bytes per memlet access,
+    wcr_commits per WCR element write."""
+    npts = 1
+    for _, _, n in rvals:
+        npts *= n
+    for m in op.members:
+        if m.entry is None:
+            _count_tasklet(ex, m.state, m.tasklet, counters, 1, env)
+            continue
+        counters.map_iterations += npts
+        _count_scope(ex, m.state, m.entry, counters, npts, env, op, m, rvals)
+
+
+def _count_tasklet(ex, st, t, counters, mult, env):
+    for e in st.in_edges(t) + st.out_edges(t):
+        if e.memlet is None:
+            continue
+        vol = _volume(e.memlet, env)
+        if vol is None:
+            vol = 1
+        counters.bytes_moved += mult * vol * sdfg.DTYPE_BYTES[ex.g.containers[e.memlet.container].dtype]
+        if e.src is t and e.memlet.wcr is not None:
+            counters.wcr_commits += mult * vol
+
+
+def _volume(m, env):
+    v = 1
+    for b, e, s in m.subset:
+        try:
+            bv, ev, sv = (symexpr.evaluate(x, env) for x in (b, e, s))
+        except KeyError:
+            if b == e:
+                continue
+            return None
+        v *= max(0, (ev - bv) // sv + 1)
+    return v
+
+
+def _count_scope(ex, st, entry, counters, npts, env, op, member, rvals):
+    for c in P._scope_children(st, entry):
+        if isinstance(c, sdfg.Tasklet):
+            _count_tasklet(ex, st, c, counters, npts, env)
+        elif isinstance(c, sdfg.MapEntry):
+            inner = 1
+            ok = True
+            for _, (b, e, s) in c.params:
+                try:
+                    bv, ev, sv = (symexpr.evaluate(x, env) for x in (b, e, s))
+                    inner *= max(0, (ev - bv) // sv + 1)
+                except KeyError:
+                    ok = False
+            if ok:
+                counters.map_iterations += npts * inner
+                _count_scope(ex, st, c, counters, npts * inner, env, op, member, rvals)
+        elif isinstance(c, sdfg.Library):
+            for e in st.in_edges(c) + st.out_edges(c):
+                if e.memlet is not None:
+                    vol = _volume(e.memlet, env) or 1
+                    counters.bytes_moved += npts * vol * 8
+                    if e.src is c and e.memlet.wcr is not None:
+                        counters.wcr_commits += npts * vol
+
+
+# ---------------------------------------------------------------------------
+# public API (interp.py:139-150)
+
+_exec_cache: dict = {}
+
+
+def _ctx_parts(ctx):
+    bindings = dict(getattr(ctx, "bindings", {}) or {})
+    store = getattr(ctx, "store", {})
+    counters = getattr(ctx, "counters", None)
+    return bindings, store, counters
+
+
+_CACHE_MAX = 32
+
+
+def get_executor(g, bindings: dict, options=None, device: int = 0) -> GpuExecutor:
+    """Executors are cached per (graph, bindings, device): by identity for
+    Graph objects, by a hash of the schema-v1 document otherwise."""
+    if isinstance(g, sdfg.Graph):
+        graph, fkey = g, ("obj", id(g))
+    else:
+        graph = sdfg.as_graph(g)
+        fkey = ("doc", hashlib.sha1(json.dumps(graph.doc, sort_keys=True).encode()).hexdigest())
+    missing = graph.free_symbols() - set(bindings)
+    if missing:
+        raise InterpreterError(f"missing symbol bindings: {sorted(missing)}")
+    key = (fkey, tuple(sorted((k, int(v)) for k, v in bindings.items())), device)
+    ex = _exec_cache.get(key)
+    if ex is not None and (fkey[0] != "obj" or ex.g is graph):
+        return ex
+    _validate(graph)
+    try:
+        ex = GpuExecutor(graph, bindings, device=device, options=options)
+    except P.PlanError:
+        raise
+    except (KeyError, ValueError, sdfg.SchemaError) as exn:
+        raise InterpreterError(f"graph does not validate: {exn}") from exn
+    if len(_exec_cache) >= _CACHE_MAX:
+        _exec_cache.pop(next(iter(_exec_cache))).close()
+    _exec_cache[key] = ex
+    return ex
+
+
+def _validate(g: sdfg.Graph):
+    labels = {s.label for s in g.states}
+    if g.start not in labels:
+        raise InterpreterError("graph does not validate: start state missing")
+    for t in g.transitions:
+        if t.src not in labels or t.dst not in labels:
+            raise InterpreterError("graph does not validate: dangling transition")
+    for st in g.states:
+        try:
+            st.scope_parents()
+        except sdfg.SchemaError as ex:
+            raise InterpreterError(f"graph does not validate: {ex}") from None
+        for e in st.edges:
+            if e.memlet is not None:
+                c = g.containers.get(e.memlet.container)
+                if c is None:
+                    raise InterpreterError(
+                        f"graph does not validate: unknown container '{e.memlet.container}'")
+                if len(e.memlet.subset) != len(c.shape):
+                    raise InterpreterError(
+                        f"graph does not validate: memlet rank mismatch on '{c.name}'")
+        for n in st.nodes:
+            if isinstance(n, sdfg.Access) and n.container not in g.containers:
+                raise InterpreterError(f"graph does not validate: unknown container '{n.container}'")
+
+
+def interpret(g, ctx, options: InterpOptions | None = None) -> dict[str, np.ndarray]:
+    """Execute the graph on the B200; returns the non-transient containers."""
+    bindings, store, counters = _ctx_parts(ctx)
+    ex = get_executor(g, bindings, options)
+    first = not getattr(ex, "_ran", False)
+    keep = ex.prepare_inputs(store)
+    c = Counters() if counters is not None else None
+    ex.run_device(first_call=first, counters=c)
+    ex._ran = True
+    out = ex.outputs()
+    del keep
+    ex.check_flag()
+    if counters is not None and c is not None:
+        for k in ("wcr_commits", "map_iterations", "bytes_moved"):
+            setattr(counters, k, getattr(counters, k) + getattr(c, k))
+    return out
+
+
+_ = itertools

@@ -1,0 +1,371 @@
+"""Tasklet scalar expressions: parser, Python-semantics evaluator, CUDA C emitter.
+
+Grammar and semantics follow the reference's tasklet language
+(pkg/src/sdfgkit/texpr.py:89-133 evaluation, 139-306 text form).  The device
+emitter reproduces Python scalar semantics:
+
+* ``/`` is true division (int/int -> double),
+* ``//`` floors toward -inf (ints) and follows CPython/numpy float floor
+  division (``npy_divmod``) for doubles,
+* comparisons and ``and``/``or``/``not`` yield bool, bools do 0/1 arithmetic,
+* ``min``/``max`` are the Python builtins (``min(nan, 1) = nan``,
+  ``min(1, nan) = 1``), not ``fmin``/``fmax``,
+* no FMA contraction: every kernel is compiled with ``--fmad=false`` so a
+  fused tasklet chain rounds exactly like the op-by-op numpy evaluation.
+
+Documented divergence: ``math.sqrt``/``math.exp`` raise on domain/overflow
+errors in Python; the device returns IEEE NaN/inf instead.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from typing import Mapping
+
+_TOK = re.compile(
+    r"\s*(\d+\.\d*(?:[eE][-+]?\d+)?|\.\d+(?:[eE][-+]?\d+)?|\d+[eE][-+]?\d+|\d+"
+    r"|[A-Za-z_][A-Za-z_0-9]*|//|<=|>=|==|!=|[-+*/()<>?,:])"
+)
+INTRINSICS = ("sqrt", "exp", "abs", "pow", "min", "max")
+COMPARISONS = ("<", "<=", ">", ">=", "==", "!=")
+
+
+class ScalarSyntaxError(ValueError):
+    pass
+
+
+class _P:
+    def __init__(self, text: str):
+        self.toks: list[str] = []
+        pos = 0
+        while pos < len(text):
+            m = _TOK.match(text, pos)
+            if not m:
+                if text[pos:].strip():
+                    raise ScalarSyntaxError(f"bad scalar expression near {text[pos:]!r}")
+                break
+            self.toks.append(m.group(1))
+            pos = m.end()
+        self.i = 0
+
+    def peek(self):
+        return self.toks[self.i] if self.i < len(self.toks) else None
+
+    def take(self, want=None):
+        t = self.peek()
+        if t is None:
+            raise ScalarSyntaxError("unexpected end of scalar expression")
+        if want is not None and t != want:
+            raise ScalarSyntaxError(f"expected {want!r}, got {t!r}")
+        self.i += 1
+        return t
+
+    def parse(self):
+        e = self.select()
+        if self.peek() is not None:
+            raise ScalarSyntaxError(f"trailing tokens {self.toks[self.i:]}")
+        return e
+
+    def select(self):
+        c = self.or_()
+        if self.peek() == "?":
+            self.take()
+            a = self.select()
+            self.take(":")
+            b = self.select()
+            return ("sel", c, a, b)
+        return c
+
+    def or_(self):
+        e = self.and_()
+        while self.peek() == "or":
+            self.take()
+            e = ("bin", "or", e, self.and_())
+        return e
+
+    def and_(self):
+        e = self.not_()
+        while self.peek() == "and":
+            self.take()
+            e = ("bin", "and", e, self.not_())
+        return e
+
+    def not_(self):
+        if self.peek() == "not":
+            self.take()
+            return ("un", "not", self.not_())
+        return self.comparison()
+
+    def comparison(self):
+        e = self.addsub()
+        if self.peek() in COMPARISONS:
+            op = self.take()
+            return ("bin", op, e, self.addsub())
+        return e
+
+    def addsub(self):
+        e = self.muldiv()
+        while self.peek() in ("+", "-"):
+            op = self.take()
+            e = ("bin", op, e, self.muldiv())
+        return e
+
+    def muldiv(self):
+        e = self.unary()
+        while self.peek() in ("*", "/", "//"):
+            op = self.take()
+            e = ("bin", op, e, self.unary())
+        return e
+
+    def unary(self):
+        if self.peek() == "-":
+            self.take()
+            return ("un", "-", self.unary())
+        if self.peek() == "+":
+            self.take()
+            return self.unary()
+        return self.atom()
+
+    def atom(self):
+        t = self.take()
+        if re.fullmatch(r"\d+", t):
+            return ("num", int(t))
+        if re.fullmatch(r"(\d+\.\d*|\.\d+|\d+)([eE][-+]?\d+)?", t):
+            return ("num", float(t))
+        if t == "(":
+            e = self.select()
+            self.take(")")
+            return e
+        if t in INTRINSICS and self.peek() == "(":
+            self.take("(")
+            args = [self.select()]
+            while self.peek() == ",":
+                self.take()
+                args.append(self.select())
+            self.take(")")
+            return ("call", t, tuple(args))
+        if re.fullmatch(r"[A-Za-z_][A-Za-z_0-9]*", t):
+            return ("ref", t)
+        raise ScalarSyntaxError(f"unexpected token {t!r}")
+
+
+_cache: dict[str, tuple] = {}
+
+
+def parse(text: str) -> tuple:
+    e = _cache.get(text)
+    if e is None:
+        e = _P(text).parse()
+        _cache[text] = e
+    return e
+
+
+def free_names(e) -> set[str]:
+    out: set[str] = set()
+
+    def walk(x):
+        k = x[0]
+        if k == "ref":
+            out.add(x[1])
+        elif k == "un":
+            walk(x[2])
+        elif k == "bin":
+            walk(x[2])
+            walk(x[3])
+        elif k == "sel":
+            walk(x[1])
+            walk(x[2])
+            walk(x[3])
+        elif k == "call":
+            for a in x[2]:
+                walk(a)
+
+    walk(e)
+    return out
+
+
+def rename(e, mapping: Mapping[str, str]):
+    k = e[0]
+    if k == "num":
+        return e
+    if k == "ref":
+        return ("ref", mapping.get(e[1], e[1]))
+    if k == "un":
+        return ("un", e[1], rename(e[2], mapping))
+    if k == "bin":
+        return ("bin", e[1], rename(e[2], mapping), rename(e[3], mapping))
+    if k == "sel":
+        return ("sel", rename(e[1], mapping), rename(e[2], mapping), rename(e[3], mapping))
+    return ("call", e[1], tuple(rename(a, mapping) for a in e[2]))
+
+
+# ---------------------------------------------------------------------------
+# Host evaluation (used for transition conditions and by the planner for
+# constant folding of scalar-only graphs).  Mirrors texpr.evaluate exactly.
+
+_PYFN = {"sqrt": math.sqrt, "exp": math.exp, "abs": abs, "pow": pow, "min": min, "max": max}
+
+
+def evaluate(e, env: Mapping):
+    k = e[0]
+    if k == "num":
+        return e[1]
+    if k == "ref":
+        if e[1] not in env:
+            raise KeyError(f"unbound name '{e[1]}' in scalar expression")
+        return env[e[1]]
+    if k == "un":
+        v = evaluate(e[2], env)
+        return (not v) if e[1] == "not" else -v
+    if k == "bin":
+        op = e[1]
+        if op == "and":
+            return bool(evaluate(e[2], env)) and bool(evaluate(e[3], env))
+        if op == "or":
+            return bool(evaluate(e[2], env)) or bool(evaluate(e[3], env))
+        a = evaluate(e[2], env)
+        b = evaluate(e[3], env)
+        if op == "+":
+            return a + b
+        if op == "-":
+            return a - b
+        if op == "*":
+            return a * b
+        if op == "/":
+            return a / b
+        if op == "//":
+            return a // b
+        if op == "<":
+            return a < b
+        if op == "<=":
+            return a <= b
+        if op == ">":
+            return a > b
+        if op == ">=":
+            return a >= b
+        if op == "==":
+            return a == b
+        if op == "!=":
+            return a != b
+        raise ScalarSyntaxError(f"unknown operator {op!r}")
+    if k == "sel":
+        return evaluate(e[2], env) if evaluate(e[1], env) else evaluate(e[3], env)
+    if k == "call":
+        return _PYFN[e[1]](*(evaluate(a, env) for a in e[2]))
+    raise ScalarSyntaxError(f"bad node {k}")
+
+
+# ---------------------------------------------------------------------------
+# CUDA C emission.  Types: 'b' bool, 'i' int64, 'f' double.
+
+_CTYPE = {"b": "bool", "i": "long long", "f": "double"}
+
+
+def c_literal_f(v: float) -> str:
+    if math.isnan(v):
+        return "b2_nan()"
+    if math.isinf(v):
+        return "b2_inf()" if v > 0 else "(-b2_inf())"
+    return v.hex() if v != 0 or math.copysign(1.0, v) > 0 else "(-0.0)"
+
+
+def _join(t1: str, t2: str) -> str:
+    if "f" in (t1, t2):
+        return "f"
+    return "i"
+
+
+def _as(code: str, have: str, want: str) -> str:
+    if have == want:
+        return code
+    if want == "f":
+        return f"((double)({code}))"
+    if want == "i":
+        return f"((long long)({code}))"
+    return f"(({code}) != 0)"
+
+
+def emit(e, types: Mapping[str, str], name_of=lambda n: n) -> tuple[str, str]:
+    """Return (C code, type) for expression ``e``.  ``types`` gives the type
+    of every free name ('b'/'i'/'f')."""
+    k = e[0]
+    if k == "num":
+        v = e[1]
+        if isinstance(v, float):
+            return c_literal_f(v), "f"
+        return (f"{v}LL" if v >= 0 else f"({v}LL)"), "i"
+    if k == "ref":
+        if e[1] not in types:
+            raise KeyError(f"unbound name '{e[1]}' in scalar expression")
+        return name_of(e[1]), types[e[1]]
+    if k == "un":
+        c, t = emit(e[2], types, name_of)
+        if e[1] == "not":
+            return f"(!({_as(c, t, 'b')}))", "b"
+        if t == "b":
+            return f"(-({_as(c, t, 'i')}))", "i"
+        return f"(-({c}))", t
+    if k == "bin":
+        op = e[1]
+        a, ta = emit(e[2], types, name_of)
+        b, tb = emit(e[3], types, name_of)
+        if op in ("and", "or"):
+            cop = "&&" if op == "and" else "||"
+            return f"({_as(a, ta, 'b')} {cop} {_as(b, tb, 'b')})", "b"
+        if op in COMPARISONS:
+            t = _join(ta, tb)
+            return f"({_as(a, ta, t)} {op} {_as(b, tb, t)})", "b"
+        if op == "/":
+            return f"({_as(a, ta, 'f')} / {_as(b, tb, 'f')})", "f"
+        t = _join(ta, tb)
+        if op == "//":
+            if t == "f":
+                return f"b2_floordiv_d({_as(a, ta, 'f')}, {_as(b, tb, 'f')})", "f"
+            return f"b2_floordiv_ll({_as(a, ta, 'i')}, {_as(b, tb, 'i')})", "i"
+        if op in ("+", "-", "*"):
+            if ta == "b" and tb == "b" and op == "*":
+                return f"({a} && {b})", "b"
+            return f"({_as(a, ta, t)} {op} {_as(b, tb, t)})", t
+        raise ScalarSyntaxError(f"unknown operator {op!r}")
+    if k == "sel":
+        c, tc = emit(e[1], types, name_of)
+        a, ta = emit(e[2], types, name_of)
+        b, tb = emit(e[3], types, name_of)
+        t = "b" if ta == tb == "b" else _join(ta, tb)
+        return f"({_as(c, tc, 'b')} ? {_as(a, ta, t)} : {_as(b, tb, t)})", t
+    if k == "call":
+        fn = e[1]
+        args = [emit(a, types, name_of) for a in e[2]]
+        if fn == "sqrt":
+            return f"sqrt({_as(*args[0], 'f')})", "f"
+        if fn == "exp":
+            return f"exp({_as(*args[0], 'f')})", "f"
+        if fn == "abs":
+            c, t = args[0]
+            if t == "f":
+                return f"fabs({c})", "f"
+            return f"b2_abs_ll({_as(c, t, 'i')})", "i"
+        if fn == "pow":
+            (a, ta), (b, tb) = args
+            if ta != "f" and tb != "f" and e[2][1][0] == "num" and e[2][1][1] >= 0:
+                return f"b2_ipow({_as(a, ta, 'i')}, {_as(b, tb, 'i')})", "i"
+            return f"pow({_as(a, ta, 'f')}, {_as(b, tb, 'f')})", "f"
+        if fn in ("min", "max"):
+            c, t = args[0]
+            for c2, t2 in args[1:]:
+                tt = _join(t, t2) if not (t == t2 == "b") else "b"
+                helper = "b2_pymin" if fn == "min" else "b2_pymax"
+                c = f"{helper}({_as(c, t, tt)}, {_as(c2, t2, tt)})"
+                t = tt
+            return c, t
+        raise ScalarSyntaxError(f"unknown intrinsic {fn}")
+    raise ScalarSyntaxError(f"bad node {k}")
+
+
+def ctype(t: str) -> str:
+    return _CTYPE[t]
+
+
+def cast(code: str, have: str, want: str) -> str:
+    return _as(code, have, want)

@@ -1,0 +1,190 @@
+"""CPU tier: oracle pinned to the reference, IR/parsers, planner, NVRTC
+compilation of every generated kernel, and the C ABI exports."""
+
+import math
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, MANIFEST, ROOT, golden_cases, load_case, rel_err
+
+
+# --- the oracle restatement is pinned bitwise to the reference ------------------
+
+@pytest.mark.parametrize("name,variant,case", golden_cases(1),
+                         ids=lambda x: x if isinstance(x, str) else x.get("file", ""))
+def test_oracle_restatement_matches_reference(name, variant, case):
+    from oracle import interp_ref
+    from paper_2107_00555_b200 import sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.{variant}.json")
+    d, inputs = load_case(case)
+    c = interp_ref.Counters()
+    out = interp_ref.interpret(g, case["symbols"], inputs, counters=c)
+    key = f"interp_{variant}/"
+    for k in [f[len(key):] for f in d.files if f.startswith(key)]:
+        assert np.array_equal(out[k], d[key + k], equal_nan=True), f"{name}.{variant}:{k}"
+    ref = case["counters"][variant]
+    assert (c.map_iterations, c.wcr_commits, c.bytes_moved) == (
+        ref["map_iterations"], ref["wcr_commits"], ref["bytes_moved"])
+
+
+def test_reference_kats():
+    """KATs of pkg/tests/test_interp.py:17-40, 122-139 against the oracle."""
+    from oracle import interp_ref
+    from paper_2107_00555_b200 import sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "jacobi_1d.raw.json")
+    out = interp_ref.interpret(g, {"N": 4, "TSTEPS": 2},
+                               {"A": np.array([0.0, 3.0, 0.0, 3.0]), "B": np.zeros(4)})
+    assert np.array_equal(out["B"], [0.0, 0.99999, 1.99998, 0.0])
+    g = sdfg.load(GOLDEN / "graphs" / "wcr_sum.raw.json")
+    c = interp_ref.Counters()
+    out = interp_ref.interpret(g, {"NI": 2, "NJ": 2}, {"alpha": 0.0, "C": np.ones((2, 2))},
+                               counters=c)
+    assert out["alpha"][()] == 4.0 and c.wcr_commits == 4
+    g = sdfg.load(GOLDEN / "graphs" / "gemm.raw.json")
+    A = np.array([[1.0, 2.0], [3.0, 4.0]])
+    out = interp_ref.interpret(g, {"NI": 2, "NJ": 2, "NK": 2},
+                               {"A": A, "B": np.eye(2), "C": np.zeros((2, 2)),
+                                "alpha": 1.0, "beta": 0.0})
+    assert np.array_equal(out["C"], A)
+    g = sdfg.load(GOLDEN / "graphs" / "jacobi_2d.raw.json")
+    out = interp_ref.interpret(g, {"N": 6, "TSTEPS": 2},
+                               {"A": np.full((6, 6), 3.0), "B": np.full((6, 6), 3.0)})
+    assert np.allclose(out["B"][1:-1, 1:-1], 3.0, rtol=0, atol=1e-14)
+
+
+def test_reference_interp_equals_oracle_in_manifest():
+    """Raw graphs interpret bitwise-equal to evaluate_program (reference
+    criterion test_oracle_suite.py:47-48) — recorded at generation time."""
+    for name, ent in MANIFEST["kernels"].items():
+        for case in ent["cases"]:
+            assert case["interp_equals_oracle"]["raw"], (name, case["file"])
+
+
+# --- parsers and IR --------------------------------------------------------------
+
+def test_symexpr():
+    from paper_2107_00555_b200 import symexpr as S
+
+    e = S.parse("(-4) * N + N * N + 4")
+    assert S.evaluate(e, {"N": 10}) == 64
+    assert S.evaluate(S.parse("-7 // 2"), {}) == -4
+    assert S.evaluate(S.parse("min(N, 3) + max(1, M)"), {"N": 5, "M": 0}) == 4
+    assert S.affine(S.parse("k0 + 1"), ("k0",), {}) == (1, {"k0": 1})
+    assert S.affine(S.parse("2 * (i + N)"), ("i",), {"N": 3}) == (6, {"i": 2})
+    assert S.affine(S.parse("i * j"), ("i", "j"), {}) is None
+    assert S.interval(S.parse("i - 2 * j"), {"i": (0, 5), "j": (1, 3)}, {}) == (-6, 3)
+    dims = S.parse_subset("1:N - 2:1, k0 + 1")
+    assert [list(r) for r in S.eval_subset(dims, {"N": 5, "k0": 2})] == [[1, 2, 3], [3]]
+
+
+def test_scalar_semantics_host():
+    from paper_2107_00555_b200 import scalar as T
+
+    assert T.evaluate(T.parse("i / NPT"), {"i": 3, "NPT": 4}) == 0.75
+    assert T.evaluate(T.parse("-7.0 // 2.0"), {}) == -4.0
+    assert T.evaluate(T.parse("(a < b) * c"), {"a": 1.0, "b": 2.0, "c": 5.0}) == 5.0
+    assert math.isnan(T.evaluate(T.parse("min(x, 1.0)"), {"x": float("nan")}))
+    assert T.evaluate(T.parse("min(1.0, x)"), {"x": float("nan")}) == 1.0
+    assert T.evaluate(T.parse("c ? 1 : 2"), {"c": 0}) == 2
+    code, ty = T.emit(T.parse("i / NPT <= in1 and in1 < 2"), {"i": "i", "NPT": "i", "in1": "f"})
+    assert ty == "b" and "(double)" in code
+    assert T.c_literal_f(0.2) == (0.2).hex()
+
+
+def test_graph_loader_all_golden():
+    from paper_2107_00555_b200 import sdfg
+
+    for p in sorted((GOLDEN / "graphs").glob("*.json")):
+        g = sdfg.load(p)
+        for st in g.states:
+            st.topological()
+            st.scope_parents()
+        assert g.start in {s.label for s in g.states}
+
+
+def test_schema_errors():
+    from paper_2107_00555_b200 import sdfg
+
+    with pytest.raises(sdfg.SchemaError):
+        sdfg.loads("{}")
+    with pytest.raises(sdfg.SchemaError):
+        sdfg.from_dict({"version": 2})
+    with pytest.raises(sdfg.SchemaError):
+        sdfg.loads("not json")
+
+
+# --- planner and generated code ------------------------------------------------
+
+def test_fusion_collapses_heat3d_chain():
+    """heat_3d's ~16 maps per sweep (reference subgraph_fusion crashes on it,
+    SURVEY.md §0) fuse into one kernel per half-sweep with every
+    intermediate in registers."""
+    from paper_2107_00555_b200 import plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
+    pl = P.Planner(g, {"N": 400, "TSTEPS": 100}).build()
+    maps = [op for op in pl.all_ops if isinstance(op, P.MapGroup)]
+    assert len(maps) == 2
+    assert all(len(m.members) >= 15 for m in maps), [len(m.members) for m in maps]
+    temps = [n for n, c in g.containers.items() if c.transient]
+    assert all(pl.placement[t] == "reg" for t in temps)
+
+
+def test_jacobi_stencil_not_fused_across_sweeps():
+    from paper_2107_00555_b200 import plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "jacobi_2d.raw.json")
+    pl = P.Planner(g, {"N": 2000, "TSTEPS": 100}).build()
+    maps = [op for op in pl.all_ops if isinstance(op, P.MapGroup)]
+    assert len(maps) == 2  # B-sweep and A-sweep need a global barrier
+
+
+def test_all_generated_kernels_compile_for_sm100a():
+    """Every kernel the planner generates for every golden graph compiles
+    with NVRTC for sm_100a (no GPU needed)."""
+    from paper_2107_00555_b200 import codegen, plan as P, runtime as rt, sdfg
+
+    rt.load_library()
+    n = 0
+    for name, ent in MANIFEST["kernels"].items():
+        for v in ent["variants"]:
+            g = sdfg.load(GOLDEN / "graphs" / f"{name}.{v}.json")
+            pl = P.Planner(g, ent["cases"][-1]["symbols"]).build()
+            for op in pl.all_ops:
+                if isinstance(op, P.MapGroup):
+                    spec = codegen.generate(pl, op, {}, f"b2_map_{g.name}_{op.idx}")
+                    cub, _ = rt.get_cubin(rt.family_source("prelude.cuh") + "\n" + spec.source,
+                                          spec.name)
+                    assert len(cub) > 0
+                    n += 1
+    assert n > 50
+
+
+# --- C ABI -----------------------------------------------------------------------
+
+def test_libb2_exports_every_declared_symbol():
+    from paper_2107_00555_b200 import runtime as rt
+
+    header = (ROOT / "include" / "b2.h").read_text()
+    declared = set(re.findall(r"\b(b2_\w+)\s*\(", header))
+    lib = rt.load_library()
+    for sym in sorted(declared):
+        assert hasattr(lib, sym), f"libb2.so does not export {sym}"
+    assert declared == set(rt.EXPORTS)
+    assert lib.b2_version() == 1
+
+
+def test_no_gpu_fails_loudly():
+    """Without a device the backend raises instead of falling back to CPU."""
+    from paper_2107_00555_b200 import runtime as rt
+
+    n = __import__("ctypes").c_int(0)
+    rt.lib().b2_device_count(__import__("ctypes").byref(n))
+    if n.value > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(rt.BackendUnavailable):
+        rt.device(0)
