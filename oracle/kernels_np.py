@@ -1,0 +1,152 @@
+"""CPU ORACLE — test infrastructure only (tests/, smoke(), bench.py's CPU
+baseline leg); never the product path.
+
+numpy restatements of the reference's CPU path for the benchmark programs,
+i.e. what ``sdfgkit.frontend.evaluate_program`` (pkg/src/sdfgkit/frontend/
+oracle.py:37-70) does on them: every slice statement evaluated as
+whole-array numpy binary ops, left to right (eval_expr, oracle.py:205-262),
+then assigned (exec_assign, oracle.py:126-156); ``@`` is numpy/BLAS
+(oracle.py:238); explicit ``map[...]`` bodies run per element (oracle.py:
+116-124) — restated here vectorised with the same per-element op order.
+These reproduce evaluate_program bitwise (pinned by tests against the golden
+vectors from the reference) and run at BASELINE.json's config sizes.
+
+Programs: jacobi_2d / gemver / atax / bicg are the reference corpus
+(pkg/tests/corpus/*.dpy); heat_3d and the NPBench-sweep kernels are this
+repo's DSL programs (programs/*.dpy).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import pathlib
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+
+
+def jacobi_2d(A, B, TSTEPS):
+    for _t in range(1, TSTEPS):
+        B[1:-1, 1:-1] = 0.2 * (A[1:-1, 1:-1] + A[1:-1, :-2] + A[1:-1, 2:] + A[2:, 1:-1] + A[:-2, 1:-1])
+        A[1:-1, 1:-1] = 0.2 * (B[1:-1, 1:-1] + B[1:-1, :-2] + B[1:-1, 2:] + B[2:, 1:-1] + B[:-2, 1:-1])
+    return {"A": A, "B": B}
+
+
+def _heat_rhs(A):
+    return (0.125 * (A[2:, 1:-1, 1:-1] - 2.0 * A[1:-1, 1:-1, 1:-1] + A[:-2, 1:-1, 1:-1])
+            + 0.125 * (A[1:-1, 2:, 1:-1] - 2.0 * A[1:-1, 1:-1, 1:-1] + A[1:-1, :-2, 1:-1])
+            + 0.125 * (A[1:-1, 1:-1, 2:] - 2.0 * A[1:-1, 1:-1, 1:-1] + A[1:-1, 1:-1, 0:-2])
+            + A[1:-1, 1:-1, 1:-1])
+
+
+def heat_3d(A, B, TSTEPS):
+    for _t in range(1, TSTEPS):
+        B[1:-1, 1:-1, 1:-1] = _heat_rhs(A)
+        A[1:-1, 1:-1, 1:-1] = _heat_rhs(B)
+    return {"A": A, "B": B}
+
+
+def heat_3d_sweeps(A, B, sweeps):
+    """``sweeps`` half-steps (bounded CPU-baseline sample)."""
+    for s in range(sweeps):
+        if s % 2 == 0:
+            B[1:-1, 1:-1, 1:-1] = _heat_rhs(A)
+        else:
+            A[1:-1, 1:-1, 1:-1] = _heat_rhs(B)
+
+
+def gemver(alpha, beta, A, u1, v1, u2, v2, w, x, y, z):
+    # explicit map: A[i, j] = A[i, j] + u1[i] * v1[j] + u2[i] * v2[j] (per element,
+    # left to right: (A + u1*v1) + u2*v2)
+    A[:, :] = (A + np.outer(u1, v1)) + np.outer(u2, v2)
+    x[:] = x + beta * (y @ A) + z
+    w[:] = alpha * (A @ x)
+    return {"A": A, "x": x, "w": w}
+
+
+def atax(A, x, y):
+    y[:] = (A @ x) @ A
+    return {"y": y}
+
+
+def bicg(A, s, q, p, r):
+    s[:] = r @ A
+    q[:] = A @ p
+    return {"s": s, "q": q}
+
+
+def go_fast(a, out):
+    trace = 0.0
+    for i in range(a.shape[0]):
+        e2 = math.exp(2.0 * a[i, i])
+        trace += (e2 - 1.0) / (e2 + 1.0)
+    out[:] = a + trace
+    return {"out": out}
+
+
+def azimint_naive(rmax, data, radius, res):
+    NPT = res.shape[0]
+    i = np.arange(NPT, dtype=np.float64)[:, None]
+    lo = rmax * i / NPT
+    hi = rmax * (i + 1) / NPT
+    mask = (lo <= radius[None, :]) & (radius[None, :] < hi)
+    # the map's WCR sums run lexicographically (i outer, k inner): sequential in k
+    acc = np.zeros(NPT)
+    cnt = np.zeros(NPT)
+    for k in range(radius.shape[0]):
+        acc = acc + mask[:, k] * data[k]
+        cnt = cnt + mask[:, k] * 1.0
+    with np.errstate(invalid="ignore", divide="ignore"):
+        res[:] = acc / cnt
+    return {"res": res}
+
+
+def matmul(A, B):
+    return A @ B
+
+
+# ---------------------------------------------------------------------------
+# compiled C restatement (oracle/c/stencils.c, OpenMP over planes)
+
+_lib = None
+
+
+def c_lib():
+    global _lib
+    if _lib is None:
+        p = HERE / "liboracle.so"
+        if not p.exists():
+            raise FileNotFoundError(f"{p} missing: run `make -C oracle`")
+        _lib = ctypes.CDLL(str(p))
+        for fn in ("oracle_heat_3d", "oracle_jacobi_2d", "oracle_heat_3d_sweeps"):
+            f = getattr(_lib, fn)
+            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long, ctypes.c_long,
+                          ctypes.c_int]
+            f.restype = None
+    return _lib
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def heat_3d_c(A, B, TSTEPS, threads=0):
+    assert A.flags.c_contiguous and B.flags.c_contiguous and A.dtype == np.float64
+    c_lib().oracle_heat_3d(A.ctypes.data, B.ctypes.data, A.shape[0], TSTEPS, threads)
+    return {"A": A, "B": B}
+
+
+def heat_3d_sweeps_c(A, B, sweeps, threads=0):
+    c_lib().oracle_heat_3d_sweeps(A.ctypes.data, B.ctypes.data, A.shape[0], sweeps, threads)
+
+
+def jacobi_2d_c(A, B, TSTEPS, threads=0):
+    assert A.flags.c_contiguous and B.flags.c_contiguous and A.dtype == np.float64
+    c_lib().oracle_jacobi_2d(A.ctypes.data, B.ctypes.data, A.shape[0], TSTEPS, threads)
+    return {"A": A, "B": B}

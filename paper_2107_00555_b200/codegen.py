@@ -48,6 +48,7 @@ class KernelSpec:
         self.sites: list[str] = []  # device OOB guard site descriptions
         self.uses_flag = False
         self.params: list[str] = []
+        self.vec = 1
         self.kernel = None  # runtime.Kernel
 
     def arg_index(self, desc) -> int:
@@ -139,14 +140,21 @@ class _Gen:
             self.emit(f"const {CT[c.dtype]} {v} = b2_oob({o}, {size}, {site}, flag) ? "
                       f"({CT[c.dtype]})0 : {p}[{o}];")
             return v, t
-        if depth == 0:
-            self.spec.checks.append((m.container, m.subset, env))
+        self.spec.checks.append((m.container, m.subset, env))
+        if m.container not in self.written:
+            key = (m.container, off)
+            hit = self.cse.get(key)
+            if hit is None:
+                hit = self.fresh("ld")
+                self.emit(f"const {CT[c.dtype]} {hit} = {p}[{off}];")
+                self.cse[key] = hit
+            return hit, t
         return f"{p}[{off}]", t
 
     def _site(self, desc: str) -> int:
         self.spec.uses_flag = True
         self.spec.sites.append(desc)
-        return len(self.spec.sites) - 1
+        return self.group.idx * 4096 + len(self.spec.sites) - 1
 
     def write(self, m: sdfg.Memlet, code: str, vt: str, env: dict, depth: int):
         c = self.cont(m.container)
@@ -212,8 +220,7 @@ class _Gen:
     def tasklet(self, st: sdfg.State, t: sdfg.Tasklet, env: dict, depth: int):
         types: dict[str, str] = {}
         cname: dict[str, str] = {}
-        self.emit(f"{{  // tasklet {t.name} (node {t.id})")
-        self.ind += 2
+        self.emit(f"// tasklet {t.name} (node {t.id})")
         for e in st.in_edges(t):
             if e.memlet is None:
                 continue
@@ -247,8 +254,6 @@ class _Gen:
             key = e.src_conn if e.src_conn in results else t.outs[0]
             v, ty = results[key]
             self.write(e.memlet, v, ty, env, depth)
-        self.ind -= 2
-        self.emit("}")
 
     def scope(self, st: sdfg.State, entry: sdfg.MapEntry, env: dict, depth: int):
         for c in P._scope_children(st, entry):
@@ -331,6 +336,8 @@ class _Gen:
         grp = self.group
         spec = self.spec
         k = len(grp.params)
+        # constant (non loop-assigned) ranges are baked into the source
+        self.const_ranges = [_const_range(self.pl, r) for r in grp.ranges]
         if grp.schedule == "scalar":
             mode = "scalar"
         elif grp.schedule == "sequential":
@@ -338,19 +345,31 @@ class _Gen:
         else:
             mode = "flat"
             if k >= 2:
-                last = _const_len(self.pl, grp.ranges[-1])
-                prev = _const_len(self.pl, grp.ranges[-2])
-                if last is not None and prev is not None and last >= 16 and prev >= 4:
+                last = self.const_ranges[-1]
+                prev = self.const_ranges[-2]
+                if last is not None and prev is not None and last[2] >= 16 and prev[2] >= 4:
                     mode = "tile2"
         spec.mode = mode
+        vec = 1
+        if mode == "tile2":
+            vec = _pick_vec(self.const_ranges[-1][2])
+        elif mode == "flat" and k == 1 and self.const_ranges[0] is not None:
+            vec = 4 if self.const_ranges[0][2] >= 4 * 256 * 148 else 1
+        spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, 8, 1)}[mode]
 
-        # body first (collects containers/symbols), then the prologue
+        # containers written anywhere in this group: the rest are read-only
+        self.written = set()
+        for mem in grp.members:
+            for a in self.pl.member_accesses(mem, grp.params):
+                if a[1]:
+                    self.written.add(a[0])
+        self.cse = {}
+
         env = {p: f"p_{p}" for p in grp.params}
         body_lines_start = len(self.lines)
         self.ind = 6
-        # registers for placed transients touched by this group
         for mem in grp.members:
             menv = {mp: env[gp] for mp, gp in mem.rename.items()}
             if mem.tasklet is not None:
@@ -369,18 +388,32 @@ class _Gen:
             if pl == "reg":
                 continue
             base = self.arg(("ptr", name))
-            pro.append(f"  {CT[c.dtype]} *__restrict__ c_{name} = ({CT[c.dtype]} *){base};")
-            for d in range(len(c.shape)):
-                pro.append(f"  const b2_ll st_{name}_{d} = {self.arg(('stride', name, d))};")
-            pro.append(f"  const b2_ll sz_{name} = {self.arg(('size', name))};")
+            ro = name not in self.written and pl == "memory"
+            q = "const " if ro else ""
+            pro.append(f"  {q}{CT[c.dtype]} *__restrict__ c_{name} = ({q}{CT[c.dtype]} *){base};")
+            shape = self.shapes[name]
+            st = _row_major(shape)
+            for d in range(len(shape)):
+                pro.append(f"  constexpr b2_ll st_{name}_{d} = {st[d]}LL;")
+            n = 1
+            for x in shape:
+                n *= x
+            pro.append(f"  constexpr b2_ll sz_{name} = {n}LL;")
         for s in spec.syms:
-            pro.append(f"  const b2_ll s_{s} = {self.arg(('sym', s))};")
-        if spec.uses_flag or True:
-            pro.append(f"  int *flag = (int *){self.arg(('flag',))};")
+            if s in self.pl.fixed:
+                pro.append(f"  constexpr b2_ll s_{s} = {int(self.pl.fixed[s])}LL;")
+            else:
+                pro.append(f"  const b2_ll s_{s} = {self.arg(('sym', s))};")
+        pro.append(f"  int *flag = (int *){self.arg(('flag',))};")
+        pro.append("  (void)flag;")
         for i in range(k):
-            pro.append(f"  const b2_ll rb{i} = {self.arg(('rb', i))};")
-            pro.append(f"  const b2_ll rs{i} = {self.arg(('rs', i))};")
-            pro.append(f"  const b2_ll rl{i} = {self.arg(('rl', i))};")
+            cr = self.const_ranges[i]
+            if cr is not None:
+                pro.append(f"  constexpr b2_ll rb{i} = {cr[0]}LL, rs{i} = {cr[1]}LL, rl{i} = {cr[2]}LL;")
+            else:
+                pro.append(f"  const b2_ll rb{i} = {self.arg(('rb', i))};")
+                pro.append(f"  const b2_ll rs{i} = {self.arg(('rs', i))};")
+                pro.append(f"  const b2_ll rl{i} = {self.arg(('rl', i))};")
         privates = [n for n in spec.containers if self.place(n) == "private"]
         if privates:
             pro.append("  const b2_ll tflat = ((b2_ll)blockIdx.x * blockDim.y + threadIdx.y) * "
@@ -394,11 +427,14 @@ class _Gen:
         def reg_decls(indent):
             return [" " * indent + f"{CT[self.g.containers[n].dtype]} r_{n} = 0;" for n in regs]
 
+        def shift(lines, by):
+            return [(" " * by + ln) if by >= 0 else ln[-by:] for ln in lines]
+
         loop: list[str] = []
         if mode == "scalar":
             loop.append("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
             loop += reg_decls(4)
-            loop += [ln[2:] for ln in body]
+            loop += shift(body, -2)
             loop.append("  }")
         elif mode == "seq":
             loop.append("  if (blockIdx.x == 0 && threadIdx.x == 0) {")
@@ -413,8 +449,12 @@ class _Gen:
         elif mode == "flat":
             tot = " * ".join(f"rl{i}" for i in range(k))
             loop.append(f"  const b2_ll total = {tot};")
-            loop.append("  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < total; "
-                        "f += (b2_ll)gridDim.x * blockDim.x) {")
+            loop.append(f"  for (b2_ll f0 = (b2_ll)blockIdx.x * blockDim.x * {vec}; f0 < total; "
+                        f"f0 += (b2_ll)gridDim.x * blockDim.x * {vec}) {{")
+            loop.append("#pragma unroll")
+            loop.append(f"  for (int v = 0; v < {vec}; ++v) {{")
+            loop.append("    const b2_ll f = f0 + (b2_ll)v * blockDim.x + threadIdx.x;")
+            loop.append("    if (f >= total) break;")
             loop.append("    b2_ll rem = f;")
             for i in reversed(range(k)):
                 p = grp.params[i]
@@ -424,12 +464,14 @@ class _Gen:
                     loop.append(f"    const b2_ll i{i} = rem;")
                 loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
             loop += reg_decls(4)
-            loop += [ln[2:] for ln in body]
+            loop += shift(body, -2)
+            loop.append("  }")
             loop.append("  }")
         else:  # tile2
             x, y = k - 1, k - 2
-            loop.append(f"  const b2_ll tiles_x = (rl{x} + 31) / 32;")
-            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
+            tw = 32 * vec
+            loop.append(f"  constexpr b2_ll tiles_x = (rl{x} + {tw - 1}) / {tw};")
+            loop.append(f"  constexpr b2_ll tiles_y = (rl{y} + 7) / 8;")
             outer = " * ".join(f"rl{i}" for i in range(k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({outer});")
             loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
@@ -440,29 +482,55 @@ class _Gen:
                     loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
                 else:
                     loop.append(f"    const b2_ll i{i} = rem;")
-            loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
             loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
-            loop.append(f"    if (i{x} >= rl{x} || i{y} >= rl{y}) continue;")
+            loop.append(f"    if (i{y} >= rl{y}) continue;")
+            loop.append("#pragma unroll")
+            loop.append(f"    for (int v = 0; v < {vec}; ++v) {{")
+            loop.append(f"    const b2_ll i{x} = tx * {tw} + v * 32 + threadIdx.x;")
+            loop.append(f"    if (i{x} >= rl{x}) break;")
             for i, p in enumerate(grp.params):
                 loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
             loop += reg_decls(4)
-            loop += [ln[2:] for ln in body]
+            loop += shift(body, -2)
+            loop.append("    }")
             loop.append("  }")
         src = [f"// generated by paper_2107_00555_b200.codegen for state "
-               f"'{grp.state.label}', group of {len(grp.members)} scope(s)",
+               f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
                "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
         spec.source = "\n".join(src + pro + loop + ["}"]) + "\n"
         return spec
 
 
-def _const_len(planner: P.Planner, rng) -> int | None:
+def _row_major(shape) -> list[int]:
+    st = [1] * len(shape)
+    acc = 1
+    for d in range(len(shape) - 1, -1, -1):
+        st[d] = acc
+        acc *= shape[d]
+    return st
+
+
+def _pick_vec(n: int) -> int:
+    """Points per thread along the innermost parameter: the largest of 4/2/1
+    whose 32*vec-wide tiles waste at most 12% of the row."""
+    for v in (4, 2):
+        tw = 32 * v
+        waste = (-(-n // tw) * tw - n) / max(1, n)
+        if waste <= 0.13:
+            return v
+    return 1
+
+
+def _const_range(planner: P.Planner, rng):
     b, e, s = rng
     try:
         env = dict(planner.fixed)
         bv, ev, sv = (symexpr.evaluate(x, env) for x in (b, e, s))
     except KeyError:
         return None
-    return max(0, (ev - bv) // sv + 1)
+    if sv < 1:
+        return None
+    return bv, sv, max(0, (ev - bv) // sv + 1)
 
 
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str) -> KernelSpec:
@@ -498,12 +566,13 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         total = 1
         for v in rl:
             total *= v
-        blocks = max(1, min((total + 255) // 256, MAX_BLOCKS * 8))
+        blocks = max(1, min((total + 256 * spec.vec - 1) // (256 * spec.vec), MAX_BLOCKS * 8))
         if spec.private:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (256, 1, 1)
     k = len(rl)
-    tiles = ((rl[k - 1] + 31) // 32) * ((rl[k - 2] + 7) // 8)
+    tw = 32 * spec.vec
+    tiles = ((rl[k - 1] + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:
         tiles *= v
     blocks = max(1, min(tiles, MAX_BLOCKS * 8))

@@ -352,6 +352,7 @@ int gemm_impl(int64_t M, int64_t N, int64_t K, const T *A, int64_t rsa, int64_t 
   if (M <= 0 || N <= 0) return B2_OK;
   constexpr int BM = 64, BN = 64, BK = 16, TM = 4, TN = 4;
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  B2_CLEAR_ERROR();
   gemm_kernel<T, BM, BN, BK, TM, TN><<<grid, 256, 0, (cudaStream_t)stream>>>(
       M, N, K, A, rsa, csa, B, rsb, csb, C, rsc, csc, wcr);
   B2_LAUNCH_CHECK("gemm launch");
@@ -371,6 +372,7 @@ extern "C" int b2_copy_view(const b2_view_t *dst, const b2_view_t *src, int wcr,
                                          cudaMemcpyDeviceToDevice, (cudaStream_t)stream),
                          "copy_view memcpy");
   }
+  B2_CLEAR_ERROR();
   copy_view_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       to_dev(dst), dst->dtype, to_dev(src), src->dtype, n, wcr);
   B2_LAUNCH_CHECK("copy_view launch");
@@ -380,6 +382,7 @@ extern "C" int b2_copy_view(const b2_view_t *dst, const b2_view_t *src, int wcr,
 extern "C" int b2_fill_view(const b2_view_t *dst, double value, void *stream) {
   int64_t n = numel(dst);
   if (n == 0) return B2_OK;
+  B2_CLEAR_ERROR();
   fill_view_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(to_dev(dst), dst->dtype,
                                                                         value, n);
   B2_LAUNCH_CHECK("fill_view launch");
@@ -411,11 +414,13 @@ extern "C" int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axe
   bool isint = (in->dtype == B2_I64 || in->dtype == B2_I32 || in->dtype == B2_BOOL);
   if (isint) {
     long long ident = op == B2_WCR_MUL ? 1 : (op == B2_WCR_MIN ? INT64_MAX : (op == B2_WCR_MAX ? INT64_MIN : 0));
+    B2_CLEAR_ERROR();
     reduce_kernel<long long, true><<<grid, threads, 0, (cudaStream_t)stream>>>(
         to_dev(out), out->dtype, to_dev(&kept), to_dev(&red), (const char *)in->base,
         in->dtype, nout, nred, op, wcr, ident);
   } else {
     double ident = op == B2_WCR_MUL ? 1.0 : (op == B2_WCR_MIN ? INFINITY : (op == B2_WCR_MAX ? -INFINITY : 0.0));
+    B2_CLEAR_ERROR();
     reduce_kernel<double, false><<<grid, threads, 0, (cudaStream_t)stream>>>(
         to_dev(out), out->dtype, to_dev(&kept), to_dev(&red), (const char *)in->base,
         in->dtype, nout, nred, op, wcr, ident);

@@ -267,8 +267,49 @@ class GpuExecutor:
         else:
             self._run_states(counters, eager=True)
 
+    _dry = False
+    _prof = None
+
+    def _prof_event_pair(self):
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        rt.check(rt.lib().b2_event_create(ctypes.byref(a)), "event")
+        rt.check(rt.lib().b2_event_create(ctypes.byref(b)), "event")
+        return a.value, b.value
+
+    def profile_launches(self) -> dict:
+        """One eager pass with a CUDA-event pair around every map-kernel
+        launch on the executor's stream.  Returns {kernel: (launches,
+        total_ms, points_per_launch)}."""
+        self._prof = []
+        try:
+            rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
+            self._run_states(None, eager=True)
+            self.sync()
+            out: dict = {}
+            for name, npts, (a, b) in self._prof:
+                ms = ctypes.c_float()
+                rt.check(rt.lib().b2_event_elapsed_ms(a, b, ctypes.byref(ms)), "elapsed")
+                n, tot, _ = out.get(name, (0, 0.0, npts))
+                out[name] = (n + 1, tot + ms.value, npts)
+                rt.lib().b2_event_destroy(a)
+                rt.lib().b2_event_destroy(b)
+            return out
+        finally:
+            self._prof = None
+
+    def _instantiate_children(self):
+        """Walk the state machine without launching anything so nested
+        executors (which allocate HBM) exist before stream capture."""
+        self._dry = True
+        try:
+            self._run_states(None, eager=False)
+        finally:
+            self._dry = False
+
     def _capture(self, counters):
         L = rt.lib()
+        self._instantiate_children()
+        self.launches = 0
         rt.check(L.b2_capture_begin(self.stream), "capture")
         tc = Counters()
         try:
@@ -283,6 +324,7 @@ class GpuExecutor:
         rt.check(L.b2_capture_end(self.stream, ctypes.byref(ge)), "capture end")
         self.graph_exec = ge.value
         self._trace_counters = tc
+        self.trace_launches = self.launches  # kernels per replay of the captured graph
 
     _trace_counters = None
 
@@ -327,6 +369,10 @@ class GpuExecutor:
     # -- ops -----------------------------------------------------------------------
 
     def _exec_op(self, op, sym, counters):
+        if self._dry:
+            if isinstance(op, P.NestedOp):
+                self._exec_nested(op, sym, None, dry=True)
+            return
         if isinstance(op, P.MapGroup):
             self._exec_map(op, sym, counters)
         elif isinstance(op, P.CopyOp):
@@ -385,7 +431,13 @@ class GpuExecutor:
         grid, block = codegen.launch_geometry(spec, [n for _, _, n in rvals])
         blob = codegen.pack_args(spec, env, rvals, self.buf.ptr, self.buf.strides, self.buf.size,
                                  self.scratch, self.flag)
+        if self._prof is not None:
+            ev = self._prof_event_pair()
+            rt.lib().b2_event_record(ev[0], self.stream)
         rt.launch(spec.kernel, grid, block, blob, self.stream)
+        if self._prof is not None:
+            rt.lib().b2_event_record(ev[1], self.stream)
+            self._prof.append((spec.name, npts, ev))
         self.launches += 1
         if counters is not None:
             _count_map(self, op, rvals, counters, env)
@@ -527,7 +579,7 @@ class GpuExecutor:
             if om.wcr is not None:
                 counters.wcr_commits += nin
 
-    def _exec_nested(self, op: P.NestedOp, sym, counters):
+    def _exec_nested(self, op: P.NestedOp, sym, counters, dry: bool = False):
         """Nested graph (interp.py:491-517): inner containers alias the outer
         memlet views when those are whole contiguous containers, else they
         are copied in/out through b2_copy_view."""
@@ -558,6 +610,9 @@ class GpuExecutor:
                                 external=external)
             child._external = external
             self.children[key] = child
+        if dry:
+            child._instantiate_children()
+            return
         for e in ins:
             conn = e.dst_conn
             if conn in child._external:
@@ -593,11 +648,9 @@ class GpuExecutor:
         self.sync()
         if v[0]:
             site = int(v[0]) - 1
-            desc = "?"
-            for spec in self.specs.values():
-                if site < len(spec.sites):
-                    desc = spec.sites[site]
-                    break
+            spec = self.specs.get(site // 4096)
+            desc = spec.sites[site % 4096] if spec is not None and site % 4096 < len(spec.sites) \
+                else "?"
             raise OutOfBoundsError(f"out-of-bounds access detected on the device ({desc})")
         for ch in self.children.values():
             ch.check_flag()

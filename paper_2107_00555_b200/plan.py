@@ -438,6 +438,11 @@ class Planner:
 
     # -- convenience -------------------------------------------------------------
 
+    def shapes(self, bindings: dict | None = None) -> dict:
+        env = dict(bindings or self.fixed)
+        return {n: tuple(symexpr.evaluate(d, env) for d in c.shape)
+                for n, c in self.g.containers.items()}
+
     def symbol_env(self, env: dict) -> dict:
         e = dict(self.fixed)
         e.update(env)

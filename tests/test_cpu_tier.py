@@ -156,7 +156,7 @@ def test_all_generated_kernels_compile_for_sm100a():
             pl = P.Planner(g, ent["cases"][-1]["symbols"]).build()
             for op in pl.all_ops:
                 if isinstance(op, P.MapGroup):
-                    spec = codegen.generate(pl, op, {}, f"b2_map_{g.name}_{op.idx}")
+                    spec = codegen.generate(pl, op, pl.shapes(ent["cases"][-1]["symbols"]), f"b2_map_{g.name}_{op.idx}")
                     cub, _ = rt.get_cubin(rt.family_source("prelude.cuh") + "\n" + spec.source,
                                           spec.name)
                     assert len(cub) > 0
