@@ -1,9 +1,374 @@
-"""Pattern rules that fold MATMUL library nodes of BLAS-2 shape (and the
-elementwise map that feeds one) into single rowpass-family passes.
-Filled in by the rowpass family; the identity rule keeps the op list."""
+"""BLAS-2 planning: MATMUL library nodes in matrix-vector form, and the
+gemver / atax / bicg fusions, lowered onto the rowpass family
+(csrc/families/rowpass.cuh).
+
+Reference semantics: MATMUL executes ``np.matmul`` on the (squeezed) memlet
+views and writes the reshaped result (pkg/src/sdfgkit/interp.py:450-460);
+the programs come from the reference corpus (pkg/tests/corpus/gemver.dpy,
+atax.dpy, bicg.dpy) lowered by frontend/lower.py:255-266.
+
+Fusion rules over a straight-line op sequence (plan.Planner):
+  P1 gemver head  elementwise map writing X[i, j] (full matrix, identity
+                  point) immediately followed by ``y @ X`` or ``X @ v``:
+                  the map becomes the rowpass prologue (X' written back in
+                  the same pass that feeds the product)
+  P2 atax         ``t = X @ v`` followed by ``y = t @ X``: one pass, the row
+                  dot feeds the column accumulation (coef = dot)
+  P3 bicg         ``s = r @ X`` and ``q = X @ p`` adjacent, independent
+  P0 single       any lone 2D@1D / 1D@2D product
+Operand R of the family must be row-contiguous: a view with unit column
+stride is used as is; one with unit row stride is used transposed (the dot
+and axpy roles swap).  Anything else stays on b2_gemm_f64.
+"""
 
 from __future__ import annotations
 
+import ctypes
+import struct
 
-def fuse(planner, ops):
-    return ops
+from . import codegen, plan as P, runtime as rt, sdfg, symexpr
+
+TPB = 512
+MAX_CW = 8192
+
+
+class _View:
+    def __init__(self, container, offset, dims):
+        self.container = container
+        self.offset = offset
+        self.dims = dims  # [(len, stride)]
+
+
+def _view(planner: P.Planner, m: sdfg.Memlet, kept, shapes) -> _View | None:
+    try:
+        ranges = symexpr.eval_subset(m.subset, planner.fixed)
+    except KeyError:
+        return None
+    shape = shapes[m.container]
+    if len(ranges) != len(shape):
+        return None
+    for d, r in enumerate(ranges):
+        if len(r) and (r.start < 0 or r[-1] >= shape[d]):
+            return None
+    st = codegen._row_major(shape)
+    off = sum(r.start * st[d] for d, r in enumerate(ranges))
+    dims = [(len(r), st[d] * r.step) for d, r in enumerate(ranges)]
+    if kept is not None:
+        if len(kept) != len(dims):
+            return None
+        dims = [dd for dd, k in zip(dims, kept) if k]
+    return _View(m.container, off, dims)
+
+
+class MV:
+    """One MATMUL node in matrix-vector form, normalised to R = row-contiguous
+    matrix: kind 'dot' (out[m] = R[m,:] . v) or 'axpy' (out[n] = u . R[:, n])."""
+
+    def __init__(self, op, kind, R, vec, out, out_wcr):
+        self.op = op
+        self.kind = kind
+        self.R = R  # (container, offset, M, N, rs)
+        self.vec = vec  # _View 1-D
+        self.out = out  # _View 1-D
+        self.out_wcr = out_wcr
+
+
+def _mv(planner: P.Planner, op: P.LibOp, shapes) -> MV | None:
+    if not isinstance(op, P.LibOp) or op.kind != "matmul" or op.rowpass is not None:
+        return None
+    n = op.node
+    st = op.state
+    ins = {e.dst_conn: e for e in st.in_edges(n) if e.memlet is not None}
+    outs = [e for e in st.out_edges(n) if e.memlet is not None]
+    if "a" not in ins or "b" not in ins or len(outs) != 1:
+        return None
+    g = planner.g
+    for e in (ins["a"], ins["b"], outs[0]):
+        if g.containers[e.memlet.container].dtype != "f64":
+            return None
+    a = _view(planner, ins["a"].memlet, n.attrs.get("a_kept"), shapes)
+    b = _view(planner, ins["b"].memlet, n.attrs.get("b_kept"), shapes)
+    o = _view(planner, outs[0].memlet, None, shapes)
+    if a is None or b is None or o is None:
+        return None
+    odims = [d for d in o.dims if d[0] != 1]
+    if outs[0].memlet.wcr not in (None, "add"):
+        return None
+    if len(a.dims) == 2 and len(b.dims) == 1:  # X @ v
+        (M, rs), (K, cs) = a.dims
+        if b.dims[0][0] != K or len(odims) != 1 or odims[0][0] != M:
+            return None
+        out = _View(o.container, o.offset, odims)
+        if cs == 1:
+            return MV(op, "dot", (a.container, a.offset, M, K, rs), b, out, outs[0].memlet.wcr)
+        if rs == 1:
+            return MV(op, "axpy", (a.container, a.offset, K, M, cs), b, out, outs[0].memlet.wcr)
+        return None
+    if len(a.dims) == 1 and len(b.dims) == 2:  # u @ X
+        (K, rs), (N, cs) = b.dims
+        if a.dims[0][0] != K or len(odims) != 1 or odims[0][0] != N:
+            return None
+        out = _View(o.container, o.offset, odims)
+        if cs == 1:
+            return MV(op, "axpy", (b.container, b.offset, K, N, rs), a, out, outs[0].memlet.wcr)
+        if rs == 1:
+            return MV(op, "dot", (b.container, b.offset, N, K, cs), a, out, outs[0].memlet.wcr)
+        return None
+    return None
+
+
+def _prologue_ok(planner: P.Planner, grp: P.MapGroup, R, shapes):
+    """P1: a parallel 2-param map writing only R's container, at the identity
+    point over the full matrix, and reading it only there."""
+    if not isinstance(grp, P.MapGroup) or grp.schedule != "parallel" or len(grp.params) != 2:
+        return None
+    cont, off, M, N, rs = R
+    shape = shapes[cont]
+    if len(shape) != 2 or off != 0:
+        return None
+    acc = []
+    for mem in grp.members:
+        acc += planner.member_accesses(mem, grp.params)
+    p0, p1 = grp.params
+    ident = ((0, ((p0, 1),)), (0, ((p1, 1),)))
+    writes = {a[0] for a in acc if a[1]}
+    if writes != {cont}:
+        return None
+    for a in acc:
+        if a[0] == cont and (a[4] != ident or a[2] is not None or a[3] != 0):
+            return None
+    rng = [codegen._const_range(planner, r) for r in grp.ranges]
+    if rng != [(0, 1, shape[0]), (0, 1, shape[1])]:
+        return None
+    # orientation: R rows are X rows (rs == shape[1]) or X columns (transposed)
+    if rs == shape[1] and (M, N) == (shape[0], shape[1]):
+        return {"m": p0, "n": p1}
+    if rs == shape[0] and (M, N) == (shape[1], shape[0]):
+        return {"m": p1, "n": p0}
+    return None
+
+
+def _reads(planner, op) -> set:
+    out = set()
+    if isinstance(op, P.LibOp):
+        for e in op.state.in_edges(op.node):
+            if e.memlet is not None:
+                out.add(e.memlet.container)
+    return out
+
+
+def fuse(planner: P.Planner, ops: list) -> list:
+    shapes = planner.shapes()
+    out = []
+    i = 0
+    while i < len(ops):
+        op = ops[i]
+        nxt = ops[i + 1] if i + 1 < len(ops) else None
+        mv = _mv(planner, op, shapes)
+        # P1: prologue map + product on the map's matrix
+        if isinstance(op, P.MapGroup) and nxt is not None:
+            mv2 = _mv(planner, nxt, shapes)
+            if mv2 is not None:
+                roles = _prologue_ok(planner, op, mv2.R, shapes)
+                if roles is not None and mv2.vec.container != mv2.R[0]:
+                    rp = RowPass(planner, [mv2], prologue=op, roles=roles)
+                    if rp.ok:
+                        nxt.rowpass = rp
+                        nxt.prologue = op
+                        out.append(nxt)
+                        i += 2
+                        continue
+        if mv is not None and nxt is not None:
+            mv2 = _mv(planner, nxt, shapes)
+            if mv2 is not None and mv2.R == mv.R:
+                # P2 atax: dot then axpy whose coefficient vector is the dot output
+                if (mv.kind == "dot" and mv2.kind == "axpy" and mv2.vec.container == mv.out.container
+                        and mv2.vec.offset == mv.out.offset and mv2.vec.dims == mv.out.dims
+                        and mv.out_wcr is None):
+                    rp = RowPass(planner, [mv, mv2], coef_from_dot=True)
+                    if rp.ok:
+                        op.rowpass = rp
+                        op.fused = [nxt.node]
+                        out.append(op)
+                        i += 2
+                        continue
+                # P3 bicg: independent dot + axpy on the same matrix
+                if {mv.kind, mv2.kind} == {"dot", "axpy"}:
+                    outs = {mv.out.container, mv2.out.container}
+                    if not (outs & (_reads(planner, op) | _reads(planner, nxt))):
+                        rp = RowPass(planner, [mv, mv2])
+                        if rp.ok:
+                            op.rowpass = rp
+                            op.fused = [nxt.node]
+                            out.append(op)
+                            i += 2
+                            continue
+        if mv is not None:
+            rp = RowPass(planner, [mv])
+            if rp.ok:
+                op.rowpass = rp
+        out.append(op)
+        i += 1
+    return out
+
+
+class RowPass:
+    """A planned rowpass launch (main kernel + deterministic finalize)."""
+
+    def __init__(self, planner: P.Planner, mvs: list, prologue: P.MapGroup | None = None,
+                 roles: dict | None = None, coef_from_dot: bool = False):
+        self.planner = planner
+        self.mvs = mvs
+        self.prologue = prologue
+        self.roles = roles or {}
+        self.coef_from_dot = coef_from_dot
+        self.R = mvs[0].R
+        self.dot = next((m for m in mvs if m.kind == "dot"), None)
+        self.axpy = next((m for m in mvs if m.kind == "axpy"), None)
+        cont, off, M, N, rs = self.R
+        self.M, self.N, self.rs = M, N, rs
+        self.cw = min(N, MAX_CW)
+        self.ctiles = -(-N // self.cw) if N else 1
+        self.ok = M > 0 and N > 0 and not (coef_from_dot and self.ctiles > 1)
+        if self.dot is not None and self.dot.vec.dims[0][0] != N:
+            self.ok = False
+        if self.axpy is not None and self.axpy.vec.dims[0][0] != M and not coef_from_dot:
+            self.ok = False
+
+    # -- compile ---------------------------------------------------------------
+
+    def source(self, shapes, name: str) -> str:
+        M, N, rs, cw = self.M, self.N, self.rs, self.cw
+        kpt = -(-cw // TPB)
+        dot, axpy = self.dot, self.axpy
+        smem_doubles = (cw if axpy else 0) + (cw if dot else 0) + 64
+        self.smem = smem_doubles * 8
+        est_regs = 4 * kpt + 40  # x / xn double arrays + addressing
+        blocks_per_sm = max(1, min(4, (200 * 1024) // max(1, self.smem),
+                                   65536 // (TPB * est_regs)))
+        self.G = min(M, 148 * blocks_per_sm)
+        L = []
+        L.append(f"#define RP_NAME b2_rp_{name}")
+        L.append(f"#define RP_FIN_NAME b2_rpf_{name}")
+        for k, v in (("RP_M", M), ("RP_N", N), ("RP_RS", rs), ("RP_CW", cw), ("RP_TPB", TPB),
+                     ("RP_KPT", kpt), ("RP_G", self.G), ("RP_CTILES", self.ctiles),
+                     ("RP_DOT", int(dot is not None)), ("RP_AXPY", int(axpy is not None)),
+                     ("RP_PROLOGUE", int(self.prologue is not None)),
+                     ("RP_WRITEBACK", int(self.prologue is not None))):
+            L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")
+        nbase = 8
+        pro_src = ""
+        if self.prologue is not None:
+            cont = self.R[0]
+            env = {self.roles["m"]: "m", self.roles["n"]: "n"}
+            spec = codegen.point_function(
+                self.planner, self.prologue, shapes, name, env, {cont: "x"}, nbase,
+                "double rp_elem(const RpArgs &a, const RpRow &rr, b2_ll m, b2_ll n, double x)",
+                f"r_{cont}")
+            self.pro_args = spec.args
+            pro_src = spec.source
+        else:
+            self.pro_args = []
+        nargs = nbase + len(self.pro_args)
+        L.append("struct RpArgs { long long w[%d]; };" % nargs)
+        L.append("struct RpRow { int unused; };")
+        L.append("__device__ __forceinline__ void rp_row_setup(const RpArgs &, b2_ll, RpRow &) {}")
+        L.append(pro_src)
+        if dot is not None:
+            vinc = dot.vec.dims[0][1]
+            oinc = dot.out.dims[0][1]
+            L.append("__device__ __forceinline__ double rp_dot_vec(const RpArgs &a, b2_ll n) "
+                     f"{{ return ((const double *)a.w[3])[n * {vinc}LL]; }}")
+            add = "*p + d" if dot.out_wcr == "add" else "d"
+            if self.ctiles == 1:
+                L.append("__device__ __forceinline__ void rp_store_dot(const RpArgs &a, b2_ll m, "
+                         f"double d, int) {{ double *p = (double *)a.w[4] + m * {oinc}LL; *p = {add}; }}")
+            else:
+                L.append("__device__ __forceinline__ void rp_store_dot(const RpArgs &a, b2_ll m, "
+                         f"double d, int t) {{ ((double *)a.w[2])[(b2_ll)t * {M}LL + m] = d; }}")
+            L.append("__device__ __forceinline__ void rp_store_dot_final(const RpArgs &a, b2_ll m, "
+                     f"double d) {{ double *p = (double *)a.w[4] + m * {oinc}LL; *p = {add}; }}")
+        else:
+            L.append("__device__ __forceinline__ double rp_dot_vec(const RpArgs &, b2_ll) { return 0.0; }")
+            L.append("__device__ __forceinline__ void rp_store_dot(const RpArgs &, b2_ll, double, int) {}")
+            L.append("__device__ __forceinline__ void rp_store_dot_final(const RpArgs &, b2_ll, double) {}")
+        if axpy is not None:
+            ainc = axpy.out.dims[0][1]
+            add = "*p + s" if axpy.out_wcr == "add" else "s"
+            if self.coef_from_dot:
+                L.append("__device__ __forceinline__ double rp_coef(const RpArgs &, b2_ll, double d) "
+                         "{ return d; }")
+            else:
+                uinc = axpy.vec.dims[0][1]
+                L.append("__device__ __forceinline__ double rp_coef(const RpArgs &a, b2_ll m, double) "
+                         f"{{ return ((const double *)a.w[5])[m * {uinc}LL]; }}")
+            L.append("__device__ __forceinline__ void rp_store_axpy(const RpArgs &a, b2_ll n, double s) "
+                     f"{{ double *p = (double *)a.w[6] + n * {ainc}LL; *p = {add}; }}")
+        else:
+            L.append("__device__ __forceinline__ double rp_coef(const RpArgs &, b2_ll, double d) "
+                     "{ return d; }")
+            L.append("__device__ __forceinline__ void rp_store_axpy(const RpArgs &, b2_ll, double) {}")
+        return (rt.family_source("prelude.cuh") + "\n" + "\n".join(L) + "\n"
+                + rt.family_source("rowpass.cuh"))
+
+    def compile(self, ex):
+        name = f"{ex.g.name}_{self.mvs[0].op.idx}"
+        src = self.source(ex.buf.shape, name)
+        self.kmain = rt.get_kernel(src, f"b2_rp_{name}", max_smem=self.smem)
+        self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
+        ws = 0
+        if self.axpy is not None:
+            ws += self.G * self.N * 8
+        self.ws_axpy = ex.buf.alloc(max(8, self.G * self.N * 8)) if self.axpy is not None else 0
+        self.ws_dot = ex.buf.alloc(max(8, self.ctiles * self.M * 8)) if self.dot is not None else 0
+
+    # -- run ---------------------------------------------------------------------
+
+    def _ptr(self, ex, view):
+        return ex.buf.ptr[view.container] + 8 * view.offset
+
+    def run(self, ex, sym, counters):
+        cont, off = self.R[0], self.R[1]
+        w = [0] * 8
+        w[0] = ex.buf.ptr[cont] + 8 * off
+        w[1] = self.ws_axpy
+        w[2] = self.ws_dot
+        if self.dot is not None:
+            w[3] = self._ptr(ex, self.dot.vec)
+            w[4] = self._ptr(ex, self.dot.out)
+        if self.axpy is not None:
+            if not self.coef_from_dot:
+                w[5] = self._ptr(ex, self.axpy.vec)
+            w[6] = self._ptr(ex, self.axpy.out)
+        for d in self.pro_args:
+            if d[0] == "ptr":
+                w.append(ex.buf.ptr[d[1]])
+            elif d[0] == "flag":
+                w.append(ex.flag)
+            else:
+                raise P.PlanError(f"unsupported prologue argument {d}")
+        blob = struct.pack(f"<{len(w)}q", *w)
+        rt.launch(self.kmain, (self.G, self.ctiles, 1), (TPB, 1, 1), blob, ex.stream, self.smem)
+        nfin = max(self.N if self.axpy is not None else 0,
+                   self.M if (self.dot is not None and self.ctiles > 1) else 0)
+        if nfin:
+            rt.launch(self.kfin, ((nfin + 255) // 256, 1, 1), (256, 1, 1), blob, ex.stream)
+            ex.launches += 1
+        ex.launches += 1
+        if counters is not None:
+            self._count(ex, sym, counters)
+
+    def _count(self, ex, sym, counters):
+        from .machine import _count_map
+
+        if self.prologue is not None:
+            rv = codegen.range_values(self.prologue, sym)
+            _count_map(ex, self.prologue, rv, counters, sym)
+        for mv in self.mvs:
+            M, N = self.M, self.N
+            counters.bytes_moved += 8 * (M * N + mv.vec.dims[0][0] + mv.out.dims[0][0])
+            if mv.out_wcr is not None:
+                counters.wcr_commits += mv.out.dims[0][0]
+
+
+_ = ctypes

@@ -71,6 +71,10 @@ class _Gen:
         self.uid = 0
         self.regs: list[str] = []
         self.ind = 2
+        self.arg_base = 0
+        self.place_override: dict[str, str] = {}
+        self.written: set = set()
+        self.cse: dict = {}
 
     # -- helpers ---------------------------------------------------------------
 
@@ -83,7 +87,7 @@ class _Gen:
 
     def arg(self, desc) -> str:
         i = self.spec.arg_index(desc)
-        return f"a.w[{i}]"
+        return f"a.w[{self.arg_base + i}]"
 
     def sym(self, name: str) -> str:
         if name not in self.spec.syms:
@@ -105,6 +109,8 @@ class _Gen:
         return self.g.containers[name]
 
     def place(self, name: str) -> str:
+        if name in self.place_override:
+            return self.place_override[name]
         return self.pl.placement.get(name, "memory")
 
     def offset(self, name: str, idx_codes: list[str]) -> str:
@@ -531,6 +537,58 @@ def _const_range(planner: P.Planner, rng):
     if sv < 1:
         return None
     return bv, sv, max(0, (ev - bv) // sv + 1)
+
+
+def point_function(planner: P.Planner, group: P.MapGroup, shapes: dict, fname: str,
+                   env: dict, regs: dict, arg_base: int, signature: str, ret: str):
+    """Emit the per-point body of ``group`` as a __device__ function (used to
+    inline an elementwise map into another family, e.g. the rowpass
+    prologue).  ``env`` maps group params to C expressions; ``regs`` maps
+    containers to register names that replace their memory accesses."""
+    gen = _Gen(planner, group, shapes, fname)
+    gen.arg_base = arg_base
+    gen.place_override = {c: "reg" for c in regs}
+    for mem in group.members:
+        for a in planner.member_accesses(mem, group.params):
+            if a[1]:
+                gen.written.add(a[0])
+    gen.ind = 2
+    for mem in group.members:
+        menv = {mp: env[gp] for mp, gp in mem.rename.items()}
+        if mem.tasklet is not None:
+            gen.tasklet(mem.state, mem.tasklet, menv, 0)
+        else:
+            gen.scope(mem.state, mem.entry, menv, 0)
+    body = gen.lines
+    decl = []
+    for name in gen.spec.containers:
+        if name in regs:
+            continue
+        c = planner.g.containers[name]
+        ro = name not in gen.written
+        q = "const " if ro else ""
+        decl.append(f"  {q}{CT[c.dtype]} *__restrict__ c_{name} = ({q}{CT[c.dtype]} *){gen.arg(('ptr', name))};")
+        st = _row_major(shapes[name])
+        for d in range(len(st)):
+            decl.append(f"  constexpr b2_ll st_{name}_{d} = {st[d]}LL;")
+        n = 1
+        for x in shapes[name]:
+            n *= x
+        decl.append(f"  constexpr b2_ll sz_{name} = {n}LL;")
+    for sname in gen.spec.syms:
+        if sname in planner.fixed:
+            decl.append(f"  constexpr b2_ll s_{sname} = {int(planner.fixed[sname])}LL;")
+        else:
+            raise P.PlanError("loop-assigned symbol in a fused prologue")
+    if gen.spec.uses_flag:
+        raise P.PlanError("guarded accesses in a fused prologue")
+    src = [f"__device__ __forceinline__ {signature} {{"]
+    src += decl
+    src += [f"  {CT[planner.g.containers[c].dtype]} r_{c} = {r};" for c, r in regs.items()]
+    src += body
+    src += [f"  return {ret};", "}"]
+    gen.spec.source = "\n".join(src) + "\n"
+    return gen.spec
 
 
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str) -> KernelSpec:

@@ -1,0 +1,134 @@
+// rowpass.cuh — one-HBM-pass BLAS-2 family (f64) for the MATMUL library
+// node in its matrix-vector forms (np.matmul 2D@1D / 1D@2D, interp.py:
+// 450-460) and their fusions in gemver / atax / bicg.
+//
+// R is an M x N row-contiguous matrix view (row stride RP_RS).  One pass over
+// R computes, per row m,
+//     x'[m,n] = PROLOGUE(x[m,n])        (optional elementwise map, written back)
+//     dot[m]  = sum_n x'[m,n] * v[n]    (optional;  A @ v)
+//     acc[n] += coef(m) * x'[m,n]       (optional;  u @ A, coef = u[m] or dot[m])
+// Blocks own interleaved rows (m = blockIdx.x + i * gridDim.x) so concurrently
+// running CTAs stream neighbouring rows; grid.y tiles columns in RP_CW chunks
+// whose v / acc slices live in shared memory; the next row is prefetched into
+// registers while the current row's dot is block-reduced.  Column partials go
+// to a workspace reduced by rp_finalize in a fixed order (deterministic).
+//
+// The including translation unit defines RP_* constants, struct RpArgs and
+// the hooks rp_row_setup / rp_elem / rp_dot_vec / rp_coef / rp_store_dot.
+
+#ifndef RP_KPT
+#error "rowpass.cuh needs RP_KPT"
+#endif
+
+__device__ __forceinline__ double rp_block_sum(double v, double *red, int parity) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[parity * 32 + w] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < RP_TPB / 32; ++i) t += red[parity * 32 + i];
+  return t;
+}
+
+extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_constant__ RpArgs a) {
+  extern __shared__ double rp_smem[];
+  double *acc_s = rp_smem;                     // [RP_CW] column accumulators
+  double *v_s = rp_smem + (RP_AXPY ? RP_CW : 0);  // [RP_CW] dot vector slice
+  double *red = v_s + (RP_DOT ? RP_CW : 0);     // [2][32] reduction scratch
+  const int tid = threadIdx.x;
+  const b2_ll c0 = (b2_ll)blockIdx.y * RP_CW;
+  const int cw = (int)((RP_N - c0) < RP_CW ? (RP_N - c0) : RP_CW);
+  for (int j = tid; j < cw; j += RP_TPB) {
+    if (RP_AXPY) acc_s[j] = 0.0;
+    if (RP_DOT) v_s[j] = rp_dot_vec(a, c0 + j);
+  }
+  __syncthreads();
+  const double *__restrict__ R = (const double *)a.w[0];
+  double x[RP_KPT], xn[RP_KPT];
+  b2_ll m = blockIdx.x;
+  if (m < RP_M) {
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) {
+      const int j = tid + k * RP_TPB;
+      x[k] = (j < cw) ? R[m * RP_RS + c0 + j] : 0.0;
+    }
+  }
+  int parity = 0;
+  for (; m < RP_M; m += gridDim.x) {
+    const b2_ll mn = m + gridDim.x;
+    if (mn < RP_M) {
+#pragma unroll
+      for (int k = 0; k < RP_KPT; ++k) {
+        const int j = tid + k * RP_TPB;
+        xn[k] = (j < cw) ? R[mn * RP_RS + c0 + j] : 0.0;
+      }
+    }
+#if RP_PROLOGUE
+    {
+      RpRow rr;
+      rp_row_setup(a, m, rr);
+#pragma unroll
+      for (int k = 0; k < RP_KPT; ++k) {
+        const int j = tid + k * RP_TPB;
+        if (j < cw) {
+          x[k] = rp_elem(a, rr, m, c0 + j, x[k]);
+#if RP_WRITEBACK
+          ((double *)a.w[0])[m * RP_RS + c0 + j] = x[k];
+#endif
+        }
+      }
+    }
+#endif
+#if RP_DOT
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) {
+      const int j = tid + k * RP_TPB;
+      if (j < cw) p += x[k] * v_s[j];
+    }
+    const double d = rp_block_sum(p, red, parity);
+    parity ^= 1;
+    if (tid == 0) rp_store_dot(a, m, d, blockIdx.y);
+#else
+    const double d = 0.0;
+#endif
+#if RP_AXPY
+    const double c = rp_coef(a, m, d);
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) {
+      const int j = tid + k * RP_TPB;
+      if (j < cw) acc_s[j] += c * x[k];
+    }
+#endif
+    (void)d;
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) x[k] = xn[k];
+  }
+#if RP_AXPY
+  double *ws = (double *)a.w[1];
+  for (int j = tid; j < cw; j += RP_TPB) ws[(b2_ll)blockIdx.x * RP_N + c0 + j] = acc_s[j];
+#endif
+}
+
+// out[n] (wcr)= sum over G row-groups of ws[g][n]  (+ per-tile dot partials)
+extern "C" __global__ void __launch_bounds__(256) RP_FIN_NAME(const __grid_constant__ RpArgs a) {
+  const b2_ll i = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x;
+#if RP_AXPY
+  if (i < RP_N) {
+    const double *ws = (const double *)a.w[1];
+    double s = 0.0;
+    for (int g = 0; g < RP_G; ++g) s += ws[(b2_ll)g * RP_N + i];
+    rp_store_axpy(a, i, s);
+  }
+#endif
+#if RP_DOT && RP_CTILES > 1
+  if (i < RP_M) {
+    const double *wd = (const double *)a.w[2];
+    double s = 0.0;
+    for (int t = 0; t < RP_CTILES; ++t) s += wd[(b2_ll)t * RP_M + i];
+    rp_store_dot_final(a, i, s);
+  }
+#endif
+}
