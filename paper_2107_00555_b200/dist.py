@@ -1,5 +1,547 @@
-"""Multi-GPU execution (placeholder until the slab executor lands)."""
+"""Distributed execution: block (slab) distribution along axis 0 with
+automatic halo exchange, one process per GPU.
+
+Reference: the distributed extensions of the paper (§distributed;
+SPEC.md:505-603) — block-distributed arrays, halo exchange, Allreduce — whose
+``sdfgkit.dist`` source is absent from the mounted reference;
+semantics here follow SPEC.md:514-517/587 and pkg/tests/test_dist.py
+(distributed results must equal the shared-memory oracle).
+
+``slab_decompose`` analyses a program graph: containers indexed on axis 0 by
+the first parameter of every map that touches them (``p0 + c``) are block
+distributed.  Each map's p0 iteration range is split into P contiguous
+chunks that depend only on the range, so fused chains stay aligned; rank r
+computes its chunk and *owns* the rows it writes.  Local arrays hold the
+contiguous row window the rank reads or writes; memlets are rewritten to
+local rows.  Before an op reads a container written since the last exchange,
+``Owned_r ∩ Needed_s`` row blocks move between ranks over the communicator
+(NCCL send/recv over NVLink on GPUs, gloo on CPU in the tests).  Results are
+bitwise identical to one device: every point runs the same tasklet chain on
+the same values.
+
+ProcessGrid / block_indices mirror the reference dist API names (cli.py:
+22-25, test_dist.py:5-10) for 1-D and 2-D grids (SUMMA uses the latter).
+"""
+
+from __future__ import annotations
+
+import copy
+import math
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import plan as P, sdfg, symexpr
+
+
+class DistError(ValueError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# process grids (reference API shape)
+
+
+class ProcessGrid:
+    def __init__(self, dims):
+        self.dims = tuple(int(d) for d in dims)
+        if not self.dims or any(d < 1 for d in self.dims):
+            raise DistError(f"bad grid {dims}")
+
+    @property
+    def size(self) -> int:
+        return math.prod(self.dims)
+
+    def coords(self, r: int) -> tuple:
+        out = []
+        for d in reversed(self.dims):
+            out.append(r % d)
+            r //= d
+        return tuple(reversed(out))
+
+    def rank_of(self, coords) -> int:
+        r = 0
+        for c, d in zip(coords, self.dims):
+            r = r * d + c
+        return r
+
+    @staticmethod
+    def parse(text: str) -> "ProcessGrid":
+        return ProcessGrid([int(x) for x in text.lower().split("x")])
+
+    @staticmethod
+    def squarest(p: int) -> "ProcessGrid":
+        """Squarest factorisation with rows >= columns."""
+        best = (p, 1)
+        for c in range(1, int(math.isqrt(p)) + 1):
+            if p % c == 0:
+                best = (p // c, c)
+        return ProcessGrid(best)
+
+    def __repr__(self):
+        return "x".join(map(str, self.dims))
+
+
+def block_indices(extent: int, griddim: int, coord: int, block: int | None = None) -> range:
+    """Indices of ``extent`` owned by ``coord`` of ``griddim``: contiguous
+    near-equal blocks (block=None) or block-cyclic with block size ``block``."""
+    if block is None:
+        lo = extent * coord // griddim
+        hi = extent * (coord + 1) // griddim
+        return range(lo, hi)
+    idx = []
+    for start in range(coord * block, extent, griddim * block):
+        idx.extend(range(start, min(start + block, extent)))
+    return idx  # type: ignore[return-value]
+
+
+# ---------------------------------------------------------------------------
+# slab decomposition
+
+
+@dataclass
+class _MapInfo:
+    state: str
+    entry_id: int
+    p0: str
+    lo: int  # global p0 range (inclusive)
+    hi: int
+    reads: dict = field(default_factory=dict)  # container -> set of offsets
+    writes: dict = field(default_factory=dict)
+
+
+def _chunk(lo: int, hi: int, P_: int, r: int) -> tuple[int, int]:
+    n = hi - lo + 1
+    a = lo + n * r // P_
+    b = lo + n * (r + 1) // P_ - 1
+    return a, b
+
+
+class SlabPlan:
+    def __init__(self, g: sdfg.Graph, bindings: dict, nranks: int):
+        self.g = g
+        self.bindings = {k: int(v) for k, v in bindings.items()}
+        self.P = nranks
+        self.extent: dict[str, int] = {}
+        self.maps: list[_MapInfo] = []
+        self._analyse()
+        self._rows()
+
+    def _analyse(self):
+        g = self.g
+        env = dict(self.bindings)
+        loopish = set()
+        for t in g.transitions:
+            loopish |= set(t.assignments)
+        for k in loopish:
+            env.pop(k, None)
+        dist: set[str] = set()
+        infos = []
+        for st in g.states:
+            parents = st.scope_parents()
+            for n in st.topological():
+                if parents.get(n.id) is not None:
+                    continue
+                if isinstance(n, sdfg.MapEntry):
+                    info = self._map_info(st, n, env)
+                    if info is not None:
+                        infos.append(info)
+                        dist |= set(info.reads) | set(info.writes)
+        if not dist:
+            raise DistError("no map indexes a container along axis 0 by its first parameter")
+        self.dist = dist
+        self.maps = infos
+        # every other node must not touch distributed containers
+        slab = {(mi.state, mi.entry_id) for mi in infos}
+        for st in g.states:
+            parents = st.scope_parents()
+            for n in st.topological():
+                if parents.get(n.id) is not None or isinstance(n, sdfg.MapExit):
+                    continue
+                if isinstance(n, sdfg.MapEntry):
+                    if (st.label, n.id) in slab:
+                        continue
+                    inner = set()
+                    for c2 in P._scope_children(st, n):
+                        for e2 in st.in_edges(c2) + st.out_edges(c2):
+                            if e2.memlet is not None:
+                                inner.add(e2.memlet.container)
+                    if inner & dist:
+                        raise DistError(f"map {n.id} in state {st.label} touches a distributed "
+                                        "container but is not slab-parallel along axis 0")
+                    continue
+                edges = st.in_edges(n) + st.out_edges(n)
+                touched = {e.memlet.container for e in edges if e.memlet is not None}
+                if isinstance(n, sdfg.Access):
+                    touched = {n.container} if any(isinstance(e.src, sdfg.Access)
+                                                   for e in st.in_edges(n)) else set()
+                if touched & dist:
+                    raise DistError(f"node {n.id} in state {st.label} accesses a distributed "
+                                    "container outside a slab-parallel map")
+        for c in dist:
+            desc = g.containers[c]
+            self.extent[c] = symexpr.evaluate(desc.shape[0], self.bindings)
+
+    def _map_info(self, st, entry, env):
+        if entry.schedule not in ("parallel", "distributed_hint") or not entry.params:
+            return None
+        p0 = entry.param_names[0]
+        b, e, s = entry.params[0][1]
+        try:
+            lo, hi, step = (symexpr.evaluate(x, env) for x in (b, e, s))
+        except KeyError:
+            return None
+        if step != 1:
+            return None
+        info = _MapInfo(st.label, entry.id, p0, lo, hi)
+        uses_p0 = False
+        for c in P._scope_children(st, entry):
+            edges = []
+            if isinstance(c, sdfg.Tasklet):
+                edges = st.in_edges(c) + st.out_edges(c)
+            elif isinstance(c, (sdfg.MapEntry, sdfg.Library, sdfg.Nested)):
+                return None  # nested scopes: keep replicated (not slab-parallel)
+            for e2 in edges:
+                m = e2.memlet
+                if m is None or not m.subset:
+                    continue
+                b0, e0, _ = m.subset[0]
+                a = symexpr.affine(b0, (p0,), env)
+                if a is None or a[1] != {p0: 1} or b0 != e0:
+                    continue
+                for d in m.subset[1:]:
+                    for x in d:
+                        if p0 in symexpr.free_symbols(x):
+                            return None
+                uses_p0 = True
+                tgt = info.writes if e2.src is c else info.reads
+                tgt.setdefault(m.container, set()).add(a[0])
+                if e2.src is c and m.wcr is not None:
+                    return None
+        return info if uses_p0 else None
+
+    def _rows(self):
+        """Per rank and container: owned rows (written) and needed rows
+        (read), and the local window [lo, hi)."""
+        self.owned = [{c: set() for c in self.dist} for _ in range(self.P)]
+        self.needed = [{c: set() for c in self.dist} for _ in range(self.P)]
+        for r in range(self.P):
+            for mi in self.maps:
+                a, b = _chunk(mi.lo, mi.hi, self.P, r)
+                if b < a:
+                    continue
+                for c, offs in mi.writes.items():
+                    for o in offs:
+                        self.owned[r][c] |= set(range(a + o, b + o + 1))
+                for c, offs in mi.reads.items():
+                    for o in offs:
+                        self.needed[r][c] |= set(range(a + o, b + o + 1))
+        for c in self.dist:
+            seen = set()
+            for r in range(self.P):
+                if self.owned[r][c] & seen:
+                    raise DistError(f"ranks write overlapping rows of '{c}'")
+                seen |= self.owned[r][c]
+        self.window = []
+        for r in range(self.P):
+            w = {}
+            for c in self.dist:
+                rows = self.owned[r][c] | self.needed[r][c]
+                if not rows:
+                    w[c] = (0, 0)
+                else:
+                    lo, hi = min(rows), max(rows) + 1
+                    if lo < 0 or hi > self.extent[c]:
+                        raise DistError(f"rows of '{c}' out of range on rank {r}")
+                    w[c] = (lo, hi)
+            self.window.append(w)
+
+    def transfers(self, c: str, r: int):
+        """(sends, recvs) for container c on rank r: lists of (peer, lo, hi)
+        global row blocks (contiguous runs)."""
+        sends, recvs = [], []
+        for s in range(self.P):
+            if s == r:
+                continue
+            for peer, rows, out in ((s, self.owned[r][c] & self.needed[s][c], sends),
+                                    (s, self.owned[s][c] & self.needed[r][c], recvs)):
+                for lo, hi in _runs(rows):
+                    out.append((peer, lo, hi))
+        return sends, recvs
+
+    def local_graph(self, r: int) -> sdfg.Graph:
+        """Copy of the graph for rank r: distributed containers hold their row
+        window, slab maps iterate the rank's chunk, memlets address local rows."""
+        g = copy.deepcopy(self.g)
+        win = self.window[r]
+        for c in self.dist:
+            lo, hi = win[c]
+            desc = g.containers[c]
+            desc.shape = [("c", max(1, hi - lo))] + list(desc.shape[1:])
+        by_key = {(mi.state, mi.entry_id): mi for mi in self.maps}
+        for st in g.states:
+            parents = st.scope_parents()
+            for n in st.nodes:
+                if not isinstance(n, sdfg.MapEntry):
+                    continue
+                mi = by_key.get((st.label, n.id))
+                if mi is None or parents.get(n.id) is not None:
+                    continue
+                a, b = _chunk(mi.lo, mi.hi, self.P, r)
+                if b < a:
+                    a, b = 1, 0  # empty chunk
+                n.params[0] = (n.params[0][0], (("c", a), ("c", b), ("c", 1)))
+                for c2 in P._scope_children(st, n):
+                    if not isinstance(c2, sdfg.Tasklet):
+                        continue
+                    for e2 in st.in_edges(c2) + st.out_edges(c2):
+                        m = e2.memlet
+                        if m is None or m.container not in self.dist or not m.subset:
+                            continue
+                        base = win[m.container][0]
+                        b0, e0, s0 = m.subset[0]
+                        m.subset = [(("-", b0, ("c", base)), ("-", e0, ("c", base)), s0)] \
+                            + list(m.subset[1:])
+            st._topo = None
+            st._parents = None
+        return g
+
+
+def _runs(rows: set):
+    if not rows:
+        return []
+    xs = sorted(rows)
+    out = []
+    start = prev = xs[0]
+    for x in xs[1:]:
+        if x != prev + 1:
+            out.append((start, prev + 1))
+            start = x
+        prev = x
+    out.append((start, prev + 1))
+    return out
+
+
+def slab_decompose(g, bindings: dict, nranks: int) -> SlabPlan:
+    return SlabPlan(sdfg.as_graph(g), bindings, nranks)
+
+
+# ---------------------------------------------------------------------------
+# runtime: halo exchange with torch.distributed
+
+
+class HaloExchanger:
+    """Dirty-tracking exchange of owned rows before they are read remotely.
+    ``rows_of(c, lo, hi)`` returns a torch tensor viewing global rows
+    [lo, hi) of container c's local buffer on this rank."""
+
+    def __init__(self, plan: SlabPlan, rank: int, rows_of):
+        import torch.distributed as tdist
+
+        self.tdist = tdist
+        self.plan = plan
+        self.rank = rank
+        self.rows_of = rows_of
+        self.dirty: set[str] = set()
+        self.xfer = {c: plan.transfers(c, rank) for c in plan.dist}
+        self.exchanges = 0
+        self.bytes_sent = 0
+
+    def before(self, reads):
+        need = [c for c in sorted(reads) if c in self.dirty]
+        if need:
+            self.exchange(need)
+
+    def after(self, writes):
+        for c in writes:
+            if c in self.plan.dist:
+                self.dirty.add(c)
+
+    def exchange(self, conts):
+        ops = []
+        td = self.tdist
+        for c in conts:
+            sends, recvs = self.xfer[c]
+            for peer, lo, hi in sends:
+                t = self.rows_of(c, lo, hi)
+                ops.append(td.P2POp(td.isend, t, peer))
+                self.bytes_sent += t.numel() * t.element_size()
+            for peer, lo, hi in recvs:
+                ops.append(td.P2POp(td.irecv, self.rows_of(c, lo, hi), peer))
+            self.dirty.discard(c)
+        if ops:
+            for req in td.batch_isend_irecv(ops):
+                req.wait()
+        self.exchanges += 1
+
+
+class _CudaArray:
+    """__cuda_array_interface__ wrapper so torch can view libb2 buffers."""
+
+    def __init__(self, ptr: int, shape, typestr="<f8"):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+_TYPESTR = {"f64": "<f8", "i64": "<i8", "i32": "<i4", "bool": "|b1"}
+
+
+class SlabGpuRunner:
+    """One rank of a slab-distributed program on its own GPU."""
+
+    def __init__(self, g, bindings: dict, rank: int, world: int, device: int):
+        import torch
+
+        from .machine import GpuExecutor, InterpOptions
+
+        self.torch = torch
+        self.g = sdfg.as_graph(g)
+        self.plan = slab_decompose(self.g, bindings, world)
+        self.rank = rank
+        self.lg = self.plan.local_graph(rank)
+        stream = torch.cuda.current_stream(device).cuda_stream
+        self.ex = GpuExecutor(self.lg, bindings, device=device, stream=stream,
+                              options=InterpOptions())
+        self.ex.capturable = False  # halo exchanges run between kernels
+        self.xchg = HaloExchanger(self.plan, rank, self._rows_of)
+        self.ex.op_hook = self._hook
+
+    def _rows_of(self, c, lo, hi):
+        desc = self.lg.containers[c]
+        wlo = self.plan.window[self.rank][c][0]
+        row = 1
+        for d in self.ex.buf.shape[c][1:]:
+            row *= d
+        esz = sdfg.DTYPE_BYTES[desc.dtype]
+        ptr = self.ex.buf.ptr[c] + (lo - wlo) * row * esz
+        return self.torch.as_tensor(_CudaArray(ptr, ((hi - lo) * row,), _TYPESTR[desc.dtype]),
+                                    device=f"cuda:{self.torch.cuda.current_device()}")
+
+    def _hook(self, op, reads, writes, phase):
+        if phase == "pre":
+            self.xchg.before(reads)
+        else:
+            self.xchg.after(writes)
+
+    def load_inputs(self, full_inputs: dict):
+        """Every rank passes the same full host inputs; each uploads its window."""
+        local = {}
+        for name, c in self.lg.containers.items():
+            if c.transient:
+                continue
+            arr = np.asarray(full_inputs[name])
+            if name in self.plan.dist:
+                lo, hi = self.plan.window[self.rank][name]
+                arr = arr[lo:hi] if hi > lo else arr[:1]
+            local[name] = arr
+        keep = self.ex.prepare_inputs(local)
+        self.ex.sync()
+        del keep
+        self.xchg.dirty.clear()
+
+    def run(self):
+        self.ex.run_device(first_call=True)
+
+    def gather(self, full_inputs: dict) -> dict | None:
+        """Owned rows of every non-transient distributed container to rank 0."""
+        import torch.distributed as tdist
+
+        torch = self.torch
+        self.ex.sync()
+        out = {}
+        for name, c in self.lg.containers.items():
+            if c.transient:
+                continue
+            if name not in self.plan.dist:
+                if self.rank == 0:
+                    out[name] = self.ex.download(name)
+                continue
+            full = np.array(full_inputs[name], dtype=np.float64, copy=True) if self.rank == 0 else None
+            for r in range(self.plan.P):
+                for lo, hi in _runs(self.plan.owned[r][name]):
+                    if r == self.rank:
+                        t = self._rows_of(name, lo, hi)
+                        if self.rank == 0:
+                            full[lo:hi] = t.cpu().numpy().reshape(full[lo:hi].shape)
+                        else:
+                            tdist.send(t.contiguous(), 0)
+                    elif self.rank == 0:
+                        row = int(np.prod(full.shape[1:]))
+                        buf = torch.empty((hi - lo) * row, dtype=torch.float64, device="cuda")
+                        tdist.recv(buf, r)
+                        full[lo:hi] = buf.cpu().numpy().reshape(full[lo:hi].shape)
+            if self.rank == 0:
+                out[name] = full
+        self.ex.sync()
+        return out if self.rank == 0 else None
 
 
 def bench_slab(args, W):
-    raise NotImplementedError("multi-GPU slab execution is not implemented yet")
+    """bench.py --gpus N under torchrun: strong-scaled slab run of the
+    workload, max-over-ranks device time, one JSON line from rank 0."""
+    import json
+
+    import torch
+    import torch.distributed as tdist
+
+    from . import runtime as rt
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    if not tdist.is_initialized():
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import pathlib
+
+    root = pathlib.Path(__file__).resolve().parent.parent
+    syms = W["syms"]
+    g = sdfg.load(root / "tests" / "golden" / "graphs" / f"{W['graph']}.json")
+    from bench import make_inputs, peaks  # noqa: E402
+
+    inputs = make_inputs(g, syms)
+    runner = SlabGpuRunner(g, syms, rank, world, local)
+    runner.load_inputs(inputs)
+    for _ in range(args.warmup):
+        runner.run()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    start.record()
+    for _ in range(args.steps):
+        runner.run()
+    end.record()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    tdist.barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    run_bytes = W["sweeps"](syms) * W["sweep_bytes"](syms)
+    value = run_bytes / (ms / 1e3) / 1e9
+    _ = time.perf_counter() - t0
+    if rank == 0:
+        peak, kind = peaks()
+        line = {
+            "metric": f"{args.workload}_f64_algorithmic_hbm_GBps", "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (make_inputs semantics, seed 0)",
+            "config": {"workload": W["desc"], "parallelism": f"slab{world} (axis-0 block "
+                       "distribution, NCCL halo exchange)",
+                       "halo_bytes_per_step": runner.xchg.bytes_sent // max(1, args.steps +
+                                                                            args.warmup)},
+            "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
+                         "frac": value / world / peak, "peak_kind": kind, "traffic": None,
+                         "note": "per-GPU share of the whole-job algorithmic bandwidth"},
+            "gpu_launches": runner.ex.launches,
+        }
+        print(json.dumps(line), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
+    _ = rt

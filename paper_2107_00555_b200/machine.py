@@ -368,11 +368,21 @@ class GpuExecutor:
 
     # -- ops -----------------------------------------------------------------------
 
+    op_hook = None  # callable(op, reads, writes, phase) used by the slab executor
+
     def _exec_op(self, op, sym, counters):
         if self._dry:
             if isinstance(op, P.NestedOp):
                 self._exec_nested(op, sym, None, dry=True)
             return
+        if self.op_hook is not None:
+            self.op_hook(op, self.planner.op_reads[op.idx], self.planner.op_writes[op.idx], "pre")
+            self._exec_op_inner(op, sym, counters)
+            self.op_hook(op, self.planner.op_reads[op.idx], self.planner.op_writes[op.idx], "post")
+        else:
+            self._exec_op_inner(op, sym, counters)
+
+    def _exec_op_inner(self, op, sym, counters):
         if isinstance(op, P.MapGroup):
             self._exec_map(op, sym, counters)
         elif isinstance(op, P.CopyOp):

@@ -383,8 +383,14 @@ class Planner:
     def _collect_sites(self):
         self.sites: dict[str, list[Site]] = {}
 
+        self.op_reads: dict[int, set] = {op.idx: set() for op in self.all_ops}
+        self.op_writes: dict[int, set] = {op.idx: set() for op in self.all_ops}
+
         def add(op, c, w, wcr, depth, point):
             self.sites.setdefault(c, []).append(Site(op.idx, c, w, wcr, depth, point))
+            (self.op_writes if w else self.op_reads)[op.idx].add(c)
+            if w and wcr is not None:
+                self.op_reads[op.idx].add(c)
 
         for op in self.all_ops:
             if isinstance(op, MapGroup):
