@@ -352,7 +352,7 @@ class RowPass:
         nfin = max(self.N if self.axpy is not None else 0,
                    self.M if (self.dot is not None and self.ctiles > 1) else 0)
         if nfin:
-            rt.launch(self.kfin, ((nfin + 255) // 256, 1, 1), (256, 1, 1), blob, ex.stream)
+            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 8, 1), blob, ex.stream)
             ex.launches += 1
         ex.launches += 1
         if counters is not None:

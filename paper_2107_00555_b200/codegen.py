@@ -30,6 +30,8 @@ CT = {"f64": "double", "i64": "b2_ll", "i32": "int", "bool": "bool"}
 TC = {"f64": "f", "i64": "i", "i32": "i", "bool": "b"}
 
 MAX_BLOCKS = 148 * 16
+STENCIL_MODE = True  # shared-memory plane ring for constant-offset reads
+STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 
 
 class KernelSpec:
@@ -75,6 +77,152 @@ class _Gen:
         self.place_override: dict[str, str] = {}
         self.written: set = set()
         self.cse: dict = {}
+        self.stencil: dict = {}
+
+    def _stencil_loop(self, k: int, vec: int, reg_decls, body: list) -> list:
+        """Stencil mode: each CTA owns a (8 x 32*vec) tile of the two inner
+        dims (3-D) or a 256*vec span of the inner dim (2-D) and marches over a
+        chunk of SCH planes along dim 0.  Every halo'd plane of each stencil
+        container is fetched once into a shared-memory ring of SDEPTH planes
+        (coalesced cooperative loads), so each input element is read from
+        L2/HBM ~once instead of once per neighbour."""
+        grp = self.group
+        L: list[str] = []
+        tk = (32 if k == 3 else 256) * vec
+        mins = [min(st["min"][d] for st in self.stencil.values()) for d in range(k)]
+        maxs = [max(st["max"][d] for st in self.stencil.values()) for d in range(k)]
+        for st in self.stencil.values():
+            st["min"], st["max"] = tuple(mins), tuple(maxs)
+        depth = maxs[0] - mins[0] + 1
+        sk = tk + maxs[-1] - mins[-1]
+        sj = 8 + maxs[1] - mins[1] if k == 3 else 1
+        L.append(f"  constexpr int SDEPTH = {depth}, SCH = {STENCIL_CHUNK}, TK = {tk};")
+        for c in self.stencil:
+            ct = CT[self.g.containers[c].dtype]
+            if k == 3:
+                L.append(f"  __shared__ {ct} sm_{c}[SDEPTH][{sj}][{sk}];")
+            else:
+                L.append(f"  __shared__ {ct} sm_{c}[SDEPTH][{sk}];")
+        x = k - 1
+        L.append(f"  constexpr b2_ll ntx = (rl{x} + TK - 1) / TK;")
+        L.append("  constexpr b2_ll nty = " + ("(rl1 + 7) / 8;" if k == 3 else "1;"))
+        L.append("  constexpr b2_ll nch = (rl0 + SCH - 1) / SCH;")
+        L.append("  const int tid = threadIdx.y * blockDim.x + threadIdx.x;")
+        L.append("  for (b2_ll vb = blockIdx.x; vb < ntx * nty * nch; vb += gridDim.x) {")
+        L.append("    const b2_ll txt = vb % ntx; b2_ll rem = vb / ntx;")
+        L.append("    const b2_ll tyt = rem % nty; const b2_ll ch = rem / nty;")
+        L.append("    const b2_ll i0 = ch * SCH;")
+        L.append("    const b2_ll nit = (rl0 - i0) < SCH ? (rl0 - i0) : SCH;")
+        L.append("    const b2_ll kx0 = txt * TK;")
+        if k == 3:
+            L.append("    const b2_ll jy0 = tyt * 8;")
+        L.append("    __syncthreads();")
+        # plane loader: row index (dim 0) relative to the map origin
+        for c in self.stencil:
+            shp = self.shapes[c]
+            ct = CT[self.g.containers[c].dtype]
+            L.append(f"    auto load_{c} = [&](b2_ll rel0, int slot) {{")
+            L.append(f"      const b2_ll g0 = rb0 + rel0;")
+            L.append(f"      const bool ok0 = g0 >= 0 && g0 < {shp[0]}LL;")
+            L.append(f"      for (int e = tid; e < {sj * sk}; e += {256}) {{")
+            if k == 3:
+                L.append(f"        const int jj = e / {sk}, kk = e % {sk};")
+                L.append(f"        const b2_ll g1 = rb1 + jy0 + ({mins[1]}) + jj;")
+                L.append(f"        const b2_ll g2 = rb2 + kx0 + ({mins[2]}) + kk;")
+                L.append(f"        const bool ok = ok0 && g1 >= 0 && g1 < {shp[1]}LL && g2 >= 0 && "
+                         f"g2 < {shp[2]}LL;")
+                L.append(f"        sm_{c}[slot][jj][kk] = ok ? c_{c}[g0 * st_{c}_0 + g1 * st_{c}_1 + "
+                         f"g2] : ({ct})0;")
+            else:
+                L.append(f"        const int kk = e;")
+                L.append(f"        const b2_ll g1 = rb1 + kx0 + ({mins[1]}) + kk;")
+                L.append(f"        const bool ok = ok0 && g1 >= 0 && g1 < {shp[1]}LL;")
+                L.append(f"        sm_{c}[slot][kk] = ok ? c_{c}[g0 * st_{c}_0 + g1] : ({ct})0;")
+            L.append("      }")
+            L.append("    };")
+        for c in self.stencil:
+            L.append(f"    for (int d = {mins[0]}; d < {maxs[0]}; ++d) load_{c}(i0 + d, d - ({mins[0]}));")
+        L.append("    for (b2_ll it = 0; it < nit; ++it) {")
+        for c in self.stencil:
+            L.append(f"      load_{c}(i0 + it + ({maxs[0]}), (int)((it + {maxs[0] - mins[0]}) % SDEPTH));")
+        L.append("      __syncthreads();")
+        L.append(f"      const b2_ll p_{grp.params[0]} = rb0 + i0 + it;")
+        inner = "      "
+        if k == 3:
+            L.append("      if (jy0 + threadIdx.y < rl1) {")
+            L.append(f"      const b2_ll p_{grp.params[1]} = rb1 + jy0 + threadIdx.y;")
+        L.append("#pragma unroll")
+        L.append(f"      for (int v = 0; v < {vec}; ++v) {{")
+        step = 32 if k == 3 else 256
+        L.append(f"        const b2_ll ix = kx0 + threadIdx.x + {step} * v;")
+        L.append(f"        if (ix >= rl{x}) break;")
+        L.append(f"        const b2_ll p_{grp.params[x]} = rb{x} + ix;")
+        L += reg_decls(8)
+        L += [inner + ln for ln in body]
+        L.append("      }")
+        if k == 3:
+            L.append("      }")
+        L.append("      __syncthreads();")
+        L.append("    }")
+        L.append("  }")
+        return L
+
+    def _stencil_offsets(self, m: sdfg.Memlet, env: dict) -> tuple:
+        offs = []
+        for d, (b, _, _) in enumerate(m.subset):
+            a = symexpr.affine(b, tuple(env), self.pl.fixed)
+            offs.append(a[0])
+        return tuple(offs)
+
+    def _stencil_analysis(self) -> dict:
+        """Containers read (never written) by the group only at constant
+        offsets from the point, dimension d indexed by parameter d: these are
+        staged through a shared-memory plane ring (stencil mode)."""
+        grp = self.group
+        k = len(grp.params)
+        reads: dict[str, set] = {}
+        written = set()
+        for mem in grp.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if w:
+                    written.add(c)
+                    continue
+                if depth != 0 or pt is None:
+                    reads[c] = None
+                    continue
+                if reads.get(c, set()) is None:
+                    continue
+                offs = []
+                ok = len(pt) == k
+                for d, key in enumerate(pt if ok else ()):
+                    c0, co = key
+                    if co != ((grp.params[d], 1),):
+                        ok = False
+                        break
+                    offs.append(c0)
+                if not ok:
+                    reads[c] = None
+                else:
+                    reads.setdefault(c, set()).add(tuple(offs))
+        out = {}
+        for c, offs in reads.items():
+            if offs is None or c in written or self.place(c) != "memory":
+                continue
+            if len(self.shapes[c]) != k:
+                continue
+            lo = tuple(min(o[d] for o in offs) for d in range(k))
+            hi = tuple(max(o[d] for o in offs) for d in range(k))
+            if lo == hi:
+                continue  # no halo: plain loads are as good
+            if max(h - l for h, l in zip(hi, lo)) > 4:
+                continue
+            out[c] = {"offs": offs, "min": lo, "max": hi}
+        if out:  # one plane ring geometry shared by every staged container
+            mins = tuple(min(st["min"][d] for st in out.values()) for d in range(k))
+            maxs = tuple(max(st["max"][d] for st in out.values()) for d in range(k))
+            for st in out.values():
+                st["min"], st["max"] = mins, maxs
+        return out
 
     # -- helpers ---------------------------------------------------------------
 
@@ -134,6 +282,23 @@ class _Gen:
         pl = self.place(m.container)
         if pl == "reg":
             return f"r_{m.container}", t
+        if depth == 0 and m.container in self.stencil:
+            self.spec.checks.append((m.container, m.subset, env))
+            offs = self._stencil_offsets(m, env)
+            key = (m.container, offs)
+            hit = self.cse.get(key)
+            if hit is None:
+                st = self.stencil[m.container]
+                hit = self.fresh("sm")
+                slot = f"((it + {offs[0] - st['min'][0]}) % SDEPTH)"
+                if len(offs) == 3:
+                    ix = (f"[{slot}][threadIdx.y + {offs[1] - st['min'][1]}]"
+                          f"[threadIdx.x + 32 * v + {offs[2] - st['min'][2]}]")
+                else:
+                    ix = f"[{slot}][threadIdx.x + 256 * v + {offs[1] - st['min'][1]}]"
+                self.emit(f"const {CT[c.dtype]} {hit} = sm_{m.container}{ix};")
+                self.cse[key] = hit
+            return hit, t
         idx = [symexpr.to_c(b, self.name_of(env)) for b, _, _ in m.subset]
         off = self.offset(m.container, idx)
         p = self.ptr(m.container)
@@ -355,15 +520,25 @@ class _Gen:
                 prev = self.const_ranges[-2]
                 if last is not None and prev is not None and last[2] >= 16 and prev[2] >= 4:
                     mode = "tile2"
+        if (mode in ("tile2", "flat") and k in (2, 3) and STENCIL_MODE
+                and all(r is not None and r[1] == 1 for r in self.const_ranges)
+                and all(r[2] >= 8 for r in self.const_ranges)):
+            self.stencil = self._stencil_analysis()
+            if self.stencil:
+                mode = "stencil"
         spec.mode = mode
         vec = 1
         if mode == "tile2":
             vec = _pick_vec(self.const_ranges[-1][2])
+        elif mode == "stencil":
+            vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
+                (2 if self.const_ranges[-1][2] >= 1024 else 1)
         elif mode == "flat" and k == 1 and self.const_ranges[0] is not None:
             vec = 4 if self.const_ranges[0][2] >= 4 * 256 * 148 else 1
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1)}[mode]
+                      "tile2": (32, 8, 1),
+                      "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
         self.written = set()
@@ -473,6 +648,8 @@ class _Gen:
             loop += shift(body, -2)
             loop.append("  }")
             loop.append("  }")
+        elif mode == "stencil":
+            loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
         else:  # tile2
             x, y = k - 1, k - 2
             tw = 32 * vec
@@ -629,6 +806,10 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (256, 1, 1)
     k = len(rl)
+    if spec.mode == "stencil":
+        tk = (32 if k == 3 else 256) * spec.vec
+        nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
+        return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
     tw = 32 * spec.vec
     tiles = ((rl[k - 1] + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:

@@ -112,17 +112,30 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
 #endif
 }
 
-// out[n] (wcr)= sum over G row-groups of ws[g][n]  (+ per-tile dot partials)
+// out[n] (wcr)= sum over G row-groups of ws[g][n]  (+ per-tile dot partials).
+// Block 32 x 8: 32 columns per block, the 8 thread rows split the G partials
+// (strided), then thread row 0 adds the 8 sums in a fixed order.
 extern "C" __global__ void __launch_bounds__(256) RP_FIN_NAME(const __grid_constant__ RpArgs a) {
-  const b2_ll i = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ double part[8][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const b2_ll i = (b2_ll)blockIdx.x * 32 + tx;
 #if RP_AXPY
-  if (i < RP_N) {
+  {
     const double *ws = (const double *)a.w[1];
     double s = 0.0;
-    for (int g = 0; g < RP_G; ++g) s += ws[(b2_ll)g * RP_N + i];
-    rp_store_axpy(a, i, s);
+    if (i < RP_N)
+      for (int g = ty; g < RP_G; g += 8) s += ws[(b2_ll)g * RP_N + i];
+    part[ty][tx] = s;
+    __syncthreads();
+    if (ty == 0 && i < RP_N) {
+      double t = part[0][tx];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t += part[k][tx];
+      rp_store_axpy(a, i, t);
+    }
   }
 #endif
+  if (ty != 0) return;
 #if RP_DOT && RP_CTILES > 1
   if (i < RP_M) {
     const double *wd = (const double *)a.w[2];
