@@ -32,6 +32,7 @@ TC = {"f64": "f", "i64": "i", "i32": "i", "bool": "b"}
 MAX_BLOCKS = 148 * 16
 STENCIL_MODE = True  # shared-memory plane ring for constant-offset reads
 STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
+STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
 
 
 class KernelSpec:
@@ -93,7 +94,8 @@ class _Gen:
         maxs = [max(st["max"][d] for st in self.stencil.values()) for d in range(k)]
         for st in self.stencil.values():
             st["min"], st["max"] = tuple(mins), tuple(maxs)
-        depth = maxs[0] - mins[0] + 1
+        pref = STENCIL_PREFETCH
+        depth = maxs[0] - mins[0] + 1 + pref
         sk = tk + maxs[-1] - mins[-1]
         sj = 8 + maxs[1] - mins[1] if k == 3 else 1
         L.append(f"  constexpr int SDEPTH = {depth}, SCH = {STENCIL_CHUNK}, TK = {tk};")
@@ -131,8 +133,9 @@ class _Gen:
                 L.append(f"        const b2_ll g2 = rb2 + kx0 + ({mins[2]}) + kk;")
                 L.append(f"        const bool ok = ok0 && g1 >= 0 && g1 < {shp[1]}LL && g2 >= 0 && "
                          f"g2 < {shp[2]}LL;")
-                L.append(f"        sm_{c}[slot][jj][kk] = ok ? c_{c}[g0 * st_{c}_0 + g1 * st_{c}_1 + "
-                         f"g2] : ({ct})0;")
+                L.append(f"        b2_cp_async<sizeof({ct})>(&sm_{c}[slot][jj][kk], ok ? "
+                         f"(const void *)(c_{c} + g0 * st_{c}_0 + g1 * st_{c}_1 + g2) : "
+                         f"(const void *)c_{c}, ok);")
             else:
                 L.append(f"        const int kk = e;")
                 L.append(f"        const b2_ll g1 = rb1 + kx0 + ({mins[1]}) + kk;")
@@ -140,11 +143,22 @@ class _Gen:
                 L.append(f"        sm_{c}[slot][kk] = ok ? c_{c}[g0 * st_{c}_0 + g1] : ({ct})0;")
             L.append("      }")
             L.append("    };")
+        # cp.async pipeline: planes [min0, max0 + PREF) in flight before the
+        # march; each iteration issues plane it + max0 + PREF and waits for
+        # plane it + max0 (one commit group per plane)
+        L.append(f"    for (int d = {mins[0]}; d < {maxs[0] + pref}; ++d) {{")
         for c in self.stencil:
-            L.append(f"    for (int d = {mins[0]}; d < {maxs[0]}; ++d) load_{c}(i0 + d, d - ({mins[0]}));")
+            L.append(f"      if (d - ({maxs[0]}) < nit) load_{c}(i0 + d, d - ({mins[0]}));")
+        L.append("      b2_cp_commit();")
+        L.append("    }")
         L.append("    for (b2_ll it = 0; it < nit; ++it) {")
+        L.append(f"      if (it + {pref} < nit) {{")
         for c in self.stencil:
-            L.append(f"      load_{c}(i0 + it + ({maxs[0]}), (int)((it + {maxs[0] - mins[0]}) % SDEPTH));")
+            L.append(f"        load_{c}(i0 + it + ({maxs[0] + pref}), "
+                     f"(int)((it + {maxs[0] - mins[0] + pref}) % SDEPTH));")
+        L.append("      }")
+        L.append("      b2_cp_commit();")
+        L.append(f"      b2_cp_wait<{pref}>();")
         L.append("      __syncthreads();")
         L.append(f"      const b2_ll p_{grp.params[0]} = rb0 + i0 + it;")
         inner = "      "
@@ -520,7 +534,7 @@ class _Gen:
                 prev = self.const_ranges[-2]
                 if last is not None and prev is not None and last[2] >= 16 and prev[2] >= 4:
                     mode = "tile2"
-        if (mode in ("tile2", "flat") and k in (2, 3) and STENCIL_MODE
+        if (mode in ("tile2", "flat") and k == 3 and STENCIL_MODE
                 and all(r is not None and r[1] == 1 for r in self.const_ranges)
                 and all(r[2] >= 8 for r in self.const_ranges)):
             self.stencil = self._stencil_analysis()

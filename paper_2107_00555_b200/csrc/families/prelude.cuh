@@ -158,6 +158,21 @@ __device__ __forceinline__ double b2_warp_sum(double v) {
   return v;
 }
 
+// ---- asynchronous global -> shared copies (LDGSTS), zero-fill when !valid ----
+template <int BYTES>
+__device__ __forceinline__ void b2_cp_async(void *smem, const void *gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? BYTES : 0;
+  if (BYTES == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+                 "n"(BYTES), "r"(n));
+}
+__device__ __forceinline__ void b2_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void b2_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 // Device-side bounds guard for accesses the host cannot check statically
 // (memlets inside nested scopes): records the first violation.
 __device__ __forceinline__ bool b2_oob(b2_ll off, b2_ll size, int site, int *flag) {

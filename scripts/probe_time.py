@@ -31,3 +31,6 @@ for r in range(reps):
     rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(ms)))
     print(f"rep {r}: device {ms.value:.3f} ms  wall {1e3*(time.time()-t):.1f} ms  launches={ex.launches}", flush=True)
 ex.check_flag()
+prof = ex.profile_launches()
+for k, (n, tot, npts) in sorted(prof.items(), key=lambda kv: -kv[1][1]):
+    print(f"  kernel {k}: {n} launches, {tot/n*1e3:.1f} us avg, {tot:.3f} ms total")
