@@ -21,6 +21,7 @@ Thread mappings (chosen at plan time):
 
 from __future__ import annotations
 
+import os
 import struct
 
 from . import plan as P
@@ -540,6 +541,12 @@ class _Gen:
             self.stencil = self._stencil_analysis()
             if self.stencil:
                 mode = "stencil"
+        force = os.environ.get("B2_FORCE_MODE")  # tuning knob: flat | tile2 | stencil
+        if force and mode in ("flat", "tile2", "stencil") and k >= 1:
+            if force == "stencil" and not self.stencil:
+                pass
+            elif force != "tile2" or k >= 2:
+                mode = force
         spec.mode = mode
         vec = 1
         if mode == "tile2":
@@ -547,8 +554,13 @@ class _Gen:
         elif mode == "stencil":
             vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
                 (2 if self.const_ranges[-1][2] >= 1024 else 1)
-        elif mode == "flat" and k == 1 and self.const_ranges[0] is not None:
-            vec = 4 if self.const_ranges[0][2] >= 4 * 256 * 148 else 1
+        elif mode == "flat" and all(r is not None for r in self.const_ranges):
+            total = 1
+            for r in self.const_ranges:
+                total *= r[2]
+            vec = 4 if total >= 4 * 256 * 148 else 1
+        if os.environ.get("B2_VEC"):
+            vec = int(os.environ["B2_VEC"])
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, 8, 1),
