@@ -24,7 +24,7 @@ from __future__ import annotations
 import os
 import struct
 
-from . import plan as P
+from . import plan as P  # noqa: E402
 from . import scalar, sdfg, symexpr
 
 CT = {"f64": "double", "i64": "b2_ll", "i32": "int", "bool": "bool"}
@@ -34,6 +34,7 @@ MAX_BLOCKS = 148 * 16
 STENCIL_MODE = True  # shared-memory plane ring for constant-offset reads
 STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
+HOIST_LOADS = os.environ.get("B2_HOIST", "1") != "0"  # batch read-only loads per thread
 
 
 class KernelSpec:
@@ -332,7 +333,11 @@ class _Gen:
             hit = self.cse.get(key)
             if hit is None:
                 hit = self.fresh("ld")
-                self.emit(f"const {CT[c.dtype]} {hit} = {p}[{off}];")
+                if self.hoist:
+                    self.hoisted.append((hit, CT[c.dtype], f"{p}[{off}]"))
+                    hit = f"{hit}[v]"
+                else:
+                    self.emit(f"const {CT[c.dtype]} {hit} = {p}[{off}];")
                 self.cse[key] = hit
             return hit, t
         return f"{p}[{off}]", t
@@ -545,12 +550,18 @@ class _Gen:
         if force and mode in ("flat", "tile2", "stencil") and k >= 1:
             if force == "stencil" and not self.stencil:
                 pass
+            elif force == "march" and (k < 3 or any(r is None for r in self.const_ranges)):
+                pass
             elif force != "tile2" or k >= 2:
                 mode = force
+        if mode != "stencil":
+            self.stencil = {}
         spec.mode = mode
         vec = 1
         if mode == "tile2":
             vec = _pick_vec(self.const_ranges[-1][2])
+        elif mode == "march":
+            vec = 8
         elif mode == "stencil":
             vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
                 (2 if self.const_ranges[-1][2] >= 1024 else 1)
@@ -563,7 +574,7 @@ class _Gen:
             vec = int(os.environ["B2_VEC"])
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1),
+                      "tile2": (32, 8, 1), "march": (32, 8, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -573,6 +584,10 @@ class _Gen:
                 if a[1]:
                     self.written.add(a[0])
         self.cse = {}
+        # batch the read-only loads of all `vec` points of a thread ahead of
+        # their arithmetic: memory-level parallelism without extra warps
+        self.hoist = mode in ("flat", "tile2", "march") and vec > 1 and HOIST_LOADS
+        self.hoisted = []
 
         env = {p: f"p_{p}" for p in grp.params}
         body_lines_start = len(self.lines)
@@ -653,30 +668,46 @@ class _Gen:
             for _ in grp.params:
                 loop.append("  }")
             loop.append("  }")
-        elif mode == "flat":
+        def vloop(header: list) -> list:
+            """Per-thread loop over its `vec` points: phase 1 issues every
+            hoisted read-only load of every point, phase 2 does the math."""
+            out: list[str] = []
+            if self.hoisted:
+                for name, ct, _ in self.hoisted:
+                    out.append(f"    {ct} {name}[{vec}];")
+                out.append("#pragma unroll")
+                out.append(f"    for (int v = 0; v < {vec}; ++v) {{")
+                out += header
+                for name, _, expr in self.hoisted:
+                    out.append(f"    {name}[v] = {expr};")
+                out.append("    }")
+            out.append("#pragma unroll")
+            out.append(f"    for (int v = 0; v < {vec}; ++v) {{")
+            out += header
+            out += reg_decls(4)
+            out += shift(body, -2)
+            out.append("    }")
+            return out
+
+        if mode == "flat":
             tot = " * ".join(f"rl{i}" for i in range(k))
             loop.append(f"  const b2_ll total = {tot};")
             loop.append(f"  for (b2_ll f0 = (b2_ll)blockIdx.x * blockDim.x * {vec}; f0 < total; "
                         f"f0 += (b2_ll)gridDim.x * blockDim.x * {vec}) {{")
-            loop.append("#pragma unroll")
-            loop.append(f"  for (int v = 0; v < {vec}; ++v) {{")
-            loop.append("    const b2_ll f = f0 + (b2_ll)v * blockDim.x + threadIdx.x;")
-            loop.append("    if (f >= total) break;")
-            loop.append("    b2_ll rem = f;")
+            hdr = ["    const b2_ll f = f0 + (b2_ll)v * blockDim.x + threadIdx.x;",
+                   "    if (f >= total) break;", "    b2_ll rem = f;"]
             for i in reversed(range(k)):
                 p = grp.params[i]
                 if i > 0:
-                    loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
+                    hdr.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
                 else:
-                    loop.append(f"    const b2_ll i{i} = rem;")
-                loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
-            loop += reg_decls(4)
-            loop += shift(body, -2)
-            loop.append("  }")
+                    hdr.append(f"    const b2_ll i{i} = rem;")
+                hdr.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
+            loop += vloop(hdr)
             loop.append("  }")
         elif mode == "stencil":
             loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
-        else:  # tile2
+        elif mode == "tile2":
             x, y = k - 1, k - 2
             tw = 32 * vec
             loop.append(f"  constexpr b2_ll tiles_x = (rl{x} + {tw - 1}) / {tw};")
@@ -693,15 +724,38 @@ class _Gen:
                     loop.append(f"    const b2_ll i{i} = rem;")
             loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
             loop.append(f"    if (i{y} >= rl{y}) continue;")
-            loop.append("#pragma unroll")
-            loop.append(f"    for (int v = 0; v < {vec}; ++v) {{")
-            loop.append(f"    const b2_ll i{x} = tx * {tw} + v * 32 + threadIdx.x;")
-            loop.append(f"    if (i{x} >= rl{x}) break;")
+            hdr = [f"    const b2_ll i{x} = tx * {tw} + v * 32 + threadIdx.x;",
+                   f"    if (i{x} >= rl{x}) break;"]
             for i, p in enumerate(grp.params):
-                loop.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
-            loop += reg_decls(4)
-            loop += shift(body, -2)
-            loop.append("    }")
+                hdr.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
+            loop += vloop(hdr)
+            loop.append("  }")
+        elif mode == "march":
+            # 32 x 8 tiles over dims (k-2, k-1); each thread walks `vec`
+            # consecutive indices of dim 0 (unrolled) so the compiler reuses the
+            # overlapping dim-0 neighbours of a stencil from registers
+            x, y = k - 1, k - 2
+            loop.append(f"  constexpr b2_ll tiles_x = (rl{x} + 31) / 32;")
+            loop.append(f"  constexpr b2_ll tiles_y = (rl{y} + 7) / 8;")
+            loop.append(f"  constexpr b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
+            mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
+            loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({mid}) * tiles_z;")
+            # dim-0 chunk varies fastest: CTAs sharing a chunk-boundary plane run
+            # back to back, so that plane is an L2 hit for the second one
+            loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
+            loop.append("    const b2_ll tz = vb % tiles_z; b2_ll rem = vb / tiles_z;")
+            loop.append("    const b2_ll tx = rem % tiles_x; rem /= tiles_x;")
+            loop.append("    const b2_ll ty = rem % tiles_y; rem /= tiles_y;")
+            for i in reversed(range(1, k - 2)):
+                loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
+            loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
+            loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
+            loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
+            for i in range(1, k):
+                loop.append(f"    const b2_ll p_{grp.params[i]} = rb{i} + rs{i} * i{i};")
+            hdr = [f"    const b2_ll i0 = tz * {vec} + v;", "    if (i0 >= rl0) break;",
+                   f"    const b2_ll p_{grp.params[0]} = rb0 + rs0 * i0;"]
+            loop += vloop(hdr)
             loop.append("  }")
         src = [f"// generated by paper_2107_00555_b200.codegen for state "
                f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
@@ -836,6 +890,14 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         tk = (32 if k == 3 else 256) * spec.vec
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
         return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
+    if spec.mode == "march":
+        nvb = -(-rl[k - 1] // 32) * -(-rl[k - 2] // 8) * -(-rl[0] // spec.vec)
+        for v in rl[1: k - 2]:
+            nvb *= v
+        blocks = max(1, min(nvb, MAX_BLOCKS * 8))
+        if spec.private:
+            blocks = max(1, min(blocks, MAX_BLOCKS))
+        return (blocks, 1, 1), (32, 8, 1)
     tw = 32 * spec.vec
     tiles = ((rl[k - 1] + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:
