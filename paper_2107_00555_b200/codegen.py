@@ -31,10 +31,10 @@ CT = {"f64": "double", "i64": "b2_ll", "i32": "int", "bool": "bool"}
 TC = {"f64": "f", "i64": "i", "i32": "i", "bool": "b"}
 
 MAX_BLOCKS = 148 * 16
-STENCIL_MODE = True  # shared-memory plane ring for constant-offset reads
+STENCIL_MODE = os.environ.get("B2_STENCIL", "0") == "1"  # smem plane ring (slower on B200: off)
 STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
-HOIST_LOADS = os.environ.get("B2_HOIST", "1") != "0"  # batch read-only loads per thread
+HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (slower: off)
 
 
 class KernelSpec:
@@ -540,7 +540,10 @@ class _Gen:
                 prev = self.const_ranges[-2]
                 if last is not None and prev is not None and last[2] >= 16 and prev[2] >= 4:
                     mode = "tile2"
-        if (mode in ("tile2", "flat") and k == 3 and STENCIL_MODE
+            if (mode == "tile2" and k == 3 and self.const_ranges[0] is not None
+                    and self.const_ranges[0][2] >= 16):
+                mode = "march"  # measured best for 3-D sweeps (heat_3d: 207 us vs 247 tile2)
+        if (mode in ("tile2", "flat", "march") and k == 3 and STENCIL_MODE
                 and all(r is not None and r[1] == 1 for r in self.const_ranges)
                 and all(r[2] >= 8 for r in self.const_ranges)):
             self.stencil = self._stencil_analysis()
@@ -740,14 +743,13 @@ class _Gen:
             loop.append(f"  constexpr b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
             mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({mid}) * tiles_z;")
-            # dim-0 chunk varies fastest: CTAs sharing a chunk-boundary plane run
-            # back to back, so that plane is an L2 hit for the second one
+            # plane tiles vary fastest (measured better than chunk-fastest order)
             loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
-            loop.append("    const b2_ll tz = vb % tiles_z; b2_ll rem = vb / tiles_z;")
-            loop.append("    const b2_ll tx = rem % tiles_x; rem /= tiles_x;")
+            loop.append("    const b2_ll tx = vb % tiles_x; b2_ll rem = vb / tiles_x;")
             loop.append("    const b2_ll ty = rem % tiles_y; rem /= tiles_y;")
             for i in reversed(range(1, k - 2)):
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
+            loop.append("    const b2_ll tz = rem;")
             loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
             loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
             loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
