@@ -150,3 +150,68 @@ def jacobi_2d_c(A, B, TSTEPS, threads=0):
     assert A.flags.c_contiguous and B.flags.c_contiguous and A.dtype == np.float64
     c_lib().oracle_jacobi_2d(A.ctypes.data, B.ctypes.data, A.shape[0], TSTEPS, threads)
     return {"A": A, "B": B}
+
+
+def conv2d_bias(inp, w, bias, out):
+    """programs/conv2d_bias.dpy: per output element the 7-D map accumulates
+    over (ki, kj, ci) in lexicographic order after the bias init."""
+    NB, H, W_, CI = inp.shape
+    K = w.shape[0]
+    HO, WO = out.shape[1], out.shape[2]
+    out[...] = bias[None, None, None, :]
+    for ki in range(K):
+        for kj in range(K):
+            for ci in range(CI):
+                out += inp[:, ki:ki + HO, kj:kj + WO, ci, None] * w[ki, kj, ci, :]
+    return {"out": out}
+
+
+def _get_acc(pos, mass, acc, G, softening):
+    acc[...] = 0.0
+    N = pos.shape[0]
+    for j in range(N):  # lexicographic (i, j): per i the WCR sum runs over j in order
+        dx = pos[j, 0] - pos[:, 0]
+        dy = pos[j, 1] - pos[:, 1]
+        dz = pos[j, 2] - pos[:, 2]
+        inv = np.power(dx * dx + dy * dy + dz * dz + softening * softening, -1.5)
+        acc[:, 0] += G * (dx * inv) * mass[j]
+        acc[:, 1] += G * (dy * inv) * mass[j]
+        acc[:, 2] += G * (dz * inv) * mass[j]
+
+
+def nbody(mass, pos, vel, acc, E, G, softening, dt, NT):
+    """programs/nbody.dpy (NPBench nbody, leapfrog + energies)."""
+    _get_acc(pos, mass, acc, G, softening)
+    for _t in range(NT):
+        vel[:] = vel + acc * (dt / 2.0)
+        pos[:] = pos + vel * dt
+        _get_acc(pos, mass, acc, G, softening)
+        vel[:] = vel + acc * (dt / 2.0)
+    N = pos.shape[0]
+    E[0] = 0.0
+    E[1] = 0.0
+    for i in range(N):
+        E[0] += 0.5 * mass[i] * (vel[i, 0] * vel[i, 0] + vel[i, 1] * vel[i, 1] + vel[i, 2] * vel[i, 2])
+    for i in range(N):
+        dx = pos[:, 0] - pos[i, 0]
+        dy = pos[:, 1] - pos[i, 1]
+        dz = pos[:, 2] - pos[i, 2]
+        jj = np.arange(N)
+        term = -(G * mass[i] * mass) * (i < jj) / np.sqrt(dx * dx + dy * dy + dz * dz + (i == jj))
+        for j in range(N):
+            E[1] += term[j]
+    return {"mass": mass, "pos": pos, "vel": vel, "acc": acc, "E": E}
+
+
+def softmax(x, out):
+    """programs/softmax.dpy: row max by a sequential scan, exp(x - max), row
+    sum by WCR in l order, divide."""
+    mx = x[..., 0].copy()
+    for l in range(1, x.shape[-1]):
+        mx = np.maximum(mx, x[..., l]) if False else np.where(x[..., l] > mx, x[..., l], mx)
+    ex = np.exp(x - mx[..., None])
+    sm = np.zeros(x.shape[:-1])
+    for l in range(x.shape[-1]):
+        sm = sm + ex[..., l]
+    out[...] = ex / sm[..., None]
+    return {"out": out}

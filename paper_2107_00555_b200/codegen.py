@@ -81,6 +81,8 @@ class _Gen:
         self.written: set = set()
         self.cse: dict = {}
         self.stencil: dict = {}
+        self.hoist = False
+        self.hoisted: list = []
 
     def _stencil_loop(self, k: int, vec: int, reg_decls, body: list) -> list:
         """Stencil mode: each CTA owns a (8 x 32*vec) tile of the two inner

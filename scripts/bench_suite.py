@@ -1,0 +1,179 @@
+"""Every BASELINE.json config on one B200: device time per program run (CUDA
+graph replay, inputs resident), dominant kernel and its roofline fraction,
+and the reference CPU path (numpy port of evaluate_program) on a bounded
+sample.  Writes profiles/bench_suite.json.  (bench.py is the driver's single
+headline line; this is the per-config table the DESIGN/profiles cite.)
+
+    python scripts/bench_suite.py [--only name,...] [--reps 5]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import pathlib
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from bench import ClockSampler, make_inputs, peaks  # noqa: E402
+
+
+def _b(*shapes):
+    return 8 * sum(int(np.prod(s)) for s in shapes)
+
+
+# name: graph, symbols, bound, algorithmic work per run (bytes or flop), unit
+SUITE = {
+    "jacobi_2d": ("jacobi_2d.raw", {"N": 2000, "TSTEPS": 100}, "hbm",
+                  198 * (8 * 2000 ** 2 + 8 * 1998 ** 2), "B"),
+    "gemver": ("gemver.raw", {"N": 8000}, "hbm", 24 * 8000 ** 2 + 10 * 8 * 8000, "B"),
+    "atax": ("atax.raw", {"M": 8000, "N": 8000}, "hbm", 8 * 8000 ** 2 + 3 * 8 * 8000, "B"),
+    "bicg": ("bicg.raw", {"N": 8000, "M": 8000}, "hbm", 8 * 8000 ** 2 + 4 * 8 * 8000, "B"),
+    "heat_3d": ("heat_3d.raw", {"N": 400, "TSTEPS": 100}, "hbm",
+                198 * (8 * 400 ** 3 + 8 * 398 ** 3), "B"),
+    "matmul_f64": ("matmul.raw", {"M": 16384, "K": 16384, "N": 16384}, "fp64",
+                   2 * 16384 ** 3, "flop"),
+    "go_fast": ("go_fast.raw", {"N": 12000}, "hbm", 16 * 12000 ** 2, "B"),
+    "azimint_naive": ("azimint_naive.raw", {"N": 1000000, "NPT": 1000}, "compute",
+                      1000000 * 1000, "pairs"),
+    "conv2d_bias": ("conv2d_bias.raw", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16, "K": 20,
+                                        "HO": 237, "WO": 237}, "fp64",
+                    2 * 8 * 237 * 237 * 16 * 20 * 20 * 3, "flop"),
+    "nbody": ("nbody.raw", {"N": 100, "NT": 1000}, "launch", 1000, "steps"),
+}
+
+
+def cpu_port(name, syms, inputs):
+    """Bounded sample of the reference CPU path; returns (work/s, seconds, desc)."""
+    from oracle import kernels_np as K
+
+    x = {k: (np.array(v, copy=True) if np.ndim(v) else float(v)) for k, v in inputs.items()}
+    t = time.perf_counter()
+    if name == "jacobi_2d":
+        K.jacobi_2d(x["A"], x["B"], 3)
+        work, desc = 4 * (8 * 2000 ** 2 + 8 * 1998 ** 2), "2 iterations (4 sweeps)"
+    elif name == "heat_3d":
+        K.heat_3d_sweeps(x["A"], x["B"], 2)
+        work, desc = 2 * (8 * 400 ** 3 + 8 * 398 ** 3), "2 sweeps"
+    elif name in ("gemver", "atax", "bicg"):
+        fn = getattr(K, name)
+        import inspect
+        args = [x[p] for p in inspect.signature(fn).parameters]
+        fn(*args)
+        work, desc = SUITE[name][3], "full run (OpenBLAS GEMV + numpy)"
+    elif name == "matmul_f64":
+        n = 4096
+        A = np.ascontiguousarray(x["A"][:n, :n])
+        B = np.ascontiguousarray(x["B"][:n, :n])
+        t = time.perf_counter()
+        A @ B
+        work, desc = 2 * n ** 3, "4096^3 sub-problem (OpenBLAS dgemm)"
+    elif name == "go_fast":
+        K.go_fast(x["a"], x["out"])
+        work, desc = SUITE[name][3], "full run"
+    elif name == "conv2d_bias":
+        sl = slice(0, 1)
+        K.conv2d_bias(x["inp"][sl], x["w"], x["bias"], x["out"][sl])
+        work, desc = SUITE[name][3] // 8, "1 of 8 images"
+    elif name == "azimint_naive":
+        n = 20000
+        K.azimint_naive(x["rmax"], x["data"][:n], x["radius"][:n], x["res"])
+        work, desc = n * 1000, f"{n} of 1e6 samples"
+    elif name == "nbody":
+        K.nbody(x["mass"], x["pos"], x["vel"], x["acc"], x["E"], x["G"], x["softening"],
+                x["dt"], 10)
+        work, desc = 10, "10 of 1000 steps"
+    else:
+        return None
+    dt = time.perf_counter() - t
+    return work / dt, dt, desc
+
+
+def run_one(name, reps):
+    from paper_2107_00555_b200 import runtime as rt, sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    gname, syms, bound, work, unit = SUITE[name]
+    g = sdfg.load(ROOT / "tests" / "golden" / "graphs" / f"{gname}.json")
+    inputs = make_inputs(g, syms)
+    if name == "nbody":
+        inputs["dt"] = np.float64(0.01)
+        inputs["softening"] = np.float64(0.1)
+    t0 = time.time()
+    ex = GpuExecutor(g, syms)
+    plan_s = time.time() - t0
+    ex.prepare_inputs(inputs)
+    ex.sync()
+    L = rt.lib()
+    ex.run_device(first_call=True)
+    ex.sync()
+    e0, e1 = ctypes.c_void_p(), ctypes.c_void_p()
+    L.b2_event_create(ctypes.byref(e0))
+    L.b2_event_create(ctypes.byref(e1))
+    times = []
+    with ClockSampler() as clk:
+        for _ in range(reps):
+            L.b2_event_record(e0, ex.stream)
+            ex.run_device(first_call=False)
+            L.b2_event_record(e1, ex.stream)
+            ms = ctypes.c_float()
+            rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(ms)))
+            times.append(ms.value)
+    ex.check_flag()
+    ms = float(np.median(times))
+    prof = ex.profile_launches()
+    top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else (None, (0, 0.0, 0))
+    hbm, _ = peaks()
+    rate = work / (ms / 1e3)
+    res = {"graph": gname, "symbols": syms, "ms_per_run": ms, "work": work, "work_unit": unit,
+           "rate": rate, "bound": bound, "plan_compile_s": plan_s,
+           "launches_per_run": getattr(ex, "trace_launches", None),
+           "top_kernel": top[0], "top_kernel_ms_total": top[1][1],
+           "top_kernel_launches": top[1][0],
+           "kernels": {k: {"launches": n, "ms_total": tot} for k, (n, tot, _) in prof.items()},
+           "clocks": clk.summary()}
+    if bound == "hbm":
+        res["GBps"] = rate / 1e9
+        res["frac_of_measured_hbm"] = rate / 1e9 / hbm
+    elif unit == "flop":
+        res["TFLOPs"] = rate / 1e12
+    cpu = cpu_port(name, syms, inputs)
+    if cpu is not None:
+        res["cpu_port"] = {"rate": cpu[0], "seconds": cpu[1], "sample": cpu[2], "cores": 1,
+                           "kind": "port (numpy evaluate_program restatement)"}
+        res["speedup_vs_cpu_port"] = rate / cpu[0]
+    ex.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "bench_suite.json"))
+    args = ap.parse_args()
+    names = [n for n in SUITE if not args.only or n in args.only.split(",")]
+    out_p = pathlib.Path(args.out)
+    results = json.loads(out_p.read_text()) if out_p.exists() else {}
+    for n in names:
+        try:
+            results[n] = run_one(n, args.reps)
+            r = results[n]
+            extra = f"{r.get('GBps', 0):.0f} GB/s ({r.get('frac_of_measured_hbm', 0):.2f})" \
+                if "GBps" in r else f"{r['rate']:.3e} {r['work_unit']}/s"
+            print(f"{n:14s} {r['ms_per_run']:9.3f} ms  {extra}  top={r['top_kernel']}", flush=True)
+        except Exception as ex:  # noqa: BLE001
+            results[n] = {"error": f"{type(ex).__name__}: {ex}"[:2000]}
+            print(f"{n:14s} ERROR {results[n]['error'][:300]}", flush=True)
+    out_p.parent.mkdir(exist_ok=True)
+    out_p.write_text(json.dumps(results, indent=1) + "\n")
+
+
+if __name__ == "__main__":
+    main()

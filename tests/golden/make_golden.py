@@ -71,11 +71,13 @@ SIZES = {
     "conv2d_bias": [{"NB": 2, "H": 6, "W": 6, "CI": 2, "CO": 3, "K": 3, "HO": 4, "WO": 4},
                     {"NB": 1, "H": 9, "W": 8, "CI": 3, "CO": 5, "K": 2, "HO": 8, "WO": 7}],
     "nbody": [{"N": 5, "NT": 2}, {"N": 9, "NT": 1}],
+    "matmul": [{"M": 4, "K": 6, "N": 5}, {"M": 67, "K": 45, "N": 129}],
 }
 ONLY = sys.argv[1:]
 CORPUS = ["adi", "atax", "bicg", "doitgen", "fig4_loop", "gemm", "gemver", "gesummv",
           "jacobi_1d", "jacobi_2d", "k2mm", "k3mm", "mvt", "wcr_sum"]
-REPO_PROGRAMS = ["heat_3d", "go_fast", "softmax", "azimint_naive", "conv2d_bias", "nbody"]
+REPO_PROGRAMS = ["heat_3d", "go_fast", "softmax", "azimint_naive", "conv2d_bias", "nbody",
+                 "matmul"]
 SEEDS = (0, 1)
 
 

@@ -188,3 +188,27 @@ def test_no_gpu_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(rt.BackendUnavailable):
         rt.device(0)
+
+
+def test_rowpass_fusions_plan_and_compile():
+    """gemver / atax / bicg fold their MATMUL nodes (and gemver's A-update
+    map) into single rowpass passes that compile for sm_100a."""
+    from paper_2107_00555_b200 import plan as P, runtime as rt, sdfg
+
+    rt.load_library()
+    want = {"gemver.raw": ["axpy+pro", "dot"], "atax.raw": ["dot,axpy+coefdot"],
+            "bicg.raw": ["axpy,dot"]}
+    for name, kinds in want.items():
+        g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+        syms = {"gemver.raw": {"N": 8000}, "atax.raw": {"M": 8000, "N": 8000},
+                "bicg.raw": {"N": 8000, "M": 8000}}[name]
+        pl = P.Planner(g, syms).build()
+        got = []
+        for op in pl.all_ops:
+            if isinstance(op, P.LibOp) and op.rowpass is not None:
+                rp = op.rowpass
+                got.append(",".join(m.kind for m in rp.mvs) + ("+pro" if rp.prologue else "")
+                           + ("+coefdot" if rp.coef_from_dot else ""))
+                src = rp.source(pl.shapes(), f"{g.name}_{op.idx}")
+                assert rt.get_cubin(src, f"b2_rp_{g.name}_{op.idx}")[0]
+        assert got == kinds, (name, got)

@@ -52,3 +52,25 @@ def test_other_ports(name):
                 assert np.array_equal(v, ref, equal_nan=True), (name, k)
             else:  # BLAS: same library as the reference run here
                 assert np.allclose(v, ref, rtol=1e-13, atol=1e-13), (name, k)
+
+
+@pytest.mark.parametrize("name", ["conv2d_bias", "nbody", "softmax"])
+def test_sweep_ports(name):
+    fn = getattr(K, name)
+    ent = MANIFEST["kernels"][name]
+    for case in ent["cases"]:
+        d, x = load_case(case)
+        params = ent["params"]
+        args = []
+        for p in params:
+            if p in x:
+                args.append(x[p].copy() if x[p].ndim else float(x[p]))
+            else:
+                args.append(case["symbols"][p])
+        out = fn(*args)
+        for k, v in out.items():
+            ref = d["oracle/" + k]
+            if name in ("softmax", "nbody"):  # vectorised exp/pow vs scalar calls: <= 1 ulp
+                assert np.allclose(v, ref, rtol=1e-14, atol=0), (name, k)
+            else:
+                assert np.array_equal(v, ref, equal_nan=True), (name, k, np.abs(v - ref).max())
