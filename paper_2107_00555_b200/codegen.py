@@ -35,6 +35,7 @@ STENCIL_MODE = os.environ.get("B2_STENCIL", "0") == "1"  # smem plane ring (slow
 STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
 HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (slower: off)
+REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
 
 
 class KernelSpec:
@@ -83,6 +84,105 @@ class _Gen:
         self.stencil: dict = {}
         self.hoist = False
         self.hoisted: list = []
+        self.red = None  # reduction mode: target key -> accumulator info
+        self.red_targets: dict = {}
+        self.red_pout: list = []
+        self.red_full = False
+
+    def _wkey(self, m: sdfg.Memlet, env: dict):
+        rename = {mp: v[2:] for mp, v in env.items() if isinstance(v, str) and v.startswith("p_")}
+        keys = tuple(self.group.params) + tuple(sorted(self.pl.loopish))
+        return (m.container, tuple(P.canon(P.rn(b, rename), keys, self.pl.fixed)
+                                   for b, _, _ in m.subset))
+
+    def _reduction_plan(self):
+        """Reduction schedule for a parallel map whose only HBM writes are WCR
+        commits (ir.py:72-91) that do not depend on some parameters R: each
+        thread owns a point of the other parameters and runs R sequentially in
+        a register accumulator (lexicographic order, bitwise equal to the
+        reference when it owns the whole reduction), committing once."""
+        grp = self.group
+        if grp.schedule != "parallel" or not grp.params:
+            return None
+        if any(r is None for r in self.const_ranges):
+            return None
+        targets: dict = {}
+        deps_all: set = set()
+        reads: set = set()
+        for mem in grp.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if not w:
+                    reads.add(c)
+                    continue
+                if self.place(c) == "reg":
+                    continue
+                if wcr is None or depth != 0 or pt is None or self.place(c) != "memory":
+                    return None
+                deps = {p for key in pt for (p, _) in key[1]}
+                targets[(c, pt)] = (wcr, deps)
+                deps_all |= deps
+        if not targets or reads & {c for (c, _) in targets}:
+            return None
+        R = [p for p in grp.params if p not in deps_all]
+        if not R:
+            return None
+        pout = [p for p in grp.params if p in deps_all]
+        return R, pout, targets
+
+    def _reduce_loop(self, R, pout, reg_decls, body) -> list:
+        grp = self.group
+        idx = {p: i for i, p in enumerate(grp.params)}
+        nout = 1
+        for p in pout:
+            nout *= self.const_ranges[idx[p]][2]
+        nred = 1
+        for p in R:
+            nred *= self.const_ranges[idx[p]][2]
+        full = self.red_full
+        C = 1 if full else max(1, min(-(-148 * 512 // max(1, nout)), -(-nred // 16)))
+        self.spec.red_threads = nout * C
+        L = [f"  constexpr b2_ll NOUT = {nout}LL, NRED = {nred}LL, NCH = {C}LL;",
+             "  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUT * NCH; "
+             "f += (b2_ll)gridDim.x * blockDim.x) {",
+             "    b2_ll rem = f % NOUT;", "    const b2_ll ch = f / NOUT; (void)ch;"]
+        for p in reversed(pout):
+            i = idx[p]
+            L.append(f"    const b2_ll q{i} = rem % rl{i}; rem /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * q{i};")
+        for t in self.red.values():
+            a, ct = t["acc"], t["ct"]
+            if full and t["exclusive"]:
+                L.append(f"    {ct} {a} = {t['target']};")
+            else:
+                L.append(f"    {ct} {a} = ({ct})0; bool have_{a} = false;")
+        if full:
+            for p in R:
+                i = idx[p]
+                L.append(f"    for (b2_ll j{i} = 0; j{i} < rl{i}; ++j{i}) {{")
+                L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
+        else:
+            L.append("    const b2_ll lo = ch * NRED / NCH, hi = (ch + 1) * NRED / NCH;")
+            L.append("    for (b2_ll rf = lo; rf < hi; ++rf) {")
+            L.append("    b2_ll rr = rf;")
+            for p in reversed(R):
+                i = idx[p]
+                L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
+                L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
+        L += reg_decls(4)
+        L += body
+        if full:
+            for _ in R:
+                L.append("    }")
+        else:
+            L.append("    }")
+        for t in self.red.values():
+            a = t["acc"]
+            if full and t["exclusive"]:
+                L.append(f"    {t['target']} = {a};")
+            else:
+                L.append(f"    if (have_{a}) b2_atomic_{t['wcr']}(&{t['target']}, {a});")
+        L.append("  }")
+        return L
 
     def _stencil_loop(self, k: int, vec: int, reg_decls, body: list) -> list:
         """Stencil mode: each CTA owns a (8 x 32*vec) tile of the two inner
@@ -364,6 +464,23 @@ class _Gen:
             else:
                 self.emit(f"b2_wcr_{m.wcr}(&{tgt}, ({ct})({val}));")
             return
+        if self.red is not None and m.wcr is not None and depth == 0:
+            key = self._wkey(m, env)
+            t = self.red.get(key)
+            if t is None:
+                idx = [symexpr.to_c(b, self.name_of(env)) for b, _, _ in m.subset]
+                self.spec.checks.append((m.container, m.subset, env))
+                t = {"acc": self.fresh("acc"), "ct": ct, "wcr": m.wcr,
+                     "target": f"{self.ptr(m.container)}[{self.offset(m.container, idx)}]",
+                     "exclusive": self.red_targets[key][1] == set(self.red_pout)}
+                self.red[key] = t
+            a = t["acc"]
+            if self.red_full and t["exclusive"]:
+                self.emit(f"b2_wcr_{m.wcr}(&{a}, ({ct})({val}));")
+            else:
+                self.emit(f"if (have_{a}) b2_wcr_{m.wcr}(&{a}, ({ct})({val})); "
+                          f"else {{ {a} = ({ct})({val}); have_{a} = true; }}")
+            return
         # subset may cover several elements: broadcast assignment
         loops = []
         idx = []
@@ -561,6 +678,22 @@ class _Gen:
                 mode = force
         if mode != "stencil":
             self.stencil = {}
+        if mode in ("flat", "tile2", "march") and REDUCE_MODE:
+            rp = self._reduction_plan()
+            if rp is not None:
+                R, pout, targets = rp
+                mode = "reduce"
+                self.red = {}
+                self.red_targets = targets
+                self.red_pout = pout
+                nout = 1
+                for p in pout:
+                    nout *= self.const_ranges[grp.params.index(p)][2]
+                nred = 1
+                for p in R:
+                    nred *= self.const_ranges[grp.params.index(p)][2]
+                self.red_full = nout >= 148 * 256 or nred <= 64
+                self.red_R = R
         spec.mode = mode
         vec = 1
         if mode == "tile2":
@@ -579,7 +712,7 @@ class _Gen:
             vec = int(os.environ["B2_VEC"])
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1), "march": (32, 8, 1),
+                      "tile2": (32, 8, 1), "march": (32, 8, 1), "reduce": (256, 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -712,6 +845,8 @@ class _Gen:
             loop.append("  }")
         elif mode == "stencil":
             loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
+        elif mode == "reduce":
+            loop += self._reduce_loop(self.red_R, self.red_pout, reg_decls, shift(body, -2))
         elif mode == "tile2":
             x, y = k - 1, k - 2
             tw = 32 * vec
@@ -890,6 +1025,9 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (256, 1, 1)
     k = len(rl)
+    if spec.mode == "reduce":
+        n = getattr(spec, "red_threads", 1)
+        return (max(1, min(-(-n // 256), MAX_BLOCKS * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "stencil":
         tk = (32 if k == 3 else 256) * spec.vec
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
