@@ -462,7 +462,7 @@ class _Gen:
             if m.wcr is None:
                 self.emit(f"{tgt} = {val};")
             else:
-                self.emit(f"b2_wcr_{m.wcr}(&{tgt}, ({ct})({val}));")
+                self.emit(f"{tgt} = b2_op_{m.wcr}({tgt}, ({ct})({val}));")
             return
         if self.red is not None and m.wcr is not None and depth == 0:
             key = self._wkey(m, env)
@@ -476,10 +476,10 @@ class _Gen:
                 self.red[key] = t
             a = t["acc"]
             if self.red_full and t["exclusive"]:
-                self.emit(f"b2_wcr_{m.wcr}(&{a}, ({ct})({val}));")
+                self.emit(f"{a} = b2_op_{m.wcr}({a}, ({ct})({val}));")
             else:
-                self.emit(f"if (have_{a}) b2_wcr_{m.wcr}(&{a}, ({ct})({val})); "
-                          f"else {{ {a} = ({ct})({val}); have_{a} = true; }}")
+                self.emit(f"{a} = have_{a} ? b2_op_{m.wcr}({a}, ({ct})({val})) : ({ct})({val}); "
+                          f"have_{a} = true;")
             return
         # subset may cover several elements: broadcast assignment
         loops = []
@@ -517,7 +517,7 @@ class _Gen:
         elif shared:
             self.emit(f"b2_atomic_{m.wcr}(&{target}, ({ct})({val}));")
         else:
-            self.emit(f"b2_wcr_{m.wcr}(&{target}, ({ct})({val}));")
+            self.emit(f"{target} = b2_op_{m.wcr}({target}, ({ct})({val}));")
         if guarded:
             self.ind -= 2
             self.emit("}")

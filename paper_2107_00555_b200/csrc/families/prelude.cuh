@@ -61,6 +61,22 @@ __device__ __forceinline__ b2_ll b2_npmax(b2_ll a, b2_ll b) { return a > b ? a :
 __device__ __forceinline__ int b2_npmin(int a, int b) { return a < b ? a : b; }
 __device__ __forceinline__ int b2_npmax(int a, int b) { return a > b ? a : b; }
 
+// ---- write-conflict resolution on values (register accumulators) ----------
+// Value form: taking the address of a register accumulator inside a
+// data-dependent branch made nvcc 12.9 emit a non-terminating loop for sm_100a.
+template <typename T>
+__device__ __forceinline__ T b2_op_add(T a, T v) { return a + v; }
+template <typename T>
+__device__ __forceinline__ T b2_op_mul(T a, T v) { return a * v; }
+template <typename T>
+__device__ __forceinline__ T b2_op_min(T a, T v) { return b2_npmin(a, v); }
+template <typename T>
+__device__ __forceinline__ T b2_op_max(T a, T v) { return b2_npmax(a, v); }
+__device__ __forceinline__ bool b2_op_add(bool a, bool v) { return a || v; }
+__device__ __forceinline__ bool b2_op_mul(bool a, bool v) { return a && v; }
+__device__ __forceinline__ bool b2_op_min(bool a, bool v) { return a && v; }
+__device__ __forceinline__ bool b2_op_max(bool a, bool v) { return a || v; }
+
 // ---- write-conflict resolution commits -----------------------------------
 // Plain read-modify-write (the location is private to the thread).
 template <typename T>
