@@ -154,7 +154,10 @@ class _Gen:
             if full and t["exclusive"]:
                 L.append(f"    {ct} {a} = {t['target']};")
             else:
-                L.append(f"    {ct} {a} = ({ct})0; bool have_{a} = false;")
+                ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
+                if ct != "double" and t["wcr"] in ("min", "max"):
+                    ident = "0"  # integer min/max: committed only when iterations ran
+                L.append(f"    {ct} {a} = ({ct})({ident});")
         if full:
             for p in R:
                 i = idx[p]
@@ -180,7 +183,8 @@ class _Gen:
             if full and t["exclusive"]:
                 L.append(f"    {t['target']} = {a};")
             else:
-                L.append(f"    if (have_{a}) b2_atomic_{t['wcr']}(&{t['target']}, {a});")
+                cond = "" if full else "if (lo < hi) "
+                L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
         L.append("  }")
         return L
 
@@ -478,8 +482,9 @@ class _Gen:
             if self.red_full and t["exclusive"]:
                 self.emit(f"{a} = b2_op_{m.wcr}({a}, ({ct})({val}));")
             else:
-                self.emit(f"{a} = have_{a} ? b2_op_{m.wcr}({a}, ({ct})({val})) : ({ct})({val}); "
-                          f"have_{a} = true;")
+                # accumulator starts at the WCR identity (a data-dependent
+                # first-value select here also hung under nvcc 12.9 / sm_100a)
+                self.emit(f"{a} = b2_op_{m.wcr}({a}, ({ct})({val}));")
             return
         # subset may cover several elements: broadcast assignment
         loops = []
