@@ -165,7 +165,11 @@ class _Gen:
                 L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         else:
             L.append("    const b2_ll lo = ch * NRED / NCH, hi = (ch + 1) * NRED / NCH;")
-            L.append("    for (b2_ll rf = lo; rf < hi; ++rf) {")
+            # 32-bit induction variable when it fits: with a 64-bit one and
+            # all-constexpr bounds, nvcc 12.9 (sm_100a) emitted a loop that never
+            # terminated (reproduced standalone; int form is correct)
+            it = "int" if nred < 2 ** 31 else "b2_ll"
+            L.append(f"    for ({it} rf = ({it})lo; rf < ({it})hi; ++rf) {{")
             L.append("    b2_ll rr = rf;")
             for p in reversed(R):
                 i = idx[p]
