@@ -996,6 +996,151 @@ def point_function(planner: P.Planner, group: P.MapGroup, shapes: dict, fname: s
     return gen.spec
 
 
+def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelSpec:
+    """One kernel for a device loop region (loops.py): parallel loops over
+    threads, the rest of the nest as structured sequential C per thread.
+    Every memory access inside is device-guarded (depth 1) because its index
+    depends on loop symbols the host does not enumerate."""
+    from . import loops as LP
+
+    loops_all = LP.find_loops(planner)
+    par_vars = [l.var for l in reg.par]
+    dummy = P.MapGroup("map", planner.g.states[0], params=list(par_vars),
+                       ranges=[], schedule="parallel" if par_vars else "scalar")
+    dummy.idx = reg.idx
+    gen = _Gen(planner, dummy, shapes, name)
+    assigned = LP.assigned_symbols(planner, reg) - set(par_vars)
+    sym_types = {}
+
+    def name_of(n):
+        return gen.sym(n)
+
+    def cond_c(c):
+        types = {n: "i" for n in scalar.free_names(c)}
+        for n in types:
+            gen.sym(n)
+        code, t = scalar.emit(c, types, lambda n: f"s_{n}")
+        return scalar.cast(code, t, "b")
+
+    def emit_ops(h):
+        for op in planner.ops[h]:
+            if not isinstance(op, P.MapGroup):
+                raise P.PlanError("non-map op inside a device loop region")
+            for mem in op.members:
+                if mem.tasklet is not None:
+                    gen.tasklet(mem.state, mem.tasklet, {}, 1)
+                    continue
+                env = {}
+                heads = []
+                for p, (b, e, s) in mem.entry.params:
+                    v = gen.fresh(f"p_{p}")
+                    heads.append(f"for (b2_ll {v} = {symexpr.to_c(b, gen.name_of(env))}; "
+                                 f"{v} <= {symexpr.to_c(e, gen.name_of(env))}; "
+                                 f"{v} += {symexpr.to_c(s, gen.name_of(env))})")
+                    env[p] = v
+                for hd in heads:
+                    gen.emit(hd + " {")
+                    gen.ind += 2
+                gen.scope(mem.state, mem.entry, env, 1)
+                for _ in heads:
+                    gen.ind -= 2
+                    gen.emit("}")
+
+    def follow(t):
+        for k, v in t.assignments.items():
+            if k in par_vars:
+                continue  # parallel loop variables come from the thread index
+            gen.emit(f"s_{k} = {symexpr.to_c(v, name_of)};")
+
+    def block(cur, stop):
+        guard_budget = 0
+        while cur != stop:
+            guard_budget += 1
+            if guard_budget > 10000:
+                raise P.PlanError("unstructured control flow in loop region")
+            if cur in loops_all and cur in reg.heads:
+                L = loops_all[cur]
+                gen.emit(f"while ({cond_c(L.cond)}) {{")
+                gen.ind += 2
+                follow(L.t_in)
+                block(L.body_entry, L.guard)
+                gen.ind -= 2
+                gen.emit("}")
+                follow(L.t_out)
+                cur = L.exit
+                continue
+            emit_ops(cur)
+            outs = planner.g.out_transitions(planner.chain_end[cur])
+            if len(outs) != 1:
+                raise P.PlanError("branching inside a device loop region")
+            follow(outs[0])
+            cur = outs[0].dst
+
+    gen.ind = 6
+    if reg.par:
+        inner = reg.par[-1]
+        follow(inner.t_in)
+        block(inner.body_entry, inner.guard)
+    else:
+        root = reg.loop
+        gen.emit(f"while ({cond_c(root.cond)}) {{")
+        gen.ind += 2
+        follow(root.t_in)
+        block(root.body_entry, root.guard)
+        gen.ind -= 2
+        gen.emit("}")
+    body = gen.lines
+    spec = gen.spec
+    pro = [f'extern "C" __global__ void __launch_bounds__(256) {name}'
+           "(const __grid_constant__ B2Args a) {"]
+    for cname in spec.containers:
+        c = planner.g.containers[cname]
+        if gen.place(cname) == "reg":
+            continue
+        pro.append(f"  {CT[c.dtype]} *__restrict__ c_{cname} = ({CT[c.dtype]} *){gen.arg(('ptr', cname))};")
+        st = _row_major(shapes[cname])
+        for d in range(len(st)):
+            pro.append(f"  constexpr b2_ll st_{cname}_{d} = {st[d]}LL;")
+        n = 1
+        for x in shapes[cname]:
+            n *= x
+        pro.append(f"  constexpr b2_ll sz_{cname} = {n}LL;")
+    pro.append(f"  int *flag = (int *){gen.arg(('flag',))};")
+    pro.append("  (void)flag;")
+    npar = gen.arg(("npar",))
+    pro.append(f"  const b2_ll NPAR = {npar};")
+    for k, l in enumerate(reg.par):
+        pro.append(f"  const b2_ll pb{k} = {gen.arg(('pb', k))}, ps{k} = {gen.arg(('ps', k))}, "
+                   f"pn{k} = {gen.arg(('pn', k))};")
+    loop = ["  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NPAR; "
+            "f += (b2_ll)gridDim.x * blockDim.x) {", "    b2_ll rem = f; (void)rem;"]
+    for k in reversed(range(len(reg.par))):
+        loop.append(f"    const b2_ll s_{reg.par[k].var} = pb{k} + ps{k} * (rem % pn{k}); "
+                    f"rem /= pn{k};")
+    for s in spec.syms:
+        if s in par_vars:
+            continue
+        if s in assigned:
+            loop.append(f"    b2_ll s_{s} = {gen.arg(('sym', s))};")
+        elif s in planner.fixed:
+            loop.append(f"    constexpr b2_ll s_{s} = {int(planner.fixed[s])}LL;")
+        else:
+            loop.append(f"    const b2_ll s_{s} = {gen.arg(('sym', s))};")
+    for cname in spec.containers:
+        if gen.place(cname) == "reg":
+            loop.append(f"    {CT[planner.g.containers[cname].dtype]} r_{cname} = 0;")
+    loop += [ln[2:] for ln in body]
+    loop.append("  }")
+    spec.source = "\n".join(
+        [f"// generated by paper_2107_00555_b200.codegen: device loop region at "
+         f"'{reg.loop.guard}' ({len(reg.par)} parallel loop(s))",
+         "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))] + pro + loop + ["}"]) + "\n"
+    spec.mode = "region"
+    spec.block = (256, 1, 1)
+    spec.params = []
+    return spec
+
+
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str) -> KernelSpec:
     gen = _Gen(planner, group, shapes, name)
     spec = gen.build()

@@ -24,6 +24,7 @@ import ctypes
 import hashlib
 import itertools
 import json
+import struct
 from dataclasses import dataclass, field
 from typing import Mapping
 
@@ -176,7 +177,15 @@ class GpuExecutor:
 
     def _compile(self):
         self.specs: dict[int, codegen.KernelSpec] = {}
+        for reg in self.planner.regions:
+            name = f"b2_loop_{self.g.name}_{reg.idx}"
+            spec = codegen.generate_region(self.planner, reg, self.buf.shape, name)
+            spec.kernel = rt.get_kernel(rt.family_source("prelude.cuh") + "\n" + spec.source, name)
+            self.specs[reg.idx] = spec
+            reg.spec = spec
         for op in self.planner.all_ops:
+            if op.idx in self.planner.in_region:
+                continue
             if isinstance(op, P.MapGroup):
                 name = f"b2_map_{self.g.name}_{op.idx}"
                 spec = codegen.generate(self.planner, op, self.buf.shape, name)
@@ -337,6 +346,15 @@ class GpuExecutor:
         cur = g.start
         steps = 0
         while cur is not None:
+            reg = self.planner.region_at.get(cur)
+            if reg is not None:
+                if not self._dry:
+                    self._exec_region(reg, sym, counters)
+                else:
+                    self._region_final(reg, sym)
+                cur = reg.loop.exit
+                steps += 1
+                continue
             for op in self.planner.ops[cur]:
                 self._exec_op(op, sym, counters)
             cur = self.planner.chain_end[cur]
@@ -356,6 +374,58 @@ class GpuExecutor:
             steps += 1
             if steps > self.opt.max_transitions:
                 raise InterpreterError("transition budget exceeded (infinite loop?)")
+
+    def _region_trips(self, reg, sym):
+        from . import loops as LP
+
+        trips = []
+        for k, L in enumerate(reg.par):
+            start = sym[L.var] if k == 0 else symexpr.evaluate(L.entry_edge.assignments[L.var], sym)
+            trips.append((start, L.step, LP.trip(L, start, sym)))
+        return trips
+
+    def _region_final(self, reg, sym):
+        """Host copy of the root loop variable after the region (the host
+        never sees the per-iteration values)."""
+        from . import loops as LP
+
+        root = reg.loop
+        vals = LP.trip(root, sym[root.var], sym)
+        sym[root.var] = vals[-1] + root.step if vals else sym[root.var]
+        for k, v in root.t_out.assignments.items():  # the exit edge (host side)
+            sym[k] = symexpr.evaluate(v, sym)
+
+    def _exec_region(self, reg, sym, counters):
+        spec = reg.spec
+        trips = self._region_trips(reg, sym) if reg.par else []
+        npar = 1
+        for _, _, vals in trips:
+            npar *= len(vals)
+        if npar > 0:
+            vals = []
+            for d in spec.args:
+                k = d[0]
+                if k == "ptr":
+                    vals.append(self.buf.ptr[d[1]])
+                elif k == "flag":
+                    vals.append(self.flag)
+                elif k == "npar":
+                    vals.append(npar)
+                elif k == "pb":
+                    vals.append(trips[d[1]][0])
+                elif k == "ps":
+                    vals.append(trips[d[1]][1])
+                elif k == "pn":
+                    vals.append(len(trips[d[1]][2]))
+                elif k == "sym":
+                    vals.append(int(sym.get(d[1], 0)))
+                else:
+                    raise AssertionError(d)
+            blob = struct.pack(f"<{len(vals)}q", *vals)
+            grid = (max(1, min(-(-npar // 256), codegen.MAX_BLOCKS * 8)), 1, 1)
+            rt.launch(spec.kernel, grid, (256, 1, 1), blob, self.stream)
+            self.launches += 1
+        self._region_final(reg, sym)
 
     def _eval_cond(self, cond, sym):
         env = {}

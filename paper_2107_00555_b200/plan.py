@@ -175,6 +175,17 @@ class Planner:
             self.chain_end[head] = chain[-1].label
         self._collect_sites()
         self._place()
+        from . import loops
+
+        self.regions = loops.find_regions(self)
+        self.region_at = {}
+        self.in_region: set[int] = set()
+        for i, reg in enumerate(self.regions):
+            reg.idx = 100000 + i
+            self.region_at[reg.loop.guard] = reg
+            for h in reg.heads:
+                for op in self.ops[h]:
+                    self.in_region.add(op.idx)
         return self
 
     def _state_ops(self, st: sdfg.State) -> list[Op]:

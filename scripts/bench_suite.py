@@ -46,6 +46,10 @@ SUITE = {
                                         "HO": 237, "WO": 237}, "fp64",
                     2 * 8 * 237 * 237 * 16 * 20 * 20 * 3, "flop"),
     "nbody": ("nbody.raw", {"N": 100, "NT": 1000}, "launch", 1000, "steps"),
+    # statement-level algorithmic bytes: max scan reads x; ex = exp(x - mx) reads x,
+    # writes ex; row sum reads ex; out = ex / sm reads ex, writes out
+    "softmax": ("softmax.raw", {"N": 64, "H": 16, "SM": 512}, "hbm",
+                6 * 8 * 64 * 16 * 512 * 512, "B"),
 }
 
 
@@ -85,6 +89,10 @@ def cpu_port(name, syms, inputs):
         n = 20000
         K.azimint_naive(x["rmax"], x["data"][:n], x["radius"][:n], x["res"])
         work, desc = n * 1000, f"{n} of 1e6 samples"
+    elif name == "softmax":
+        xs = np.ascontiguousarray(x["x"][:1])
+        K.softmax(xs, np.empty_like(xs))
+        work, desc = SUITE[name][3] // 64, "1 of 64 batches"
     elif name == "nbody":
         K.nbody(x["mass"], x["pos"], x["vel"], x["acc"], x["E"], x["G"], x["softening"],
                 x["dt"], 10)
