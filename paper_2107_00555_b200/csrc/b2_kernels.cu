@@ -429,9 +429,17 @@ extern "C" int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axe
   return B2_OK;
 }
 
+int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                  int64_t ldb, double *C, int64_t rsc, int64_t csc, int accumulate,
+                  void *stream);
+
 extern "C" int b2_gemm_f64(int64_t M, int64_t N, int64_t K, const double *A, int64_t rsa,
                            int64_t csa, const double *B, int64_t rsb, int64_t csb, double *C,
                            int64_t rsc, int64_t csc, int wcr, void *stream) {
+  // FP64 tensor cores (DMMA) for row-major operands of non-trivial size
+  if (csa == 1 && csb == 1 && (wcr == B2_WCR_NONE || wcr == B2_WCR_ADD) && M >= 16 &&
+      N >= 16 && K >= 4 && M * N * K >= (1LL << 18))
+    return b2_dgemm_dmma(M, N, K, A, rsa, B, rsb, C, rsc, csc, wcr == B2_WCR_ADD, stream);
   return gemm_impl<double>(M, N, K, A, rsa, csa, B, rsb, csb, C, rsc, csc, wcr, stream);
 }
 
