@@ -227,7 +227,19 @@ class RowPass:
         self.axpy = next((m for m in mvs if m.kind == "axpy"), None)
         cont, off, M, N, rs = self.R
         self.M, self.N, self.rs = M, N, rs
-        self.cw = min(N, MAX_CW)
+        # prologue reads of 1-D containers indexed by the column alone (gemver's
+        # v1[j], v2[j]) are staged once per CTA in shared memory
+        self.staged: list[str] = []
+        if prologue is not None:
+            ncol = self.roles["n"]
+            for mem in prologue.members:
+                for (c, w, wcr, depth, pt) in planner.member_accesses(mem, prologue.params):
+                    if (not w and c != cont and depth == 0 and pt == ((0, ((ncol, 1),)),)
+                            and len(planner.g.containers[c].shape) == 1
+                            and planner.g.containers[c].dtype == "f64" and c not in self.staged):
+                        self.staged.append(c)
+        cap = MAX_CW if not self.staged else 4096
+        self.cw = min(N, cap)
         self.ctiles = -(-N // self.cw) if N else 1
         self.ok = M > 0 and N > 0 and not (coef_from_dot and self.ctiles > 1)
         if self.dot is not None and self.dot.vec.dims[0][0] != N:
@@ -239,18 +251,20 @@ class RowPass:
 
     def source(self, shapes, name: str) -> str:
         M, N, rs, cw = self.M, self.N, self.rs, self.cw
-        kpt = -(-cw // TPB)
+        tpb = self.tpb = 1024 if cw >= 4096 else TPB  # 32 warps: twice the loads in flight
+        kpt = -(-cw // tpb)
         dot, axpy = self.dot, self.axpy
-        smem_doubles = (cw if axpy else 0) + (cw if dot else 0) + 64
+        stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64
+        smem_doubles = stage_base + cw * len(self.staged)
         self.smem = smem_doubles * 8
         est_regs = 4 * kpt + 40  # x / xn double arrays + addressing
         blocks_per_sm = max(1, min(4, (200 * 1024) // max(1, self.smem),
-                                   65536 // (TPB * est_regs)))
+                                   65536 // (tpb * est_regs)))
         self.G = min(M, 148 * blocks_per_sm)
         L = []
         L.append(f"#define RP_NAME b2_rp_{name}")
         L.append(f"#define RP_FIN_NAME b2_rpf_{name}")
-        for k, v in (("RP_M", M), ("RP_N", N), ("RP_RS", rs), ("RP_CW", cw), ("RP_TPB", TPB),
+        for k, v in (("RP_M", M), ("RP_N", N), ("RP_RS", rs), ("RP_CW", cw), ("RP_TPB", tpb),
                      ("RP_KPT", kpt), ("RP_G", self.G), ("RP_CTILES", self.ctiles),
                      ("RP_DOT", int(dot is not None)), ("RP_AXPY", int(axpy is not None)),
                      ("RP_PROLOGUE", int(self.prologue is not None)),
@@ -261,10 +275,11 @@ class RowPass:
         if self.prologue is not None:
             cont = self.R[0]
             env = {self.roles["m"]: "m", self.roles["n"]: "n"}
+            colstage = {c: f"{stage_base + i * cw}" for i, c in enumerate(self.staged)}
             spec = codegen.point_function(
                 self.planner, self.prologue, shapes, name, env, {cont: "x"}, nbase,
-                "double rp_elem(const RpArgs &a, const RpRow &rr, b2_ll m, b2_ll n, double x)",
-                f"r_{cont}")
+                "double rp_elem(const RpArgs &a, const RpRow &rr, b2_ll m, b2_ll n, double x, "
+                "int jl)", f"r_{cont}", colstage=colstage)
             self.pro_args = spec.args
             pro_src = spec.source
         else:
@@ -273,7 +288,17 @@ class RowPass:
         L.append("struct RpArgs { long long w[%d]; };" % nargs)
         L.append("struct RpRow { int unused; };")
         L.append("__device__ __forceinline__ void rp_row_setup(const RpArgs &, b2_ll, RpRow &) {}")
+        L.append("extern __shared__ double rp_smem[];")
         L.append(pro_src)
+        # stage the column vectors of this CTA's column tile
+        stage = ["__device__ __forceinline__ void rp_stage_cols(const RpArgs &a, b2_ll c0, int cw, "
+                 "int tid) {"]
+        for i, c in enumerate(self.staged):
+            ai = nbase + self.pro_args.index(("ptr", c))
+            stage.append(f"  for (int j = tid; j < cw; j += RP_TPB) rp_smem[{stage_base + i * cw} + j]"
+                         f" = ((const double *)a.w[{ai}])[c0 + j];")
+        stage.append("}")
+        L.append("\n".join(stage))
         if dot is not None:
             vinc = dot.vec.dims[0][1]
             oinc = dot.out.dims[0][1]
@@ -352,7 +377,8 @@ class RowPass:
         if prof is not None:
             ev = ex._prof_event_pair()
             rt.lib().b2_event_record(ev[0], ex.stream)
-        rt.launch(self.kmain, (self.G, self.ctiles, 1), (TPB, 1, 1), blob, ex.stream, self.smem)
+        rt.launch(self.kmain, (self.G, self.ctiles, 1), (self.tpb, 1, 1), blob, ex.stream,
+                  self.smem)
         if prof is not None:
             rt.lib().b2_event_record(ev[1], ex.stream)
             prof.append((self.kmain.name, self.M * self.N, ev))

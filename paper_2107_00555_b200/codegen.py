@@ -84,6 +84,7 @@ class _Gen:
         self.stencil: dict = {}
         self.hoist = False
         self.hoisted: list = []
+        self.colstage: dict = {}
         self.red = None  # reduction mode: target key -> accumulator info
         self.red_targets: dict = {}
         self.red_pout: list = []
@@ -408,6 +409,9 @@ class _Gen:
         pl = self.place(m.container)
         if pl == "reg":
             return f"r_{m.container}", t
+        if pl == "colstage":  # staged column vector (rowpass prologue)
+            self.spec.arg_index(("ptr", m.container))
+            return f"rp_smem[{self.colstage[m.container]} + jl]", t
         if depth == 0 and m.container in self.stencil:
             self.spec.checks.append((m.container, m.subset, env))
             offs = self._stencil_offsets(m, env)
@@ -945,7 +949,8 @@ def _const_range(planner: P.Planner, rng):
 
 
 def point_function(planner: P.Planner, group: P.MapGroup, shapes: dict, fname: str,
-                   env: dict, regs: dict, arg_base: int, signature: str, ret: str):
+                   env: dict, regs: dict, arg_base: int, signature: str, ret: str,
+                   colstage: dict | None = None):
     """Emit the per-point body of ``group`` as a __device__ function (used to
     inline an elementwise map into another family, e.g. the rowpass
     prologue).  ``env`` maps group params to C expressions; ``regs`` maps
@@ -953,6 +958,9 @@ def point_function(planner: P.Planner, group: P.MapGroup, shapes: dict, fname: s
     gen = _Gen(planner, group, shapes, fname)
     gen.arg_base = arg_base
     gen.place_override = {c: "reg" for c in regs}
+    gen.colstage = dict(colstage or {})
+    for c in gen.colstage:
+        gen.place_override[c] = "colstage"
     for mem in group.members:
         for a in planner.member_accesses(mem, group.params):
             if a[1]:
@@ -967,7 +975,7 @@ def point_function(planner: P.Planner, group: P.MapGroup, shapes: dict, fname: s
     body = gen.lines
     decl = []
     for name in gen.spec.containers:
-        if name in regs:
+        if name in regs or name in gen.colstage:
             continue
         c = planner.g.containers[name]
         ro = name not in gen.written

@@ -44,6 +44,7 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
     if (RP_AXPY) acc_s[j] = 0.0;
     if (RP_DOT) v_s[j] = rp_dot_vec(a, c0 + j);
   }
+  rp_stage_cols(a, c0, cw, tid);
   __syncthreads();
   const double *__restrict__ R = (const double *)a.w[0];
   double x[RP_KPT], xn[RP_KPT];
@@ -73,7 +74,7 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
       for (int k = 0; k < RP_KPT; ++k) {
         const int j = tid + k * RP_TPB;
         if (j < cw) {
-          x[k] = rp_elem(a, rr, m, c0 + j, x[k]);
+          x[k] = rp_elem(a, rr, m, c0 + j, x[k], j);
 #if RP_WRITEBACK
           ((double *)a.w[0])[m * RP_RS + c0 + j] = x[k];
 #endif
