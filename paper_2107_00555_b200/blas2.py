@@ -24,6 +24,7 @@ and axpy roles swap).  Anything else stays on b2_gemm_f64.
 from __future__ import annotations
 
 import ctypes
+import os
 import struct
 
 from . import codegen, plan as P, runtime as rt, sdfg, symexpr
@@ -251,7 +252,8 @@ class RowPass:
 
     def source(self, shapes, name: str) -> str:
         M, N, rs, cw = self.M, self.N, self.rs, self.cw
-        tpb = self.tpb = 1024 if cw >= 4096 else TPB  # 32 warps: twice the loads in flight
+        tpb = int(os.environ.get("B2_RP_TPB", TPB))
+        self.tpb = tpb
         kpt = -(-cw // tpb)
         dot, axpy = self.dot, self.axpy
         stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64
