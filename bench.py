@@ -285,8 +285,32 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="heat_3d", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="heat_3d",
+                    choices=sorted(WORKLOADS) + ["matmul", "matmul_f32"])
+    ap.add_argument("--n", type=int, default=16384, help="SUMMA size (matmul workloads)")
     args = ap.parse_args()
+    if args.workload.startswith("matmul"):
+        if args.impl == "reference":
+            rank = int(os.environ.get("RANK", "0"))
+            if rank == 0:
+                from oracle import kernels_np as K
+                n = 4096
+                rng = np.random.default_rng(0)
+                A, B = rng.uniform(-1, 1, (n, n)), rng.uniform(-1, 1, (n, n))
+                t = time.perf_counter()
+                K.matmul(A, B)
+                dt = time.perf_counter() - t
+                v = 2 * n ** 3 / dt / 1e12
+                print(json.dumps({"impl": "reference", "metric": f"summa_{args.workload}_TFLOPs",
+                                  "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+                                  "cpu_baseline": {"value": v, "unit": "TFLOP/s", "kind": "port",
+                                                   "cores": os.cpu_count(),
+                                                   "sample": "4096^3 numpy/OpenBLAS dgemm"},
+                                  "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}), flush=True)
+            return
+        from paper_2107_00555_b200.dist import bench_summa
+        return bench_summa(args, args.n, "f32" if args.workload.endswith("f32") else "f64")
     W = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, W)

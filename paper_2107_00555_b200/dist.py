@@ -478,6 +478,160 @@ class SlabGpuRunner:
         return out if self.rank == 0 else None
 
 
+# ---------------------------------------------------------------------------
+# SUMMA: block-distributed MATMUL (DIST_MATMUL)
+
+
+class Summa:
+    """C = A @ B with A (M x K), B (K x N), C (M x N) block-distributed on a
+    ProcessGrid (Pr x Pc): rank (i, j) owns A[i-th row block, j-th col
+    block], B likewise and C[i, j].  K is cut into L = lcm(Pr, Pc) panels;
+    for panel l the owner column of A's panel broadcasts it along grid row i
+    and the owner row of B's panel broadcasts it along grid column j
+    (torch.distributed broadcast on row / column sub-communicators: NCCL over
+    NVLink on GPUs), and every rank accumulates the local product
+    (``gemm(c, a, b)``: libb2 DMMA DGEMM / f32 GEMM on GPUs).  The next
+    panel's broadcasts are issued before the current panel's GEMM so the
+    transfer overlaps the math."""
+
+    def __init__(self, grid: ProcessGrid, rank: int, M: int, N: int, K: int):
+        import torch.distributed as tdist
+
+        if len(grid.dims) != 2:
+            raise DistError("SUMMA needs a 2-D process grid")
+        self.td = tdist
+        self.grid = grid
+        self.rank = rank
+        Pr, Pc = grid.dims
+        if M % Pr or N % Pc or K % math.lcm(Pr, Pc):
+            raise DistError("uneven block distribution (SPEC.md:588)")
+        self.M, self.N, self.K = M, N, K
+        self.i, self.j = grid.coords(rank)
+        self.L = math.lcm(Pr, Pc)
+        self.kb = K // self.L
+        # every rank creates every row/column group in the same order
+        self.row_groups = [tdist.new_group([grid.rank_of((r, c)) for c in range(Pc)])
+                           for r in range(Pr)]
+        self.col_groups = [tdist.new_group([grid.rank_of((r, c)) for r in range(Pr)])
+                           for c in range(Pc)]
+
+    def local_shapes(self):
+        Pr, Pc = self.grid.dims
+        return (self.M // Pr, self.K // Pc), (self.K // Pr, self.N // Pc), (self.M // Pr, self.N // Pc)
+
+    def blocks_of(self, A, B):
+        """This rank's blocks of full A, B (host arrays) — for tests/bench."""
+        (am, ak), (bk, bn), _ = self.local_shapes()
+        return (A[self.i * am:(self.i + 1) * am, self.j * ak:(self.j + 1) * ak],
+                B[self.i * bk:(self.i + 1) * bk, self.j * bn:(self.j + 1) * bn])
+
+    def run(self, a_local, b_local, c_local, gemm, new_buffer):
+        """a_local/b_local/c_local: torch tensors (device or host); gemm(c, a,
+        b) accumulates; new_buffer(shape) returns an uninitialised tensor."""
+        Pr, Pc = self.grid.dims
+        per_a = self.L // Pc  # panels per A column block
+        per_b = self.L // Pr  # panels per B row block
+        kb = self.kb
+        am = self.M // Pr
+        bn = self.N // Pc
+        bufs = [(new_buffer((am, kb)), new_buffer((kb, bn))) for _ in range(2)]
+
+        def issue(l, slot):
+            pa, pb = bufs[slot]
+            ca, la = divmod(l, per_a)  # owner grid column of A's panel, local panel
+            rb, lb = divmod(l, per_b)  # owner grid row of B's panel
+            if self.j == ca:
+                pa.copy_(a_local[:, la * kb:(la + 1) * kb])
+            if self.i == rb:
+                pb.copy_(b_local[lb * kb:(lb + 1) * kb, :])
+            w1 = self.td.broadcast(pa, self.grid.rank_of((self.i, ca)),
+                                   group=self.row_groups[self.i], async_op=True)
+            w2 = self.td.broadcast(pb, self.grid.rank_of((rb, self.j)),
+                                   group=self.col_groups[self.j], async_op=True)
+            return w1, w2
+
+        pending = issue(0, 0)
+        for l in range(self.L):
+            nxt = issue(l + 1, (l + 1) % 2) if l + 1 < self.L else None
+            for w in pending:
+                w.wait()
+            pa, pb = bufs[l % 2]
+            gemm(c_local, pa, pb)
+            pending = nxt
+        return c_local
+
+
+def bench_summa(args, n: int = 16384, dtype: str = "f64"):
+    """bench.py --workload matmul[_f32]: SUMMA over all ranks (squarest grid),
+    libb2 DMMA / f32 GEMM per panel, NCCL panel broadcasts.  Prints the JSON
+    line from rank 0 (TFLOP/s of the whole job, max-over-ranks time)."""
+    import json
+
+    import torch
+    import torch.distributed as tdist
+
+    from . import runtime as rt
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    if not tdist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        tdist.init_process_group("nccl", rank=rank, world_size=world,
+                                 device_id=torch.device("cuda", local))
+    rt.device(local)
+    grid = ProcessGrid.squarest(world)
+    s = Summa(grid, rank, n, n, n)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    (am, ak), (bk, bn), (cm, cn) = s.local_shapes()
+    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    a = torch.rand((am, ak), dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    b = torch.rand((bk, bn), dtype=tdt, device="cuda", generator=gen) * 2 - 1
+    c = torch.zeros((cm, cn), dtype=tdt, device="cuda")
+    L = rt.lib()
+    fn = L.b2_gemm_f64 if dtype == "f64" else L.b2_gemm_f32
+
+    def gemm(cc, pa, pb):
+        stream = torch.cuda.current_stream().cuda_stream
+        rt.check(fn(pa.shape[0], pb.shape[1], pa.shape[1], pa.data_ptr(), pa.stride(0), 1,
+                    pb.data_ptr(), pb.stride(0), 1, cc.data_ptr(), cc.stride(0), 1,
+                    rt.WCR_CODE["add"], stream), "summa gemm")
+
+    def buf(shape):
+        return torch.empty(shape, dtype=tdt, device="cuda")
+
+    for _ in range(args.warmup):
+        s.run(a, b, c, gemm, buf)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        s.run(a, b, c, gemm, buf)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    flop = 2.0 * n ** 3
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"summa_matmul_{dtype}_TFLOPs", "value": flop / (ms / 1e3) / 1e12,
+            "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": dtype, "data": "synthetic uniform(-1,1)",
+            "config": {"workload": f"SUMMA M=N=K={n} {dtype} (BASELINE configs[3])",
+                       "grid": str(grid), "panels": s.L,
+                       "parallelism": f"summa{grid}"}}), flush=True)
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
 def bench_slab(args, W):
     """bench.py --gpus N under torchrun: strong-scaled slab run of the
     workload, max-over-ranks device time, one JSON line from rank 0."""

@@ -191,3 +191,56 @@ def test_slab_run_matches_single_device(name, syms, world):
                 full[c][x] = row
     for c in ref:
         assert np.array_equal(full[c], ref[c]), f"{name} {c} differs from single device"
+
+
+def _summa_worker(rank, world, port, dims, M, N, K, q):
+    import torch
+    import torch.distributed as tdist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(11)
+        A = rng.uniform(-1, 1, (M, K))
+        B = rng.uniform(-1, 1, (K, N))
+        grid = dist.ProcessGrid(dims)
+        s = dist.Summa(grid, rank, M, N, K)
+        a, b = s.blocks_of(A, B)
+        c = torch.zeros(s.local_shapes()[2], dtype=torch.float64)
+        s.run(torch.from_numpy(np.ascontiguousarray(a)), torch.from_numpy(np.ascontiguousarray(b)),
+              c, lambda cc, pa, pb: cc.add_(pa @ pb),
+              lambda shape: torch.empty(shape, dtype=torch.float64))
+        i, j = grid.coords(rank)
+        q.put((i, j, c.numpy().copy()))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims", [(1, 1), (2, 1), (2, 2), (4, 2)])
+def test_summa_matches_shared_memory_matmul(dims):
+    """SUMMA on 1x1 / 2x1 / 2x2 / 4x2 grids (the BASELINE
+    SUMMA grids) equals A @ B."""
+    import torch.multiprocessing as mp
+
+    M, N, K = 32, 24, 40
+    world = dims[0] * dims[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_summa_worker, args=(r, world, port, dims, M, N, K, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(11)
+    A = rng.uniform(-1, 1, (M, K))
+    B = rng.uniform(-1, 1, (K, N))
+    C = np.zeros((M, N))
+    bm, bn = M // dims[0], N // dims[1]
+    for i, j, c in parts:
+        C[i * bm:(i + 1) * bm, j * bn:(j + 1) * bn] = c
+    assert np.max(np.abs(C - A @ B)) <= 1e-12 * max(1.0, np.max(np.abs(A @ B)))
