@@ -195,7 +195,7 @@ def run_ours(args, W):
     from paper_2107_00555_b200.machine import get_executor
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    if world > 1 or args.gpus > 1 or os.environ.get("B2_FORCE_SLAB"):
         from paper_2107_00555_b200.dist import bench_slab
         return bench_slab(args, W)
 

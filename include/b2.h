@@ -141,6 +141,24 @@ B2_API int b2_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
 B2_API int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axes_mask, int op, int wcr,
               void *stream);
 
+/* ---- multi-GPU: NCCL on the executor stream (graph-capturable) ----------
+ * Replaces the simulated ISEND/IRECV/WAITALL/BCAST/DIST_MATMUL events of the
+ * reference's rank simulator (interp.py:443-447, 483-489). */
+typedef struct {
+  void *ptr;
+  size_t bytes;
+  int peer;
+  int send; /* 1 = send, 0 = receive */
+} b2_p2p_t;
+B2_API int b2_nccl_unique_id(void *out128);
+B2_API int b2_nccl_init(int nranks, int rank, const void *id128, void **comm);
+B2_API int b2_nccl_destroy(void *comm);
+/* One grouped batch of point-to-point transfers (halo exchange). */
+B2_API int b2_nccl_group_p2p(void *comm, int n, const b2_p2p_t *ops, void *stream);
+B2_API int b2_nccl_bcast(void *comm, void *buf, size_t bytes, int root, void *stream);
+/* In-place Allreduce of a WCR-reduced f64 output (op = B2_WCR_*). */
+B2_API int b2_nccl_allreduce_f64(void *comm, double *buf, size_t count, int wcr, void *stream);
+
 /* Matrix-vector products (np.matmul 2D@1D / 1D@2D) and their fusions
  * (gemver / atax / bicg) are JIT "rowpass" family kernels: see
  * paper_2107_00555_b200/csrc/families/rowpass.cuh. */

@@ -337,17 +337,25 @@ class HaloExchanger:
     ``rows_of(c, lo, hi)`` returns a torch tensor viewing global rows
     [lo, hi) of container c's local buffer on this rank."""
 
-    def __init__(self, plan: SlabPlan, rank: int, rows_of):
-        import torch.distributed as tdist
+    def __init__(self, plan: SlabPlan, rank: int, rows_of=None, transport=None):
+        if transport is None:
+            import torch.distributed as tdist
 
-        self.tdist = tdist
+            self.tdist = tdist
         self.plan = plan
         self.rank = rank
         self.rows_of = rows_of
+        self.transport = transport  # callable([(send?, peer, container, lo, hi)]) or None
         self.dirty: set[str] = set()
         self.xfer = {c: plan.transfers(c, rank) for c in plan.dist}
         self.exchanges = 0
         self.bytes_sent = 0
+
+    def flush(self):
+        """Exchange everything still dirty (end of a run: the next run, or a
+        replay of the captured graph, starts from consistent halos)."""
+        if self.dirty:
+            self.exchange(sorted(self.dirty))
 
     def before(self, reads):
         need = [c for c in sorted(reads) if c in self.dirty]
@@ -360,6 +368,16 @@ class HaloExchanger:
                 self.dirty.add(c)
 
     def exchange(self, conts):
+        if self.transport is not None:
+            plan_ops = []
+            for c in conts:
+                sends, recvs = self.xfer[c]
+                plan_ops += [(True, peer, c, lo, hi) for peer, lo, hi in sends]
+                plan_ops += [(False, peer, c, lo, hi) for peer, lo, hi in recvs]
+                self.dirty.discard(c)
+            self.bytes_sent += self.transport(plan_ops)
+            self.exchanges += 1
+            return
         ops = []
         td = self.tdist
         for c in conts:
@@ -388,8 +406,51 @@ class _CudaArray:
 _TYPESTR = {"f64": "<f8", "i64": "<i8", "i32": "<i4", "bool": "|b1"}
 
 
+class NcclComm:
+    """A NCCL communicator owned by libb2 (include/b2.h b2_nccl_*): its
+    send/recv/broadcast are issued on the executor's stream, so they are
+    captured into the same CUDA graph as the kernels.  The unique id is
+    bootstrapped over the torch.distributed process group."""
+
+    def __init__(self, rank: int, world: int):
+        import ctypes
+
+        import torch.distributed as tdist
+
+        from . import runtime as rt
+
+        self.rt = rt
+        self.rank, self.world = rank, world
+        idbuf = ctypes.create_string_buffer(128)
+        if rank == 0:
+            rt.check(rt.lib().b2_nccl_unique_id(idbuf), "nccl id")
+        obj = [idbuf.raw if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        idbuf = ctypes.create_string_buffer(obj[0], 128)
+        comm = ctypes.c_void_p()
+        rt.check(rt.lib().b2_nccl_init(world, rank, idbuf, ctypes.byref(comm)), "nccl init")
+        self.comm = comm.value
+
+    def p2p(self, ops, stream) -> int:
+        """ops: [(send?, peer, ptr, bytes)] as one NCCL group; returns bytes sent."""
+        rt = self.rt
+        arr = (rt.P2P * max(1, len(ops)))()
+        sent = 0
+        for i, (send, peer, ptr, nbytes) in enumerate(ops):
+            arr[i].ptr, arr[i].bytes, arr[i].peer, arr[i].send = ptr, nbytes, peer, int(send)
+            sent += nbytes if send else 0
+        rt.check(rt.lib().b2_nccl_group_p2p(self.comm, len(ops), arr, stream), "nccl p2p")
+        return sent
+
+    def close(self):
+        self.rt.lib().b2_nccl_destroy(self.comm)
+
+
 class SlabGpuRunner:
-    """One rank of a slab-distributed program on its own GPU."""
+    """One rank of a slab-distributed program on its own GPU: the local graph
+    runs through a normal GpuExecutor (fused kernels, CUDA-graph capture of
+    the whole state machine) whose op hook inserts the halo exchanges as
+    NCCL group send/recv on the same stream — one graph launch per run."""
 
     def __init__(self, g, bindings: dict, rank: int, world: int, device: int):
         import torch
@@ -401,12 +462,27 @@ class SlabGpuRunner:
         self.plan = slab_decompose(self.g, bindings, world)
         self.rank = rank
         self.lg = self.plan.local_graph(rank)
-        stream = torch.cuda.current_stream(device).cuda_stream
-        self.ex = GpuExecutor(self.lg, bindings, device=device, stream=stream,
-                              options=InterpOptions())
-        self.ex.capturable = False  # halo exchanges run between kernels
-        self.xchg = HaloExchanger(self.plan, rank, self._rows_of)
+        self.ex = GpuExecutor(self.lg, bindings, device=device, options=InterpOptions())
+        self.nccl = NcclComm(rank, world) if world > 1 else None
+        self.xchg = HaloExchanger(self.plan, rank, self._rows_of, transport=self._transport)
         self.ex.op_hook = self._hook
+
+    def _rows_ptr(self, c, lo, hi):
+        desc = self.lg.containers[c]
+        wlo = self.plan.window[self.rank][c][0]
+        row = 1
+        for d in self.ex.buf.shape[c][1:]:
+            row *= d
+        esz = sdfg.DTYPE_BYTES[desc.dtype]
+        return self.ex.buf.ptr[c] + (lo - wlo) * row * esz, (hi - lo) * row * esz
+
+    def _transport(self, ops) -> int:
+        if not ops:
+            return 0
+        if self.nccl is None:
+            raise DistError("halo exchange without a communicator")
+        return self.nccl.p2p([(s, peer) + self._rows_ptr(c, lo, hi) for s, peer, c, lo, hi in ops],
+                             self.ex.stream)
 
     def _rows_of(self, c, lo, hi):
         desc = self.lg.containers[c]
@@ -422,8 +498,10 @@ class SlabGpuRunner:
     def _hook(self, op, reads, writes, phase):
         if phase == "pre":
             self.xchg.before(reads)
-        else:
+        elif phase == "post":
             self.xchg.after(writes)
+        else:  # end of the run
+            self.xchg.flush()
 
     def load_inputs(self, full_inputs: dict):
         """Every rank passes the same full host inputs; each uploads its window."""
@@ -660,18 +738,26 @@ def bench_slab(args, W):
     runner.load_inputs(inputs)
     for _ in range(args.warmup):
         runner.run()
+    runner.ex.sync()
     torch.cuda.synchronize()
     tdist.barrier()
     torch.cuda.synchronize()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
+    import ctypes
+
+    L = rt.lib()
+    e0, e1 = ctypes.c_void_p(), ctypes.c_void_p()
+    rt.check(L.b2_event_create(ctypes.byref(e0)))
+    rt.check(L.b2_event_create(ctypes.byref(e1)))
+    runner.ex.sync()
+    tdist.barrier()
     t0 = time.perf_counter()
-    start.record()
+    rt.check(L.b2_event_record(e0, runner.ex.stream))  # events on the launching stream
     for _ in range(args.steps):
         runner.run()
-    end.record()
-    torch.cuda.synchronize()
-    ms = start.elapsed_time(end) / args.steps
+    rt.check(L.b2_event_record(e1, runner.ex.stream))
+    msf = ctypes.c_float()
+    rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(msf)))
+    ms = msf.value / args.steps
     tdist.barrier()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -693,7 +779,7 @@ def bench_slab(args, W):
             "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
                          "frac": value / world / peak, "peak_kind": kind, "traffic": None,
                          "note": "per-GPU share of the whole-job algorithmic bandwidth"},
-            "gpu_launches": runner.ex.launches,
+            "gpu_launches": getattr(runner.ex, "trace_launches", 0) * args.steps,
         }
         print(json.dumps(line), flush=True)
     tdist.barrier()

@@ -374,6 +374,8 @@ class GpuExecutor:
             steps += 1
             if steps > self.opt.max_transitions:
                 raise InterpreterError("transition budget exceeded (infinite loop?)")
+        if self.op_hook is not None and not self._dry:
+            self.op_hook(None, set(), set(), "end")
 
     def _region_trips(self, reg, sym):
         from . import loops as LP

@@ -74,8 +74,14 @@ EXPORTS = [
     "b2_module_unload", "b2_module_function", "b2_func_set_max_smem", "b2_launch",
     "b2_launch_count", "b2_capture_begin", "b2_capture_end", "b2_graph_launch",
     "b2_graph_destroy", "b2_copy_view", "b2_fill_view", "b2_gemm_f64", "b2_gemm_f32",
-    "b2_reduce",
+    "b2_reduce", "b2_nccl_unique_id", "b2_nccl_init", "b2_nccl_destroy", "b2_nccl_group_p2p",
+    "b2_nccl_bcast", "b2_nccl_allreduce_f64",
 ]
+
+
+class P2P(ctypes.Structure):
+    _fields_ = [("ptr", ctypes.c_void_p), ("bytes", ctypes.c_size_t), ("peer", ctypes.c_int),
+                ("send", ctypes.c_int)]
 
 _lock = threading.Lock()
 _lib = None
@@ -129,6 +135,12 @@ _SIGS = {
                      ctypes.c_int, _vp], ctypes.c_int),
     "b2_reduce": ([ctypes.POINTER(View), ctypes.POINTER(View), ctypes.c_uint, ctypes.c_int,
                    ctypes.c_int, _vp], ctypes.c_int),
+    "b2_nccl_unique_id": ([_vp], ctypes.c_int),
+    "b2_nccl_init": ([ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(_vp)], ctypes.c_int),
+    "b2_nccl_destroy": ([_vp], ctypes.c_int),
+    "b2_nccl_group_p2p": ([_vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
+    "b2_nccl_bcast": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
+    "b2_nccl_allreduce_f64": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
 }
 
 

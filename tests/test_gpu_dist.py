@@ -1,0 +1,77 @@
+"""Multi-GPU plumbing checks that fit on ONE GPU: libb2's NCCL communicator
+(world size 1, send/recv to self inside a captured CUDA graph) and the slab
+runner's capture path.  The multi-rank logic itself is covered by the gloo
+tests in test_dist.py."""
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch
+    import torch.distributed as tdist
+
+    if not tdist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        tdist.init_process_group("gloo", rank=0, world_size=1)
+    yield
+    _ = torch
+
+
+def test_nccl_self_p2p_captured_in_graph(pg):
+    from paper_2107_00555_b200 import dist, runtime as rt
+
+    rt.device(0)
+    L = rt.lib()
+    comm = dist.NcclComm(0, 1)
+    n = 1 << 16
+    a = np.arange(n, dtype=np.float64)
+    pa, pb = ctypes.c_void_p(), ctypes.c_void_p()
+    rt.check(L.b2_malloc(ctypes.byref(pa), n * 8))
+    rt.check(L.b2_malloc(ctypes.byref(pb), n * 8))
+    s = ctypes.c_void_p()
+    rt.check(L.b2_stream_create(ctypes.byref(s)))
+    rt.check(L.b2_memcpy_h2d(pa, a.ctypes.data, n * 8, s))
+    rt.check(L.b2_memset(pb, 0, n * 8, s))
+    rt.check(L.b2_stream_sync(s))
+    rt.check(L.b2_capture_begin(s))
+    comm.p2p([(True, 0, pa.value, n * 8), (False, 0, pb.value, n * 8)], s.value)
+    ge = ctypes.c_void_p()
+    rt.check(L.b2_capture_end(s, ctypes.byref(ge)))
+    rt.check(L.b2_graph_launch(ge, s))
+    out = np.empty(n)
+    rt.check(L.b2_memcpy_d2h(out.ctypes.data, pb, n * 8, s))
+    rt.check(L.b2_stream_sync(s))
+    assert np.array_equal(out, a)
+    comm.close()
+
+
+def test_slab_runner_single_rank_matches_oracle(pg):
+    from oracle import kernels_np as K
+    from paper_2107_00555_b200 import dist, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
+    syms = {"N": 40, "TSTEPS": 6}
+    rng = np.random.default_rng(3)
+    A = rng.uniform(-1, 1, (40, 40, 40))
+    B = rng.uniform(-1, 1, (40, 40, 40))
+    r = dist.SlabGpuRunner(g, syms, 0, 1, 0)
+    r.load_inputs({"A": A, "B": B})
+    r.run()
+    out = r.gather({"A": A, "B": B})
+    K.heat_3d_c(A, B, 6)
+    assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
