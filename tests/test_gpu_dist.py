@@ -57,6 +57,8 @@ def test_nccl_self_p2p_captured_in_graph(pg):
     rt.check(L.b2_memcpy_d2h(out.ctypes.data, pb, n * 8, s))
     rt.check(L.b2_stream_sync(s))
     assert np.array_equal(out, a)
+    # a captured graph keeps NCCL work alive: destroy it before the communicator
+    rt.check(L.b2_graph_destroy(ge))
     comm.close()
 
 
