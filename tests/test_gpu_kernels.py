@@ -71,3 +71,32 @@ def test_jacobi2d_config_size_bitwise_vs_c_oracle():
     out = _run("jacobi_2d.raw", {"N": 2000, "TSTEPS": 100}, {"A": A.copy(), "B": B.copy()})
     K.jacobi_2d_c(A, B, 100)
     assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
+
+
+@pytest.mark.parametrize("M,K,N", [(512, 256, 384), (300, 200, 452), (1024, 1000, 768)])
+def test_sgemm_vs_numpy(M, K, N):
+    """f32 GEMM (SUMMA f32 config): rtol 1e-5 against an f64 product of the
+    f32-rounded inputs."""
+    import ctypes
+
+    from paper_2107_00555_b200 import runtime as rt
+
+    rt.device(0)
+    L = rt.lib()
+    rng = np.random.default_rng(M + N)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    ptr = []
+    for arr in (A, B, np.zeros((M, N), np.float32)):
+        p = ctypes.c_void_p()
+        rt.check(L.b2_malloc(ctypes.byref(p), arr.nbytes))
+        rt.check(L.b2_memcpy_h2d(p, arr.ctypes.data, arr.nbytes, None))
+        ptr.append(p)
+    rt.check(L.b2_gemm_f32(M, N, K, ptr[0], K, 1, ptr[1], N, 1, ptr[2], N, 1, 0, None))
+    C = np.empty((M, N), np.float32)
+    rt.check(L.b2_memcpy_d2h(C.ctypes.data, ptr[2], C.nbytes, None))
+    rt.check(L.b2_device_sync())
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    assert rel_err(C, ref) <= 1e-5
+    for p in ptr:
+        L.b2_free(p)
