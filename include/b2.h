@@ -96,6 +96,8 @@ B2_API int b2_event_create(void **ev);
 B2_API int b2_event_destroy(void *ev);
 B2_API int b2_event_record(void *ev, void *stream);
 B2_API int b2_event_elapsed_ms(void *start, void *end, float *ms);
+/* `stream` waits for `ev` (fork/join of side streams, also inside capture). */
+B2_API int b2_stream_wait_event(void *stream, void *ev);
 B2_API int b2_host_register(void *p, size_t bytes);
 B2_API int b2_host_unregister(void *p);
 

@@ -55,6 +55,7 @@ class KernelSpec:
         self.uses_flag = False
         self.params: list[str] = []
         self.vec = 1
+        self.dyn0 = False  # range of the first parameter is a runtime argument
         self.kernel = None  # runtime.Kernel
 
     def arg_index(self, desc) -> int:
@@ -708,6 +709,12 @@ class _Gen:
                 self.red_full = nout >= 148 * 256 or nred <= 64
                 self.red_R = R
         spec.mode = mode
+        # slab executors launch a map's chunk in pieces (boundary rows first,
+        # interior overlapped with the halo exchange): keep dim 0's range a
+        # runtime argument so one kernel serves every piece
+        self.dyn0 = (bool(getattr(self.pl, "dynamic_p0", False)) and k >= 1
+                     and mode in ("flat", "tile2", "march"))
+        spec.dyn0 = self.dyn0
         vec = 1
         if mode == "tile2":
             vec = _pick_vec(self.const_ranges[-1][2])
@@ -781,7 +788,13 @@ class _Gen:
         pro.append("  (void)flag;")
         for i in range(k):
             cr = self.const_ranges[i]
-            if cr is not None:
+            if cr is not None and i == 0 and self.dyn0:
+                # runtime start/length, compile-time stride: the compiler still
+                # sees that consecutive i0 of one thread are adjacent planes
+                pro.append(f"  const b2_ll rb0 = {self.arg(('rb', 0))};")
+                pro.append(f"  constexpr b2_ll rs0 = {cr[1]}LL;")
+                pro.append(f"  const b2_ll rl0 = {self.arg(('rl', 0))};")
+            elif cr is not None:
                 pro.append(f"  constexpr b2_ll rb{i} = {cr[0]}LL, rs{i} = {cr[1]}LL, rl{i} = {cr[2]}LL;")
             else:
                 pro.append(f"  const b2_ll rb{i} = {self.arg(('rb', i))};")
@@ -863,8 +876,8 @@ class _Gen:
         elif mode == "tile2":
             x, y = k - 1, k - 2
             tw = 32 * vec
-            loop.append(f"  constexpr b2_ll tiles_x = (rl{x} + {tw - 1}) / {tw};")
-            loop.append(f"  constexpr b2_ll tiles_y = (rl{y} + 7) / 8;")
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + {tw - 1}) / {tw};")
+            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
             outer = " * ".join(f"rl{i}" for i in range(k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({outer});")
             loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
@@ -888,9 +901,9 @@ class _Gen:
             # consecutive indices of dim 0 (unrolled) so the compiler reuses the
             # overlapping dim-0 neighbours of a stencil from registers
             x, y = k - 1, k - 2
-            loop.append(f"  constexpr b2_ll tiles_x = (rl{x} + 31) / 32;")
-            loop.append(f"  constexpr b2_ll tiles_y = (rl{y} + 7) / 8;")
-            loop.append(f"  constexpr b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + 31) / 32;")
+            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
+            loop.append(f"  const b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
             mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({mid}) * tiles_z;")
             # plane tiles vary fastest (measured better than chunk-fastest order)

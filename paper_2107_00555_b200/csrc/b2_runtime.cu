@@ -182,6 +182,10 @@ extern "C" int b2_event_elapsed_ms(void *a, void *b, float *ms) {
   if (rc) return rc;
   return b2_cuda_check(cudaEventElapsedTime(ms, (cudaEvent_t)a, (cudaEvent_t)b), "elapsed");
 }
+extern "C" int b2_stream_wait_event(void *s, void *ev) {
+  return b2_cuda_check(cudaStreamWaitEvent((cudaStream_t)s, (cudaEvent_t)ev, 0),
+                       "stream wait event");
+}
 extern "C" int b2_host_register(void *p, size_t n) {
   return b2_cuda_check(cudaHostRegister(p, n, cudaHostRegisterDefault), "host register");
 }

@@ -271,6 +271,43 @@ class SlabPlan:
                     out.append((peer, lo, hi))
         return sends, recvs
 
+    def boundary(self, r: int, keys, b: int, n: int, force: bool = False):
+        """For the slab maps `keys` ((state, entry id), fused into one launch
+        iterating global p0 = b .. b+n-1 on rank r): (n_lo, n_hi, conts) —
+        how many leading / trailing iterations produce rows other ranks read,
+        and the distributed containers written that have transfers.  None when
+        the launch cannot be split that way."""
+        if n <= 0:
+            return None
+        by_key = {(mi.state, mi.entry_id): mi for mi in self.maps}
+        its, conts = set(), set()
+        for key in keys:
+            mi = by_key.get(key)
+            if mi is None:
+                return None
+            for c, offs in mi.writes.items():
+                sends, recvs = self.transfers(c, r)
+                if sends or recvs:
+                    conts.add(c)
+                for _, glo, ghi in sends:
+                    for o in offs:
+                        # the local graph keeps global iteration indices
+                        for row in range(glo, ghi):
+                            if 0 <= row - o - b < n:
+                                its.add(row - o - b)
+        if force and not its:
+            its = {0, n - 1}
+        if not its and not conts:
+            return None
+        its = sorted(its)
+        n_lo = 0
+        while n_lo < len(its) and its[n_lo] == n_lo:
+            n_lo += 1
+        rest = its[n_lo:]
+        if rest != list(range(n - len(rest), n)):
+            return None  # boundary rows are not at the chunk ends
+        return n_lo, len(rest), conts
+
     def local_graph(self, r: int) -> sdfg.Graph:
         """Copy of the graph for rank r: distributed containers hold their row
         window, slab maps iterate the rank's chunk, memlets address local rows."""
@@ -452,9 +489,17 @@ class SlabGpuRunner:
     the whole state machine) whose op hook inserts the halo exchanges as
     NCCL group send/recv on the same stream — one graph launch per run."""
 
-    def __init__(self, g, bindings: dict, rank: int, world: int, device: int):
+    def __init__(self, g, bindings: dict, rank: int, world: int, device: int,
+                 overlap: bool | None = None, force_split: bool = False):
+        import ctypes
+        import os
+
+        if overlap is None:
+            overlap = os.environ.get("B2_SLAB_OVERLAP", "1") != "0"
+
         import torch
 
+        from . import runtime as rt
         from .machine import GpuExecutor, InterpOptions
 
         self.torch = torch
@@ -462,10 +507,66 @@ class SlabGpuRunner:
         self.plan = slab_decompose(self.g, bindings, world)
         self.rank = rank
         self.lg = self.plan.local_graph(rank)
-        self.ex = GpuExecutor(self.lg, bindings, device=device, options=InterpOptions())
+        self.ex = GpuExecutor(self.lg, bindings, device=device, options=InterpOptions(),
+                              dynamic_p0=overlap)
         self.nccl = NcclComm(rank, world) if world > 1 else None
         self.xchg = HaloExchanger(self.plan, rank, self._rows_of, transport=self._transport)
         self.ex.op_hook = self._hook
+        self._exchanged: set[str] = set()
+        self.force_split = force_split
+        self.splits = 0
+        if overlap:
+            s, e0, e1 = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+            rt.check(rt.lib().b2_stream_create(ctypes.byref(s)), "stream")
+            rt.check(rt.lib().b2_event_create(ctypes.byref(e0)), "event")
+            rt.check(rt.lib().b2_event_create(ctypes.byref(e1)), "event")
+            self.side, self.ev_fork, self.ev_join = s.value, e0.value, e1.value
+            self.ex.map_split = self._split
+
+    def _boundary(self, op, rvals):
+        b, s, n = rvals[0]
+        if s != 1 or any(m.entry is None for m in op.members):
+            return None
+        keys = [(m.state.label, m.entry.id) for m in op.members]
+        return self.plan.boundary(self.rank, keys, b, n, force=self.force_split)
+
+    def _split(self, ex, op, rvals, env) -> bool:
+        """Boundary iterations and the halo exchange of their rows on the side
+        stream, the interior on the executor stream, joined before the next
+        op: the exchange hides behind the interior sweep."""
+        from . import runtime as rt
+
+        if ex.specs[op.idx].private:
+            return False  # per-thread scratch cannot be shared by concurrent launches
+        bd = self._boundary(op, rvals)
+        if bd is None:
+            return False
+        n_lo, n_hi, conts = bd
+        if conts & set(ex.planner.op_reads[op.idx]):
+            return False  # the receives would race with the op's own reads
+        n = rvals[0][2]
+        L = rt.lib()
+        rt.check(L.b2_event_record(self.ev_fork, ex.stream), "event")
+        rt.check(L.b2_stream_wait_event(self.side, self.ev_fork), "wait")
+        ex.launch_map_rows(op, rvals, env, 0, n_lo, self.side)
+        ex.launch_map_rows(op, rvals, env, n - n_hi, n, self.side)
+        if conts:
+            ops = []
+            for c in sorted(conts):
+                sends, recvs = self.xchg.xfer[c]
+                ops += [(True, peer, c, lo, hi) for peer, lo, hi in sends]
+                ops += [(False, peer, c, lo, hi) for peer, lo, hi in recvs]
+            if ops:
+                self.xchg.bytes_sent += self.nccl.p2p(
+                    [(sd, peer) + self._rows_ptr(c, lo, hi) for sd, peer, c, lo, hi in ops],
+                    self.side)
+                self.xchg.exchanges += 1
+        rt.check(L.b2_event_record(self.ev_join, self.side), "event")
+        ex.launch_map_rows(op, rvals, env, n_lo, n - n_hi, ex.stream)
+        rt.check(L.b2_stream_wait_event(ex.stream, self.ev_join), "wait")
+        self._exchanged = set(conts)
+        self.splits += 1
+        return True
 
     def _rows_ptr(self, c, lo, hi):
         desc = self.lg.containers[c]
@@ -498,8 +599,11 @@ class SlabGpuRunner:
     def _hook(self, op, reads, writes, phase):
         if phase == "pre":
             self.xchg.before(reads)
+            self._exchanged = set()
         elif phase == "post":
-            self.xchg.after(writes)
+            # containers the split launch already exchanged stay clean
+            self.xchg.after(set(writes) - self._exchanged)
+            self._exchanged = set()
         else:  # end of the run
             self.xchg.flush()
 
@@ -734,10 +838,14 @@ def bench_slab(args, W):
     from bench import make_inputs, peaks  # noqa: E402
 
     inputs = make_inputs(g, syms)
-    runner = SlabGpuRunner(g, syms, rank, world, local)
+    runner = SlabGpuRunner(g, syms, rank, world, local,
+                           force_split=os.environ.get("B2_SLAB_FORCE_SPLIT") == "1")
     runner.load_inputs(inputs)
+    halo_per_run = None
     for _ in range(args.warmup):
         runner.run()
+        if halo_per_run is None:
+            halo_per_run = runner.xchg.bytes_sent  # the trace is captured once
     runner.ex.sync()
     torch.cuda.synchronize()
     tdist.barrier()
@@ -774,8 +882,8 @@ def bench_slab(args, W):
             "data": "synthetic (make_inputs semantics, seed 0)",
             "config": {"workload": W["desc"], "parallelism": f"slab{world} (axis-0 block "
                        "distribution, NCCL halo exchange)",
-                       "halo_bytes_per_step": runner.xchg.bytes_sent // max(1, args.steps +
-                                                                            args.warmup)},
+                       "halo_bytes_sent_per_step_rank0": halo_per_run,
+                       "overlap_splits_per_step": runner.splits},
             "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
                          "frac": value / world / peak, "peak_kind": kind, "traffic": None,
                          "note": "per-GPU share of the whole-job algorithmic bandwidth"},

@@ -123,12 +123,14 @@ class GpuExecutor:
     persist; inputs are re-uploaded each call)."""
 
     def __init__(self, g: sdfg.Graph, bindings: dict, device: int = 0, stream=None,
-                 options: InterpOptions | None = None, external: dict | None = None):
+                 options: InterpOptions | None = None, external: dict | None = None,
+                 dynamic_p0: bool = False):
         rt.device(device)
         self.g = g
         self.bindings = {k: int(v) for k, v in bindings.items()}
         self.opt = options or InterpOptions()
         self.planner = P.Planner(g, self.bindings).build()
+        self.planner.dynamic_p0 = dynamic_p0
         self.buf = _Buffers()
         self.flag = self.buf.alloc(8)
         if stream is None:
@@ -444,6 +446,24 @@ class GpuExecutor:
     # -- ops -----------------------------------------------------------------------
 
     op_hook = None  # callable(op, reads, writes, phase) used by the slab executor
+    # callable(executor, op, rvals, env) -> bool: launches a dyn0 map group in
+    # pieces itself (slab executor: boundary rows + exchange || interior)
+    map_split = None
+
+    def launch_map_rows(self, op: P.MapGroup, rvals, env, i_lo: int, i_hi: int, stream):
+        """Launch map group `op` restricted to iterations [i_lo, i_hi) of its
+        first parameter, on `stream` (kernel compiled with spec.dyn0)."""
+        if i_hi <= i_lo:
+            return
+        spec = self.specs[op.idx]
+        assert spec.dyn0, "map group was not compiled with a runtime dim-0 range"
+        b, s, _ = rvals[0]
+        sub = [(b + s * i_lo, s, i_hi - i_lo)] + list(rvals[1:])
+        grid, block = codegen.launch_geometry(spec, [n for _, _, n in sub])
+        blob = codegen.pack_args(spec, env, sub, self.buf.ptr, self.buf.strides, self.buf.size,
+                                 self.scratch, self.flag)
+        rt.launch(spec.kernel, grid, block, blob, stream)
+        self.launches += 1
 
     def _exec_op(self, op, sym, counters):
         if self._dry:
@@ -512,6 +532,11 @@ class GpuExecutor:
         if op.params and npts == 0:
             return
         if not self._check_bounds(spec, rvals, env, op.state.label, f"map group {op.idx}"):
+            return
+        if self.map_split is not None and spec.dyn0 and self._prof is None \
+                and self.map_split(self, op, rvals, env):
+            if counters is not None:
+                _count_map(self, op, rvals, counters, env)
             return
         grid, block = codegen.launch_geometry(spec, [n for _, _, n in rvals])
         blob = codegen.pack_args(spec, env, rvals, self.buf.ptr, self.buf.strides, self.buf.size,

@@ -48,6 +48,37 @@ def test_heat3d_partition_covers_interior(P):
         assert all(hi - lo == 1 for _, lo, hi in recvs)
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_heat3d_boundary_iterations(P):
+    """The overlapped slab launch computes exactly the planes other ranks
+    read first: one leading plane when a lower neighbour exists, one trailing
+    plane when an upper one does."""
+    plan = dist.slab_decompose(_graph("heat_3d.raw"), {"N": 40, "TSTEPS": 3}, P)
+    for mi in plan.maps:
+        if not set(mi.writes) & {"A", "B"}:
+            # transients are never exchanged
+            assert plan.boundary(0, [(mi.state, mi.entry_id)], mi.lo, 5) is None
+            continue
+        for r in range(P):
+            a, b = dist._chunk(mi.lo, mi.hi, P, r)
+            bd = plan.boundary(r, [(mi.state, mi.entry_id)], a, b - a + 1)
+            n_lo, n_hi, conts = bd
+            assert (n_lo, n_hi) == (int(r > 0), int(r < P - 1))
+            assert conts == set(mi.writes)
+            # the boundary planes are exactly the rows sent to neighbours
+            sent = {row for c in conts for _, lo, hi in plan.transfers(c, r)[0]
+                    for row in range(lo, hi)}
+            o = next(iter(next(iter(mi.writes.values()))))
+            its = set(range(n_lo)) | set(range(b - a + 1 - n_hi, b - a + 1))
+            assert {a + i + o for i in its} == sent
+    # single rank: nothing to split unless forced
+    p1 = dist.slab_decompose(_graph("heat_3d.raw"), {"N": 40, "TSTEPS": 3}, 1)
+    mi = p1.maps[0]
+    assert p1.boundary(0, [(mi.state, mi.entry_id)], mi.lo, mi.hi - mi.lo + 1) is None
+    assert p1.boundary(0, [(mi.state, mi.entry_id)], mi.lo, mi.hi - mi.lo + 1,
+                       force=True)[:2] == (1, 1)
+
+
 def test_local_graph_shapes_and_ranges():
     plan = dist.slab_decompose(_graph("jacobi_2d.raw"), {"N": 20, "TSTEPS": 3}, 2)
     lg = plan.local_graph(1)

@@ -75,8 +75,10 @@ def test_jacobi2d_config_size_bitwise_vs_c_oracle():
 
 @pytest.mark.parametrize("M,K,N", [(512, 256, 384), (300, 200, 452), (1024, 1000, 768)])
 def test_sgemm_vs_numpy(M, K, N):
-    """f32 GEMM (SUMMA f32 config): rtol 1e-5 against an f64 product of the
-    f32-rounded inputs."""
+    """f32 GEMM (SUMMA f32 config): rtol 1e-5 (norm-wise) against an f64
+    product of the f32-rounded inputs, and no less accurate
+    than numpy's own f32 matmul (element-wise errors of an f32 K-term sum
+    grow with K, so an element-wise 1e-5 bound does not hold for either)."""
     import ctypes
 
     from paper_2107_00555_b200 import runtime as rt
@@ -97,6 +99,9 @@ def test_sgemm_vs_numpy(M, K, N):
     rt.check(L.b2_memcpy_d2h(C.ctypes.data, ptr[2], C.nbytes, None))
     rt.check(L.b2_device_sync())
     ref = A.astype(np.float64) @ B.astype(np.float64)
-    assert rel_err(C, ref) <= 1e-5
+    ours = np.linalg.norm(C - ref) / np.linalg.norm(ref)
+    assert ours <= 1e-5
+    npf32 = np.linalg.norm((A @ B).astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert ours <= 10 * npf32 + 1e-7
     for p in ptr:
         L.b2_free(p)
