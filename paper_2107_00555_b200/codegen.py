@@ -36,6 +36,8 @@ STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
 HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (slower: off)
 REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
+# branch-free unrolled copy of the per-thread point loop for full tiles
+MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
 
 
 class KernelSpec:
@@ -894,7 +896,14 @@ class _Gen:
                    f"    if (i{x} >= rl{x}) break;"]
             for i, p in enumerate(grp.params):
                 hdr.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
-            loop += vloop(hdr)
+            if MARCH_FULL and vec > 1:
+                loop.append(f"    if (tx * {tw} + {tw} <= rl{x}) {{")
+                loop += vloop([hdr[0]] + hdr[2:])
+                loop.append("    } else {")
+                loop += vloop(hdr)
+                loop.append("    }")
+            else:
+                loop += vloop(hdr)
             loop.append("  }")
         elif mode == "march":
             # 32 x 8 tiles over dims (k-2, k-1); each thread walks `vec`
@@ -920,7 +929,16 @@ class _Gen:
                 loop.append(f"    const b2_ll p_{grp.params[i]} = rb{i} + rs{i} * i{i};")
             hdr = [f"    const b2_ll i0 = tz * {vec} + v;", "    if (i0 >= rl0) break;",
                    f"    const b2_ll p_{grp.params[0]} = rb0 + rs0 * i0;"]
-            loop += vloop(hdr)
+            if MARCH_FULL and vec > 1:
+                # full plane tiles take a branch-free copy of the unrolled
+                # loop so loads of later planes can issue before earlier math
+                loop.append(f"    if (tz * {vec} + {vec} <= rl0) {{")
+                loop += vloop([hdr[0], hdr[2]])
+                loop.append("    } else {")
+                loop += vloop(hdr)
+                loop.append("    }")
+            else:
+                loop += vloop(hdr)
             loop.append("  }")
         src = [f"// generated by paper_2107_00555_b200.codegen for state "
                f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
