@@ -434,6 +434,9 @@ int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
                   void *stream);
 int b2_sgemm_128(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
                  int64_t ldb, float *C, int64_t ldc, int accumulate, void *stream);
+int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+                int64_t ldb, float *C, int64_t ldc, int accumulate, void *stream);
+int b2_sgemm_tc_enabled();
 
 extern "C" int b2_gemm_f64(int64_t M, int64_t N, int64_t K, const double *A, int64_t rsa,
                            int64_t csa, const double *B, int64_t rsb, int64_t csb, double *C,
@@ -448,6 +451,10 @@ extern "C" int b2_gemm_f64(int64_t M, int64_t N, int64_t K, const double *A, int
 extern "C" int b2_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa,
                            int64_t csa, const float *B, int64_t rsb, int64_t csb, float *C,
                            int64_t rsc, int64_t csc, int wcr, void *stream) {
+  // tcgen05 (3xTF32) for large problems: the split pass re-lays both operands
+  if (csa == 1 && csb == 1 && csc == 1 && (wcr == B2_WCR_NONE || wcr == B2_WCR_ADD) &&
+      M >= 128 && N >= 256 && K >= 32 && M * N * K >= (1LL << 27) && b2_sgemm_tc_enabled())
+    return b2_sgemm_tc(M, N, K, A, rsa, B, rsb, C, rsc, wcr == B2_WCR_ADD, stream);
   if (csa == 1 && csb == 1 && csc == 1 && (wcr == B2_WCR_NONE || wcr == B2_WCR_ADD) &&
       rsa % 4 == 0 && rsb % 4 == 0 && (((uintptr_t)A | (uintptr_t)B) & 15) == 0 &&
       M * N * K >= (1LL << 18))

@@ -1,0 +1,409 @@
+// b2_tcgemm.cu — FP32 GEMM on the 5th-generation tensor cores (tcgen05,
+// kind::tf32) with the 3xTF32 split, for the SUMMA f32 configuration.
+//
+// The reference has no float32 type; the f32 MatMul config
+// is defined against an f64 product of the f32 inputs at rtol 1e-5.  One TF32
+// product keeps only 10 mantissa bits, so each operand is split into
+// hi = rna_tf32(x) and lo = x - hi (exact in fp32) and
+//   A B ~= lo(A) hi(B) + hi(A) lo(B) + hi(A) hi(B)
+// which is a single TF32 GEMM over a K dimension three times as long:
+//   A' = [lo(A) | hi(A) | hi(A)]   (M x 3K, K-major; interleaved per 32-wide
+//   B' = [hi(B) | lo(B) | hi(B)]^T (N x 3K, K-major)  k block, see split_a)
+// A' and B' are produced by two HBM-bound split kernels into a workspace;
+// the GEMM then runs entirely on the tensor cores:
+//   * CTA tile 128 x 256, K step 32 (one 128-byte swizzle atom of fp32),
+//     4-stage TMA -> shared memory ring (48 KB per stage, SWIZZLE_128B),
+//   * warp 0 lane 0 issues the TMA loads (mbarrier complete_tx),
+//   * warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=8) x 4 per stage into
+//     a 128 x 256 fp32 accumulator in TMEM and releases each stage with
+//     tcgen05.commit,
+//   * long in-TMEM accumulations lose accuracy (the error grows with the
+//     accumulation length), so the MMA warp accumulates chunks of 128 k into
+//     two alternating 256-column TMEM buffers and eight epilogue warps drain
+//     each finished chunk with tcgen05.ld into an fp32 register accumulator
+//     (IEEE adds) while the next chunk accumulates; the WCR (C = / += result)
+//     is applied once at the end.
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "b2.h"
+#include "b2_internal.h"
+
+namespace {
+
+constexpr int TM = 128, TN = 256, TK = 32, STAGES = 4;
+constexpr int A_BYTES = TM * TK * 4;  // 16 KB
+constexpr int B_BYTES = TN * TK * 4;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 128;
+constexpr uint32_t TMEM_COLS = 512;  // two 256-column chunk accumulators
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+// instruction descriptor: D f32 (bit 4), A/B tf32 (bits 7, 10), K-major
+// operands, N >> 3 at bit 17, M >> 4 at bit 24
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TN >> 3) << 17) |
+                           ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "B2_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra B2_DONE;\n\t"
+      "bra B2_WAIT;\n\t"
+      "B2_DONE:\n\t}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row core-matrix
+// groups 1024 bytes apart (SBO), sm100 descriptor version 1
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float *out) {
+  uint32_t v[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) out[j] = __uint_as_float(v[j]);
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    tc_sgemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+             int64_t M, int64_t N, int nk, int chunk, float *__restrict__ C, int64_t ldc,
+             int accumulate) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + STAGES * A_BYTES;
+  uint64_t *full = (uint64_t *)(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;  // [2] chunk accumulated in TMEM buffer b
+  uint64_t *tempty = tfull + 2;      // [2] TMEM buffer b drained by the epilogue
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tb) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) + 1) & 1);
+        mbar_expect_tx(&full[s], STAGE_BYTES);
+        tma_load_2d(sa + s * A_BYTES, &ta, &full[s], kb * TK, m0);
+        tma_load_2d(sb + s * B_BYTES, &tb, &full[s], kb * TK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // MMA issuer: chunk j accumulates in TMEM buffer j & 1 (256 columns)
+      for (int kb = 0; kb < nk; ++kb) {
+        const int j = kb / chunk, b = j & 1;
+        const bool first = kb - j * chunk == 0;
+        if (first && j >= 2) {
+          mbar_wait(&tempty[b], ((j >> 1) + 1) & 1);
+          fence_after();
+        }
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        fence_after();
+        const uint64_t da = sw128_desc(smem_u32(sa + s * A_BYTES));
+        const uint64_t db = sw128_desc(smem_u32(sb + s * B_BYTES));
+#pragma unroll
+        for (int k = 0; k < TK / 8; ++k)  // 8 tf32 = 32 bytes = 2 descriptor units
+          mma_tf32(tmem + (uint32_t)(b * TN), da + 2 * k, db + 2 * k, !(first && k == 0));
+        mma_commit(&empty[s]);
+        if (kb - j * chunk == chunk - 1 || kb == nk - 1) mma_commit(&tfull[b]);
+      }
+    }
+  } else {
+    // epilogue warps: warp w may read TMEM lanes 32 * (w % 4) ..; the eight
+    // warps split the 256 columns in two halves.  Chunk partial sums are added
+    // into an fp32 register accumulator (IEEE adds) as they complete.
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    float acc[TN / 2];
+#pragma unroll
+    for (int i = 0; i < TN / 2; ++i) acc[i] = 0.f;
+    const int nchunks = (nk + chunk - 1) / chunk;
+    for (int j = 0; j < nchunks; ++j) {
+      const int b = j & 1;
+      mbar_wait(&tfull[b], (j >> 1) & 1);
+      fence_after();
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * TN + half * (TN / 2));
+#pragma unroll
+      for (int c = 0; c < TN / 2; c += 16) {
+        float v[16];
+        tmem_ld16(base + (uint32_t)c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+    const int64_t row = m0 + q * 32 + lane;
+    if (row < M) {
+      float *crow = C + row * ldc + n0 + half * (TN / 2);
+      const int64_t ncol = N - (n0 + half * (TN / 2));
+#pragma unroll
+      for (int i = 0; i < TN / 2; ++i)
+        if (i < ncol) crow[i] = accumulate ? crow[i] + acc[i] : acc[i];
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t u;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+  return __uint_as_float(u);
+}
+
+// A (M x K, row stride lda) -> A' (M x Kp): per 32-wide k block b the 96
+// columns [lo | hi | hi] of A[:, 32b : 32b + 32] (zero past K), so any range
+// of k blocks is a contiguous range of A' columns
+__global__ void split_a(const float *__restrict__ A, int64_t lda, int64_t M, int64_t K,
+                        int64_t Kp, float *__restrict__ Ap) {
+  const int64_t total = M * Kp;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = f / Kp, kk = f - i * Kp;
+    const int64_t kb = kk / (3 * TK);
+    const int r = (int)(kk - kb * 3 * TK), seg = r / TK;
+    const int64_t k = kb * TK + (r - seg * TK);
+    float out = 0.f;
+    if (k < K) {
+      const float a = A[i * lda + k];
+      const float hi = tf32_rna(a);
+      out = seg == 0 ? a - hi : hi;
+    }
+    Ap[f] = out;
+  }
+}
+
+// B (K x N, row stride ldb) -> B'^T (N x Kp): per k block [hi | lo | hi],
+// through a 32 x 32 shared tile so both the read and the write are coalesced
+__global__ void split_bt(const float *__restrict__ B, int64_t ldb, int64_t K, int64_t N,
+                         int64_t Kp, float *__restrict__ Bt) {
+  __shared__ float t[32][33];
+  const int64_t kb = blockIdx.y, k0 = kb * 32, n0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t k = k0 + ty + 8 * r, n = n0 + tx;
+    t[ty + 8 * r][tx] = (k < K && n < N) ? B[k * ldb + n] : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t n = n0 + ty + 8 * r;
+    if (n < N) {
+      const float b = t[tx][ty + 8 * r];
+      const float hi = tf32_rna(b);
+      float *dst = Bt + n * Kp + kb * 3 * TK + tx;
+      dst[0] = hi;
+      dst[TK] = b - hi;
+      dst[2 * TK] = hi;
+    }
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        p)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+int make_map(CUtensorMap *map, const float *base, uint64_t inner, uint64_t outer,
+             uint32_t box_outer) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return b2_fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 4};
+  cuuint32_t box[2] = {(cuuint32_t)TK, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return b2_fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return B2_OK;
+}
+
+int64_t tc_chunk_kblocks() {
+  static int64_t c = -1;
+  if (c < 0) {
+    const char *e = getenv("B2_TC_CHUNK");  // k elements per accumulation chunk
+    const int64_t k = e ? atoll(e) : 128;
+    c = k > 0 ? (k + TK - 1) / TK : ((int64_t)1 << 28);
+  }
+  return c;
+}
+
+// split-operand workspace, grown on demand (one process drives one GPU)
+float *g_ws = nullptr;
+size_t g_ws_bytes = 0;
+
+}  // namespace
+
+// C (row stride ldc, unit column stride) (=|+=) A @ B, A row-major M x K
+// (row stride lda), B row-major K x N (row stride ldb).
+int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
+                int64_t ldb, float *C, int64_t ldc, int accumulate, void *stream) {
+  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * 3 * TK;
+  const size_t need = (size_t)(M + N) * (size_t)Kp * sizeof(float);
+  cudaStream_t s = (cudaStream_t)stream;
+  B2_CLEAR_ERROR();
+  if (need > g_ws_bytes) {
+    if (g_ws) {
+      cudaStreamSynchronize(s);
+      cudaFree(g_ws);
+      g_ws = nullptr;
+      g_ws_bytes = 0;
+    }
+    if (cudaMalloc(&g_ws, need) != cudaSuccess) {
+      g_ws = nullptr;
+      return b2_fail(B2_ERR_CUDA, "tc sgemm workspace (%zu bytes)", need);
+    }
+    g_ws_bytes = need;
+  }
+  float *Ap = g_ws, *Bt = g_ws + (size_t)M * Kp;
+  split_a<<<148 * 16, 256, 0, s>>>(A, lda, M, K, Kp, Ap);
+  B2_LAUNCH_CHECK("split_a");
+  dim3 tb(32, 8), gb((unsigned)((N + 31) / 32), (unsigned)nkb);
+  split_bt<<<gb, tb, 0, s>>>(B, ldb, K, N, Kp, Bt);
+  B2_LAUNCH_CHECK("split_bt");
+  CUtensorMap ma, mb;
+  int rc = make_map(&ma, Ap, (uint64_t)Kp, (uint64_t)M, TM);
+  if (rc) return rc;
+  rc = make_map(&mb, Bt, (uint64_t)Kp, (uint64_t)N, TN);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
+        cudaSuccess)
+      return b2_fail(B2_ERR_CUDA, "tc sgemm smem attribute");
+    attr = true;
+  }
+  dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
+  tc_sgemm<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, (int)(3 * nkb),
+                                             (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate);
+  B2_LAUNCH_CHECK("tc sgemm");
+  return B2_OK;
+}
+
+int b2_sgemm_tc_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("B2_TC_SGEMM");
+    on = !(e && e[0] == '0');
+  }
+  return on;
+}

@@ -105,3 +105,40 @@ def test_sgemm_vs_numpy(M, K, N):
     assert ours <= 10 * npf32 + 1e-7
     for p in ptr:
         L.b2_free(p)
+
+
+@pytest.mark.parametrize("M,K,N,acc", [(1024, 512, 1024, False), (1000, 300, 777, True),
+                                       (256, 4096, 512, False)])
+def test_tc_sgemm_3xtf32_vs_numpy(M, K, N, acc):
+    """tcgen05 3xTF32 path of b2_gemm_f32 (large problems), incl. ragged tiles
+    (TMA zero fill, guarded epilogue) and WCR add: same bar as above."""
+    import ctypes
+
+    from paper_2107_00555_b200 import runtime as rt
+
+    rt.device(0)
+    L = rt.lib()
+    rng = np.random.default_rng(M * 7 + N)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    C0 = rng.uniform(-1, 1, (M, N)).astype(np.float32) if acc else np.zeros((M, N), np.float32)
+    ptr = []
+    for arr in (A, B, C0):
+        p = ctypes.c_void_p()
+        rt.check(L.b2_malloc(ctypes.byref(p), arr.nbytes))
+        rt.check(L.b2_memcpy_h2d(p, arr.ctypes.data, arr.nbytes, None))
+        ptr.append(p)
+    n0 = L.b2_launch_count()
+    rt.check(L.b2_gemm_f32(M, N, K, ptr[0], K, 1, ptr[1], N, 1, ptr[2], N, 1,
+                           1 if acc else 0, None))
+    assert L.b2_launch_count() - n0 >= 3  # split A, split B, tensor-core GEMM
+    C = np.empty((M, N), np.float32)
+    rt.check(L.b2_memcpy_d2h(C.ctypes.data, ptr[2], C.nbytes, None))
+    rt.check(L.b2_device_sync())
+    ref = C0.astype(np.float64) + A.astype(np.float64) @ B.astype(np.float64)
+    ours = np.linalg.norm(C - ref) / np.linalg.norm(ref)
+    assert ours <= 1e-5, ours
+    npf32 = np.linalg.norm((C0 + A @ B).astype(np.float64) - ref) / np.linalg.norm(ref)
+    assert ours <= 10 * npf32 + 1e-7
+    for p in ptr:
+        L.b2_free(p)
