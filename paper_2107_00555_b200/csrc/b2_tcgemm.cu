@@ -137,7 +137,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
 __global__ void __launch_bounds__(THREADS, 1)
     tc_sgemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
              int64_t M, int64_t N, int nk, int chunk, float *__restrict__ C, int64_t ldc,
-             int accumulate) {
+             int accumulate, int num_m, int num_n, int group_m) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t *sa = smem;
@@ -148,7 +148,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t *tempty = tfull + 2;      // [2] TMEM buffer b drained by the epilogue
   uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * TM, n0 = blockIdx.x * TN;
+  // grouped rasterisation: concurrently resident CTAs cover a group_m-tall
+  // band of tiles, so their A and B k-slabs are shared through L2
+  const int pid = blockIdx.x, per_group = group_m * num_n;
+  const int first_m = (pid / per_group) * group_m;
+  const int gsize = num_m - first_m < group_m ? num_m - first_m : group_m;
+  const int m0 = (first_m + (pid % per_group) % gsize) * TM;
+  const int n0 = ((pid % per_group) / gsize) * TN;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -392,9 +398,16 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
       return b2_fail(B2_ERR_CUDA, "tc sgemm smem attribute");
     attr = true;
   }
-  dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM));
-  tc_sgemm<<<grid, THREADS, SMEM_BYTES, s>>>(ma, mb, M, N, (int)(3 * nkb),
-                                             (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate);
+  const int num_m = (int)((M + TM - 1) / TM), num_n = (int)((N + TN - 1) / TN);
+  static int group_m = -1;
+  if (group_m < 0) {
+    const char *e = getenv("B2_TC_GROUP");
+    group_m = e ? atoi(e) : 16;
+    if (group_m < 1) group_m = 1;
+  }
+  tc_sgemm<<<num_m * num_n, THREADS, SMEM_BYTES, s>>>(
+      ma, mb, M, N, (int)(3 * nkb), (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate, num_m,
+      num_n, group_m);
   B2_LAUNCH_CHECK("tc sgemm");
   return B2_OK;
 }
