@@ -13,6 +13,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "b2.h"
 #include "b2_internal.h"
@@ -98,14 +99,19 @@ template <bool VEC>
 __global__ void __launch_bounds__(256, 1)
     dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
                const double *__restrict__ B, int64_t ldb, double *__restrict__ C, int64_t rsc,
-               int64_t csc, int accumulate) {
+               int64_t csc, int accumulate, int num_m, int num_n, int group_m) {
   extern __shared__ __align__(16) double smem[];
   double *As = smem;
   double *Bs = smem + STAGES * AS_TILE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  // grouped rasterisation: resident CTAs cover a group_m-tall band of tiles
+  const int pid = blockIdx.x, per_group = group_m * num_n;
+  const int first_m = (pid / per_group) * group_m;
+  const int gsize = num_m - first_m < group_m ? num_m - first_m : group_m;
+  const int64_t m0 = (int64_t)(first_m + (pid % per_group) % gsize) * BM;
+  const int64_t n0 = (int64_t)((pid % per_group) / gsize) * BN;
   const int ktiles = (int)((K + BK - 1) / BK);
 
   double acc[4][4][4];
@@ -189,14 +195,21 @@ int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
   }
   const bool vec = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
                    (((uintptr_t)B & 15) == 0);
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  const int num_m = (int)((M + BM - 1) / BM), num_n = (int)((N + BN - 1) / BN);
+  static int group_m = -1;
+  if (group_m < 0) {
+    const char *e = getenv("B2_DGEMM_GROUP");
+    group_m = e ? atoi(e) : 16;
+    if (group_m < 1) group_m = 1;
+  }
+  const unsigned grid = (unsigned)(num_m * num_n);
   B2_CLEAR_ERROR();
   if (vec)
-    dgemm_dmma<true><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(M, N, K, A, lda, B, ldb, C,
-                                                                        rsc, csc, accumulate);
+    dgemm_dmma<true><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(
+        M, N, K, A, lda, B, ldb, C, rsc, csc, accumulate, num_m, num_n, group_m);
   else
-    dgemm_dmma<false><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(M, N, K, A, lda, B, ldb, C,
-                                                                         rsc, csc, accumulate);
+    dgemm_dmma<false><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(
+        M, N, K, A, lda, B, ldb, C, rsc, csc, accumulate, num_m, num_n, group_m);
   B2_LAUNCH_CHECK("dgemm launch");
   return B2_OK;
 }
