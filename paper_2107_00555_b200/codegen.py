@@ -38,6 +38,7 @@ HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (s
 REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
+MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 
 
 class KernelSpec:
@@ -92,6 +93,7 @@ class _Gen:
         self.red_targets: dict = {}
         self.red_pout: list = []
         self.red_full = False
+        self.ptr_override: dict[str, str] = {}  # container -> C pointer name
 
     def _wkey(self, m: sdfg.Memlet, env: dict):
         rename = {mp: v[2:] for mp, v in env.items() if isinstance(v, str) and v.startswith("p_")}
@@ -401,6 +403,8 @@ class _Gen:
         return " + ".join(terms)
 
     def ptr(self, name: str) -> str:
+        if name in self.ptr_override:
+            return self.ptr_override[name]
         pl = self.place(name)
         return f"pv_{name}" if pl == "private" else f"c_{name}"
 
@@ -734,7 +738,7 @@ class _Gen:
             vec = int(os.environ["B2_VEC"])
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1), "march": (32, 8, 1), "reduce": (256, 1, 1),
+                      "tile2": (32, 8, 1), "march": (32, MARCH_BY, 1), "reduce": (256, 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -762,7 +766,8 @@ class _Gen:
         self.lines = self.lines[:body_lines_start]
 
         pro: list[str] = []
-        pro.append(f'extern "C" __global__ void __launch_bounds__(256) '
+        nthr = spec.block[0] * spec.block[1] * spec.block[2]
+        pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}) '
                    f"{spec.name}(const __grid_constant__ B2Args a) {{")
         for name in spec.containers:
             c = self.g.containers[name]
@@ -910,8 +915,9 @@ class _Gen:
             # consecutive indices of dim 0 (unrolled) so the compiler reuses the
             # overlapping dim-0 neighbours of a stencil from registers
             x, y = k - 1, k - 2
+            by = MARCH_BY
             loop.append(f"  const b2_ll tiles_x = (rl{x} + 31) / 32;")
-            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
+            loop.append(f"  const b2_ll tiles_y = (rl{y} + {by - 1}) / {by};")
             loop.append(f"  const b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
             mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({mid}) * tiles_z;")
@@ -922,7 +928,7 @@ class _Gen:
             for i in reversed(range(1, k - 2)):
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
             loop.append("    const b2_ll tz = rem;")
-            loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
+            loop.append(f"    const b2_ll i{y} = ty * {by} + threadIdx.y;")
             loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
             loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
             for i in range(1, k):
@@ -1226,13 +1232,13 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
         return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
     if spec.mode == "march":
-        nvb = -(-rl[k - 1] // 32) * -(-rl[k - 2] // 8) * -(-rl[0] // spec.vec)
+        nvb = -(-rl[k - 1] // 32) * -(-rl[k - 2] // MARCH_BY) * -(-rl[0] // spec.vec)
         for v in rl[1: k - 2]:
             nvb *= v
         blocks = max(1, min(nvb, MAX_BLOCKS * 8))
         if spec.private:
             blocks = max(1, min(blocks, MAX_BLOCKS))
-        return (blocks, 1, 1), (32, 8, 1)
+        return (blocks, 1, 1), (32, MARCH_BY, 1)
     tw = 32 * spec.vec
     tiles = ((rl[k - 1] + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:

@@ -196,6 +196,7 @@ class GpuExecutor:
                 self.specs[op.idx] = spec
             elif isinstance(op, P.LibOp) and op.rowpass is not None:
                 op.rowpass.compile(self)
+        self._compile_pairs()
         # private scratch sized for the largest grid of the owning kernel
         for idx, spec in self.specs.items():
             for n in spec.private:
@@ -203,6 +204,88 @@ class GpuExecutor:
                 threads = codegen.MAX_BLOCKS * 256
                 self.scratch[n] = self.buf.alloc(per * threads)
                 self.buf.nbytes[n + "#scratch"] = per * threads
+
+    def _compile_pairs(self):
+        """Temporal pairs of stencil sweeps (temporal.py): one kernel for
+        two consecutive groups, writing the second's output into a
+        ping-pong buffer the executor swaps in afterwards."""
+        from . import temporal
+
+        self.pairs: dict[int, tuple] = {}
+        self.pair_second: set[int] = set()
+        if self.planner.dynamic_p0 or any(isinstance(op, P.NestedOp)
+                                          for op in self.planner.all_ops):
+            return
+        for g1, g2, X, Y, o1, emin, emax in temporal.find_pairs(self.planner):
+            if g1.idx not in self.specs or g2.idx not in self.specs:
+                continue
+            name = f"b2_pair_{self.g.name}_{g1.idx}"
+            try:
+                spec = temporal.generate_pair(self.planner, g1, g2, X, Y, o1, emin, emax,
+                                              self.buf.shape, name)
+            except P.PlanError:
+                continue
+            alt = Y + "#alt"
+            if alt not in self.buf.ptr:
+                self.buf.ptr[alt] = self.buf.alloc(self.buf.nbytes[Y])
+                self.buf.nbytes[alt] = self.buf.nbytes[Y]
+            spec.kernel = rt.get_kernel(rt.family_source("prelude.cuh") + "\n" + spec.source,
+                                        name)
+            self.pairs[g1.idx] = (g2, spec, Y)
+            self.pair_second.add(g2.idx)
+
+    def _pp_begin(self):
+        self._pp_flip = {spec_y: False for (_, _, spec_y) in self.pairs.values()}
+        self._pp_synced: set = set()
+
+    def _pp_end(self):
+        """Leave every ping-ponged container in its original buffer (the
+        captured graph and the next upload/download use fixed addresses)."""
+        for y, flipped in getattr(self, "_pp_flip", {}).items():
+            if flipped:
+                alt = y + "#alt"
+                rt.check(rt.lib().b2_memcpy_d2d(self.buf.ptr[alt], self.buf.ptr[y],
+                                                self.buf.nbytes[y], self.stream), "pp copy")
+                self.buf.ptr[y], self.buf.ptr[alt] = self.buf.ptr[alt], self.buf.ptr[y]
+        self._pp_flip = {}
+
+    def _exec_pair(self, g1, sym, counters):
+        g2, spec, y = self.pairs[g1.idx]
+        rv1 = codegen.range_values(g1, sym)
+        rv2 = codegen.range_values(g2, sym)
+        if not self._check_bounds(self.specs[g1.idx], rv1, sym, g1.state.label,
+                                  f"map group {g1.idx}"):
+            return
+        if not self._check_bounds(self.specs[g2.idx], rv2, sym, g2.state.label,
+                                  f"map group {g2.idx}"):
+            return
+        alt = y + "#alt"
+        if y not in self._pp_synced:
+            # the pair writes only the interior of Y#alt: start it as a copy
+            rt.check(rt.lib().b2_memcpy_d2d(self.buf.ptr[alt], self.buf.ptr[y],
+                                            self.buf.nbytes[y], self.stream), "pp init")
+            self._pp_synced.add(y)
+        from . import temporal
+
+        grid, block = temporal.pair_geometry(spec)
+        blob = codegen.pack_args(spec, sym, rv2, self.buf.ptr, self.buf.strides, self.buf.size,
+                                 self.scratch, self.flag)
+        if self._prof is not None:
+            ev = self._prof_event_pair()
+            rt.lib().b2_event_record(ev[0], self.stream)
+        rt.launch(spec.kernel, grid, block, blob, self.stream)
+        if self._prof is not None:
+            rt.lib().b2_event_record(ev[1], self.stream)
+            n = 1
+            for _, _, k in rv2:
+                n *= k
+            self._prof.append((spec.name, 2 * n, ev))
+        self.launches += 1
+        self.buf.ptr[y], self.buf.ptr[alt] = self.buf.ptr[alt], self.buf.ptr[y]
+        self._pp_flip[y] = not self._pp_flip.get(y, False)
+        if counters is not None:
+            _count_map(self, g1, rv1, counters, sym)
+            _count_map(self, g2, rv2, counters, sym)
 
     def close(self):
         if self.graph_exec is not None:
@@ -345,6 +428,8 @@ class GpuExecutor:
     def _run_states(self, counters, eager: bool):
         g = self.g
         sym = dict(self.bindings)
+        if not self._dry:
+            self._pp_begin()
         cur = g.start
         steps = 0
         while cur is not None:
@@ -376,6 +461,8 @@ class GpuExecutor:
             steps += 1
             if steps > self.opt.max_transitions:
                 raise InterpreterError("transition budget exceeded (infinite loop?)")
+        if not self._dry:
+            self._pp_end()
         if self.op_hook is not None and not self._dry:
             self.op_hook(None, set(), set(), "end")
 
@@ -469,6 +556,11 @@ class GpuExecutor:
         if self._dry:
             if isinstance(op, P.NestedOp):
                 self._exec_nested(op, sym, None, dry=True)
+            return
+        if op.idx in self.pair_second:
+            return  # ran inside the pair kernel of its predecessor
+        if op.idx in self.pairs:
+            self._exec_pair(op, sym, counters)
             return
         if self.op_hook is not None:
             self.op_hook(op, self.planner.op_reads[op.idx], self.planner.op_writes[op.idx], "pre")
