@@ -38,6 +38,7 @@ HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (s
 REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
+ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reductions
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 
 
@@ -195,6 +196,90 @@ class _Gen:
             else:
                 cond = "" if full else "if (lo < hi) "
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
+        L.append("  }")
+        return L
+
+    def _rowred_plan(self):
+        """Row-reduction schedule for a parallel map whose WCR targets do not
+        depend on its last (contiguous) parameter L but whose other memory
+        writes are full points (softmax: ``ex = exp(x - mx)`` plus
+        ``sm += ex`` over L).  One warp per output row: lanes stride L
+        (coalesced loads/stores), accumulate in registers, combine with a
+        fixed xor-shuffle tree and commit once.  The sum is re-associated
+        (within the rel_err 1e-12 contract)."""
+        grp = self.group
+        k = len(grp.params)
+        if grp.schedule != "parallel" or k < 2 or any(r is None for r in self.const_ranges):
+            return None
+        if self.const_ranges[-1][2] < 32:
+            return None
+        last = grp.params[-1]
+        targets: dict = {}
+        reads: dict = {}
+        pointw: dict = {}
+        for mem in grp.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if not w:
+                    reads.setdefault(c, set()).add(pt)
+                    continue
+                if self.place(c) == "reg":
+                    continue
+                if depth != 0 or pt is None or self.place(c) != "memory":
+                    return None
+                deps = {p for key in pt for (p, _) in key[1]}
+                if wcr is None:
+                    if deps != set(grp.params) or pointw.get(c, pt) != pt:
+                        return None
+                    pointw[c] = pt
+                    continue
+                if last in deps or self.g.containers[c].dtype != "f64":
+                    return None
+                targets[(c, pt)] = (wcr, deps)
+        if not targets:
+            return None
+        if set(reads) & {c for (c, _) in targets}:
+            return None
+        for c, pt in pointw.items():  # a written container is only re-read at its own point
+            if reads.get(c, {pt}) != {pt}:
+                return None
+        return [last], list(grp.params[:-1]), targets
+
+    def _rowred_loop(self, pout, reg_decls, body) -> list:
+        grp = self.group
+        idx = {p: i for i, p in enumerate(grp.params)}
+        nout = 1
+        for p in pout:
+            nout *= self.const_ranges[idx[p]][2]
+        self.spec.red_threads = nout * 32
+        iL = len(grp.params) - 1
+        L = [f"  constexpr b2_ll NOUT = {nout}LL;",
+             "  const int lane = threadIdx.x & 31;",
+             "  for (b2_ll row = ((b2_ll)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < NOUT;",
+             "       row += ((b2_ll)gridDim.x * blockDim.x) >> 5) {",
+             "    b2_ll rem = row;"]
+        for p in reversed(pout):
+            i = idx[p]
+            L.append(f"    const b2_ll q{i} = rem % rl{i}; rem /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * q{i};")
+        for t in self.red.values():
+            ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
+            L.append(f"    {t['ct']} {t['acc']} = ({t['ct']})({ident});")
+        L.append(f"    for (int j{iL} = lane; j{iL} < (int)rl{iL}; j{iL} += 32) {{")
+        L.append(f"    const b2_ll p_{grp.params[-1]} = rb{iL} + rs{iL} * j{iL};")
+        L += reg_decls(4)
+        L += body
+        L.append("    }")
+        for t in self.red.values():
+            a = t["acc"]
+            L.append(f"    for (int o = 16; o > 0; o >>= 1) {a} = b2_op_{t['wcr']}({a}, "
+                     f"__shfl_xor_sync(0xffffffffu, {a}, o));")
+        L.append("    if (lane == 0) {")
+        for t in self.red.values():
+            if t["exclusive"]:
+                L.append(f"      {t['target']} = b2_op_{t['wcr']}({t['target']}, {t['acc']});")
+            else:
+                L.append(f"      b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
+        L.append("    }")
         L.append("  }")
         return L
 
@@ -714,6 +799,16 @@ class _Gen:
                     nred *= self.const_ranges[grp.params.index(p)][2]
                 self.red_full = nout >= 148 * 256 or nred <= 64
                 self.red_R = R
+        if mode in ("flat", "tile2", "march") and ROWRED_MODE:
+            rp = self._rowred_plan()
+            if rp is not None:
+                R, pout, targets = rp
+                mode = "rowred"
+                self.red = {}
+                self.red_targets = targets
+                self.red_pout = pout
+                self.red_full = False
+                self.red_R = R
         spec.mode = mode
         # slab executors launch a map's chunk in pieces (boundary rows first,
         # interior overlapped with the halo exchange): keep dim 0's range a
@@ -739,6 +834,7 @@ class _Gen:
         spec.vec = vec
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, 8, 1), "march": (32, MARCH_BY, 1), "reduce": (256, 1, 1),
+                      "rowred": (256, 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -880,6 +976,8 @@ class _Gen:
             loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
         elif mode == "reduce":
             loop += self._reduce_loop(self.red_R, self.red_pout, reg_decls, shift(body, -2))
+        elif mode == "rowred":
+            loop += self._rowred_loop(self.red_pout, reg_decls, shift(body, -2))
         elif mode == "tile2":
             x, y = k - 1, k - 2
             tw = 32 * vec
@@ -1224,7 +1322,7 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (256, 1, 1)
     k = len(rl)
-    if spec.mode == "reduce":
+    if spec.mode in ("reduce", "rowred"):
         n = getattr(spec, "red_threads", 1)
         return (max(1, min(-(-n // 256), MAX_BLOCKS * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "stencil":

@@ -39,7 +39,8 @@ SUITE = {
                 198 * (8 * 400 ** 3 + 8 * 398 ** 3), "B"),
     "matmul_f64": ("matmul.raw", {"M": 16384, "K": 16384, "N": 16384}, "fp64",
                    2 * 16384 ** 3, "flop"),
-    "go_fast": ("go_fast.raw", {"N": 12000}, "hbm", 16 * 12000 ** 2, "B"),
+    # the reference pipeline (parse | optimize) turns the trace loop into a WCR map
+    "go_fast": ("go_fast.pipe", {"N": 12000}, "hbm", 16 * 12000 ** 2, "B"),
     "azimint_naive": ("azimint_naive.raw", {"N": 1000000, "NPT": 1000}, "compute",
                       1000000 * 1000, "pairs"),
     "conv2d_bias": ("conv2d_bias.raw", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16, "K": 20,

@@ -1,2 +1,3 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 900 python -m pytest tests -m gpu -q -o faulthandler_timeout=200 2>&1 | tail -3
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x -o faulthandler_timeout=200 2>&1 | tail -3
+timeout -s KILL 300 python scripts/probe_time.py softmax.raw '{"N": 64, "H": 16, "SM": 512}' 3 2>&1 | grep -E "rep 2|kernel|Error" | head -4

@@ -14,4 +14,6 @@ $P gemver.raw '{"N": 8000}' 2 > gpurun_out/plain3.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:b2_rp_gemver_0 -s 1 -c 1 -o gpurun_out/prof_gemver $P gemver.raw '{"N": 8000}' 2 > gpurun_out/ncu3.log 2>&1
 $P matmul.raw '{"M": 4096, "K": 4096, "N": 4096}' 2 > gpurun_out/plain4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:dgemm -s 1 -c 1 -o gpurun_out/prof_dgemm $P matmul.raw '{"M": 4096, "K": 4096, "N": 4096}' 2 > gpurun_out/ncu4.log 2>&1
+python scripts/probe_sgemm.py 4096 2 > gpurun_out/plain5.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:tc_sgemm -s 1 -c 1 -o gpurun_out/prof_tcsgemm python scripts/probe_sgemm.py 4096 2 > gpurun_out/ncu5.log 2>&1
 echo done
