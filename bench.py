@@ -49,14 +49,21 @@ WORKLOADS = {
         "desc": "heat_3d float64 N=400 TSTEPS=100 (BASELINE configs[2])",
         "sweeps": lambda s: 2 * (s["TSTEPS"] - 1), "sweep_bytes": lambda s: _heat_bytes(s["N"]),
         "points": lambda s: (s["N"] - 2) ** 3,
+        "l2_note": "inputs (2 x N^3 f64 = 1 GB) larger than the 126 MB L2; no flush",
     },
     "jacobi_2d": {
         "graph": "jacobi_2d.raw", "syms": {"N": 2000, "TSTEPS": 100},
         "desc": "jacobi_2d float64 N=2000 TSTEPS=100 (BASELINE configs[0])",
         "sweeps": lambda s: 2 * (s["TSTEPS"] - 1), "sweep_bytes": lambda s: _jac_bytes(s["N"]),
         "points": lambda s: (s["N"] - 2) ** 2,
+        "l2_resident": True,
+        "l2_note": "2 x 32 MB inputs fit in L2: 256 MB memset between timed steps "
+                   "(outside the per-step events); within a run the sweeps are L2-resident",
     },
 }
+
+
+FLUSH_BYTES = 256 << 20
 
 
 def peaks():
@@ -68,36 +75,47 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons streamed (every 50 ms) during the
+    timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index=0):
         self.samples = []
-        self.stop = threading.Event()
         self.gpu = gpu_index
-        self.t = threading.Thread(target=self.run, daemon=True)
+        self.proc = None
+        self.t = None
 
-    def run(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
-        while not self.stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"],
-                                     capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:  # noqa: BLE001
-                pass
-            self.stop.wait(0.2)
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.strip().split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self.t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self.stop.set()
-        self.t.join(timeout=10)
+        if self.proc is not None:
+            time.sleep(0.06)  # at least one sample even for short regions
+            self.proc.terminate()  # our own child, by handle
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            if self.t is not None:
+                self.t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
@@ -126,29 +144,39 @@ def make_inputs(g, syms, seed=0):
     return out
 
 
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def cpu_sample(workload, syms, sweeps=2):
     """The reference's CPU path (numpy port of evaluate_program) on a bounded
-    sample: ``sweeps`` half-steps at the full config size.  Returns
-    (GB/s algorithmic, seconds, description)."""
+    sample: ``sweeps`` half-steps at the full config size, the planes split
+    over every host thread (same per-element op order).  Returns (GB/s
+    algorithmic, seconds, description, threads)."""
     from oracle import kernels_np as K
 
     N = syms["N"]
+    th = cpu_threads()
     rng = np.random.default_rng(0)
     if workload == "heat_3d":
         A = rng.uniform(-1, 1, (N, N, N))
         B = rng.uniform(-1, 1, (N, N, N))
         t = time.perf_counter()
-        K.heat_3d_sweeps(A, B, sweeps)
+        K.heat_3d_sweeps_mt(A, B, sweeps, th)
         dt = time.perf_counter() - t
         byts = sweeps * _heat_bytes(N)
     else:
         A = rng.uniform(-1, 1, (N, N))
         B = rng.uniform(-1, 1, (N, N))
         t = time.perf_counter()
-        K.jacobi_2d(A, B, 1 + sweeps // 2)
+        K.jacobi_2d_sweeps_mt(A, B, sweeps, th)
         dt = time.perf_counter() - t
-        byts = 2 * (sweeps // 2) * _jac_bytes(N)
-    return byts / dt / 1e9, dt, f"{sweeps} sweeps of {workload} N={N} via numpy (evaluate_program port)"
+        byts = sweeps * _jac_bytes(N)
+    return (byts / dt / 1e9, dt, f"{sweeps} sweeps of {workload} N={N} via numpy "
+            f"(evaluate_program port, planes split over {th} threads)", th)
 
 
 def run_reference(args, W):
@@ -160,7 +188,7 @@ def run_reference(args, W):
         cpu_sample(args.workload, syms, 2)
     vals, ts = [], []
     for _ in range(args.steps):
-        v, dt, desc = cpu_sample(args.workload, syms, 2)
+        v, dt, desc, th = cpu_sample(args.workload, syms, 2)
         vals.append(v)
         ts.append(dt)
     value = float(np.median(vals))
@@ -170,7 +198,7 @@ def run_reference(args, W):
         "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": W["desc"], "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": th, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -214,18 +242,35 @@ def run_ours(args, W):
     ex.sync()
     launches_per_step = getattr(ex, "trace_launches", None)
 
-    e0, e1 = ctypes.c_void_p(), ctypes.c_void_p()
-    L.b2_event_create(ctypes.byref(e0))
-    L.b2_event_create(ctypes.byref(e1))
+    # one event pair per step; when the working set fits in L2 (jacobi_2d's
+    # 2 x 32 MB) a 256 MB memset between steps evicts it, outside the events
+    flush = W.get("l2_resident", False)
+    fbuf = ctypes.c_void_p()
+    if flush:
+        rt.check(L.b2_malloc(ctypes.byref(fbuf), FLUSH_BYTES))
+    evs = []
+    for _ in range(args.steps):
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        L.b2_event_create(ctypes.byref(a))
+        L.b2_event_create(ctypes.byref(b))
+        evs.append((a, b))
     with ClockSampler() as clk:
         ex.sync()
-        L.b2_event_record(e0, ex.stream)
-        for _ in range(args.steps):
+        for a, b in evs:
+            if flush:
+                rt.check(L.b2_memset(fbuf, 0, FLUSH_BYTES, ex.stream))
+            L.b2_event_record(a, ex.stream)
             ex.run_device(first_call=False)
-        L.b2_event_record(e1, ex.stream)
+            L.b2_event_record(b, ex.stream)
+        ex.sync()
+    tot_ms = 0.0
+    for a, b in evs:
         ms = ctypes.c_float()
-        rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(ms)))
-    ms_per_step = ms.value / args.steps
+        rt.check(L.b2_event_elapsed_ms(a, b, ctypes.byref(ms)))
+        tot_ms += ms.value
+    ms_per_step = tot_ms / args.steps
+    if flush:
+        L.b2_free(fbuf)
     value = run_bytes / (ms_per_step / 1e3) / 1e9
     ex.check_flag()
 
@@ -254,7 +299,7 @@ def run_ours(args, W):
     h2d = sum(v.nbytes for v in host.values())
     d2h = sum(np.asarray(v).nbytes for v in out.values())
 
-    cpu_v, cpu_dt, cpu_desc = cpu_sample(args.workload, syms, 2)
+    cpu_v, cpu_dt, cpu_desc, cpu_th = cpu_sample(args.workload, syms, 2)
 
     line = {
         "metric": metric_name(args.workload), "value": value, "unit": "GB/s", "n_gpus": 1,
@@ -262,14 +307,14 @@ def run_ours(args, W):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (make_inputs semantics, seed 0)",
         "config": {"workload": W["desc"], "graph": f"tests/golden/graphs/{W['graph']}.json",
-                   "l2": "inputs (2 x N^3 f64) larger than the 126 MB L2; no flush needed",
+                   "l2": W["l2_note"],
                    "algorithmic_bytes_per_step": run_bytes},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "traffic": traffic_from_profiles(args.workload), "kernel": name,
                      "launch_ms": avg_ms, "launches_per_step": nl, "step_share": step_share,
                      "bytes_per_launch": per_launch},
-        "cpu_baseline": {"value": cpu_v, "unit": "GB/s", "cores": 1, "kind": "port",
+        "cpu_baseline": {"value": cpu_v, "unit": "GB/s", "cores": cpu_th, "kind": "port",
                          "sample": cpu_desc, "seconds": cpu_dt},
         "e2e": {"value": run_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},

@@ -58,6 +58,48 @@ def heat_3d_sweeps(A, B, sweeps):
             A[1:-1, 1:-1, 1:-1] = _heat_rhs(B)
 
 
+def _slabs(n_planes, threads):
+    """Interior planes 1..n-2 split into contiguous [lo, hi) chunks."""
+    lo, hi = 1, n_planes - 1
+    k = max(1, min(threads, hi - lo))
+    return [(lo + (hi - lo) * i // k, lo + (hi - lo) * (i + 1) // k) for i in range(k)]
+
+
+def heat_3d_sweeps_mt(A, B, sweeps, threads):
+    """heat_3d_sweeps on ``threads`` host threads: each thread evaluates the
+    same whole-slice expression on a contiguous slab of planes (numpy releases
+    the GIL), so every element sees the same op order — bitwise equal."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    parts = _slabs(A.shape[0], threads)
+    with ThreadPoolExecutor(len(parts)) as pool:
+        for s in range(sweeps):
+            src, dst = (A, B) if s % 2 == 0 else (B, A)
+
+            def work(b, src=src, dst=dst):
+                lo, hi = b
+                dst[lo:hi, 1:-1, 1:-1] = _heat_rhs(src[lo - 1:hi + 1])
+            list(pool.map(work, parts))
+
+
+def jacobi_2d_sweeps_mt(A, B, sweeps, threads):
+    from concurrent.futures import ThreadPoolExecutor
+
+    parts = _slabs(A.shape[0], threads)
+
+    def rhs(X, lo, hi):
+        return 0.2 * (X[lo:hi, 1:-1] + X[lo:hi, :-2] + X[lo:hi, 2:] + X[lo + 1:hi + 1, 1:-1]
+                      + X[lo - 1:hi - 1, 1:-1])
+    with ThreadPoolExecutor(len(parts)) as pool:
+        for s in range(sweeps):
+            src, dst = (A, B) if s % 2 == 0 else (B, A)
+
+            def work(b, src=src, dst=dst):
+                lo, hi = b
+                dst[lo:hi, 1:-1] = rhs(src, lo, hi)
+            list(pool.map(work, parts))
+
+
 def gemver(alpha, beta, A, u1, v1, u2, v2, w, x, y, z):
     # explicit map: A[i, j] = A[i, j] + u1[i] * v1[j] + u2[i] * v2[j] (per element,
     # left to right: (A + u1*v1) + u2*v2)

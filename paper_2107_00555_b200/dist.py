@@ -852,27 +852,59 @@ def bench_slab(args, W):
     torch.cuda.synchronize()
     import ctypes
 
+    from bench import FLUSH_BYTES, ClockSampler  # noqa: E402
+
     L = rt.lib()
-    e0, e1 = ctypes.c_void_p(), ctypes.c_void_p()
-    rt.check(L.b2_event_create(ctypes.byref(e0)))
-    rt.check(L.b2_event_create(ctypes.byref(e1)))
+    flush = W.get("l2_resident", False)
+    fbuf = ctypes.c_void_p()
+    if flush:
+        rt.check(L.b2_malloc(ctypes.byref(fbuf), FLUSH_BYTES))
+    evs = []
+    for _ in range(args.steps):
+        a, b = ctypes.c_void_p(), ctypes.c_void_p()
+        rt.check(L.b2_event_create(ctypes.byref(a)))
+        rt.check(L.b2_event_create(ctypes.byref(b)))
+        evs.append((a, b))
     runner.ex.sync()
     tdist.barrier()
-    t0 = time.perf_counter()
-    rt.check(L.b2_event_record(e0, runner.ex.stream))  # events on the launching stream
-    for _ in range(args.steps):
-        runner.run()
-    rt.check(L.b2_event_record(e1, runner.ex.stream))
-    msf = ctypes.c_float()
-    rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(msf)))
-    ms = msf.value / args.steps
+    with ClockSampler(local) as clk:
+        for a, b in evs:  # events on the launching stream, one pair per step
+            if flush:
+                rt.check(L.b2_memset(fbuf, 0, FLUSH_BYTES, runner.ex.stream))
+            rt.check(L.b2_event_record(a, runner.ex.stream))
+            runner.run()
+            rt.check(L.b2_event_record(b, runner.ex.stream))
+        runner.ex.sync()
+    ms = 0.0
+    for a, b in evs:
+        msf = ctypes.c_float()
+        rt.check(L.b2_event_elapsed_ms(a, b, ctypes.byref(msf)))
+        ms += msf.value
+    ms /= args.steps
     tdist.barrier()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     run_bytes = W["sweeps"](syms) * W["sweep_bytes"](syms)
     value = run_bytes / (ms / 1e3) / 1e9
-    _ = time.perf_counter() - t0
+    # end to end through the distributed API: every rank uploads its window
+    # of the host inputs, runs, and the owned rows are gathered to rank 0
+    e2e_steps = max(1, min(args.steps, 3))
+    tdist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        runner.load_inputs(inputs)
+        runner.run()
+        out = runner.gather(inputs)
+    tdist.barrier()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    h2d = sum(np.asarray(v).nbytes for v in inputs.values())
+    d2h = sum(np.asarray(v).nbytes for v in out.values()) if out else 0
+    if flush:
+        L.b2_free(fbuf)
     if rank == 0:
         peak, kind = peaks()
         line = {
@@ -881,13 +913,17 @@ def bench_slab(args, W):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (make_inputs semantics, seed 0)",
             "config": {"workload": W["desc"], "parallelism": f"slab{world} (axis-0 block "
-                       "distribution, NCCL halo exchange)",
+                       "distribution, NCCL halo exchange)", "l2": W.get("l2_note"),
                        "halo_bytes_sent_per_step_rank0": halo_per_run,
                        "overlap_splits_per_step": runner.splits},
             "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
                          "frac": value / world / peak, "peak_kind": kind, "traffic": None,
                          "note": "per-GPU share of the whole-job algorithmic bandwidth"},
+            "e2e": {"value": run_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
+                    "note": "slab windows uploaded from host, owned rows gathered to rank 0"},
             "gpu_launches": getattr(runner.ex, "trace_launches", 0) * args.steps,
+            "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     tdist.barrier()

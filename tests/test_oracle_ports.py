@@ -74,3 +74,25 @@ def test_sweep_ports(name):
                 assert np.allclose(v, ref, rtol=1e-14, atol=0), (name, k)
             else:
                 assert np.array_equal(v, ref, equal_nan=True), (name, k, np.abs(v - ref).max())
+
+
+def test_threaded_cpu_ports_bitwise():
+    """The reference-arm ports split planes over host threads: same
+    per-element op order, so bitwise equal to the serial restatement."""
+    import numpy as np
+
+    from oracle import kernels_np as K
+
+    rng = np.random.default_rng(11)
+    A = rng.uniform(-1, 1, (37, 30, 29))
+    B = rng.uniform(-1, 1, (37, 30, 29))
+    A2, B2 = A.copy(), B.copy()
+    K.heat_3d_sweeps(A, B, 5)
+    K.heat_3d_sweeps_mt(A2, B2, 5, 6)
+    assert np.array_equal(A, A2) and np.array_equal(B, B2)
+    A = rng.uniform(-1, 1, (101, 77))
+    B = rng.uniform(-1, 1, (101, 77))
+    A2, B2 = A.copy(), B.copy()
+    K.jacobi_2d(A, B, 4)  # 3 iterations = 6 sweeps
+    K.jacobi_2d_sweeps_mt(A2, B2, 6, 4)
+    assert np.array_equal(A, A2) and np.array_equal(B, B2)
