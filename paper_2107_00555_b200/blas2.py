@@ -31,6 +31,8 @@ from . import codegen, plan as P, runtime as rt, sdfg, symexpr
 
 TPB = 512
 MAX_CW = 8192
+TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpass.cuh)
+SMEM_BUDGET = 220 * 1024
 
 
 class _View:
@@ -256,13 +258,29 @@ class RowPass:
         self.tpb = tpb
         kpt = -(-cw // tpb)
         dot, axpy = self.dot, self.axpy
-        stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64
-        smem_doubles = stage_base + cw * len(self.staged)
-        self.smem = smem_doubles * 8
-        est_regs = 4 * kpt + 40  # x / xn double arrays + addressing
-        blocks_per_sm = max(1, min(4, (200 * 1024) // max(1, self.smem),
-                                   65536 // (tpb * est_regs)))
-        self.G = min(M, 148 * blocks_per_sm)
+        # TMA row ring when every row slice is a 16-byte aligned, 16-byte
+        # multiple (1-D bulk copies); else the register-prefetch kernel
+        nst = len(self.staged)
+        ring_s = (SMEM_BUDGET // 8 - nst * cw - 64) // cw if cw else 0
+        off = self.R[1]
+        # (gemver's prologue + write-back pass measured faster with the
+        # register-prefetch kernel at 2-3 CTAs/SM: 184 vs 254 us)
+        self.tma = (TMA_ROWS and self.prologue is None and rs % 2 == 0 and off % 2 == 0
+                    and N % 2 == 0 and cw % 2 == 0 and ring_s >= 2)
+        if self.tma:
+            self.ring = min(4, ring_s)
+            stage_base = 0
+            self.smem = (nst * cw + 64 + self.ring * cw) * 8
+            self.G = min(M, 148)
+        else:
+            self.ring = 0
+            stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64
+            smem_doubles = stage_base + cw * nst
+            self.smem = smem_doubles * 8
+            est_regs = 4 * kpt + 40  # x / xn double arrays + addressing
+            blocks_per_sm = max(1, min(4, (200 * 1024) // max(1, self.smem),
+                                       65536 // (tpb * est_regs)))
+            self.G = min(M, 148 * blocks_per_sm)
         L = []
         L.append(f"#define RP_NAME b2_rp_{name}")
         L.append(f"#define RP_FIN_NAME b2_rpf_{name}")
@@ -270,7 +288,9 @@ class RowPass:
                      ("RP_KPT", kpt), ("RP_G", self.G), ("RP_CTILES", self.ctiles),
                      ("RP_DOT", int(dot is not None)), ("RP_AXPY", int(axpy is not None)),
                      ("RP_PROLOGUE", int(self.prologue is not None)),
-                     ("RP_WRITEBACK", int(self.prologue is not None))):
+                     ("RP_WRITEBACK", int(self.prologue is not None)),
+                     ("RP_TMA", int(self.tma)), ("RP_S", max(1, self.ring)),
+                     ("RP_NSTAGED", nst)):
             L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")
         nbase = 8
         pro_src = ""

@@ -189,6 +189,36 @@ __device__ __forceinline__ void b2_cp_commit() { asm volatile("cp.async.commit_g
 template <int N>
 __device__ __forceinline__ void b2_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---- TMA bulk copies (cp.async.bulk, 1-D) completed on an mbarrier ----------
+__device__ __forceinline__ void b2_mbar_init(unsigned long long *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(b)),
+               "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void b2_mbar_wait(unsigned long long *b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "B2_MW:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra B2_MD;\n\t"
+      "bra B2_MW;\n\t"
+      "B2_MD:\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity)
+      : "memory");
+}
+// dst, src 16-byte aligned; bytes a multiple of 16
+__device__ __forceinline__ void b2_bulk_load(void *dst, const void *src, unsigned bytes,
+                                             unsigned long long *bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+
 // Device-side bounds guard for accesses the host cannot check statically
 // (memlets inside nested scopes): records the first violation.
 __device__ __forceinline__ bool b2_oob(b2_ll off, b2_ll size, int site, int *flag) {

@@ -32,6 +32,99 @@ __device__ __forceinline__ double rp_block_sum(double v, double *red, int parity
   return t;
 }
 
+#if RP_TMA
+// TMA variant: rows stream through an RP_S-deep ring of shared-memory row
+// buffers filled by 1-D bulk copies (cp.async.bulk + mbarrier), so up to
+// RP_S rows per SM are in flight without register staging; the dot vector
+// slice and the column accumulators live in registers.  Shared layout:
+// [staged column vectors (RP_NSTAGED x RP_CW)] [reduction scratch 64] [ring].
+extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_constant__ RpArgs a) {
+  extern __shared__ __align__(16) double rp_smem[];
+  __shared__ __align__(8) unsigned long long rp_bar[RP_S];
+  double *red = rp_smem + RP_NSTAGED * RP_CW;
+  double *ring = red + 64;
+  const int tid = threadIdx.x;
+  const b2_ll c0 = (b2_ll)blockIdx.y * RP_CW;
+  const int cw = (int)((RP_N - c0) < RP_CW ? (RP_N - c0) : RP_CW);
+  const unsigned bytes = (unsigned)cw * 8u;
+  const double *__restrict__ R = (const double *)a.w[0];
+  rp_stage_cols(a, c0, cw, tid);
+  double vreg[RP_KPT], acc[RP_KPT];
+#pragma unroll
+  for (int k = 0; k < RP_KPT; ++k) {
+    const int j = tid + k * RP_TPB;
+    vreg[k] = (RP_DOT && j < cw) ? rp_dot_vec(a, c0 + j) : 0.0;
+    acc[k] = 0.0;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < RP_S; ++s) b2_mbar_init(&rp_bar[s], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < RP_S; ++s) {
+      const b2_ll m = blockIdx.x + (b2_ll)s * gridDim.x;
+      if (m < RP_M) b2_bulk_load(ring + s * RP_CW, R + m * RP_RS + c0, bytes, &rp_bar[s]);
+    }
+  }
+  int parity = 0;
+  int it = 0;
+  for (b2_ll m = blockIdx.x; m < RP_M; m += gridDim.x, ++it) {
+    const int s = it % RP_S;
+    b2_mbar_wait(&rp_bar[s], (unsigned)((it / RP_S) & 1));
+    double x[RP_KPT];
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) {
+      const int j = tid + k * RP_TPB;
+      x[k] = (j < cw) ? ring[s * RP_CW + j] : 0.0;
+    }
+#if RP_PROLOGUE
+    {
+      RpRow rr;
+      rp_row_setup(a, m, rr);
+#pragma unroll
+      for (int k = 0; k < RP_KPT; ++k) {
+        const int j = tid + k * RP_TPB;
+        if (j < cw) {
+          x[k] = rp_elem(a, rr, m, c0 + j, x[k], j);
+#if RP_WRITEBACK
+          ((double *)a.w[0])[m * RP_RS + c0 + j] = x[k];
+#endif
+        }
+      }
+    }
+#endif
+#if RP_DOT
+    double p = 0.0;
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) p += x[k] * vreg[k];
+    const double d = rp_block_sum(p, red, parity);  // its barrier also retires slot s
+    parity ^= 1;
+    if (tid == 0) rp_store_dot(a, m, d, blockIdx.y);
+#else
+    const double d = 0.0;
+    __syncthreads();  // every thread has read slot s
+#endif
+    if (tid == 0) {
+      const b2_ll mn = m + (b2_ll)RP_S * gridDim.x;
+      if (mn < RP_M) b2_bulk_load(ring + s * RP_CW, R + mn * RP_RS + c0, bytes, &rp_bar[s]);
+    }
+#if RP_AXPY
+    const double c = rp_coef(a, m, d);
+#pragma unroll
+    for (int k = 0; k < RP_KPT; ++k) acc[k] += c * x[k];
+#endif
+    (void)d;
+  }
+#if RP_AXPY
+  double *ws = (double *)a.w[1];
+#pragma unroll
+  for (int k = 0; k < RP_KPT; ++k) {
+    const int j = tid + k * RP_TPB;
+    if (j < cw) ws[(b2_ll)blockIdx.x * RP_N + c0 + j] = acc[k];
+  }
+#endif
+}
+#else
 extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_constant__ RpArgs a) {
   extern __shared__ double rp_smem[];
   double *acc_s = rp_smem;                     // [RP_CW] column accumulators
@@ -112,6 +205,7 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
   for (int j = tid; j < cw; j += RP_TPB) ws[(b2_ll)blockIdx.x * RP_N + c0 + j] = acc_s[j];
 #endif
 }
+#endif  // RP_TMA
 
 // out[n] (wcr)= sum over G row-groups of ws[g][n]  (+ per-tile dot partials).
 // Block 32 x 8: 32 columns per block, the 8 thread rows split the G partials
