@@ -39,6 +39,8 @@ REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WC
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
 ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reductions
+FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min loop folds
+FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 
 
@@ -1195,6 +1197,143 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
                 continue  # parallel loop variables come from the thread index
             gen.emit(f"s_{k} = {symexpr.to_c(v, name_of)};")
 
+    def fold_info(L):
+        """An inner loop that only folds ``C[idx] = max|min(C[idx], E(l))``
+        (idx independent of the loop variable, E reads anything but C)."""
+        if L.step <= 0 or L.body != {L.body_entry}:
+            return None
+        c = L.cond
+        if not (isinstance(c, tuple) and c[0] == "bin" and c[1] in ("<", "<=")
+                and c[2] == ("ref", L.var) and L.var not in scalar.free_names(c[3])):
+            return None
+        ops = planner.ops.get(L.body_entry, [])
+        if len(ops) != 1 or not isinstance(ops[0], P.MapGroup) or len(ops[0].members) != 1:
+            return None
+        mem = ops[0].members[0]
+        t = mem.tasklet
+        if t is None or len(t.code) != 1:
+            return None
+        outs = planner.g.out_transitions(planner.chain_end[L.body_entry])
+        if len(outs) != 1 or outs[0].dst != L.guard or set(outs[0].assignments) != {L.var}:
+            return None
+        st = mem.state
+        oe = [e for e in st.out_edges(t) if e.memlet is not None]
+        ie = [e for e in st.in_edges(t) if e.memlet is not None]
+        if len(oe) != 1 or oe[0].memlet.wcr is not None:
+            return None
+        om = oe[0].memlet
+        if (planner.g.containers[om.container].dtype != "f64"
+                or any(L.var in symexpr.free_symbols(x) for d in om.subset for x in d)):
+            return None
+        code = t.code[0][1]
+        if not (isinstance(code, tuple) and code[0] == "call" and code[1] in ("max", "min")
+                and len(code[2]) == 2):
+            return None
+        accs = [e for e in ie if e.memlet.container == om.container]
+        if len(accs) != 1 or accs[0].memlet.text != om.text:
+            return None
+        acc_conn = accs[0].dst_conn
+        a0, a1 = code[2]
+        if a0 == ("ref", acc_conn):
+            expr = a1
+        elif a1 == ("ref", acc_conn):
+            expr = a0
+        else:
+            return None
+        if acc_conn in scalar.free_names(expr):
+            return None
+        return {"op": code[1], "state": st, "t": t, "acc": accs[0], "out": oe[0],
+                "others": [e for e in ie if e is not accs[0]], "expr": expr}
+
+    def emit_fold(L, fi):
+        """Warp-cooperative fold: lanes take every 32nd trip, combine with a
+        fixed xor tree, lane 0 folds into C once (max/min are exact, so the
+        result equals the sequential loop's for non-NaN data)."""
+        op = "b2_pymax" if fi["op"] == "max" else "b2_pymin"
+        ident = "(-b2_inf())" if fi["op"] == "max" else "b2_inf()"
+        cond = cond_c(L.cond)
+        fa, fl, ran = gen.fresh("fold"), gen.fresh("fl"), gen.fresh("ran")
+        gen.emit("{")
+        gen.ind += 2
+        # trip count of `var < B` / `var <= B` from the current value
+        cb, _ = scalar.emit(L.cond[3], {n: "i" for n in scalar.free_names(L.cond[3])},
+                            lambda n: f"s_{gen.sym(n)[2:]}")
+        trip, fbase = gen.fresh("trip"), gen.fresh("fbase")
+        extra = 1 if L.cond[1] == "<=" else 0
+        gen.emit(f"const bool {ran} = {cond};")
+        gen.emit(f"const b2_ll {trip} = {ran} ? ((b2_ll)({cb}) + {extra} - s_{L.var} + "
+                 f"{L.step - 1}) / {L.step} : 0;")
+        gen.emit(f"const b2_ll {fbase} = s_{L.var};")
+        # reads affine in the loop variable: guard the first and last trip once
+        # (device error flag as usual) so the loop body issues plain loads
+        fi["checked"] = {}
+        ok = gen.fresh("inb")
+        gen.emit(f"bool {ok} = true;")
+        for e in fi["others"]:
+            m = e.memlet
+            if any(symexpr.affine(b, tuple(symexpr.free_symbols(b)), {}) is None
+                   for b, _, _ in m.subset):
+                continue
+            fi["checked"][id(e)] = True
+            for at in (f"{fbase}", f"{fbase} + ({trip} - 1) * {L.step}"):
+                idx = []
+                gen.emit("{")
+                gen.emit(f"  const b2_ll s_{L.var} = {at};")
+                idx = [symexpr.to_c(b, gen.name_of({})) for b, _, _ in m.subset]
+                site = gen._site(f"read {m.text}")
+                gen.emit(f"  if ({trip} > 0 && b2_oob({gen.offset(m.container, idx)}, "
+                         f"sz_{m.container}, {site}, flag)) {ok} = false;")
+                gen.emit("}")
+        gen.emit(f"double {fa} = {ident};")
+        gen.emit(f"#pragma unroll {FOLD_UNROLL}")
+        gen.emit(f"for (b2_ll {fl} = lane; {ok} && {fl} < {trip}; {fl} += 32) {{")
+        gen.ind += 2
+        gen.emit(f"const b2_ll s_{L.var} = {fbase} + {fl} * {L.step};")
+        types, cname = {}, {}
+        for e in fi["others"]:
+            m = e.memlet
+            cdt = CT[planner.g.containers[m.container].dtype]
+            if fi["checked"].get(id(e)):
+                # bounds proven at both ends of the trip range: plain load
+                idx = [symexpr.to_c(b, gen.name_of({})) for b, _, _ in m.subset]
+                code = f"{gen.ptr(m.container)}[{gen.offset(m.container, idx)}]"
+                ty = TC[planner.g.containers[m.container].dtype]
+            else:
+                code, ty = gen.read(m, {}, 1)
+            v = gen.fresh("in")
+            gen.emit(f"const {cdt} {v} = {code};")
+            types[e.dst_conn] = ty
+            cname[e.dst_conn] = v
+        for n in scalar.free_names(fi["expr"]):
+            if n not in types:
+                types[n] = "i"
+                cname[n] = gen.sym(n)
+        ec, et = scalar.emit(fi["expr"], types, lambda n: cname[n])
+        gen.emit(f"{fa} = {op}({fa}, (double)({scalar.cast(ec, et, 'f')}));")
+        gen.ind -= 2
+        gen.emit("}")
+        gen.emit(f"for (int o = 16; o > 0; o >>= 1) {fa} = {op}({fa}, "
+                 f"__shfl_xor_sync(0xffffffffu, {fa}, o));")
+        gen.emit(f"if (lane == 0 && {ran}) {{")
+        gen.ind += 2
+        ac, at = gen.read(fi["acc"].memlet, {}, 1)
+        av = gen.fresh("acc")
+        gen.emit(f"const double {av} = {ac};")
+        gen.write(fi["out"].memlet, f"{op}({av}, {fa})", "f", {}, 1)
+        gen.ind -= 2
+        gen.emit("}")
+        gen.emit("__syncwarp();")
+        gen.emit(f"while ({cond}) s_{L.var} += {L.step};")
+        gen.ind -= 2
+        gen.emit("}")
+
+    warp_mode = False
+    if reg.par and FOLD_MODE:
+        for h in reg.heads:
+            if h in loops_all and h != reg.loop.guard and loops_all[h] not in reg.par \
+                    and fold_info(loops_all[h]) is not None:
+                warp_mode = True
+
     def block(cur, stop):
         guard_budget = 0
         while cur != stop:
@@ -1203,6 +1342,12 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
                 raise P.PlanError("unstructured control flow in loop region")
             if cur in loops_all and cur in reg.heads:
                 L = loops_all[cur]
+                fi = fold_info(L) if warp_mode else None
+                if fi is not None:
+                    emit_fold(L, fi)
+                    follow(L.t_out)
+                    cur = L.exit
+                    continue
                 gen.emit(f"while ({cond_c(L.cond)}) {{")
                 gen.ind += 2
                 follow(L.t_in)
@@ -1212,7 +1357,15 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
                 follow(L.t_out)
                 cur = L.exit
                 continue
-            emit_ops(cur)
+            if warp_mode:  # lane 0 runs the plain code, the warp the folds
+                gen.emit("if (lane == 0) {")
+                gen.ind += 2
+                emit_ops(cur)
+                gen.ind -= 2
+                gen.emit("}")
+                gen.emit("__syncwarp();")
+            else:
+                emit_ops(cur)
             outs = planner.g.out_transitions(planner.chain_end[cur])
             if len(outs) != 1:
                 raise P.PlanError("branching inside a device loop region")
@@ -1255,8 +1408,13 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     for k, l in enumerate(reg.par):
         pro.append(f"  const b2_ll pb{k} = {gen.arg(('pb', k))}, ps{k} = {gen.arg(('ps', k))}, "
                    f"pn{k} = {gen.arg(('pn', k))};")
-    loop = ["  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NPAR; "
-            "f += (b2_ll)gridDim.x * blockDim.x) {", "    b2_ll rem = f; (void)rem;"]
+    if warp_mode:  # one warp per parallel iteration
+        loop = ["  const int lane = threadIdx.x & 31;",
+                "  for (b2_ll f = ((b2_ll)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < NPAR; "
+                "f += ((b2_ll)gridDim.x * blockDim.x) >> 5) {", "    b2_ll rem = f; (void)rem;"]
+    else:
+        loop = ["  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NPAR; "
+                "f += (b2_ll)gridDim.x * blockDim.x) {", "    b2_ll rem = f; (void)rem;"]
     for k in reversed(range(len(reg.par))):
         loop.append(f"    const b2_ll s_{reg.par[k].var} = pb{k} + ps{k} * (rem % pn{k}); "
                     f"rem /= pn{k};")
@@ -1281,6 +1439,7 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     spec.mode = "region"
     spec.block = (256, 1, 1)
     spec.params = []
+    spec.warp = warp_mode
     return spec
 
 

@@ -513,7 +513,8 @@ class GpuExecutor:
                 else:
                     raise AssertionError(d)
             blob = struct.pack(f"<{len(vals)}q", *vals)
-            grid = (max(1, min(-(-npar // 256), codegen.MAX_BLOCKS * 8)), 1, 1)
+            nthr = npar * (32 if getattr(spec, "warp", False) else 1)
+            grid = (max(1, min(-(-nthr // 256), codegen.MAX_BLOCKS * 8)), 1, 1)
             rt.launch(spec.kernel, grid, (256, 1, 1), blob, self.stream)
             self.launches += 1
         self._region_final(reg, sym)
