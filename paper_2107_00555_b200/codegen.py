@@ -40,6 +40,7 @@ REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WC
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
 ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reductions
 FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min loop folds
+SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 
@@ -120,10 +121,10 @@ class _Gen:
         reads: set = set()
         for mem in grp.members:
             for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if self.place(c) in ("reg", "private"):
+                    continue  # thread-local: no cross-thread effect
                 if not w:
                     reads.add(c)
-                    continue
-                if self.place(c) == "reg":
                     continue
                 if wcr is None or depth != 0 or pt is None or self.place(c) != "memory":
                     return None
@@ -867,15 +868,28 @@ class _Gen:
         nthr = spec.block[0] * spec.block[1] * spec.block[2]
         pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}) '
                    f"{spec.name}(const __grid_constant__ B2Args a) {{")
+        def _size(name):
+            n = 1
+            for x in self.shapes[name]:
+                n *= x
+            return n
+
+        # small thread-private transients (e.g. a tiled WCR's stack
+        # accumulator) live in a per-point local array, not in HBM scratch
+        small_priv = [n for n in spec.containers
+                      if self.place(n) == "private" and _size(n) <= SMALL_PRIVATE]
         for name in spec.containers:
             c = self.g.containers[name]
             pl = self.place(name)
             if pl == "reg":
                 continue
-            base = self.arg(("ptr", name))
-            ro = name not in self.written and pl == "memory"
-            q = "const " if ro else ""
-            pro.append(f"  {q}{CT[c.dtype]} *__restrict__ c_{name} = ({q}{CT[c.dtype]} *){base};")
+            if name in small_priv:
+                pro.append(f"  {CT[c.dtype]} pva_{name}[{_size(name)}];")
+            else:
+                base = self.arg(("ptr", name))
+                ro = name not in self.written and pl == "memory"
+                q = "const " if ro else ""
+                pro.append(f"  {q}{CT[c.dtype]} *__restrict__ c_{name} = ({q}{CT[c.dtype]} *){base};")
             shape = self.shapes[name]
             st = _row_major(shape)
             for d in range(len(shape)):
@@ -905,7 +919,10 @@ class _Gen:
                 pro.append(f"  const b2_ll rb{i} = {self.arg(('rb', i))};")
                 pro.append(f"  const b2_ll rs{i} = {self.arg(('rs', i))};")
                 pro.append(f"  const b2_ll rl{i} = {self.arg(('rl', i))};")
-        privates = [n for n in spec.containers if self.place(n) == "private"]
+        for n in small_priv:
+            pro.append(f"  {CT[self.g.containers[n].dtype]} *__restrict__ pv_{n} = pva_{n};")
+        privates = [n for n in spec.containers
+                    if self.place(n) == "private" and n not in small_priv]
         if privates:
             pro.append("  const b2_ll tflat = ((b2_ll)blockIdx.x * blockDim.y + threadIdx.y) * "
                        "blockDim.x + threadIdx.x;")
@@ -916,7 +933,10 @@ class _Gen:
         regs = [n for n in spec.containers if self.place(n) == "reg"]
 
         def reg_decls(indent):
-            return [" " * indent + f"{CT[self.g.containers[n].dtype]} r_{n} = 0;" for n in regs]
+            out = [" " * indent + f"{CT[self.g.containers[n].dtype]} r_{n} = 0;" for n in regs]
+            out += [" " * indent + f"for (int z = 0; z < {_size(n)}; ++z) pva_{n}[z] = 0;"
+                    for n in small_priv]
+            return out
 
         def shift(lines, by):
             return [(" " * by + ln) if by >= 0 else ln[-by:] for ln in lines]

@@ -168,3 +168,17 @@ def test_temporal_pair_bitwise(monkeypatch, N, T):
         K.heat_3d_c(A, B, T)
         assert np.array_equal(ex.download("A"), A) and np.array_equal(ex.download("B"), B)
     ex.close()
+
+
+@pytest.mark.parametrize("N,H,SM", [(2, 3, 1), (2, 3, 33), (1, 2, 64), (3, 1, 100)])
+def test_softmax_fold_and_rowred_vs_numpy_port(N, H, SM):
+    """softmax raw graph: the max loop runs as a warp fold (incl. zero-trip and
+    ragged-lane cases), the exp/sum map in row-reduction mode."""
+    from oracle import kernels_np as K
+
+    rng = np.random.default_rng(SM)
+    x = rng.uniform(-1, 1, (N, H, SM, SM))
+    out = _run("softmax.raw", {"N": N, "H": H, "SM": SM}, {"x": x, "out": np.zeros_like(x)})
+    ref = np.empty_like(x)
+    K.softmax(x.copy(), ref)
+    assert rel_err(out["out"], ref) <= 1e-12
