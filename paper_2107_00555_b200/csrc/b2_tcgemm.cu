@@ -17,6 +17,8 @@
 //   * warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=8) x 4 per stage into
 //     a 128 x 256 fp32 accumulator in TMEM and releases each stage with
 //     tcgen05.commit,
+//   * default: CTA pairs (tc_sgemm_pair, cta_group::2, 256 x 256 tiles, 6
+//     stages of 32 KB); B2_TC_PAIR=0 selects the single-CTA kernel,
 //   * long in-TMEM accumulations lose accuracy (the error grows with the
 //     accumulation length), so the MMA warp accumulates chunks of 128 k into
 //     two alternating 256-column TMEM buffers and eight epilogue warps drain
@@ -255,6 +257,180 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ---- CTA-pair variant (cta_group::2) ---------------------------------------
+// A cluster of two CTAs computes a 256 x 256 tile: CTA r loads rows
+// m0 + 128 r of A' and rows n0 + 128 r of B' (32 KB per stage, 6 stages), the
+// leader issues tcgen05.mma.cta_group::2 (M=256, N=256, K=8) reading both
+// CTAs' shared tiles, and each CTA's TMEM holds its 128 accumulator rows.
+// Both CTAs' TMA bytes complete on the leader's full barrier; MMA commits are
+// multicast to both CTAs' empty / chunk-full barriers; the peer's epilogue
+// warps release a TMEM buffer by arriving on the leader's barrier.
+constexpr int P_STAGES = 6;
+constexpr int P_A_BYTES = 128 * TK * 4;  // 16 KB
+constexpr int P_B_BYTES = 128 * TK * 4;  // 16 KB (half of N = 256)
+constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
+constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t P_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// arrive on the same-offset mbarrier of cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *b, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(b)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                                 int x, int y) {
+  // completes on the leader CTA's barrier (peer bit cleared)
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(P_IDESC), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    tc_sgemm_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                  int64_t M, int64_t N, int nk, int chunk, float *__restrict__ C, int64_t ldc,
+                  int accumulate, int num_m, int num_n, int group_m) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t *sa = smem;
+  uint8_t *sb = smem + P_STAGES * P_A_BYTES;
+  uint64_t *full = (uint64_t *)(smem + P_STAGES * P_STAGE_BYTES);
+  uint64_t *empty = full + P_STAGES;
+  uint64_t *tfull = empty + P_STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  // tiles of 256 x 256 per pair, grouped rasterisation over pairs
+  const int pid = blockIdx.x >> 1, per_group = group_m * num_n;
+  const int first_m = (pid / per_group) * group_m;
+  const int gsize = num_m - first_m < group_m ? num_m - first_m : group_m;
+  const int m0 = (first_m + (pid % per_group) % gsize) * 256;
+  const int n0 = ((pid % per_group) / gsize) * 256;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 2 * EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&ta) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tb) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // TMA producer (both CTAs): this CTA's halves of A' and B'
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % P_STAGES;
+        if (kb >= P_STAGES) mbar_wait(&empty[s], ((kb / P_STAGES) + 1) & 1);
+        if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+        tma_load_2d_pair(sa + s * P_A_BYTES, &ta, &full[s], kb * TK, m0 + (int)rank * 128);
+        tma_load_2d_pair(sb + s * P_B_BYTES, &tb, &full[s], kb * TK, n0 + (int)rank * 128);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int j = kb / chunk, b = j & 1;
+        const bool first = kb - j * chunk == 0;
+        if (first && j >= 2) {
+          mbar_wait(&tempty[b], ((j >> 1) + 1) & 1);
+          fence_after();
+        }
+        const int s = kb % P_STAGES;
+        mbar_wait(&full[s], (kb / P_STAGES) & 1);
+        fence_after();
+        const uint64_t da = sw128_desc(smem_u32(sa + s * P_A_BYTES));
+        const uint64_t db = sw128_desc(smem_u32(sb + s * P_B_BYTES));
+#pragma unroll
+        for (int k = 0; k < TK / 8; ++k)
+          mma_tf32_pair(tmem + (uint32_t)(b * 256), da + 2 * k, db + 2 * k, !(first && k == 0));
+        mma_commit_pair(&empty[s]);
+        if (kb - j * chunk == chunk - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
+      }
+    }
+  } else {
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    float acc[128];
+#pragma unroll
+    for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+    const int nchunks = (nk + chunk - 1) / chunk;
+    for (int j = 0; j < nchunks; ++j) {
+      const int b = j & 1;
+      mbar_wait(&tfull[b], (j >> 1) & 1);
+      fence_after();
+      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 256 + half * 128);
+#pragma unroll
+      for (int c = 0; c < 128; c += 16) {
+        float v[16];
+        tmem_ld16(base + (uint32_t)c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty[b], 0);  // the leader's barrier
+    }
+    const int64_t row = m0 + (int64_t)rank * 128 + q * 32 + lane;
+    if (row < M) {
+      float *crow = C + row * ldc + n0 + half * 128;
+      const int64_t ncol = N - (n0 + half * 128);
+#pragma unroll
+      for (int i = 0; i < 128; ++i)
+        if (i < ncol) crow[i] = accumulate ? crow[i] + acc[i] : acc[i];
+    }
+  }
+  fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(TMEM_COLS));
+  }
+}
+
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t u;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
@@ -394,17 +570,34 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
-        cudaSuccess)
+            cudaSuccess ||
+        cudaFuncSetAttribute(tc_sgemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             P_SMEM_BYTES) != cudaSuccess)
       return b2_fail(B2_ERR_CUDA, "tc sgemm smem attribute");
     attr = true;
   }
-  const int num_m = (int)((M + TM - 1) / TM), num_n = (int)((N + TN - 1) / TN);
-  static int group_m = -1;
+  static int group_m = -1, pair = -1;
   if (group_m < 0) {
     const char *e = getenv("B2_TC_GROUP");
-    group_m = e ? atoi(e) : 16;
+    group_m = e ? atoi(e) : 4;  // measured: 4-tile bands of 256-row pair tiles
     if (group_m < 1) group_m = 1;
+    const char *p2 = getenv("B2_TC_PAIR");
+    pair = !(p2 && p2[0] == '0');
   }
+  if (pair) {
+    CUtensorMap pa, pb;
+    rc = make_map(&pa, Ap, (uint64_t)Kp, (uint64_t)M, 128);
+    if (rc) return rc;
+    rc = make_map(&pb, Bt, (uint64_t)Kp, (uint64_t)N, 128);
+    if (rc) return rc;
+    const int pm = (int)((M + 255) / 256), pn = (int)((N + 255) / 256);
+    tc_sgemm_pair<<<2 * pm * pn, THREADS, P_SMEM_BYTES, s>>>(
+        pa, pb, M, N, (int)(3 * nkb), (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate, pm, pn,
+        group_m);
+    B2_LAUNCH_CHECK("tc sgemm pair");
+    return B2_OK;
+  }
+  const int num_m = (int)((M + TM - 1) / TM), num_n = (int)((N + TN - 1) / TN);
   tc_sgemm<<<num_m * num_n, THREADS, SMEM_BYTES, s>>>(
       ma, mb, M, N, (int)(3 * nkb), (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate, num_m,
       num_n, group_m);

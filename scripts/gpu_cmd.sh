@@ -1,3 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 900 python -m pytest tests -m gpu -q -x -o faulthandler_timeout=200 2>&1 | tail -2
-for v in raw auto pipe; do timeout -s KILL 300 python scripts/probe_time.py conv2d_bias.$v '{"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16, "K": 20, "HO": 237, "WO": 237}' 3 2>&1 | grep -E "rep 2|Error" | head -2; done
+for n in 4096 8192 16384; do for p in 0 1; do for g in 4 8 16; do
+echo "n=$n pair=$p group=$g $(B2_TC_PAIR=$p B2_TC_GROUP=$g timeout -s KILL 60 python scripts/probe_sgemm.py $n 3 2>&1 | tail -1)"
+done; done; done
