@@ -784,6 +784,8 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     def buf(shape):
         return torch.empty(shape, dtype=tdt, device="cuda")
 
+    from bench import ClockSampler  # noqa: E402
+
     for _ in range(args.warmup):
         s.run(a, b, c, gemm, buf)
     torch.cuda.synchronize()
@@ -791,25 +793,70 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        s.run(a, b, c, gemm, buf)
-    e1.record()
-    torch.cuda.synchronize()
+    n_launch0 = L.b2_launch_count()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            s.run(a, b, c, gemm, buf)
+        e1.record()
+        torch.cuda.synchronize()
+    launches = L.b2_launch_count() - n_launch0
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     flop = 2.0 * n ** 3
+    # end to end: this rank's A and B blocks from pinned host memory, the
+    # SUMMA run, C block back to pinned host memory
+    ha = a.cpu().pin_memory()
+    hb = b.cpu().pin_memory()
+    hc = torch.empty_like(c, device="cpu").pin_memory()
+    e2e_steps = max(1, min(args.steps, 2))
+    tdist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        a.copy_(ha, non_blocking=True)
+        b.copy_(hb, non_blocking=True)
+        s.run(a, b, c, gemm, buf)
+        hc.copy_(c, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    value = flop / (ms / 1e3) / 1e12
+    if dtype == "f32":
+        # 3xTF32: three TF32 products per multiply-add; TF32 dense = half the
+        # measured bf16 rate (MEASURED_PEAKS.json)
+        from bench import ROOT as _R  # noqa: E402
+
+        pk = json.loads((_R / "MEASURED_PEAKS.json").read_text())["bf16_tflops"] / 2 \
+            if (_R / "MEASURED_PEAKS.json").exists() else 1100.0
+        roof = {"bound": "tensor", "achieved": 3 * value / world, "peak": pk, "unit": "TFLOP/s",
+                "frac": 3 * value / world / pk, "traffic": None,
+                "note": "per-GPU TF32 tensor rate (3 products per fp32 MAC) incl. the operand "
+                        "split passes; peak = measured bf16 dense / 2"}
+    else:
+        roof = {"bound": "tensor", "achieved": value / world, "peak": 37.0, "unit": "TFLOP/s",
+                "frac": value / world / 37.0, "traffic": None,
+                "note": "per-GPU DMMA rate; peak = nominal FP64 tensor (no measured figure)"}
     if rank == 0:
         print(json.dumps({
-            "metric": f"summa_matmul_{dtype}_TFLOPs", "value": flop / (ms / 1e3) / 1e12,
+            "metric": f"summa_matmul_{dtype}_TFLOPs", "value": value,
             "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic uniform(-1,1)",
             "config": {"workload": f"SUMMA M=N=K={n} {dtype} (BASELINE configs[3])",
                        "grid": str(grid), "panels": s.L,
-                       "parallelism": f"summa{grid}"}}), flush=True)
+                       "parallelism": f"summa{grid}"},
+            "roofline": roof,
+            "e2e": {"value": flop / e2e_s / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": (ha.numel() + hb.numel()) * ha.element_size(),
+                    "d2h_bytes_per_step": hc.numel() * hc.element_size(),
+                    "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary()}), flush=True)
     tdist.barrier()
     tdist.destroy_process_group()
 
