@@ -119,6 +119,80 @@ def test_schema_errors():
 
 # --- planner and generated code ------------------------------------------------
 
+def _modes(name, syms):
+    from paper_2107_00555_b200 import codegen, plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+    pl = P.Planner(g, syms).build()
+    out = {}
+    for op in pl.all_ops:
+        if isinstance(op, P.MapGroup) and op.idx not in pl.in_region:
+            out[op.idx] = codegen.generate(pl, op, pl.shapes(syms), f"k{op.idx}").mode
+    regs = [codegen.generate_region(pl, r, pl.shapes(syms), "r") for r in pl.regions]
+    return out, regs, pl
+
+
+def test_kernel_mode_selection():
+    """The schedules each benchmark program gets (DESIGN.md kernel families):
+    heat_3d sweeps march along dim 0; softmax's exp+sum map is a warp-per-row
+    reduction and its max loop a warp fold; the tiled-WCR conv2d (auto graph)
+    accumulates in registers (thread-private stack accumulator in registers);
+    go_fast's trace loop (pipe graph) is a register reduction."""
+    m, _, _ = _modes("heat_3d.raw", {"N": 400, "TSTEPS": 100})
+    assert set(m.values()) == {"march"}
+    m, regs, _ = _modes("softmax.raw", {"N": 64, "H": 16, "SM": 512})
+    assert "rowred" in m.values()
+    assert len(regs) == 1 and regs[0].warp
+    m, _, _ = _modes("conv2d_bias.auto", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16,
+                                          "K": 20, "HO": 237, "WO": 237})
+    assert "reduce" in m.values()
+    m, _, _ = _modes("go_fast.pipe", {"N": 12000})
+    assert "reduce" in m.values()
+
+
+def test_temporal_pair_legality():
+    """temporal.pair_info accepts heat_3d's two sweeps (offsets in [0, 2],
+    write offset 1) and nothing in jacobi_2d's 2-D sweeps (3-D only)."""
+    from paper_2107_00555_b200 import plan as P, sdfg, temporal
+
+    g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
+    pl = P.Planner(g, {"N": 40, "TSTEPS": 5}).build()
+    ops = [op for op in pl.all_ops if isinstance(op, P.MapGroup)]
+    info = temporal.pair_info(pl, ops[0], ops[1])
+    assert info is not None
+    X, Y, o1, emin, emax = info
+    assert (X, Y, o1, emin, emax) == ("B", "A", (1, 1, 1), (0, 0, 0), (2, 2, 2))
+    assert temporal.pair_info(pl, ops[1], ops[0]) is not None  # A -> B is the same shape
+    g2 = sdfg.load(GOLDEN / "graphs" / "jacobi_2d.raw.json")
+    pl2 = P.Planner(g2, {"N": 40, "TSTEPS": 5}).build()
+    ops2 = [op for op in pl2.all_ops if isinstance(op, P.MapGroup)]
+    assert temporal.pair_info(pl2, ops2[0], ops2[1]) is None
+
+
+def test_rowpass_tma_selection():
+    """atax / bicg rows stream through the TMA bulk-copy ring; gemver's
+    prologue pass keeps the register-prefetch kernel; odd row pitches (not
+    16-byte multiples) fall back too."""
+    from paper_2107_00555_b200 import plan as P, sdfg
+
+    def rowpasses(name, syms):
+        g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+        pl = P.Planner(g, syms).build()
+        out = []
+        for op in pl.all_ops:
+            rp = getattr(op, "rowpass", None)
+            if rp is not None:
+                rp.source(pl.shapes(syms), f"t{op.idx}")
+                out.append(rp)
+        return out
+
+    assert all(rp.tma for rp in rowpasses("atax.raw", {"M": 8000, "N": 8000}))
+    assert all(rp.tma for rp in rowpasses("bicg.raw", {"N": 8000, "M": 8000}))
+    gv = rowpasses("gemver.raw", {"N": 8000})
+    assert any(not rp.tma for rp in gv)
+    assert not any(rp.tma for rp in rowpasses("atax.raw", {"M": 3000, "N": 2501}))
+
+
 def test_fusion_collapses_heat3d_chain():
     """heat_3d's ~16 maps per sweep (reference subgraph_fusion crashes on it,
     SURVEY.md §0) fuse into one kernel per half-sweep with every
