@@ -331,7 +331,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="heat_3d",
-                    choices=sorted(WORKLOADS) + ["matmul", "matmul_f32"])
+                    choices=sorted(WORKLOADS) + ["matmul", "matmul_f32", "jacobi_2d_local"])
     ap.add_argument("--n", type=int, default=16384, help="SUMMA size (matmul workloads)")
     args = ap.parse_args()
     if args.workload.startswith("matmul"):
@@ -356,6 +356,13 @@ def main():
             return
         from paper_2107_00555_b200.dist import bench_summa
         return bench_summa(args, args.n, "f32" if args.workload.endswith("f32") else "f64")
+    if args.workload == "jacobi_2d_local":
+        W = WORKLOADS["jacobi_2d"]
+        if args.impl == "reference":
+            args.workload = "jacobi_2d"
+            return run_reference(args, W)
+        from paper_2107_00555_b200.comm import bench_local_view
+        return bench_local_view(args, W)
     W = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, W)

@@ -1,0 +1,442 @@
+"""Local-view message passing on GPUs: the reference's explicit communication
+primitives executed for real, one process per GPU.
+
+The reference lowers ``comm_isend(view, peer, tag, req[k])``,
+``comm_irecv(...)`` and ``comm_waitall(req)`` to ISEND / IRECV / WAITALL
+library nodes (frontend/lower.py:434-463) whose execution ``interp`` hands to
+the rank simulator as P2P events (interp.py:443-447, 483-489); the simulator
+itself (``sdfgkit.dist``) is absent from the mounted reference, its contract
+is SPEC.md:535-541, 575-580:
+
+* a send snapshots its (strided) view when posted; a receive completes at
+  ``waitall``; messages match on (source, destination, tag), FIFO per key;
+* a send without a matching receive is a deadlock ("unmatched message"), so
+  is a receive nobody sends ("waitall pending"); overlapping outstanding
+  receives into the same elements are a race diagnostic;
+* counters: ``messages_posted`` (sends), ``messages_delivered`` (receives),
+  ``comm_bytes`` (bytes sent + received), ``collective_calls``.
+
+B200 mapping: the send snapshot is a ``b2_copy_view`` into a staging buffer,
+``waitall`` is ONE grouped NCCL send/recv batch (libb2 ``b2_nccl_group_p2p``)
+on the executor's stream — per peer, sends and receives ordered by (tag,
+posting order) on both sides, which is exactly (src, dst, tag) FIFO matching
+— followed by ``b2_copy_view`` of each received staging buffer into its
+view.  Everything is stream-ordered, so a whole local-view program (loop,
+kernels, exchanges) is captured into one CUDA graph per rank.  Because a
+mismatched NCCL batch would hang rather than report, every rank first walks
+its state machine without launching anything, records the message keys per
+``waitall``, and the ranks compare them (``check_matching``) before any
+transfer is issued.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import runtime as rt, sdfg, symexpr
+
+
+class DeadlockError(RuntimeError):
+    pass
+
+
+class SimError(RuntimeError):
+    pass
+
+
+@dataclass
+class _Msg:
+    send: bool
+    peer: int
+    tag: int
+    seq: int
+    nbytes: int
+    staging: int = 0
+    view: object = None  # receive target (runtime.View)
+    box: tuple = ()  # receive target: container + per-dim (lo, hi, step)
+
+
+def check_matching(records: list) -> None:
+    """records[r] = list of waitall epochs of rank r, each a list of
+    (send?, peer, tag, nbytes).  Raises DeadlockError unless, epoch by epoch,
+    every send r -> p with tag t has a receive on p from r with tag t of the
+    same size (FIFO per key), and vice versa."""
+    P = len(records)
+    n_ep = max((len(e) for e in records), default=0)
+    problems = []
+    for k in range(n_ep):
+        for r in range(P):
+            ep = records[r][k] if k < len(records[r]) else []
+            for send, peer, tag, nbytes in ep:
+                if not (0 <= peer < P):
+                    problems.append(f"rank {r} epoch {k}: peer {peer} outside 0..{P - 1}")
+        for r in range(P):
+            for p in range(P):
+                ep_r = records[r][k] if k < len(records[r]) else []
+                ep_p = records[p][k] if k < len(records[p]) else []
+                sends = sorted((t, i, n) for i, (s, q, t, n) in enumerate(ep_r) if s and q == p)
+                recvs = sorted((t, i, n) for i, (s, q, t, n) in enumerate(ep_p) if not s and q == r)
+                st = [(t, n) for t, _, n in sends]
+                rv = [(t, n) for t, _, n in recvs]
+                if st == rv:
+                    continue
+                extra_s = list(st)
+                for x in rv:
+                    if x in extra_s:
+                        extra_s.remove(x)
+                extra_r = list(rv)
+                for x in st:
+                    if x in extra_r:
+                        extra_r.remove(x)
+                for t, n in extra_s:
+                    problems.append(f"unmatched message {r}->{p} tag {t} ({n} B) at waitall {k}")
+                for t, n in extra_r:
+                    problems.append(f"waitall pending: rank {p} receive from {r} tag {t} "
+                                    f"({n} B) at waitall {k}")
+    if problems:
+        raise DeadlockError("; ".join(problems))
+
+
+@dataclass
+class RankComm:
+    """Executor-side handler for ISEND / IRECV / WAITALL on one rank."""
+
+    rank: int
+    world: int
+    nccl: object = None  # dist.NcclComm (libb2), also for world size 1
+    pending: list = field(default_factory=list)
+    records: list = field(default_factory=list)  # host-side keys per waitall epoch
+    _cur: list = field(default_factory=list)
+    _staging: dict = field(default_factory=dict)
+    _seq: int = 0
+    dry: bool = False
+
+    # -- host bookkeeping --------------------------------------------------------
+
+    def _args(self, ex, op, sym):
+        n = op.node
+        peer = int(symexpr.evaluate(n.attrs["peer"], sym))
+        tag = int(symexpr.evaluate(n.attrs["tag"], sym))
+        ins = {e.dst_conn: e for e in op.state.in_edges(n) if e.memlet is not None}
+        outs = {e.src_conn: e for e in op.state.out_edges(n) if e.memlet is not None}
+        return peer, tag, ins, outs
+
+    def _buffer(self, key, nbytes):
+        p = self._staging.get(key)
+        if p is None or p[1] < nbytes:
+            q = ctypes.c_void_p()
+            rt.check(rt.lib().b2_malloc(ctypes.byref(q), max(16, nbytes)), "staging")
+            p = (q.value, max(16, nbytes))
+            self._staging[key] = p
+        return p[0]
+
+    def execute(self, ex, op, sym, counters):
+        kind = op.node.kind
+        if kind in ("isend", "irecv"):
+            self._post(ex, op, sym, counters, kind == "isend")
+        elif kind == "waitall":
+            self._waitall(ex, counters)
+        else:
+            raise SimError(f"collective '{kind}' is not supported by the local-view runner")
+
+    def record_dry(self, ex, op, sym):
+        """State-machine walk without transfers: message keys only."""
+        kind = op.node.kind
+        if kind in ("isend", "irecv"):
+            peer, tag, ins, outs = self._args(ex, op, sym)
+            m = (ins if kind == "isend" else outs)["buf"].memlet
+            nbytes = _nbytes(ex, m, sym)
+            if kind == "irecv":  # race diagnostic, before any transfer
+                ranges = symexpr.eval_subset(m.subset, sym)
+                box = (m.container, tuple((r.start, r.stop, r.step) for r in ranges))
+                if any(x[5] is not None and _overlap(x[5], box) for x in self._cur):
+                    raise SimError(f"overlapping outstanding receives into '{m.container}'")
+            else:
+                box = None
+            # staging buffers exist before any (captured) run
+            self._buffer((op.idx, sum(1 for x in self._cur if x[4] == op.idx)), nbytes)
+            self._cur.append((kind == "isend", peer, tag, nbytes, op.idx, box))
+        elif kind == "waitall":
+            self.records.append([x[:4] for x in self._cur])
+            self._cur = []
+
+    def finish_dry(self):
+        if self._cur:  # posted but never waited for
+            self.records.append([x[:4] for x in self._cur])
+            self._cur = []
+
+    # -- device side -------------------------------------------------------------
+
+    def _post(self, ex, op, sym, counters, send):
+        peer, tag, ins, outs = self._args(ex, op, sym)
+        m = (ins if send else outs)["buf"].memlet
+        base, off, dt, dims = ex.view(m, sym)
+        esz = sdfg.DTYPE_BYTES[dt]
+        n = int(np.prod([d[0] for d in dims])) if dims else 1
+        nbytes = n * esz
+        key = (op.idx, sum(1 for x in self.pending if x.seq == op.idx))
+        stg = self._buffer(key, nbytes)
+        view = rt.make_view(base, off, dt, [d[0] for d in dims], [d[1] for d in dims])
+        flat = rt.make_view(stg, 0, dt, [n], [1])
+        msg = _Msg(send, peer, tag, op.idx, nbytes, stg)
+        if send:
+            # the send snapshots its view now
+            rt.check(rt.lib().b2_copy_view(ctypes.byref(flat), ctypes.byref(view), 0, ex.stream),
+                     "isend snapshot")
+            ex.launches += 1
+            if counters is not None:
+                counters.messages_posted += 1
+                counters.comm_bytes += nbytes
+        else:
+            ranges = symexpr.eval_subset(m.subset, sym)
+            box = (m.container, tuple((r.start, r.stop, r.step) for r in ranges))
+            for other in self.pending:
+                if not other.send and _overlap(other.box, box):
+                    raise SimError(f"overlapping outstanding receives into '{m.container}'")
+            msg.view, msg.box = view, box
+        self.pending.append(msg)
+
+    def _waitall(self, ex, counters):
+        if not self.pending:
+            return
+        ops = []
+        for send in (True, False):
+            for msg in sorted((x for x in self.pending if x.send == send),
+                              key=lambda x: (x.peer, x.tag)):
+                ops.append((send, msg.peer, msg.staging, msg.nbytes))
+        if self.nccl is None:
+            raise SimError("local-view transfers need a communicator")
+        self.nccl.p2p(ops, ex.stream)
+        for msg in self.pending:
+            if msg.send:
+                continue
+            n = msg.nbytes // sdfg.DTYPE_BYTES[_dtype_name(msg.view)]
+            flat = rt.make_view(msg.staging, 0, _dtype_name(msg.view), [n], [1])
+            rt.check(rt.lib().b2_copy_view(ctypes.byref(msg.view), ctypes.byref(flat), 0,
+                                           ex.stream), "irecv delivery")
+            ex.launches += 1
+            if counters is not None:
+                counters.messages_delivered += 1
+                counters.comm_bytes += msg.nbytes
+        self.pending = []
+
+    def close(self):
+        for p, _ in self._staging.values():
+            rt.lib().b2_free(p)
+        self._staging.clear()
+
+
+def _nbytes(ex, m, sym):
+    ranges = symexpr.eval_subset(m.subset, sym)
+    n = 1
+    for r in ranges:
+        n *= len(r)
+    return n * sdfg.DTYPE_BYTES[ex.g.containers[m.container].dtype]
+
+
+def _overlap(a, b) -> bool:
+    if a[0] != b[0]:
+        return False
+    for (l1, h1, s1), (l2, h2, s2) in zip(a[1], b[1]):
+        r1, r2 = set(range(l1, h1, s1)), set(range(l2, h2, s2))
+        if not (r1 & r2):
+            return False
+    return True
+
+
+_CODE_NAME = {v: k for k, v in rt.DTYPE_CODE.items()}
+
+
+def _dtype_name(view) -> str:
+    return _CODE_NAME[view.dtype]
+
+
+class LocalViewRunner:
+    """One rank of a local-view program (explicit Isend / Irecv / Waitall):
+    the rank's own symbol bindings (peers, coordinates) on top of the shared
+    ones, the graph executed by a GpuExecutor whose communication nodes go to
+    ``RankComm``; message keys are checked across ranks before the first
+    transfer.  Launched one process per GPU (torchrun); ``torch.distributed``
+    only bootstraps the NCCL communicator and carries the key check."""
+
+    def __init__(self, g, bindings: dict, rank: int, world: int, device: int):
+        import torch.distributed as tdist
+
+        from .dist import NcclComm
+        from .machine import GpuExecutor, InterpOptions
+
+        self.g = sdfg.as_graph(g)
+        self.rank, self.world = rank, world
+        self.comm = RankComm(rank, world)
+        self.ex = GpuExecutor(self.g, bindings, device=device, options=InterpOptions(),
+                              comm=self.comm)
+        # walk the state machine once without launching: message keys per waitall
+        self.comm.dry = True
+        self.ex._instantiate_children()
+        self.comm.dry = False
+        self.comm.finish_dry()
+        recs = [None] * world
+        if world > 1:
+            tdist.all_gather_object(recs, self.comm.records)
+        else:
+            recs = [self.comm.records]
+        check_matching(recs)
+        self.comm.nccl = NcclComm(rank, world)
+
+    def run(self, inputs: dict, counters=None) -> dict:
+        keep = self.ex.prepare_inputs(inputs)
+        self.ex.run_device(first_call=True, counters=counters)
+        out = self.ex.outputs()
+        del keep
+        return out
+
+    def close(self):
+        self.ex.close()
+        self.comm.close()
+        if self.comm.nccl is not None:
+            self.comm.nccl.close()
+
+
+def local_view_run(g, ctx, rank_bindings: list, device: int | None = None):
+    """sim_run-shaped entry point for local-view programs under torchrun:
+    returns (this rank's outputs, instr) with instr = {"per_rank": {r:
+    counters}, "collective_ops": 0} gathered from every rank."""
+    import os
+
+    import torch.distributed as tdist
+
+    from .machine import Counters
+
+    rank = tdist.get_rank() if tdist.is_initialized() else 0
+    world = tdist.get_world_size() if tdist.is_initialized() else 1
+    if len(rank_bindings) != world:
+        raise SimError(f"{len(rank_bindings)} rank bindings for {world} ranks")
+    b = dict(ctx.bindings)
+    b.update(rank_bindings[rank])
+    dev = int(os.environ.get("LOCAL_RANK", rank)) if device is None else device
+    runner = LocalViewRunner(g, b, rank, world, dev)
+    c = Counters()
+    out = runner.run(dict(ctx.store), c)
+    per = [None] * world
+    if world > 1:
+        tdist.all_gather_object(per, c.as_dict())
+    else:
+        per = [c.as_dict()]
+    runner.close()
+    return out, {"per_rank": {r: per[r] for r in range(world)}, "collective_ops": 0}
+
+
+def jacobi2d_rank_setup(N: int, P: int, r: int):
+    """Row-block decomposition of jacobi_2d for the local-view program
+    (programs/jacobi2d_local.dpy): rank r owns interior rows [g0, g1) of the
+    N x N grid and holds global rows [g0 - 1, g1 + 1) (halo / boundary rows
+    included).  Returns (bindings, (lo, hi)) with (lo, hi) the global row
+    window of the local arrays."""
+    if (N - 2) % P:
+        raise SimError(f"{N - 2} interior rows do not divide over {P} ranks")
+    lnx = (N - 2) // P
+    g0 = 1 + r * lnx
+    b = {"lNx": lnx, "N": N, "up": r - 1 if r > 0 else -1, "down": r + 1 if r < P - 1 else -1}
+    return b, (g0 - 1, g0 + lnx + 1)
+
+
+def bench_local_view(args, W):
+    """bench.py --workload jacobi_2d_local [--gpus N]: the local-view jacobi_2d
+    (explicit halo exchange) at the jacobi_2d config, one rank per GPU;
+    max-over-ranks device time per program run, one JSON line from rank 0."""
+    import json
+    import os
+    import pathlib
+    import time
+
+    import torch
+    import torch.distributed as tdist
+
+    from bench import FLUSH_BYTES, ClockSampler, make_inputs, peaks  # noqa: E402
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    if not tdist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29544")
+        tdist.init_process_group("gloo" if world == 1 else "nccl", rank=rank, world_size=world)
+    root = pathlib.Path(__file__).resolve().parent.parent
+    N, T = W["syms"]["N"], W["syms"]["TSTEPS"]
+    g = sdfg.load(root / "tests" / "golden" / "graphs" / "jacobi2d_local.raw.json")
+    gfull = sdfg.load(root / "tests" / "golden" / "graphs" / "jacobi_2d.raw.json")
+    full = make_inputs(gfull, {"N": N, "TSTEPS": T})
+    b, (lo, hi) = jacobi2d_rank_setup(N, world, rank)
+    b["TSTEPS"] = T
+    runner = LocalViewRunner(g, b, rank, world, local)
+    ins = {"A": np.ascontiguousarray(full["A"][lo:hi]), "B": np.ascontiguousarray(full["B"][lo:hi])}
+    ex = runner.ex
+    keep = ex.prepare_inputs(ins)
+    for i in range(args.warmup):
+        ex.run_device(first_call=(i == 0))
+    ex.sync()
+    L = rt.lib()
+    fbuf = ctypes.c_void_p()
+    rt.check(L.b2_malloc(ctypes.byref(fbuf), FLUSH_BYTES))
+    evs = []
+    for _ in range(args.steps):
+        a, e = ctypes.c_void_p(), ctypes.c_void_p()
+        rt.check(L.b2_event_create(ctypes.byref(a)))
+        rt.check(L.b2_event_create(ctypes.byref(e)))
+        evs.append((a, e))
+    tdist.barrier()
+    with ClockSampler(local) as clk:
+        for a, e in evs:
+            rt.check(L.b2_memset(fbuf, 0, FLUSH_BYTES, ex.stream))  # 2 x 32 MB fit in L2
+            rt.check(L.b2_event_record(a, ex.stream))
+            ex.run_device(first_call=False)
+            rt.check(L.b2_event_record(e, ex.stream))
+        ex.sync()
+    ms = 0.0
+    for a, e in evs:
+        f = ctypes.c_float()
+        rt.check(L.b2_event_elapsed_ms(a, e, ctypes.byref(f)))
+        ms += f.value
+    ms /= args.steps
+    t = torch.tensor([ms], dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    run_bytes = W["sweeps"](W["syms"]) * W["sweep_bytes"](W["syms"])
+    value = run_bytes / (ms / 1e3) / 1e9
+    # end to end: window upload, run, download of the owned rows
+    t0 = time.perf_counter()
+    keep2 = ex.prepare_inputs(ins)
+    ex.run_device(first_call=False)
+    out = ex.outputs()
+    e2e_s = time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    del keep, keep2
+    L.b2_free(fbuf)
+    if rank == 0:
+        peak, kind = peaks()
+        print(json.dumps({
+            "metric": "jacobi_2d_f64_algorithmic_hbm_GBps", "value": value, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (make_inputs semantics, seed 0)",
+            "config": {"workload": f"jacobi_2d N={N} TSTEPS={T} as the local-view program "
+                                   "(explicit Isend/Irecv/Waitall halo exchange)",
+                       "parallelism": f"rows{world} (NCCL grouped send/recv per waitall)",
+                       "l2": "256 MB memset between timed steps"},
+            "roofline": {"bound": "hbm", "achieved": value / world, "peak": peak, "unit": "GB/s",
+                         "frac": value / world / peak, "peak_kind": kind, "traffic": None,
+                         "note": "per-GPU share; L2-resident working set"},
+            "e2e": {"value": run_bytes / e2e_s / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": sum(v.nbytes for v in ins.values()),
+                    "d2h_bytes_per_step": sum(np.asarray(v).nbytes for v in out.values())},
+            "gpu_launches": getattr(ex, "trace_launches", 0) * args.steps,
+            "clocks": clk.summary()}), flush=True)
+    runner.close()
+    tdist.barrier()
+    tdist.destroy_process_group()

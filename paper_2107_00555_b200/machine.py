@@ -124,13 +124,14 @@ class GpuExecutor:
 
     def __init__(self, g: sdfg.Graph, bindings: dict, device: int = 0, stream=None,
                  options: InterpOptions | None = None, external: dict | None = None,
-                 dynamic_p0: bool = False):
+                 dynamic_p0: bool = False, comm=None):
         rt.device(device)
         self.g = g
         self.bindings = {k: int(v) for k, v in bindings.items()}
         self.opt = options or InterpOptions()
         self.planner = P.Planner(g, self.bindings).build()
         self.planner.dynamic_p0 = dynamic_p0
+        self.comm = comm  # comm.RankComm for local-view programs (ISEND/IRECV/WAITALL)
         self.buf = _Buffers()
         self.flag = self.buf.alloc(8)
         if stream is None:
@@ -557,6 +558,9 @@ class GpuExecutor:
         if self._dry:
             if isinstance(op, P.NestedOp):
                 self._exec_nested(op, sym, None, dry=True)
+            elif (isinstance(op, P.LibOp) and op.kind == "comm" and self.comm is not None
+                  and self.comm.dry):
+                self.comm.record_dry(self, op, sym)
             return
         if op.idx in self.pair_second:
             return  # ran inside the pair kernel of its predecessor
@@ -577,8 +581,12 @@ class GpuExecutor:
             self._exec_copy(op, sym, counters)
         elif isinstance(op, P.LibOp):
             if op.kind == "comm":
-                raise InterpreterError(
-                    f"communication node '{op.node.kind}' requires the rank simulator")
+                if self.comm is None:
+                    raise InterpreterError(
+                        f"communication node '{op.node.kind}' requires the rank simulator "
+                        "(comm.LocalViewRunner)")
+                self.comm.execute(self, op, sym, counters)
+                return
             if op.rowpass is not None:
                 op.rowpass.run(self, sym, counters)
             elif op.kind == "matmul":
@@ -915,8 +923,10 @@ def _out_strides(cd, M, N):
 
 
 def _add_counters(dst, src):
-    for k in ("wcr_commits", "map_iterations", "bytes_moved"):
-        setattr(dst, k, getattr(dst, k) + getattr(src, k))
+    for k in ("wcr_commits", "map_iterations", "bytes_moved", "messages_posted",
+              "messages_delivered", "collective_calls", "comm_bytes"):
+        if hasattr(dst, k) and hasattr(src, k):
+            setattr(dst, k, getattr(dst, k) + getattr(src, k))
 
 
 def _count_map(ex: GpuExecutor, op: P.MapGroup, rvals, counters, env):

@@ -1,0 +1,125 @@
+"""Local-view message passing (comm.py): the cross-rank message-key check on
+CPU, and the GPU runner on one rank (self-addressed messages, no-comm
+decompositions).  Multi-rank transfers are NCCL grouped send/recv — the same
+libb2 path the slab runner uses."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+
+def test_check_matching_fifo_per_key():
+    from paper_2107_00555_b200.comm import check_matching
+
+    # rank 0 sends tags 7 then 8 to rank 1; rank 1 posts the receives in the
+    # opposite order: (src, dst, tag) matching still pairs them
+    r0 = [[(True, 1, 7, 32), (True, 1, 8, 16), (False, 1, 9, 8)]]
+    r1 = [[(False, 0, 8, 16), (False, 0, 7, 32), (True, 0, 9, 8)]]
+    check_matching([r0, r1])
+    check_matching([[[]], [[]]])  # waitall on empty requests: no-op
+
+
+def test_check_matching_diagnostics():
+    from paper_2107_00555_b200.comm import DeadlockError, check_matching
+
+    with pytest.raises(DeadlockError, match="unmatched message"):
+        check_matching([[[(True, 1, 3, 16)]], [[]]])
+    with pytest.raises(DeadlockError, match="waitall pending"):
+        check_matching([[[]], [[(False, 0, 3, 16)]]])
+    with pytest.raises(DeadlockError, match="unmatched message"):  # size mismatch
+        check_matching([[[(True, 1, 3, 16)]], [[(False, 0, 3, 8)]]])
+    with pytest.raises(DeadlockError, match="outside"):
+        check_matching([[[(True, 5, 3, 16)]]])
+    # a receive posted one waitall later than its send does not match
+    with pytest.raises(DeadlockError):
+        check_matching([[[(True, 1, 1, 8)], []], [[], [(False, 0, 1, 8)]]])
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch.distributed as tdist
+
+    if not tdist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        tdist.init_process_group("gloo", rank=0, world_size=1)
+    yield
+
+
+@pytest.mark.gpu
+def test_halo_pair_self_exchange(pg):
+    """pkg/tests/test_dist.py:121-140 on one rank addressing itself: the
+    received column equals the sent one, byte and message counters match."""
+    from paper_2107_00555_b200 import ExecContext, sdfg
+    from paper_2107_00555_b200.comm import local_view_run
+
+    g = sdfg.load(GOLDEN / "graphs" / "halo_pair.raw.json")
+    lnx, lny = 4, 5
+    rng = np.random.default_rng(2)
+    A = rng.uniform(-1, 1, (lnx + 2, lny + 2))
+    ctx = ExecContext(bindings={"lNx": lnx, "lNy": lny}).bind_inputs({"A": A})
+    out, instr = local_view_run(g, ctx, [{"peer": 0, "me": 0}])
+    i, j = np.meshgrid(np.arange(lnx + 2), np.arange(lny + 2), indexing="ij")
+    buf = 0 * 100.0 + i * 10.0 + j + A
+    ref = np.zeros_like(A)
+    ref[1:-1, -1] = buf[1:-1, -2]
+    assert np.array_equal(out["A"], ref)
+    c = instr["per_rank"][0]
+    assert c["comm_bytes"] == 2 * lnx * 8
+    assert c["messages_posted"] == 1 and c["messages_delivered"] == 1
+
+
+@pytest.mark.gpu
+def test_overlapping_receives_race(pg):
+    from paper_2107_00555_b200 import ExecContext, sdfg
+    from paper_2107_00555_b200.comm import SimError, local_view_run
+
+    g = sdfg.load(GOLDEN / "graphs" / "overlap_recv.raw.json")
+    ctx = ExecContext(bindings={"lNx": 2, "lNy": 2}).bind_inputs({"A": np.zeros((4, 4))})
+    with pytest.raises(SimError, match="overlapping"):
+        local_view_run(g, ctx, [{"peer": 0}])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,T", [(12, 4), (33, 5)])
+def test_jacobi2d_local_single_rank_equals_global(pg, N, T):
+    """The local-view jacobi_2d on a 1-rank decomposition (no neighbours: the
+    halo rows are the global boundary) is bitwise the corpus jacobi_2d."""
+    from oracle import kernels_np as K
+    from paper_2107_00555_b200 import ExecContext, sdfg
+    from paper_2107_00555_b200.comm import local_view_run
+
+    g = sdfg.load(GOLDEN / "graphs" / "jacobi2d_local.raw.json")
+    rng = np.random.default_rng(N)
+    A = rng.uniform(-1, 1, (N, N))
+    B = rng.uniform(-1, 1, (N, N))
+    ctx = ExecContext(bindings={"lNx": N - 2, "N": N, "TSTEPS": T}).bind_inputs(
+        {"A": A.copy(), "B": B.copy()})
+    out, instr = local_view_run(g, ctx, [{"up": -1, "down": -1}])
+    K.jacobi_2d(A, B, T)
+    assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
+    assert instr["per_rank"][0]["messages_posted"] == 0
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_jacobi2d_rank_setup(P):
+    """Row windows of the local-view decomposition: owned interior rows tile
+    1..N-2 exactly, neighbours are adjacent ranks, edges have none."""
+    from paper_2107_00555_b200.comm import jacobi2d_rank_setup
+
+    N = 2 + 24 * 7
+    owned = []
+    for r in range(P):
+        b, (lo, hi) = jacobi2d_rank_setup(N, P, r)
+        assert hi - lo == b["lNx"] + 2
+        owned += list(range(lo + 1, hi - 1))
+        assert b["up"] == (r - 1 if r else -1) and b["down"] == (r + 1 if r < P - 1 else -1)
+    assert owned == list(range(1, N - 1))
