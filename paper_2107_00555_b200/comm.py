@@ -47,6 +47,31 @@ class SimError(RuntimeError):
     pass
 
 
+class CollectiveOrderError(RuntimeError):
+    pass
+
+
+def block_layout(shape, grid_dims, coords):
+    """Block distribution of a global view of ``shape`` over ``grid_dims``
+    (SPEC.md:532-534): grid dim d splits array dim d (a 1-D grid splits the
+    first array dim); uneven extents are an error (no implicit padding).
+    Returns (start, extent) per array dim for the rank at ``coords``."""
+    if len(grid_dims) > len(shape):
+        raise SimError(f"grid {tuple(grid_dims)} has more dims than the array {tuple(shape)}")
+    out = []
+    for d, n in enumerate(shape):
+        if d < len(grid_dims):
+            g = grid_dims[d]
+            if n % g:
+                raise SimError(f"extent {n} of dim {d} is not covered by grid dim {g} "
+                               "(divisible block sizes required)")
+            b = n // g
+            out.append((coords[d] * b, b))
+        else:
+            out.append((0, n))
+    return out
+
+
 @dataclass
 class _Msg:
     send: bool
@@ -106,6 +131,7 @@ class RankComm:
 
     rank: int
     world: int
+    grid: object = None  # dist.ProcessGrid for block collectives (default 1-D)
     nccl: object = None  # dist.NcclComm (libb2), also for world size 1
     pending: list = field(default_factory=list)
     records: list = field(default_factory=list)  # host-side keys per waitall epoch
@@ -133,14 +159,99 @@ class RankComm:
             self._staging[key] = p
         return p[0]
 
+    colls: list = field(default_factory=list)  # host-side collective sequence
+
     def execute(self, ex, op, sym, counters):
         kind = op.node.kind
         if kind in ("isend", "irecv"):
             self._post(ex, op, sym, counters, kind == "isend")
         elif kind == "waitall":
             self._waitall(ex, counters)
+        elif kind in ("block_scatter", "block_gather"):
+            self._block(ex, op, sym, counters, kind == "block_scatter")
         else:
             raise SimError(f"collective '{kind}' is not supported by the local-view runner")
+
+    # -- block collectives (root = rank 0 holds the global container) -----------
+
+    def _grid_dims(self):
+        return tuple(self.grid.dims) if self.grid is not None else (self.world,)
+
+    def _coords(self, r):
+        if self.grid is None:
+            return (r,)
+        return self.grid.coords(r)
+
+    def _block_plan(self, ex, op, sym, scatter):
+        n = op.node
+        ins = {e.dst_conn: e for e in op.state.in_edges(n) if e.memlet is not None}
+        outs = {e.src_conn: e for e in op.state.out_edges(n) if e.memlet is not None}
+        gm = (ins["a"] if scatter else outs["out"]).memlet  # global side
+        lm = (outs["out"] if scatter else ins["a"]).memlet  # local side
+        gshape = [len(r) for r in symexpr.eval_subset(gm.subset, sym)]
+        lshape = [len(r) for r in symexpr.eval_subset(lm.subset, sym)]
+        dims = self._grid_dims()
+        if int(np.prod(dims)) != self.world:
+            raise SimError(f"grid {dims} does not have {self.world} ranks")
+        blocks = [block_layout(gshape, dims, self._coords(q)) for q in range(self.world)]
+        if [e for _, e in blocks[self.rank]] != lshape:
+            raise SimError(f"local view {lshape} does not match the block "
+                           f"{[e for _, e in blocks[self.rank]]} of {gshape}")
+        esz = sdfg.DTYPE_BYTES[ex.g.containers[gm.container].dtype]
+        return gm, lm, blocks, int(np.prod(lshape)) * esz
+
+    def _block(self, ex, op, sym, counters, scatter):
+        gm, lm, blocks, nbytes = self._block_plan(ex, op, sym, scatter)
+        L = rt.lib()
+        gb, goff, gdt, gdims = ex.view(gm, sym)
+        lb, loff, ldt, ldims = ex.view(lm, sym)
+        lview = rt.make_view(lb, loff, ldt, [d[0] for d in ldims], [d[1] for d in ldims])
+        n_el = nbytes // sdfg.DTYPE_BYTES[gdt]
+
+        def gblock(q):  # view of rank q's block inside the root's global view
+            off = goff + sum(st * gd[1] for (st, _), gd in zip(blocks[q], gdims))
+            return rt.make_view(gb, off, gdt, [e for _, e in blocks[q]], [d[1] for d in gdims])
+
+        stg = [self._buffer((op.idx, "blk", q), nbytes) for q in range(self.world)]
+
+        def flat(q):
+            return rt.make_view(stg[q], 0, gdt, [n_el], [1])
+
+        ops = []
+        if scatter:
+            if self.rank == 0:
+                for q in range(self.world):
+                    v, f = gblock(q), flat(q)
+                    rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(v), 0, ex.stream), "scatter")
+                    ex.launches += 1
+                    if q:
+                        ops.append((True, q, stg[q], nbytes))
+            else:
+                ops.append((False, 0, stg[self.rank], nbytes))
+            if ops:
+                self.nccl.p2p(ops, ex.stream)
+            f = flat(self.rank)
+            rt.check(L.b2_copy_view(ctypes.byref(lview), ctypes.byref(f), 0, ex.stream), "scatter")
+            ex.launches += 1
+        else:
+            f = flat(self.rank)
+            rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(lview), 0, ex.stream), "gather")
+            ex.launches += 1
+            if self.rank == 0:
+                ops = [(False, q, stg[q], nbytes) for q in range(1, self.world)]
+            else:
+                ops = [(True, 0, stg[self.rank], nbytes)]
+            if ops:
+                self.nccl.p2p(ops, ex.stream)
+            if self.rank == 0:
+                for q in range(self.world):
+                    v, fq = gblock(q), flat(q)
+                    rt.check(L.b2_copy_view(ctypes.byref(v), ctypes.byref(fq), 0, ex.stream),
+                             "gather")
+                    ex.launches += 1
+        if counters is not None:
+            counters.collective_calls += 1
+            counters.comm_bytes += sum(x[3] for x in ops)
 
     def record_dry(self, ex, op, sym):
         """State-machine walk without transfers: message keys only."""
@@ -162,6 +273,11 @@ class RankComm:
         elif kind == "waitall":
             self.records.append([x[:4] for x in self._cur])
             self._cur = []
+        elif kind in ("block_scatter", "block_gather"):
+            gm, lm, blocks, nbytes = self._block_plan(ex, op, sym, kind == "block_scatter")
+            for q in range(self.world):
+                self._buffer((op.idx, "blk", q), nbytes)
+            self.colls.append((kind, tuple(e for _, e in blocks[0]), nbytes))
 
     def finish_dry(self):
         if self._cur:  # posted but never waited for
@@ -262,7 +378,7 @@ class LocalViewRunner:
     transfer.  Launched one process per GPU (torchrun); ``torch.distributed``
     only bootstraps the NCCL communicator and carries the key check."""
 
-    def __init__(self, g, bindings: dict, rank: int, world: int, device: int):
+    def __init__(self, g, bindings: dict, rank: int, world: int, device: int, grid=None):
         import torch.distributed as tdist
 
         from .dist import NcclComm
@@ -270,7 +386,7 @@ class LocalViewRunner:
 
         self.g = sdfg.as_graph(g)
         self.rank, self.world = rank, world
-        self.comm = RankComm(rank, world)
+        self.comm = RankComm(rank, world, grid)
         self.ex = GpuExecutor(self.g, bindings, device=device, options=InterpOptions(),
                               comm=self.comm)
         # walk the state machine once without launching: message keys per waitall
@@ -280,10 +396,14 @@ class LocalViewRunner:
         self.comm.finish_dry()
         recs = [None] * world
         if world > 1:
-            tdist.all_gather_object(recs, self.comm.records)
+            tdist.all_gather_object(recs, (self.comm.records, self.comm.colls))
         else:
-            recs = [self.comm.records]
-        check_matching(recs)
+            recs = [(self.comm.records, self.comm.colls)]
+        for r in range(world):  # collectives: same kinds, same order, everywhere
+            if recs[r][1] != recs[0][1]:
+                raise CollectiveOrderError(
+                    f"rank {r} calls collectives {recs[r][1]}, rank 0 {recs[0][1]}")
+        check_matching([x[0] for x in recs])
         self.comm.nccl = NcclComm(rank, world)
 
     def run(self, inputs: dict, counters=None) -> dict:
@@ -300,7 +420,7 @@ class LocalViewRunner:
             self.comm.nccl.close()
 
 
-def local_view_run(g, ctx, rank_bindings: list, device: int | None = None):
+def local_view_run(g, ctx, rank_bindings: list, device: int | None = None, grid=None):
     """sim_run-shaped entry point for local-view programs under torchrun:
     returns (this rank's outputs, instr) with instr = {"per_rank": {r:
     counters}, "collective_ops": 0} gathered from every rank."""
@@ -317,7 +437,7 @@ def local_view_run(g, ctx, rank_bindings: list, device: int | None = None):
     b = dict(ctx.bindings)
     b.update(rank_bindings[rank])
     dev = int(os.environ.get("LOCAL_RANK", rank)) if device is None else device
-    runner = LocalViewRunner(g, b, rank, world, dev)
+    runner = LocalViewRunner(g, b, rank, world, dev, grid)
     c = Counters()
     out = runner.run(dict(ctx.store), c)
     per = [None] * world
@@ -326,7 +446,8 @@ def local_view_run(g, ctx, rank_bindings: list, device: int | None = None):
     else:
         per = [c.as_dict()]
     runner.close()
-    return out, {"per_rank": {r: per[r] for r in range(world)}, "collective_ops": 0}
+    return out, {"per_rank": {r: per[r] for r in range(world)},
+                 "collective_ops": sum(per[r]["collective_calls"] for r in range(world))}
 
 
 def jacobi2d_rank_setup(N: int, P: int, r: int):

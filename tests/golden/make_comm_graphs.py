@@ -10,6 +10,8 @@ programs/jacobi2d_local.dpy jacobi_2d with rows block-distributed and explicit
                             halo exchange (the SPEC.md:580 local-view example)
 programs/overlap_recv.dpy   two outstanding receives into the same elements
                             (race diagnostic)
+programs/block_roundtrip.dpy block_scatter -> local map -> block_gather
+                            (SPEC.md:532-534 round trip)
 """
 
 import json
@@ -25,7 +27,7 @@ sys.path.insert(0, str(REF / "src"))
 from sdfgkit import frontend  # noqa: E402
 from sdfgkit.serialize import to_dict  # noqa: E402
 
-for name in ("halo_pair", "jacobi2d_local", "overlap_recv"):
+for name in ("halo_pair", "jacobi2d_local", "overlap_recv", "block_roundtrip"):
     g, diags = frontend.compile_source((REPO / "programs" / f"{name}.dpy").read_text())
     errs = [d for d in diags if d.severity == "error"]
     assert not errs, errs

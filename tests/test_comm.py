@@ -123,3 +123,34 @@ def test_jacobi2d_rank_setup(P):
         owned += list(range(lo + 1, hi - 1))
         assert b["up"] == (r - 1 if r else -1) and b["down"] == (r + 1 if r < P - 1 else -1)
     assert owned == list(range(1, N - 1))
+
+
+def test_block_layout_spec_examples():
+    """BlockScatter f64[4,4] over a 2x2 grid gives rank (0,1)
+    rows 0-1, cols 2-3; uneven extents are an error; a 1-D grid splits the
+    first dimension."""
+    from paper_2107_00555_b200.comm import SimError, block_layout
+    from paper_2107_00555_b200.dist import ProcessGrid
+
+    g = ProcessGrid((2, 2))
+    assert block_layout((4, 4), g.dims, g.coords(1)) == [(0, 2), (2, 2)]
+    assert block_layout((8, 3), (4,), (3,)) == [(6, 2), (0, 3)]
+    with pytest.raises(SimError, match="not covered"):
+        block_layout((5, 4), (2, 2), (0, 0))
+
+
+@pytest.mark.gpu
+def test_block_scatter_gather_roundtrip_single_rank(pg):
+    """BlockGather(map(BlockScatter(A))) on a 1x1 grid: local copies only."""
+    from paper_2107_00555_b200 import ExecContext, sdfg
+    from paper_2107_00555_b200.comm import local_view_run
+    from paper_2107_00555_b200.dist import ProcessGrid
+
+    g = sdfg.load(GOLDEN / "graphs" / "block_roundtrip.raw.json")
+    rng = np.random.default_rng(4)
+    A = rng.uniform(-1, 1, (6, 10))
+    ctx = ExecContext(bindings={"N": 6, "M": 10, "lN": 6, "lM": 10}).bind_inputs(
+        {"A": A, "B": np.zeros_like(A), "L": np.zeros_like(A)})
+    out, instr = local_view_run(g, ctx, [{}], grid=ProcessGrid((1, 1)))
+    assert np.array_equal(out["B"], A * 2.0 + 1.0)
+    assert instr["collective_ops"] == 2 and instr["per_rank"][0]["comm_bytes"] == 0
