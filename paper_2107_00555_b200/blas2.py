@@ -410,7 +410,7 @@ class RowPass:
             if prof is not None:
                 ev = ex._prof_event_pair()
                 rt.lib().b2_event_record(ev[0], ex.stream)
-            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 8, 1), blob, ex.stream)
+            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream)
             if prof is not None:
                 rt.lib().b2_event_record(ev[1], ex.stream)
                 prof.append((self.kfin.name, nfin, ev))

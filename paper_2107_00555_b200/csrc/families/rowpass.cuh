@@ -208,10 +208,14 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
 #endif  // RP_TMA
 
 // out[n] (wcr)= sum over G row-groups of ws[g][n]  (+ per-tile dot partials).
-// Block 32 x 8: 32 columns per block, the 8 thread rows split the G partials
-// (strided), then thread row 0 adds the 8 sums in a fixed order.
-extern "C" __global__ void __launch_bounds__(256) RP_FIN_NAME(const __grid_constant__ RpArgs a) {
-  __shared__ double part[8][33];
+// Block 32 x RP_FY: 32 columns per block, the RP_FY thread rows split the G
+// partials (strided, independent loads in flight), then thread row 0 adds
+// the RP_FY sums in a fixed order (deterministic).
+#ifndef RP_FY
+#define RP_FY 32
+#endif
+extern "C" __global__ void __launch_bounds__(32 * RP_FY) RP_FIN_NAME(const __grid_constant__ RpArgs a) {
+  __shared__ double part[RP_FY][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const b2_ll i = (b2_ll)blockIdx.x * 32 + tx;
 #if RP_AXPY
@@ -219,13 +223,13 @@ extern "C" __global__ void __launch_bounds__(256) RP_FIN_NAME(const __grid_const
     const double *ws = (const double *)a.w[1];
     double s = 0.0;
     if (i < RP_N)
-      for (int g = ty; g < RP_G; g += 8) s += ws[(b2_ll)g * RP_N + i];
+      for (int g = ty; g < RP_G; g += RP_FY) s += ws[(b2_ll)g * RP_N + i];
     part[ty][tx] = s;
     __syncthreads();
     if (ty == 0 && i < RP_N) {
       double t = part[0][tx];
 #pragma unroll
-      for (int k = 1; k < 8; ++k) t += part[k][tx];
+      for (int k = 1; k < RP_FY; ++k) t += part[k][tx];
       rp_store_axpy(a, i, t);
     }
   }
