@@ -569,6 +569,7 @@ class SlabGpuRunner:
         return True
 
     def _rows_ptr(self, c, lo, hi):
+        """(device address, bytes) of global rows [lo, hi) of container c."""
         desc = self.lg.containers[c]
         wlo = self.plan.window[self.rank][c][0]
         row = 1
@@ -586,14 +587,11 @@ class SlabGpuRunner:
                              self.ex.stream)
 
     def _rows_of(self, c, lo, hi):
-        desc = self.lg.containers[c]
-        wlo = self.plan.window[self.rank][c][0]
-        row = 1
-        for d in self.ex.buf.shape[c][1:]:
-            row *= d
-        esz = sdfg.DTYPE_BYTES[desc.dtype]
-        ptr = self.ex.buf.ptr[c] + (lo - wlo) * row * esz
-        return self.torch.as_tensor(_CudaArray(ptr, ((hi - lo) * row,), _TYPESTR[desc.dtype]),
+        """torch view of global rows [lo, hi) of container c's local buffer."""
+        ptr, nbytes = self._rows_ptr(c, lo, hi)
+        dt = self.lg.containers[c].dtype
+        return self.torch.as_tensor(_CudaArray(ptr, (nbytes // sdfg.DTYPE_BYTES[dt],),
+                                               _TYPESTR[dt]),
                                     device=f"cuda:{self.torch.cuda.current_device()}")
 
     def _hook(self, op, reads, writes, phase):
