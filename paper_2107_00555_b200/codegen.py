@@ -871,6 +871,7 @@ class _Gen:
         nthr = spec.block[0] * spec.block[1] * spec.block[2]
         pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}) '
                    f"{spec.name}(const __grid_constant__ B2Args a) {{")
+        pro.append("  B2_PDL_ENTRY();")
         def _size(name):
             n = 1
             for x in self.shapes[name]:
@@ -1411,7 +1412,7 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     body = gen.lines
     spec = gen.spec
     pro = [f'extern "C" __global__ void __launch_bounds__(256) {name}'
-           "(const __grid_constant__ B2Args a) {"]
+           "(const __grid_constant__ B2Args a) {", "  B2_PDL_ENTRY();"]
     for cname in spec.containers:
         c = planner.g.containers[cname]
         if gen.place(cname) == "reg":

@@ -7,6 +7,7 @@
 // test tier checks the exported symbols there).
 
 #include <cuda.h>
+#include <stdlib.h>
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
@@ -54,6 +55,7 @@ typedef CUresult (*PFN_ModuleGetFunction)(CUfunction *, CUmodule, const char *);
 typedef CUresult (*PFN_LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned,
                                      unsigned, unsigned, unsigned, CUstream, void **, void **);
 typedef CUresult (*PFN_FuncSetAttribute)(CUfunction, CUfunction_attribute, int);
+typedef CUresult (*PFN_LaunchKernelEx)(const CUlaunchConfig *, CUfunction, void **, void **);
 typedef CUresult (*PFN_GetErrorString)(CUresult, const char **);
 
 static struct {
@@ -63,6 +65,7 @@ static struct {
   PFN_ModuleUnload moduleUnload = nullptr;
   PFN_ModuleGetFunction moduleGetFunction = nullptr;
   PFN_LaunchKernel launchKernel = nullptr;
+  PFN_LaunchKernelEx launchKernelEx = nullptr;  // programmatic dependent launch
   PFN_FuncSetAttribute funcSetAttribute = nullptr;
   PFN_GetErrorString getErrorString = nullptr;
 } drv;
@@ -82,6 +85,7 @@ static int load_driver() {
     B2_GET("cuModuleUnload", moduleUnload, PFN_ModuleUnload);
     B2_GET("cuModuleGetFunction", moduleGetFunction, PFN_ModuleGetFunction);
     B2_GET("cuLaunchKernel", launchKernel, PFN_LaunchKernel);
+    B2_GET("cuLaunchKernelEx", launchKernelEx, PFN_LaunchKernelEx);
     B2_GET("cuFuncSetAttribute", funcSetAttribute, PFN_FuncSetAttribute);
     B2_GET("cuGetErrorString", getErrorString, PFN_GetErrorString);
 #undef B2_GET
@@ -270,8 +274,35 @@ extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsign
   size_t sz = args_bytes;
   void *cfg[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void *>(args),
                  CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
-  CUresult r = drv.launchKernel((CUfunction)fn, gx, gy, gz, bx, by, bz, smem, (CUstream)stream,
-                                nullptr, cfg);
+  // JIT kernels open with griddepcontrol.wait (prelude B2_PDL_ENTRY), so they
+  // may be launched programmatically: the launch overlaps the tail of the
+  // previous kernel in the stream (also as graph edges under capture)
+  static int pdl = -1;
+  if (pdl < 0) {
+    const char *e = getenv("B2_PDL");
+    pdl = !(e && e[0] == '0');
+  }
+  CUresult r;
+  if (pdl) {
+    CUlaunchAttribute at[1];
+    at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+    at[0].value.programmaticStreamSerializationAllowed = 1;
+    CUlaunchConfig lc = {};
+    lc.gridDimX = gx;
+    lc.gridDimY = gy;
+    lc.gridDimZ = gz;
+    lc.blockDimX = bx;
+    lc.blockDimY = by;
+    lc.blockDimZ = bz;
+    lc.sharedMemBytes = smem;
+    lc.hStream = (CUstream)stream;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    r = drv.launchKernelEx(&lc, (CUfunction)fn, nullptr, cfg);
+  } else {
+    r = drv.launchKernel((CUfunction)fn, gx, gy, gz, bx, by, bz, smem, (CUstream)stream,
+                         nullptr, cfg);
+  }
   if (r != CUDA_SUCCESS) return cu_check(r, "cuLaunchKernel");
   b2_count_launch();
   return B2_OK;

@@ -189,6 +189,15 @@ __device__ __forceinline__ void b2_cp_commit() { asm volatile("cp.async.commit_g
 template <int N>
 __device__ __forceinline__ void b2_cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---- programmatic dependent launch -----------------------------------------
+// Every JIT kernel starts with this: wait until the previous kernel in the
+// stream has completed (its writes visible), then let the next one launch.
+#define B2_PDL_ENTRY()                                          \
+  do {                                                          \
+    asm volatile("griddepcontrol.wait;" ::: "memory");          \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
 // ---- TMA bulk copies (cp.async.bulk, 1-D) completed on an mbarrier ----------
 __device__ __forceinline__ void b2_mbar_init(unsigned long long *b, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(

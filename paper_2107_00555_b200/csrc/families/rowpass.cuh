@@ -39,6 +39,7 @@ __device__ __forceinline__ double rp_block_sum(double v, double *red, int parity
 // slice and the column accumulators live in registers.  Shared layout:
 // [staged column vectors (RP_NSTAGED x RP_CW)] [reduction scratch 64] [ring].
 extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_constant__ RpArgs a) {
+  B2_PDL_ENTRY();
   extern __shared__ __align__(16) double rp_smem[];
   __shared__ __align__(8) unsigned long long rp_bar[RP_S];
   double *red = rp_smem + RP_NSTAGED * RP_CW;
@@ -126,6 +127,7 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
 }
 #else
 extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_constant__ RpArgs a) {
+  B2_PDL_ENTRY();
   extern __shared__ double rp_smem[];
   double *acc_s = rp_smem;                     // [RP_CW] column accumulators
   double *v_s = rp_smem + (RP_AXPY ? RP_CW : 0);  // [RP_CW] dot vector slice
@@ -215,6 +217,7 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
 #define RP_FY 32
 #endif
 extern "C" __global__ void __launch_bounds__(32 * RP_FY) RP_FIN_NAME(const __grid_constant__ RpArgs a) {
+  B2_PDL_ENTRY();
   __shared__ double part[RP_FY][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const b2_ll i = (b2_ll)blockIdx.x * 32 + tx;

@@ -260,6 +260,10 @@ def get_kernel(src: str, name: str, extra_opts=(), max_smem: int = 0) -> Kernel:
     k = _kcache.get(key)
     if k is not None:
         return k
+    # launched with programmatic stream serialization (b2_launch): every JIT
+    # kernel must wait on its predecessor before touching memory
+    if src.count("__global__") != src.count("B2_PDL_ENTRY();"):
+        raise B2Error(f"kernel source for {name} lacks B2_PDL_ENTRY() in a __global__ function")
     cub, h = get_cubin(src, name, extra_opts)
     L = lib()
     mod = ctypes.c_void_p()

@@ -169,7 +169,7 @@ def generate_pair(pl, g1, g2, X, Y, o1, emin, emax, shapes, name) -> CG.KernelSp
     SX = 32 + emax[2] - emin[2]
 
     pro = [f'extern "C" __global__ void __launch_bounds__({SX * SY}) '
-           f"{name}(const __grid_constant__ B2Args a) {{"]
+           f"{name}(const __grid_constant__ B2Args a) {{", "  B2_PDL_ENTRY();"]
     for c in spec.containers:
         if gen1.place(c) == "reg" and gen2.place(c) == "reg":
             continue

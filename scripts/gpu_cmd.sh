@@ -1,6 +1,8 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-for cfg in "8 16 1" "8 16 0" "16 16 1" "4 16 1" "8 24 1" "8 32 1" "4 32 1"; do
-  set -- $cfg
-  echo "== BY $1 vec $2 full $3"
-  B2_MARCH_BY=$1 B2_VEC=$2 B2_FULL_TILES=$3 timeout -s KILL 120 python scripts/probe_time.py heat_3d.raw '{"N":400,"TSTEPS":20}' 2 2>&1 | grep -E "kernel|Error" | head -1
+timeout -s KILL 900 python -m pytest tests -m gpu -q -x -o faulthandler_timeout=200 2>&1 | tail -2
+for p in 0 1; do echo "PDL=$p"
+B2_PDL=$p timeout -s KILL 120 python scripts/probe_time.py jacobi_2d.raw '{"N":2000,"TSTEPS":100}' 3 2>&1 | grep -E "rep 2|Error" | head -1
+B2_PDL=$p timeout -s KILL 120 python scripts/probe_time.py nbody.raw '{"N":100,"NT":1000}' 3 2>&1 | grep -E "rep 2|Error" | head -1
+B2_PDL=$p timeout -s KILL 120 python scripts/probe_time.py heat_3d.raw '{"N":400,"TSTEPS":100}' 3 2>&1 | grep -E "rep 2|Error" | head -1
+B2_PDL=$p timeout -s KILL 120 python scripts/probe_time.py gemver.raw '{"N":8000}' 3 2>&1 | grep -E "rep 2|Error" | head -1
 done
