@@ -14,7 +14,7 @@ Graphs may also be given as schema-v1 JSON (pkg/src/sdfgkit/serialize.py).
 
 from .machine import (  # noqa: F401
     Counters, ExecContext, GpuExecutor, InterpOptions, InterpreterError, OutOfBoundsError,
-    get_executor, interpret,
+    get_executor, interpret, run_twice_determinism,
 )
 from .plan import PlanError  # noqa: F401
 from .runtime import BackendUnavailable  # noqa: F401
@@ -23,4 +23,5 @@ from . import sdfg  # noqa: F401
 __all__ = [
     "interpret", "ExecContext", "InterpOptions", "Counters", "InterpreterError",
     "OutOfBoundsError", "GpuExecutor", "get_executor", "PlanError", "BackendUnavailable", "sdfg",
+    "run_twice_determinism",
 ]

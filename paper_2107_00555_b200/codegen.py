@@ -192,14 +192,74 @@ class _Gen:
                 L.append("    }")
         else:
             L.append("    }")
-        for t in self.red.values():
+        self.spec.red_fin = []
+        self.spec.red_nout, self.spec.red_nch = nout, C
+        self.red_decode = [ln for ln in L if ln.strip().startswith(("const b2_ll q", "const b2_ll p_"))
+                           and any(f"p_{p} " in ln or f"q{idx[p]} " in ln for p in pout)]
+        for k, t in enumerate(self.red.values()):
             a = t["acc"]
             if full and t["exclusive"]:
                 L.append(f"    {t['target']} = {a};")
+            elif not full and t["ct"] == "double":
+                # deterministic: chunk partials to a workspace, reduced in
+                # chunk order by the companion _fin kernel (run-to-run
+                # bitwise reproducible, like the reference, interp.py:153)
+                ws = self.arg(("ptr", f"{self.spec.name}#ws{k}"))
+                L.append(f"    ((double *){ws})[ch * NOUT + (f % NOUT)] = {a};")
+                self.spec.red_fin.append((ws, t))
             else:
                 cond = "" if full else "if (lo < hi) "
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
         L.append("  }")
+        return L
+
+    def _reduce_fin(self, pro) -> list:
+        """Companion kernel of a chunked reduction: per output, the chunk
+        partials folded in a fixed order into the target with its WCR.  Many
+        chunks: one CTA per output, 256 contiguous chunk ranges then thread 0
+        over the 256 sums; few chunks: one thread per output."""
+        spec = self.spec
+        ident = {"add": "0.0", "mul": "1.0", "min": "b2_inf()", "max": "(-b2_inf())"}
+        per_block = spec.red_nch >= 64
+        spec.red_fin_block = per_block
+        L = [f'extern "C" __global__ void __launch_bounds__(256) '
+             f"{spec.name}_fin(const __grid_constant__ B2Args a) {{", "  B2_PDL_ENTRY();"]
+        L += [ln for ln in pro[2:] if "pv_" not in ln and "tflat" not in ln]
+        L.append(f"  constexpr b2_ll NOUT = {spec.red_nout}LL;")
+        L.append(f"  constexpr int NCH = {spec.red_nch};")
+        if per_block:
+            L += ["  __shared__ double red[256];",
+                  "  constexpr int PER = (NCH + 255) / 256;",
+                  "  for (b2_ll f = blockIdx.x; f < NOUT; f += gridDim.x) {",
+                  "    b2_ll rem = f; (void)rem;"]
+        else:
+            L += ["  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUT; "
+                  "f += (b2_ll)gridDim.x * blockDim.x) {",
+                  "    b2_ll rem = f; (void)rem;"]
+        L += self.red_decode
+        for ws, t in spec.red_fin:
+            w = f"((const double *){ws})"
+            op, acc = t["wcr"], f"s_{t['acc']}"
+            if per_block:
+                L += [f"    double {acc} = {ident[op]};",
+                      "    {",
+                      "      const int c0 = (int)threadIdx.x * PER;",
+                      "      const int c1 = c0 + PER < NCH ? c0 + PER : NCH;",
+                      f"      for (int c = c0; c < c1; ++c) {acc} = b2_op_{op}({acc}, {w}[c * NOUT + f]);",
+                      "    }",
+                      f"    red[threadIdx.x] = {acc};",
+                      "    __syncthreads();",
+                      "    if (threadIdx.x == 0) {",
+                      f"      double t = red[0];",
+                      f"      for (int i = 1; i < 256; ++i) t = b2_op_{op}(t, red[i]);",
+                      f"      {t['target']} = b2_op_{op}({t['target']}, t);",
+                      "    }",
+                      "    __syncthreads();"]
+            else:
+                L += [f"    double {acc} = {w}[f];",
+                      f"    for (int c = 1; c < NCH; ++c) {acc} = b2_op_{op}({acc}, {w}[c * NOUT + f]);",
+                      f"    {t['target']} = b2_op_{op}({t['target']}, {acc});"]
+        L += ["  }", "}"]
         return L
 
     def _rowred_plan(self):
@@ -1073,7 +1133,8 @@ class _Gen:
         src = [f"// generated by paper_2107_00555_b200.codegen for state "
                f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
                "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
-        spec.source = "\n".join(src + pro + loop + ["}"]) + "\n"
+        fin = self._reduce_fin(pro) if mode == "reduce" and getattr(spec, "red_fin", None) else []
+        spec.source = "\n".join(src + pro + loop + ["}"] + fin) + "\n"
         return spec
 
 

@@ -278,9 +278,9 @@ extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsign
   // may be launched programmatically: the launch overlaps the tail of the
   // previous kernel in the stream (also as graph edges under capture)
   static int pdl = -1;
-  if (pdl < 0) {
+  if (pdl < 0) {  // opt-in, matching runtime.NVRTC_OPTS (-DB2_NO_PDL otherwise)
     const char *e = getenv("B2_PDL");
-    pdl = !(e && e[0] == '0');
+    pdl = e && e[0] == '1';
   }
   CUresult r;
   if (pdl) {

@@ -192,11 +192,17 @@ __device__ __forceinline__ void b2_cp_wait() { asm volatile("cp.async.wait_group
 // ---- programmatic dependent launch -----------------------------------------
 // Every JIT kernel starts with this: wait until the previous kernel in the
 // stream has completed (its writes visible), then let the next one launch.
+#ifdef B2_NO_PDL
+#define B2_PDL_ENTRY() \
+  do {                 \
+  } while (0)
+#else
 #define B2_PDL_ENTRY()                                          \
   do {                                                          \
     asm volatile("griddepcontrol.wait;" ::: "memory");          \
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
   } while (0)
+#endif
 
 // ---- TMA bulk copies (cp.async.bulk, 1-D) completed on an mbarrier ----------
 __device__ __forceinline__ void b2_mbar_init(unsigned long long *b, unsigned count) {

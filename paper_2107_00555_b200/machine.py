@@ -194,6 +194,15 @@ class GpuExecutor:
                 spec = codegen.generate(self.planner, op, self.buf.shape, name)
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
                 spec.kernel = rt.get_kernel(src, name)
+                spec.fin_kernel = None
+                if getattr(spec, "red_fin", None):
+                    # deterministic chunked reduction: partial workspace + fold kernel
+                    spec.fin_kernel = rt.get_kernel(src, name + "_fin")
+                    for k in range(len(spec.red_fin)):
+                        key = f"{name}#ws{k}"
+                        nb = 8 * spec.red_nout * spec.red_nch
+                        self.scratch[key] = self.buf.alloc(nb)
+                        self.buf.nbytes[key] = nb
                 self.specs[op.idx] = spec
             elif isinstance(op, P.LibOp) and op.rowpass is not None:
                 op.rowpass.compile(self)
@@ -347,7 +356,9 @@ class GpuExecutor:
                 continue  # persistent transients keep their contents (interp.py:216-219)
             self.zero(name)
         for n, p in self.scratch.items():
-            rt.check(rt.lib().b2_memset(p, 0, self.buf.nbytes[n + "#scratch"], self.stream), "memset")
+            if n + "#scratch" in self.buf.nbytes:  # per-thread private scratch (not workspaces)
+                rt.check(rt.lib().b2_memset(p, 0, self.buf.nbytes[n + "#scratch"], self.stream),
+                         "memset")
 
     # -- execution ---------------------------------------------------------------
 
@@ -646,6 +657,11 @@ class GpuExecutor:
             ev = self._prof_event_pair()
             rt.lib().b2_event_record(ev[0], self.stream)
         rt.launch(spec.kernel, grid, block, blob, self.stream)
+        if spec.fin_kernel is not None:
+            fg = spec.red_nout if spec.red_fin_block else -(-spec.red_nout // 256)
+            fg = max(1, min(fg, codegen.MAX_BLOCKS * 8))
+            rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream)
+            self.launches += 1
         if self._prof is not None:
             rt.lib().b2_event_record(ev[1], self.stream)
             self._prof.append((spec.name, npts, ev))
@@ -1080,6 +1096,24 @@ def interpret(g, ctx, options: InterpOptions | None = None) -> dict[str, np.ndar
         for k in ("wcr_commits", "map_iterations", "bytes_moved"):
             setattr(counters, k, getattr(counters, k) + getattr(c, k))
     return out
+
+
+def run_twice_determinism(g, ctx) -> bool:
+    """Two interpretations with identical contexts are bitwise identical
+    (interp.py:153-161): inputs copied per run, outputs compared exactly."""
+    import copy
+
+    bindings, store, _ = _ctx_parts(ctx)
+
+    def once():
+        c2 = ExecContext(bindings=dict(bindings))
+        c2.bind_inputs({k: copy.deepcopy(np.asarray(v)) for k, v in store.items()})
+        return interpret(g, c2)
+
+    out1, out2 = once(), once()
+    if set(out1) != set(out2):
+        return False
+    return all(np.array_equal(out1[k], out2[k]) for k in out1)
 
 
 _ = itertools

@@ -31,6 +31,11 @@ NVRTC_OPTS = [
     "-default-device",
     "-lineinfo",
 ]
+# programmatic dependent launch is opt-in (B2_PDL=1): measured slower on the
+# benchmark programs (heat_3d 41.1 vs 39.9 ms, jacobi_2d 1.92 vs 1.83 ms,
+# go_fast 0.435 vs 0.377 ms), faster only on launch-bound nbody (-3 %)
+if os.environ.get("B2_PDL", "0") != "1":  # must match b2_launch
+    NVRTC_OPTS.append("-DB2_NO_PDL")
 
 
 class BackendUnavailable(RuntimeError):

@@ -1,8 +1,9 @@
-"""Compile this repo's local-view (explicit message passing) programs with the
-REFERENCE frontend into schema-v1 graphs (run here, where /root/reference
-exists):
+"""Compile extra programs with the REFERENCE frontend (and passes) into
+schema-v1 graphs (run here, where /root/reference exists):
 
-    python tests/golden/make_comm_graphs.py
+    python tests/golden/make_extra_graphs.py
+
+Local-view (explicit message passing) programs:
 
 programs/halo_pair.dpy      column exchange between two ranks (the pattern of
                             pkg/tests/test_dist.py:105-140)
@@ -31,6 +32,27 @@ for name in ("halo_pair", "jacobi2d_local", "overlap_recv", "block_roundtrip"):
     g, diags = frontend.compile_source((REPO / "programs" / f"{name}.dpy").read_text())
     errs = [d for d in diags if d.severity == "error"]
     assert not errs, errs
+    out = HERE / "graphs" / f"{name}.raw.json"
+    out.write_text(json.dumps(to_dict(g), indent=1) + "\n")
+    print("wrote", out)
+
+# Interpreter-contract programs (the cases of pkg/tests/test_interp.py:52-121,
+# written here; compiled by the reference frontend, tile_wcr by its autoopt)
+from sdfgkit import autoopt  # noqa: E402
+
+CONTRACT = {
+    "oob_read": "def f(A: f64[N], B: f64[N], K: i64):\n    B[0] = A[K]\n",
+    "tiled_red": "def red(s: f64, A: f64[N]):\n    for i in map[0:N]:\n        s += A[i]\n",
+    "bicg_head": "def bicg(A: f64[N, M], s: f64[M], q: f64[N], p: f64[M], r: f64[N]):\n"
+                 "    s[:] = r @ A\n",
+    "bicg_tail": "def bicg(A: f64[N, M], s: f64[M], q: f64[N], p: f64[M], r: f64[N]):\n"
+                 "    q[:] = A @ p\n",
+}
+for name, src in CONTRACT.items():
+    g, diags = frontend.compile_source(src)
+    assert g is not None, diags
+    if name == "tiled_red":
+        autoopt.tile_wcr(g, 16)
     out = HERE / "graphs" / f"{name}.raw.json"
     out.write_text(json.dumps(to_dict(g), indent=1) + "\n")
     print("wrote", out)

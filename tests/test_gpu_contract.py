@@ -1,0 +1,159 @@
+"""The reference interpreter's own contract tests (pkg/tests/test_interp.py),
+run against the B200 executor on graphs the reference compiled (golden
+graphs; the extra programs come from tests/golden/make_extra_graphs.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _g(name):
+    from paper_2107_00555_b200 import sdfg
+
+    return sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+
+
+def _ctx(bindings, inputs):
+    from paper_2107_00555_b200 import ExecContext
+
+    return ExecContext(bindings=dict(bindings)).bind_inputs(inputs)
+
+
+def test_gemm_identity():
+    """test_interp.py:17-24"""
+    from paper_2107_00555_b200 import interpret
+
+    A = np.array([[1.0, 2.0], [3.0, 4.0]])
+    out = interpret(_g("gemm.raw"), _ctx({"NI": 2, "NJ": 2, "NK": 2},
+                                         {"A": A, "B": np.eye(2), "C": np.zeros((2, 2)),
+                                          "alpha": 1.0, "beta": 0.0}))
+    assert np.array_equal(out["C"], A)
+
+
+def test_jacobi_first_half_step():
+    """test_interp.py:26-32: the inexact 0.33333 coefficient, bitwise."""
+    from paper_2107_00555_b200 import interpret
+
+    out = interpret(_g("jacobi_1d.raw"), _ctx({"N": 4, "TSTEPS": 2},
+                                              {"A": np.array([0.0, 3.0, 0.0, 3.0]),
+                                               "B": np.zeros(4)}))
+    assert np.array_equal(out["B"], [0.0, 0.99999, 1.99998, 0.0])
+
+
+def test_wcr_sum_of_ones():
+    """test_interp.py:34-40: value and commit count."""
+    from paper_2107_00555_b200 import interpret
+
+    ctx = _ctx({"NI": 2, "NJ": 2}, {"alpha": 0.0, "C": np.ones((2, 2))})
+    out = interpret(_g("wcr_sum.raw"), ctx)
+    assert out["alpha"][()] == 4.0
+    assert ctx.counters.wcr_commits == 4
+
+
+@pytest.mark.parametrize("name,syms", [("gemm", {"NI": 4, "NJ": 6, "NK": 8}),
+                                       ("jacobi_2d", {"N": 6, "TSTEPS": 4})])
+def test_run_twice(name, syms):
+    """test_interp.py:44-50"""
+    from paper_2107_00555_b200 import run_twice_determinism
+    from paper_2107_00555_b200 import symexpr
+
+    g = _g(f"{name}.raw")
+    rng = np.random.default_rng(3)
+    inputs = {}
+    for n, c in g.containers.items():
+        if not c.transient:
+            shape = tuple(symexpr.evaluate(d, syms) for d in c.shape)
+            inputs[n] = rng.uniform(-1, 1, shape) if shape else float(rng.uniform(0.5, 1.5))
+    assert run_twice_determinism(g, _ctx(syms, inputs))
+
+
+def test_tiled_reduction_deterministic():
+    """test_interp.py:52-64: tile_wcr(16) reduction, run twice bitwise; and
+    the sum itself."""
+    from paper_2107_00555_b200 import interpret, run_twice_determinism
+
+    g = _g("tiled_red.raw")
+    assert run_twice_determinism(g, _ctx({"N": 64}, {"s": 0.0, "A": np.arange(64.0)}))
+    out = interpret(g, _ctx({"N": 64}, {"s": 0.0, "A": np.arange(64.0)}))
+    assert out["s"][()] == 2016.0
+
+
+def test_missing_binding():
+    """test_interp.py:66-70"""
+    from paper_2107_00555_b200 import interpret
+
+    with pytest.raises(Exception, match="missing symbol"):
+        interpret(_g("gemm.raw"), _ctx({"NI": 2, "NJ": 2}, {}))
+
+
+def test_out_of_bounds_is_hard_error():
+    """test_interp.py:72-81: the message carries the offending index."""
+    from paper_2107_00555_b200 import OutOfBoundsError, interpret
+
+    with pytest.raises(OutOfBoundsError) as exc:
+        interpret(_g("oob_read.raw"), _ctx({"N": 4, "K": 9},
+                                           {"A": np.zeros(4), "B": np.zeros(4)}))
+    assert "9" in str(exc.value)
+
+
+def test_shape_mismatch_rejected():
+    """test_interp.py:83-90"""
+    from paper_2107_00555_b200 import interpret
+
+    with pytest.raises(Exception, match="shape"):
+        interpret(_g("gemm.raw"), _ctx({"NI": 2, "NJ": 2, "NK": 2},
+                                       {"A": np.zeros((3, 3)), "B": np.eye(2),
+                                        "C": np.zeros((2, 2)), "alpha": 1.0, "beta": 0.0}))
+
+
+def test_bytes_additive_over_states():
+    """test_interp.py:93-112: splitting bicg into its two statements moves
+    the same bytes in total."""
+    from paper_2107_00555_b200 import interpret
+
+    syms = {"N": 6, "M": 4}
+    rng = np.random.default_rng(3)
+    inputs = {"A": rng.uniform(-1, 1, (6, 4)), "s": rng.uniform(-1, 1, 4),
+              "q": rng.uniform(-1, 1, 6), "p": rng.uniform(-1, 1, 4), "r": rng.uniform(-1, 1, 6)}
+    ctx = _ctx(syms, {k: v.copy() for k, v in inputs.items()})
+    interpret(_g("bicg.raw"), ctx)
+    total = ctx.counters.bytes_moved
+    assert total > 0
+    parts = 0
+    for piece in ("bicg_head.raw", "bicg_tail.raw"):
+        cp = _ctx(syms, {k: v.copy() for k, v in inputs.items()})
+        interpret(_g(piece), cp)
+        parts += cp.counters.bytes_moved
+    assert parts == total
+
+
+def test_map_iterations_counted():
+    """test_interp.py:114-121"""
+    from paper_2107_00555_b200 import interpret
+
+    ctx = _ctx({"NI": 3, "NJ": 5}, {"alpha": 0.0, "C": np.ones((3, 5))})
+    interpret(_g("wcr_sum.raw"), ctx)
+    assert ctx.counters.map_iterations == 15
+
+
+def test_jacobi_1d_constant_field():
+    """test_interp.py:123-130"""
+    from paper_2107_00555_b200 import interpret
+
+    c = 2.0
+    out = interpret(_g("jacobi_1d.raw"), _ctx({"N": 6, "TSTEPS": 2},
+                                              {"A": np.full(6, c), "B": np.full(6, c)}))
+    assert np.allclose(out["B"][1:-1], 0.99999 * c, rtol=0, atol=1e-14)
+
+
+def test_jacobi_2d_constant_field():
+    """test_interp.py:132-140: the 0.2 coefficient is exact."""
+    from paper_2107_00555_b200 import interpret
+
+    c = 3.0
+    out = interpret(_g("jacobi_2d.raw"), _ctx({"N": 6, "TSTEPS": 2},
+                                              {"A": np.full((6, 6), c), "B": np.full((6, 6), c)}))
+    assert np.allclose(out["B"][1:-1, 1:-1], c, rtol=0, atol=1e-14)

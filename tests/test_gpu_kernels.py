@@ -182,3 +182,19 @@ def test_softmax_fold_and_rowred_vs_numpy_port(N, H, SM):
     ref = np.empty_like(x)
     K.softmax(x.copy(), ref)
     assert rel_err(out["out"], ref) <= 1e-12
+
+
+def test_run_twice_bitwise_deterministic():
+    """run_twice_determinism (interp.py:153) on chunked reductions: the
+    go_fast trace (12000-term sum into one scalar) is folded in chunk order
+    by a second kernel, so repeated runs are bitwise identical."""
+    from paper_2107_00555_b200 import ExecContext, interpret, run_twice_determinism, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "go_fast.pipe.json")
+    rng = np.random.default_rng(9)
+    a = rng.uniform(-1, 1, (3000, 3000))
+    ctx = ExecContext(bindings={"N": 3000}).bind_inputs({"a": a, "out": np.zeros_like(a)})
+    assert run_twice_determinism(g, ctx)
+    outs = [interpret(g, ExecContext(bindings={"N": 3000}).bind_inputs(
+        {"a": a, "out": np.zeros_like(a)}))["out"] for _ in range(3)]
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
