@@ -882,6 +882,13 @@ class _Gen:
         vec = 1
         if mode == "tile2":
             vec = _pick_vec(self.const_ranges[-1][2])
+            npts = 1
+            for r in self.const_ranges:
+                npts *= r[2] if r is not None else 1 << 30
+            if npts <= (1 << 24):
+                # small (L2-resident) sweeps: more threads beat longer rows
+                # (jacobi_2d N=2000: 1.74 ms at vec 2 vs 1.83 at vec 4)
+                vec = min(vec, 2)
         elif mode == "march":
             # 16 planes per thread measured 3 % faster on heat_3d N=400 (202 vs
             # 209 us); short or runtime dim-0 ranges (slabs) keep 8
