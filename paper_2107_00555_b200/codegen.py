@@ -151,6 +151,11 @@ class _Gen:
         full = self.red_full
         C = 1 if full else max(1, min(-(-148 * 512 // max(1, nout)), -(-nred // 16)))
         self.spec.red_threads = nout * C
+        if not full and C <= 8:
+            # few chunks per output: whole warps stay on one chunk of 32
+            # consecutive outputs (coalesced / broadcast loads like the
+            # thread-per-output layout) and the fold happens in-block
+            return self._reduce_loop_inblock(R, pout, reg_decls, body, nout, nred, C)
         L = [f"  constexpr b2_ll NOUT = {nout}LL, NRED = {nred}LL, NCH = {C}LL;",
              "  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUT * NCH; "
              "f += (b2_ll)gridDim.x * blockDim.x) {",
@@ -211,6 +216,66 @@ class _Gen:
                 cond = "" if full else "if (lo < hi) "
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
         L.append("  }")
+        return L
+
+    def _reduce_loop_inblock(self, R, pout, reg_decls, body, nout, nred, C) -> list:
+        """Chunked reduction with every output's C chunks in one CTA: chunk
+        partials meet in shared memory and the chunk-0 thread folds them in
+        chunk order (deterministic, one kernel — no workspace pass)."""
+        grp = self.group
+        idx = {p: i for i, p in enumerate(grp.params)}
+        opb = 256 // C
+        self.spec.red_threads = -(-nout // opb) * 256
+        dts = [t for t in self.red.values() if t["ct"] == "double"]
+        L = [f"  constexpr b2_ll NOUT = {nout}LL, NRED = {nred}LL;",
+             f"  constexpr int NCH = {C}, OPB = {opb};",
+             f"  __shared__ double red_sm[{max(1, len(dts))}][256];",
+             "  for (b2_ll ob = blockIdx.x; ob * OPB < NOUT; ob += gridDim.x) {",
+             "    const int ol = (int)threadIdx.x % OPB, ch = (int)threadIdx.x / OPB;",
+             "    const b2_ll fo = ob * OPB + ol;",
+             "    const bool valid = (int)threadIdx.x < OPB * NCH && fo < NOUT;",
+             "    b2_ll rem = valid ? fo : 0;"]
+        for p in reversed(pout):
+            i = idx[p]
+            L.append(f"    const b2_ll q{i} = rem % rl{i}; rem /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * q{i};")
+        for t in self.red.values():
+            ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
+            if t["ct"] != "double" and t["wcr"] in ("min", "max"):
+                ident = "0"  # integer min/max: committed only when iterations ran
+            L.append(f"    {t['ct']} {t['acc']} = ({t['ct']})({ident});")
+        L.append("    const b2_ll lo = valid ? (b2_ll)ch * NRED / NCH : 0;")
+        L.append("    const b2_ll hi = valid ? ((b2_ll)ch + 1) * NRED / NCH : 0;")
+        it = "int" if nred < 2 ** 31 else "b2_ll"
+        L.append(f"    for ({it} rf = ({it})lo; rf < ({it})hi; ++rf) {{")
+        L.append("    b2_ll rr = rf;")
+        for p in reversed(R):
+            i = idx[p]
+            L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
+        L += reg_decls(4)
+        L += body
+        L.append("    }")
+        for k, t in enumerate(dts):
+            L.append(f"    red_sm[{k}][threadIdx.x] = {t['acc']};")
+        for t in self.red.values():
+            if t["ct"] != "double":  # integer WCR: associative, atomics stay exact
+                L.append(f"    if (lo < hi) b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
+        L.append("    __syncthreads();")
+        L.append("    if (valid && ch == 0) {")
+        for k, t in enumerate(dts):
+            op = t["wcr"]
+            L.append(f"      double s{k} = red_sm[{k}][ol];")
+            L.append(f"      for (int c = 1; c < NCH; ++c) s{k} = b2_op_{op}(s{k}, "
+                     f"red_sm[{k}][c * OPB + ol]);")
+            if t["exclusive"]:
+                L.append(f"      {t['target']} = b2_op_{op}({t['target']}, s{k});")
+            else:
+                L.append(f"      b2_atomic_{op}(&{t['target']}, s{k});")
+        L.append("    }")
+        L.append("    __syncthreads();")
+        L.append("  }")
+        self.spec.red_fin = []
         return L
 
     def _reduce_fin(self, pro) -> list:
