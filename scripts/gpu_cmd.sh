@@ -1,5 +1,5 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 900 python -m pytest tests -m gpu -q -o faulthandler_timeout=200 2>&1 | tail -2
-timeout -s KILL 200 python scripts/probe_time.py nbody.raw '{"N":100,"NT":1000}' 3 2>&1 | grep -E "rep 2|Error" | head -2
-timeout -s KILL 200 python scripts/probe_time.py go_fast.pipe '{"N":12000}' 3 2>&1 | grep -E "rep 2|Error" | head -2
-timeout -s KILL 200 python scripts/probe_time.py azimint_naive.raw '{"N": 1000000, "NPT": 1000}' 3 2>&1 | grep -E "rep 2|Error" | head -2
+mkdir -p gpurun_out/suite
+rm -f profiles/bench_suite_r01_v5.json
+timeout -s KILL 1200 python scripts/bench_suite.py --out profiles/bench_suite_r01_v5.json > gpurun_out/suite.log 2>&1; tail -12 gpurun_out/suite.log
+cp profiles/bench_suite_r01_v5.json gpurun_out/suite/
