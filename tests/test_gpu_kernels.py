@@ -198,3 +198,26 @@ def test_run_twice_bitwise_deterministic():
     outs = [interpret(g, ExecContext(bindings={"N": 3000}).bind_inputs(
         {"a": a, "out": np.zeros_like(a)}))["out"] for _ in range(3)]
     assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("name,syms,shape", [("heat_3d.raw", {"N": 24, "TSTEPS": 4}, (24, 24, 24)),
+                                             ("jacobi_2d.raw", {"N": 40, "TSTEPS": 5}, (40, 40))])
+def test_dead_interior_inputs_upload_only_faces(name, syms, shape):
+    """B's interior is overwritten before it is read, so only its boundary
+    faces are uploaded: NaNs in the input interior never reach the result."""
+    from oracle import kernels_np as K
+    from paper_2107_00555_b200 import sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+    ex = GpuExecutor(g, syms)
+    assert ex.shell_only == {"B"}
+    rng = np.random.default_rng(1)
+    A = rng.uniform(-1, 1, shape)
+    B = rng.uniform(-1, 1, shape)
+    Bn = B.copy()
+    Bn[(slice(1, -1),) * len(shape)] = np.nan
+    out = _run(name, syms, {"A": A.copy(), "B": Bn})
+    (K.heat_3d_c if len(shape) == 3 else K.jacobi_2d_c)(A, B, syms["TSTEPS"])
+    assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
+    ex.close()
