@@ -1,1 +1,2 @@
-for i in 1 2; do timeout -s KILL 300 python bench.py 2>&1 | grep metric | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['clocks'])"; done
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout -s KILL 300 python -m pytest tests/test_gpu_contract.py -q -o faulthandler_timeout=100 2>&1 | tail -8

@@ -47,6 +47,15 @@ CONTRACT = {
                  "    s[:] = r @ A\n",
     "bicg_tail": "def bicg(A: f64[N, M], s: f64[M], q: f64[N], p: f64[M], r: f64[N]):\n"
                  "    q[:] = A @ p\n",
+    # a loop whose branch condition reads a scalar container updated inside
+    # the loop (interp.py:265-274: conditions may read 0-d containers)
+    "branchy": "def branchy(TSTEPS: i32, x: f64[N], s: f64):\n"
+               "    for t in range(TSTEPS):\n"
+               "        if s > 0.0:\n"
+               "            x[:] = x * 0.5\n"
+               "            s = s - 1.0\n"
+               "        else:\n"
+               "            x[:] = x + 1.0\n",
 }
 for name, src in CONTRACT.items():
     g, diags = frontend.compile_source(src)

@@ -157,3 +157,22 @@ def test_jacobi_2d_constant_field():
     out = interpret(_g("jacobi_2d.raw"), _ctx({"N": 6, "TSTEPS": 2},
                                               {"A": np.full((6, 6), c), "B": np.full((6, 6), c)}))
     assert np.allclose(out["B"][1:-1, 1:-1], c, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("s0", [2.5, -1.0, 0.0])
+def test_condition_on_scalar_container(s0):
+    """Transitions whose condition reads a 0-d container updated inside the
+    loop (interp.py:265-274): evaluated on the host after a device sync."""
+    from paper_2107_00555_b200 import interpret
+
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, 37)
+    out = interpret(_g("branchy.raw"), _ctx({"N": 37, "TSTEPS": 6}, {"x": x.copy(), "s": s0}))
+    xr, s = x.copy(), s0
+    for _ in range(6):
+        if s > 0.0:
+            xr = xr * 0.5
+            s = s - 1.0
+        else:
+            xr = xr + 1.0
+    assert np.array_equal(out["x"], xr) and out["s"][()] == s
