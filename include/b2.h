@@ -122,6 +122,20 @@ B2_API int b2_capture_begin(void *stream);
 B2_API int b2_capture_end(void *stream, void **graph_exec);
 B2_API int b2_graph_launch(void *graph_exec, void *stream);
 B2_API int b2_graph_destroy(void *graph_exec);
+/* Device-side branch in a capture (Machine.eval_cond on a 0-d container,
+ * interp.py:265-274, without a host round trip): adds a CUDA conditional
+ * IF/ELSE node whose predicate is *flag != 0 at graph run time; the caller
+ * captures body_then / body_else on another stream with
+ * b2_capture_body_begin/end, then continues after the node with
+ * b2_capture_if_end. */
+B2_API int b2_capture_if_begin(void *stream, const int *flag, void **node, void **body_then,
+                        void **body_else);
+B2_API int b2_capture_if_end(void *stream, void *node);
+B2_API int b2_capture_body_begin(void *body_stream, void *body_graph);
+B2_API int b2_capture_body_end(void *body_stream);
+/* dev[0..3] += a0..a3 (interpreter counters accumulated by branch bodies) */
+B2_API int b2_counters_add(long long *dev, long long a0, long long a1, long long a2, long long a3,
+                    void *stream);
 
 /* ---- ahead-of-time library kernels ------------------------------------- */
 /* dst[flat] (wcr)= convert(src[flat]) over the row-major flattening of both

@@ -330,6 +330,85 @@ extern "C" int b2_capture_end(void *stream, void **graph_exec) {
   return B2_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Device-side branches inside a capture: a CUDA conditional IF/ELSE node
+// whose predicate (*flag != 0) is set on the device when the graph runs, so a
+// transition condition that reads device data needs no host round trip.
+
+namespace {
+__global__ void b2_cond_set_kernel(cudaGraphConditionalHandle h, const int *flag) {
+  cudaGraphSetConditional(h, *flag != 0 ? 1u : 0u);
+}
+__global__ void b2_counters_add_kernel(long long *c, long long a0, long long a1, long long a2,
+                                       long long a3) {
+  c[0] += a0;
+  c[1] += a1;
+  c[2] += a2;
+  c[3] += a3;
+}
+}  // namespace
+
+extern "C" int b2_capture_if_begin(void *stream, const int *flag, void **node, void **body_then,
+                                   void **body_else) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStreamCaptureStatus st;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t nd = 0;
+  B2_CLEAR_ERROR();
+  int rc = b2_cuda_check(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd),
+                         "capture info");
+  if (rc) return rc;
+  if (st != cudaStreamCaptureStatusActive) return b2_fail(B2_ERR_ARG, "stream is not capturing");
+  cudaGraphConditionalHandle h;
+  rc = b2_cuda_check(cudaGraphConditionalHandleCreate(&h, graph, 0, 0), "conditional handle");
+  if (rc) return rc;
+  b2_cond_set_kernel<<<1, 1, 0, s>>>(h, flag);
+  B2_LAUNCH_CHECK("conditional set");
+  rc = b2_cuda_check(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd),
+                     "capture info");
+  if (rc) return rc;
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 2;  // body 0 when the value is non-zero, body 1 otherwise
+  cudaGraphNode_t n = nullptr;
+  rc = b2_cuda_check(cudaGraphAddNode(&n, graph, deps, nd, &p), "conditional node");
+  if (rc) return rc;
+  *node = n;
+  *body_then = p.conditional.phGraph_out[0];
+  *body_else = p.conditional.phGraph_out[1];
+  return B2_OK;
+}
+
+extern "C" int b2_capture_if_end(void *stream, void *node) {
+  cudaGraphNode_t n = (cudaGraphNode_t)node;
+  return b2_cuda_check(cudaStreamUpdateCaptureDependencies((cudaStream_t)stream, &n, 1,
+                                                           cudaStreamSetCaptureDependencies),
+                       "capture dependencies");
+}
+
+extern "C" int b2_capture_body_begin(void *body_stream, void *body_graph) {
+  return b2_cuda_check(cudaStreamBeginCaptureToGraph((cudaStream_t)body_stream,
+                                                     (cudaGraph_t)body_graph, nullptr, nullptr,
+                                                     0, cudaStreamCaptureModeThreadLocal),
+                       "begin body capture");
+}
+
+extern "C" int b2_capture_body_end(void *body_stream) {
+  cudaGraph_t g = nullptr;
+  return b2_cuda_check(cudaStreamEndCapture((cudaStream_t)body_stream, &g), "end body capture");
+}
+
+extern "C" int b2_counters_add(long long *dev, long long a0, long long a1, long long a2,
+                               long long a3, void *stream) {
+  B2_CLEAR_ERROR();
+  b2_counters_add_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dev, a0, a1, a2, a3);
+  B2_LAUNCH_CHECK("counters add");
+  return B2_OK;
+}
+
 extern "C" int b2_graph_launch(void *graph_exec, void *stream) {
   return b2_cuda_check(cudaGraphLaunch((cudaGraphExec_t)graph_exec, (cudaStream_t)stream),
                        "graph launch");

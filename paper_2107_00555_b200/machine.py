@@ -36,6 +36,8 @@ from . import codegen, plan as P, runtime as rt, scalar, sdfg, symexpr
 _NP = {"f64": np.float64, "i64": np.int64, "i32": np.int32, "bool": np.bool_}
 # upload only the boundary faces of inputs whose interior is dead on entry
 SHELL_UPLOAD = os.environ.get("B2_SHELL_UPLOAD", "1") == "1"
+# capture container-dependent branches as CUDA conditional nodes
+DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
 
 
 class InterpreterError(RuntimeError):
@@ -144,6 +146,10 @@ class GpuExecutor:
         self.stream = stream
         self.graph_exec = None
         self.capturable = self._capturable()
+        # transitions reading 0-d containers: captured as device-side IF/ELSE
+        # conditional nodes when the branches are structured (_device_branch)
+        self.device_branching = DEVICE_BRANCHES and not self.capturable
+        self._branch_ready = False
         self.scratch: dict[str, int] = {}
         self.launches = 0
         self.children: dict[int, "GpuExecutor"] = {}
@@ -462,14 +468,156 @@ class GpuExecutor:
         resident).  Returns after enqueueing; call ``sync()`` to wait."""
         rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
         self.zero_transients(first_call)
+        if self.device_branching and self.graph_exec is None:
+            try:
+                self._prepare_branching()
+                self._capture(counters)
+                self.capturable = True
+            except _NoDeviceBranch:
+                self.device_branching = False  # unstructured: host-evaluated conditions
         if self.capturable:
             if self.graph_exec is None:
                 self._capture(counters)
+            if self.device_branching:
+                rt.check(rt.lib().b2_memset(self._devc, 0, 32, self.stream), "memset")
             rt.check(rt.lib().b2_graph_launch(self.graph_exec, self.stream), "graph launch")
             if counters is not None and self._trace_counters is not None:
                 _add_counters(counters, self._trace_counters)
+            if counters is not None and self.device_branching:
+                dc = np.zeros(4, dtype=np.int64)
+                rt.check(rt.lib().b2_memcpy_d2h(dc.ctypes.data, self._devc, 32, self.stream),
+                         "d2h")
+                self.sync()
+                counters.wcr_commits += int(dc[0])
+                counters.map_iterations += int(dc[1])
+                counters.bytes_moved += int(dc[2])
         else:
             self._run_states(counters, eager=True)
+
+    # -- device-side branches -------------------------------------------------------
+
+    def _prepare_branching(self):
+        """Everything a captured device branch needs that may not be created
+        under capture: predicate flags, the body-capture stream, counters."""
+        if self._branch_ready:
+            return
+        if any(isinstance(op, P.NestedOp) for op in self.planner.all_ops) or self.planner.regions:
+            raise _NoDeviceBranch("nested graphs / loop regions")
+        self._flags = self.buf.alloc(4 * 4096)
+        self._devc = self.buf.alloc(32)
+        bs = ctypes.c_void_p()
+        rt.check(rt.lib().b2_stream_create(ctypes.byref(bs)), "stream")
+        self._body_stream = bs.value
+        self._cond_kernels: dict = {}
+        self._branch_ready = True
+
+    def _cond_kernel(self, pred):
+        """NVRTC kernel writing int(pred) (a scalar expression over 0-d
+        containers and symbols) to a predicate flag."""
+        key = repr(pred)
+        hit = self._cond_kernels.get(key)
+        if hit is not None:
+            return hit
+        names = sorted(scalar.free_names(pred))
+        types, cname, lines, args = {}, {}, [], []
+        for n in names:
+            if n in self.g.containers:
+                c = self.g.containers[n]
+                if c.kind != "scalar":
+                    raise _NoDeviceBranch(f"condition reads non-scalar container '{n}'")
+                lines.append(f"  const {codegen.CT[c.dtype]} v_{n} = *((const {codegen.CT[c.dtype]} *)"
+                             f"a.w[{len(args)}]);")
+                args.append(("ptr", n))
+                types[n] = codegen.TC[c.dtype]
+            else:
+                lines.append(f"  const long long v_{n} = a.w[{len(args)}];")
+                args.append(("sym", n))
+                types[n] = "i"
+            cname[n] = f"v_{n}"
+        code, ty = scalar.emit(pred, types, lambda n: cname[n])
+        name = "b2_cond_" + hashlib.sha1(key.encode()).hexdigest()[:12]
+        src = "\n".join([
+            "struct B2Args { long long w[%d]; };" % (len(args) + 1),
+            f'extern "C" __global__ void {name}(const __grid_constant__ B2Args a) {{',
+            "  B2_PDL_ENTRY();", *lines,
+            f"  *((int *)a.w[{len(args)}]) = ({scalar.cast(code, ty, 'b')}) ? 1 : 0;", "}"])
+        k = rt.get_kernel(rt.family_source("prelude.cuh") + "\n" + src, name)
+        self._cond_kernels[key] = (k, args)
+        return k, args
+
+    def _device_branch(self, cur, trs, sym, counters):
+        """Transitions out of ``cur`` whose conditions read containers: host
+        parts are evaluated now; the two remaining complementary container
+        predicates become a conditional IF/ELSE node whose bodies are the two
+        branch chains, which must rejoin at one state with the same symbol
+        assignments.  Returns the next state (or raises _NoDeviceBranch)."""
+        cands = []
+        for t in trs:
+            if t.condition is None:
+                cands.append((t, []))
+                continue
+            host, dev = [], []
+            for cj in _conjuncts(t.condition):
+                names = scalar.free_names(cj)
+                if any(n in self.g.containers for n in names):
+                    if any(n not in self.g.containers and n not in sym for n in names):
+                        raise _NoDeviceBranch("condition mixes unknown names")
+                    dev.append(cj)
+                else:
+                    host.append(cj)
+            if all(bool(scalar.evaluate(h, sym)) for h in host):
+                cands.append((t, dev))
+        if cands and not cands[0][1]:  # the first feasible transition is host-decidable
+            t = cands[0][0]
+            for k2, v in t.assignments.items():
+                sym[k2] = symexpr.evaluate(v, sym)
+            return t.dst
+        if len(cands) < 2 or len(cands[0][1]) != 1 or len(cands[1][1]) != 1 \
+                or not _complementary(cands[0][1][0], cands[1][1][0]):
+            raise _NoDeviceBranch("branch predicates are not complementary")
+        (t1, (p1,)), (t2, _) = cands[0], cands[1]
+        ends = []
+        for t in (t1, t2):
+            if t.assignments or t.dst in self.planner.region_at:
+                raise _NoDeviceBranch("assignments on the branching edge")
+            end = self.planner.chain_end[t.dst]
+            outs = self.g.out_transitions(end)
+            if len(outs) != 1 or outs[0].condition is not None:
+                raise _NoDeviceBranch("branch does not rejoin unconditionally")
+            ends.append(outs[0])
+        if ends[0].dst != ends[1].dst or ends[0].assignments != ends[1].assignments:
+            raise _NoDeviceBranch("branches rejoin at different states")
+        if self._flag_next >= 4096:
+            raise _NoDeviceBranch("too many device branches")
+        L = rt.lib()
+        flag = self._flags + 4 * self._flag_next
+        self._flag_next += 1
+        k, args = self._cond_kernel(p1)
+        vals = [self.buf.ptr[a[1]] if a[0] == "ptr" else int(sym[a[1]]) for a in args] + [flag]
+        rt.launch(k, (1, 1, 1), (1, 1, 1), struct.pack(f"<{len(vals)}q", *vals), self.stream)
+        self.launches += 1
+        node, b0, b1 = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        rt.check(L.b2_capture_if_begin(self.stream, flag, ctypes.byref(node), ctypes.byref(b0),
+                                       ctypes.byref(b1)), "device branch")
+        main = self.stream
+        for t, body in ((t1, b0), (t2, b1)):
+            rt.check(L.b2_capture_body_begin(self._body_stream, body), "branch body")
+            self.stream = self._body_stream
+            try:
+                bc = Counters()
+                for op in self.planner.ops[t.dst]:
+                    if isinstance(op, P.NestedOp):
+                        raise _NoDeviceBranch("nested graph in a branch")
+                    self._exec_op(op, sym, bc)
+                rt.check(L.b2_counters_add(self._devc, bc.wcr_commits, bc.map_iterations,
+                                           bc.bytes_moved, 0, self.stream), "branch counters")
+            finally:
+                self.stream = main
+                rt.check(L.b2_capture_body_end(self._body_stream), "branch body end")
+        rt.check(L.b2_capture_if_end(self.stream, node), "device branch end")
+        for k2, v in ends[0].assignments.items():
+            sym[k2] = symexpr.evaluate(v, sym)
+        return ends[0].dst
 
     _dry = False
     _prof = None
@@ -512,8 +660,11 @@ class GpuExecutor:
 
     def _capture(self, counters):
         L = rt.lib()
-        self._instantiate_children()
+        if not self.device_branching:
+            self._instantiate_children()
         self.launches = 0
+        self._flag_next = 0
+        self._capturing = True
         rt.check(L.b2_capture_begin(self.stream), "capture")
         tc = Counters()
         try:
@@ -523,7 +674,10 @@ class GpuExecutor:
             L.b2_capture_end(self.stream, ctypes.byref(ge))
             if ge.value:
                 L.b2_graph_destroy(ge)
+            rt.lib().b2_last_error()
             raise
+        finally:
+            self._capturing = False
         ge = ctypes.c_void_p()
         rt.check(L.b2_capture_end(self.stream, ctypes.byref(ge)), "capture end")
         self.graph_exec = ge.value
@@ -556,6 +710,13 @@ class GpuExecutor:
             if not trs:
                 break
             nxt = None
+            if (getattr(self, "_capturing", False) and self.device_branching and any(
+                    t.condition is not None and any(n in g.containers
+                                                    for n in scalar.free_names(t.condition))
+                    for t in trs)):
+                nxt = self._device_branch(cur, trs, sym, counters)
+            if nxt is not None:
+                trs = []
             for t in trs:
                 if t.condition is None or self._eval_cond(t.condition, sym):
                     for k, v in t.assignments.items():
@@ -1035,6 +1196,29 @@ def _out_strides(cd, M, N):
     if len(dims) == 1 and dims[0][0] == M * N:
         return N * dims[0][1], dims[0][1]
     return None, None
+
+
+class _NoDeviceBranch(Exception):
+    """A container-dependent transition the device-branch capture cannot
+    express; the executor falls back to host-evaluated conditions."""
+
+
+def _conjuncts(e) -> list:
+    if isinstance(e, tuple) and e[0] == "bin" and e[1] == "and":
+        return _conjuncts(e[2]) + _conjuncts(e[3])
+    return [e]
+
+
+_NEGATED = {"<": ">=", ">=": "<", ">": "<=", "<=": ">", "==": "!=", "!=": "=="}
+
+
+def _complementary(a, b) -> bool:
+    if isinstance(a, tuple) and a[:2] == ("un", "not"):
+        return a[2] == b
+    if isinstance(b, tuple) and b[:2] == ("un", "not"):
+        return b[2] == a
+    return (isinstance(a, tuple) and isinstance(b, tuple) and a[0] == b[0] == "bin"
+            and _NEGATED.get(a[1]) == b[1] and a[2:] == b[2:])
 
 
 def _add_counters(dst, src):

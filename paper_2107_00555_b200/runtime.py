@@ -75,7 +75,8 @@ EXPORTS = [
     "b2_malloc", "b2_free", "b2_memcpy_h2d", "b2_memcpy_d2h", "b2_memcpy_d2d", "b2_memset",
     "b2_stream_create", "b2_stream_destroy", "b2_stream_sync", "b2_device_sync",
     "b2_event_create", "b2_event_destroy", "b2_event_record", "b2_event_elapsed_ms",
-    "b2_stream_wait_event",
+    "b2_stream_wait_event", "b2_capture_if_begin", "b2_capture_if_end", "b2_capture_body_begin",
+    "b2_capture_body_end", "b2_counters_add",
     "b2_host_register", "b2_host_unregister", "b2_jit_compile", "b2_module_load",
     "b2_module_unload", "b2_module_function", "b2_func_set_max_smem", "b2_launch",
     "b2_launch_count", "b2_capture_begin", "b2_capture_end", "b2_graph_launch",
@@ -116,6 +117,13 @@ _SIGS = {
     "b2_event_record": ([_vp, _vp], ctypes.c_int),
     "b2_event_elapsed_ms": ([_vp, _vp, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "b2_stream_wait_event": ([_vp, _vp], ctypes.c_int),
+    "b2_capture_if_begin": ([_vp, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                             ctypes.POINTER(_vp)], ctypes.c_int),
+    "b2_capture_if_end": ([_vp, _vp], ctypes.c_int),
+    "b2_capture_body_begin": ([_vp, _vp], ctypes.c_int),
+    "b2_capture_body_end": ([_vp], ctypes.c_int),
+    "b2_counters_add": ([_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
+                         ctypes.c_longlong, _vp], ctypes.c_int),
     "b2_host_register": ([_vp, ctypes.c_size_t], ctypes.c_int),
     "b2_host_unregister": ([_vp], ctypes.c_int),
     "b2_jit_compile": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p),

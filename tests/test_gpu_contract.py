@@ -176,3 +176,34 @@ def test_condition_on_scalar_container(s0):
         else:
             xr = xr + 1.0
     assert np.array_equal(out["x"], xr) and out["s"][()] == s
+
+
+@pytest.mark.parametrize("s0", [2.5, -1.0, 4.0])
+def test_device_branches_match_host_branches(monkeypatch, s0):
+    """The container-dependent branch captured as a CUDA conditional IF/ELSE
+    node gives the same outputs and counters as host-evaluated conditions,
+    across repeated graph replays with different inputs."""
+    from paper_2107_00555_b200 import machine
+
+    g = _g("branchy.raw")
+    rng = np.random.default_rng(6)
+    x = rng.uniform(-1, 1, 37)
+    res = {}
+    for mode in (True, False):
+        monkeypatch.setattr(machine, "DEVICE_BRANCHES", mode)
+        ex = machine.GpuExecutor(g, {"N": 37, "TSTEPS": 7})
+        outs = []
+        for s_in in (s0, -s0):
+            keep = ex.prepare_inputs({"x": x.copy(), "s": s_in})
+            c = machine.Counters()
+            ex.run_device(first_call=True, counters=c)
+            outs.append((ex.download("x"), ex.download("s"), c.as_dict()))
+            ex.sync()
+            del keep
+        res[mode] = outs
+        if mode:
+            assert ex.device_branching and ex.graph_exec is not None
+        ex.close()
+    for (xa, sa, ca), (xb, sb, cb) in zip(res[True], res[False]):
+        assert np.array_equal(xa, xb) and sa == sb
+        assert ca == cb
