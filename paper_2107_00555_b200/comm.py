@@ -169,8 +169,131 @@ class RankComm:
             self._waitall(ex, counters)
         elif kind in ("block_scatter", "block_gather"):
             self._block(ex, op, sym, counters, kind == "block_scatter")
+        elif kind in ("scatter", "gather"):
+            self._flat(ex, op, sym, counters, kind == "scatter")
+        elif kind == "bcast":
+            self._bcast(ex, op, sym, counters)
+        elif kind == "reduce":
+            self._reduce(ex, op, sym, counters)
         else:
             raise SimError(f"collective '{kind}' is not supported by the local-view runner")
+
+    # -- flat collectives (Scatter = 1-D block over the
+    # flattened container, Gather its inverse, Bcast from the root, Reduce
+    # with a WCR operator to the root) ---------------------------------------
+
+    def _io(self, op):
+        n = op.node
+        ins = {e.dst_conn: e for e in op.state.in_edges(n) if e.memlet is not None}
+        outs = {e.src_conn: e for e in op.state.out_edges(n) if e.memlet is not None}
+        return ins["a"].memlet, outs["out"].memlet
+
+    def _flat_plan(self, ex, op, sym, scatter):
+        am, om = self._io(op)
+        gm, lm = (am, om) if scatter else (om, am)
+        gb, goff, gdt, gdims = ex.view(gm, sym)
+        dense = all(gd[1] == int(np.prod([x[0] for x in gdims[d + 1:]]))
+                    for d, gd in enumerate(gdims))
+        if not dense:
+            raise SimError("flat scatter/gather needs a dense row-major global view")
+        n = int(np.prod([d[0] for d in gdims])) if gdims else 1
+        if n % self.world:
+            raise SimError(f"{n} elements are not covered by {self.world} ranks "
+                           "(divisible extents required)")
+        c = n // self.world
+        ln = int(np.prod([len(r) for r in symexpr.eval_subset(lm.subset, sym)]))
+        if ln != c:
+            raise SimError(f"local view has {ln} elements, the chunk {c}")
+        return gm, lm, gb, goff, gdt, c
+
+    def _flat(self, ex, op, sym, counters, scatter):
+        gm, lm, gb, goff, gdt, c = self._flat_plan(ex, op, sym, scatter)
+        L = rt.lib()
+        esz = sdfg.DTYPE_BYTES[gdt]
+        lb, loff, ldt, ldims = ex.view(lm, sym)
+        lview = rt.make_view(lb, loff, ldt, [d[0] for d in ldims], [d[1] for d in ldims])
+        stg = [self._buffer((op.idx, "flat", q), c * esz) for q in range(self.world)]
+
+        def chunk(q):
+            return rt.make_view(gb, goff + q * c, gdt, [c], [1])
+
+        def flat(q):
+            return rt.make_view(stg[q], 0, gdt, [c], [1])
+
+        ops = []
+        if scatter:
+            if self.rank == 0:
+                for q in range(self.world):
+                    v, f = chunk(q), flat(q)
+                    rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(v), 0, ex.stream), "scatter")
+                    if q:
+                        ops.append((True, q, stg[q], c * esz))
+            else:
+                ops.append((False, 0, stg[self.rank], c * esz))
+            if ops:
+                self.nccl.p2p(ops, ex.stream)
+            f = flat(self.rank)
+            rt.check(L.b2_copy_view(ctypes.byref(lview), ctypes.byref(f), 0, ex.stream), "scatter")
+        else:
+            f = flat(self.rank)
+            rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(lview), 0, ex.stream), "gather")
+            ops = ([(False, q, stg[q], c * esz) for q in range(1, self.world)] if self.rank == 0
+                   else [(True, 0, stg[self.rank], c * esz)])
+            if ops:
+                self.nccl.p2p(ops, ex.stream)
+            if self.rank == 0:
+                for q in range(self.world):
+                    v, fq = chunk(q), flat(q)
+                    rt.check(L.b2_copy_view(ctypes.byref(v), ctypes.byref(fq), 0, ex.stream), "gather")
+        ex.launches += 2
+        if counters is not None:
+            counters.collective_calls += 1
+            counters.comm_bytes += sum(x[3] for x in ops)
+
+    def _bcast(self, ex, op, sym, counters):
+        am, om = self._io(op)
+        L = rt.lib()
+        ab, aoff, adt, adims = ex.view(am, sym)
+        ob, ooff, odt, odims = ex.view(om, sym)
+        n = int(np.prod([d[0] for d in adims])) if adims else 1
+        nbytes = n * sdfg.DTYPE_BYTES[adt]
+        stg = self._buffer((op.idx, "bcast"), nbytes)
+        flat = rt.make_view(stg, 0, adt, [n], [1])
+        av = rt.make_view(ab, aoff, adt, [d[0] for d in adims] or [1], [d[1] for d in adims] or [1])
+        ov = rt.make_view(ob, ooff, odt, [d[0] for d in odims] or [1], [d[1] for d in odims] or [1])
+        if self.rank == 0:
+            rt.check(L.b2_copy_view(ctypes.byref(flat), ctypes.byref(av), 0, ex.stream), "bcast")
+        if self.world > 1:
+            self.nccl.bcast(stg, nbytes, 0, ex.stream)
+        rt.check(L.b2_copy_view(ctypes.byref(ov), ctypes.byref(flat), 0, ex.stream), "bcast")
+        ex.launches += 2
+        if counters is not None:
+            counters.collective_calls += 1
+            counters.comm_bytes += nbytes if self.world > 1 else 0
+
+    def _reduce(self, ex, op, sym, counters):
+        am, om = self._io(op)
+        L = rt.lib()
+        wcr = op.node.attrs.get("op", "add")
+        ab, aoff, adt, adims = ex.view(am, sym)
+        if adt != "f64":
+            raise SimError("reduce collective supports f64 contributions")
+        ob, ooff, odt, odims = ex.view(om, sym)
+        n = int(np.prod([d[0] for d in adims])) if adims else 1
+        stg = self._buffer((op.idx, "reduce"), 8 * n)
+        flat = rt.make_view(stg, 0, "f64", [n], [1])
+        av = rt.make_view(ab, aoff, adt, [d[0] for d in adims] or [1], [d[1] for d in adims] or [1])
+        ov = rt.make_view(ob, ooff, odt, [d[0] for d in odims] or [1], [d[1] for d in odims] or [1])
+        rt.check(L.b2_copy_view(ctypes.byref(flat), ctypes.byref(av), 0, ex.stream), "reduce")
+        if self.world > 1:
+            self.nccl.allreduce_f64(stg, n, wcr, ex.stream)
+        if self.rank == 0:  # the result lives at the root
+            rt.check(L.b2_copy_view(ctypes.byref(ov), ctypes.byref(flat),
+                                    rt.WCR_CODE[om.wcr], ex.stream), "reduce")
+        ex.launches += 2
+        if counters is not None:
+            counters.collective_calls += 1
+            counters.comm_bytes += 8 * n if self.world > 1 else 0
 
     # -- block collectives (root = rank 0 holds the global container) -----------
 
@@ -278,6 +401,17 @@ class RankComm:
             for q in range(self.world):
                 self._buffer((op.idx, "blk", q), nbytes)
             self.colls.append((kind, tuple(e for _, e in blocks[0]), nbytes))
+        elif kind in ("scatter", "gather"):
+            gm, lm, gb, goff, gdt, c = self._flat_plan(ex, op, sym, kind == "scatter")
+            for q in range(self.world):
+                self._buffer((op.idx, "flat", q), c * sdfg.DTYPE_BYTES[gdt])
+            self.colls.append((kind, c))
+        elif kind in ("bcast", "reduce"):
+            am, _ = self._io(op)
+            n = int(np.prod([len(r) for r in symexpr.eval_subset(am.subset, sym)]))
+            nb = n * sdfg.DTYPE_BYTES[ex.g.containers[am.container].dtype]
+            self._buffer((op.idx, kind), 8 * n if kind == "reduce" else nb)
+            self.colls.append((kind, n))
 
     def finish_dry(self):
         if self._cur:  # posted but never waited for

@@ -479,6 +479,15 @@ class NcclComm:
         rt.check(rt.lib().b2_nccl_group_p2p(self.comm, len(ops), arr, stream), "nccl p2p")
         return sent
 
+    def bcast(self, ptr: int, nbytes: int, root: int, stream) -> None:
+        rt = self.rt
+        rt.check(rt.lib().b2_nccl_bcast(self.comm, ptr, nbytes, root, stream), "nccl bcast")
+
+    def allreduce_f64(self, ptr: int, count: int, wcr: str, stream) -> None:
+        rt = self.rt
+        rt.check(rt.lib().b2_nccl_allreduce_f64(self.comm, ptr, count, rt.WCR_CODE[wcr], stream),
+                 "nccl allreduce")
+
     def close(self):
         self.rt.lib().b2_nccl_destroy(self.comm)
 

@@ -154,3 +154,45 @@ def test_block_scatter_gather_roundtrip_single_rank(pg):
     out, instr = local_view_run(g, ctx, [{}], grid=ProcessGrid((1, 1)))
     assert np.array_equal(out["B"], A * 2.0 + 1.0)
     assert instr["collective_ops"] == 2 and instr["per_rank"][0]["comm_bytes"] == 0
+
+
+def _doc(name):
+    import json
+
+    return json.loads((GOLDEN / "graphs" / f"{name}.json").read_text())
+
+
+@pytest.mark.gpu
+def test_flat_scatter_gather_bcast_reduce_single_rank(pg):
+    """SCATTER / GATHER (1-D blocks of the flattened container), BCAST and
+    REDUCE through the local-view runner on one rank: local
+    copies, and the collective-call counter."""
+    import json
+
+    from paper_2107_00555_b200 import ExecContext, sdfg
+    from paper_2107_00555_b200.comm import local_view_run
+
+    d = _doc("block_roundtrip.raw")
+    for st in d["states"]:
+        for n in st["nodes"]:
+            if n.get("type") == "library":
+                n["kind"] = {"block_scatter": "scatter", "block_gather": "gather"}[n["kind"]]
+    g = sdfg.loads(json.dumps(d))
+    rng = np.random.default_rng(8)
+    A = rng.uniform(-1, 1, (4, 6))
+    ctx = ExecContext(bindings={"N": 4, "M": 6, "lN": 4, "lM": 6}).bind_inputs(
+        {"A": A, "B": np.zeros_like(A), "L": np.zeros_like(A)})
+    out, instr = local_view_run(g, ctx, [{}])
+    assert np.array_equal(out["B"], A * 2.0 + 1.0) and instr["collective_ops"] == 2
+
+    # bcast of the root's A into L, then reduce of L into B (sum over ranks)
+    d2 = _doc("block_roundtrip.raw")
+    d2["states"][0]["nodes"][0]["kind"] = "bcast"
+    d2["states"][2]["nodes"][0]["kind"] = "reduce"
+    # a collective reduce is a REDUCE library node marked "comm" (interp.py:444)
+    d2["states"][2]["nodes"][0]["attrs"] = {"op": "add", "comm": True}
+    g2 = sdfg.loads(json.dumps(d2))
+    ctx2 = ExecContext(bindings={"N": 4, "M": 6, "lN": 4, "lM": 6}).bind_inputs(
+        {"A": A, "B": np.zeros_like(A), "L": np.zeros_like(A)})
+    out2, instr2 = local_view_run(g2, ctx2, [{}])
+    assert np.array_equal(out2["B"], A * 2.0 + 1.0) and instr2["collective_ops"] == 2
