@@ -43,6 +43,7 @@ FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min lo
 SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
+SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "6"))  # planes per thread, runtime dim-0 range
 
 
 class KernelSpec:
@@ -958,7 +959,12 @@ class _Gen:
             # 16 planes per thread measured 3 % faster on heat_3d N=400 (202 vs
             # 209 us); short or runtime dim-0 ranges (slabs) keep 8
             r0 = self.const_ranges[0]
-            vec = 16 if (r0 is not None and r0[2] >= 256 and not self.dyn0) else 8
+            if self.dyn0:
+                # slab executors: measured per-rank times at P=2/4/8 (heat_3d
+                # N=400, scripts/scaling_projection.py) are best at 6 planes
+                vec = SLAB_VEC
+            else:
+                vec = 16 if (r0 is not None and r0[2] >= 256) else 8
         elif mode == "stencil":
             vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
                 (2 if self.const_ranges[-1][2] >= 1024 else 1)
