@@ -265,9 +265,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 // Both CTAs' TMA bytes complete on the leader's full barrier; MMA commits are
 // multicast to both CTAs' empty / chunk-full barriers; the peer's epilogue
 // warps release a TMEM buffer by arriving on the leader's barrier.
-constexpr int P_STAGES = 6;
-constexpr int P_A_BYTES = 128 * TK * 4;  // 16 KB
-constexpr int P_B_BYTES = 128 * TK * 4;  // 16 KB (half of N = 256)
+// The pair kernel reads two-segment operands (A' = [lo | hi], B' = [hi | lo]
+// per 32-wide k block): each stage holds one raw k block and the leader
+// issues the three products lo·hi, hi·lo, hi·hi from it — hi is loaded once,
+// not twice, so the split writes 2x (not 3x) and TMA moves 2/3 of the bytes.
+constexpr int P_SEG = 128 * TK * 4;      // one 128-row x 32-k fp32 segment: 16 KB
+constexpr int P_STAGES = 3;
+constexpr int P_A_BYTES = 2 * P_SEG;     // A lo, A hi
+constexpr int P_B_BYTES = 2 * P_SEG;     // B hi, B lo (this CTA's half of N = 256)
 constexpr int P_STAGE_BYTES = P_A_BYTES + P_B_BYTES;
 constexpr int P_SMEM_BYTES = P_STAGES * P_STAGE_BYTES + 1024 + 256;
 constexpr uint32_t P_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
@@ -367,8 +372,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int s = kb % P_STAGES;
         if (kb >= P_STAGES) mbar_wait(&empty[s], ((kb / P_STAGES) + 1) & 1);
         if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
-        tma_load_2d_pair(sa + s * P_A_BYTES, &ta, &full[s], kb * TK, m0 + (int)rank * 128);
-        tma_load_2d_pair(sb + s * P_B_BYTES, &tb, &full[s], kb * TK, n0 + (int)rank * 128);
+        const int ma = m0 + (int)rank * 128, nb = n0 + (int)rank * 128;
+        tma_load_2d_pair(sa + s * P_A_BYTES, &ta, &full[s], kb * 2 * TK, ma);
+        tma_load_2d_pair(sa + s * P_A_BYTES + P_SEG, &ta, &full[s], kb * 2 * TK + TK, ma);
+        tma_load_2d_pair(sb + s * P_B_BYTES, &tb, &full[s], kb * 2 * TK, nb);
+        tma_load_2d_pair(sb + s * P_B_BYTES + P_SEG, &tb, &full[s], kb * 2 * TK + TK, nb);
       }
     }
   } else if (warp == 1) {
@@ -383,11 +391,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const int s = kb % P_STAGES;
         mbar_wait(&full[s], (kb / P_STAGES) & 1);
         fence_after();
-        const uint64_t da = sw128_desc(smem_u32(sa + s * P_A_BYTES));
-        const uint64_t db = sw128_desc(smem_u32(sb + s * P_B_BYTES));
+        const uint64_t a_lo = sw128_desc(smem_u32(sa + s * P_A_BYTES));
+        const uint64_t a_hi = sw128_desc(smem_u32(sa + s * P_A_BYTES + P_SEG));
+        const uint64_t b_hi = sw128_desc(smem_u32(sb + s * P_B_BYTES));
+        const uint64_t b_lo = sw128_desc(smem_u32(sb + s * P_B_BYTES + P_SEG));
+        const uint32_t d = tmem + (uint32_t)(b * 256);
 #pragma unroll
-        for (int k = 0; k < TK / 8; ++k)
-          mma_tf32_pair(tmem + (uint32_t)(b * 256), da + 2 * k, db + 2 * k, !(first && k == 0));
+        for (int k = 0; k < TK / 8; ++k) {  // small products first
+          mma_tf32_pair(d, a_lo + 2 * k, b_hi + 2 * k, !(first && k == 0));
+          mma_tf32_pair(d, a_hi + 2 * k, b_lo + 2 * k, 1);
+          mma_tf32_pair(d, a_hi + 2 * k, b_hi + 2 * k, 1);
+        }
         mma_commit_pair(&empty[s]);
         if (kb - j * chunk == chunk - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
       }
@@ -439,30 +453,31 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 // A (M x K, row stride lda) -> A' (M x Kp): per 32-wide k block b the 96
 // columns [lo | hi | hi] of A[:, 32b : 32b + 32] (zero past K), so any range
-// of k blocks is a contiguous range of A' columns
+// of k blocks is a contiguous range of A' columns.  Block (32, 8): lane =
+// column in the k block (coalesced read, three coalesced writes), rows 8
+// per CTA; grid (k blocks, row groups) — no per-element division.
 __global__ void split_a(const float *__restrict__ A, int64_t lda, int64_t M, int64_t K,
-                        int64_t Kp, float *__restrict__ Ap) {
-  const int64_t total = M * Kp;
-  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < total;
-       f += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = f / Kp, kk = f - i * Kp;
-    const int64_t kb = kk / (3 * TK);
-    const int r = (int)(kk - kb * 3 * TK), seg = r / TK;
-    const int64_t k = kb * TK + (r - seg * TK);
-    float out = 0.f;
+                        int64_t Kp, int segs, float *__restrict__ Ap) {
+  const int64_t kb = blockIdx.x;
+  const int64_t k = kb * TK + threadIdx.x;
+  for (int64_t i = (int64_t)blockIdx.y * 8 + threadIdx.y; i < M; i += (int64_t)gridDim.y * 8) {
+    float lo = 0.f, hi = 0.f;
     if (k < K) {
       const float a = A[i * lda + k];
-      const float hi = tf32_rna(a);
-      out = seg == 0 ? a - hi : hi;
+      hi = tf32_rna(a);
+      lo = a - hi;
     }
-    Ap[f] = out;
+    float *dst = Ap + i * Kp + kb * segs * TK + threadIdx.x;
+    dst[0] = lo;
+    dst[TK] = hi;
+    if (segs == 3) dst[2 * TK] = hi;
   }
 }
 
 // B (K x N, row stride ldb) -> B'^T (N x Kp): per k block [hi | lo | hi],
 // through a 32 x 32 shared tile so both the read and the write are coalesced
 __global__ void split_bt(const float *__restrict__ B, int64_t ldb, int64_t K, int64_t N,
-                         int64_t Kp, float *__restrict__ Bt) {
+                         int64_t Kp, int segs, float *__restrict__ Bt) {
   __shared__ float t[32][33];
   const int64_t kb = blockIdx.y, k0 = kb * 32, n0 = (int64_t)blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -478,10 +493,10 @@ __global__ void split_bt(const float *__restrict__ B, int64_t ldb, int64_t K, in
     if (n < N) {
       const float b = t[tx][ty + 8 * r];
       const float hi = tf32_rna(b);
-      float *dst = Bt + n * Kp + kb * 3 * TK + tx;
+      float *dst = Bt + n * Kp + kb * segs * TK + tx;
       dst[0] = hi;
       dst[TK] = b - hi;
-      dst[2 * TK] = hi;
+      if (segs == 3) dst[2 * TK] = hi;
     }
   }
 }
@@ -539,7 +554,17 @@ size_t g_ws_bytes = 0;
 // (row stride lda), B row-major K x N (row stride ldb).
 int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
                 int64_t ldb, float *C, int64_t ldc, int accumulate, void *stream) {
-  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * 3 * TK;
+  static int group_m = -1, pair = -1;
+  if (group_m < 0) {
+    const char *e = getenv("B2_TC_GROUP");
+    group_m = e ? atoi(e) : 4;  // measured: 4-tile bands of 256-row pair tiles
+    if (group_m < 1) group_m = 1;
+    const char *p2 = getenv("B2_TC_PAIR");
+    pair = !(p2 && p2[0] == '0');
+  }
+  // the CTA-pair kernel reads two-segment operands, the single-CTA one three
+  const int segs = pair ? 2 : 3;
+  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * segs * TK;
   const size_t need = (size_t)(M + N) * (size_t)Kp * sizeof(float);
   cudaStream_t s = (cudaStream_t)stream;
   B2_CLEAR_ERROR();
@@ -557,16 +582,14 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
     g_ws_bytes = need;
   }
   float *Ap = g_ws, *Bt = g_ws + (size_t)M * Kp;
-  split_a<<<148 * 16, 256, 0, s>>>(A, lda, M, K, Kp, Ap);
+  {
+    const unsigned ry = (unsigned)((M + 7) / 8 < 2048 ? (M + 7) / 8 : 2048);
+    split_a<<<dim3((unsigned)nkb, ry), dim3(32, 8), 0, s>>>(A, lda, M, K, Kp, segs, Ap);
+  }
   B2_LAUNCH_CHECK("split_a");
   dim3 tb(32, 8), gb((unsigned)((N + 31) / 32), (unsigned)nkb);
-  split_bt<<<gb, tb, 0, s>>>(B, ldb, K, N, Kp, Bt);
+  split_bt<<<gb, tb, 0, s>>>(B, ldb, K, N, Kp, segs, Bt);
   B2_LAUNCH_CHECK("split_bt");
-  CUtensorMap ma, mb;
-  int rc = make_map(&ma, Ap, (uint64_t)Kp, (uint64_t)M, TM);
-  if (rc) return rc;
-  rc = make_map(&mb, Bt, (uint64_t)Kp, (uint64_t)N, TN);
-  if (rc) return rc;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(tc_sgemm, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES) !=
@@ -576,14 +599,7 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
       return b2_fail(B2_ERR_CUDA, "tc sgemm smem attribute");
     attr = true;
   }
-  static int group_m = -1, pair = -1;
-  if (group_m < 0) {
-    const char *e = getenv("B2_TC_GROUP");
-    group_m = e ? atoi(e) : 4;  // measured: 4-tile bands of 256-row pair tiles
-    if (group_m < 1) group_m = 1;
-    const char *p2 = getenv("B2_TC_PAIR");
-    pair = !(p2 && p2[0] == '0');
-  }
+  int rc;
   if (pair) {
     CUtensorMap pa, pb;
     rc = make_map(&pa, Ap, (uint64_t)Kp, (uint64_t)M, 128);
@@ -591,12 +607,17 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
     rc = make_map(&pb, Bt, (uint64_t)Kp, (uint64_t)N, 128);
     if (rc) return rc;
     const int pm = (int)((M + 255) / 256), pn = (int)((N + 255) / 256);
+    // one pipeline stage = one raw 32-wide k block (both segments)
     tc_sgemm_pair<<<2 * pm * pn, THREADS, P_SMEM_BYTES, s>>>(
-        pa, pb, M, N, (int)(3 * nkb), (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate, pm, pn,
-        group_m);
+        pa, pb, M, N, (int)nkb, (int)tc_chunk_kblocks(), C, ldc, accumulate, pm, pn, group_m);
     B2_LAUNCH_CHECK("tc sgemm pair");
     return B2_OK;
   }
+  CUtensorMap ma, mb;
+  rc = make_map(&ma, Ap, (uint64_t)Kp, (uint64_t)M, TM);
+  if (rc) return rc;
+  rc = make_map(&mb, Bt, (uint64_t)Kp, (uint64_t)N, TN);
+  if (rc) return rc;
   const int num_m = (int)((M + TM - 1) / TM), num_n = (int)((N + TN - 1) / TN);
   tc_sgemm<<<num_m * num_n, THREADS, SMEM_BYTES, s>>>(
       ma, mb, M, N, (int)(3 * nkb), (int)(3 * tc_chunk_kblocks()), C, ldc, accumulate, num_m,
