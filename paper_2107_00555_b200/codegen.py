@@ -44,6 +44,7 @@ SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay i
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "6"))  # planes per thread, runtime dim-0 range
+STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 
 
 class KernelSpec:
@@ -99,6 +100,7 @@ class _Gen:
         self.red_pout: list = []
         self.red_full = False
         self.ptr_override: dict[str, str] = {}  # container -> C pointer name
+        self.read_set: set = set()
 
     def _wkey(self, m: sdfg.Memlet, env: dict):
         rename = {mp: v[2:] for mp, v in env.items() if isinstance(v, str) and v.startswith("p_")}
@@ -747,7 +749,13 @@ class _Gen:
             self.spec.checks.append((m.container, m.subset, env))
             target = f"{p}[{off}]"
         if m.wcr is None:
-            self.emit(f"{target} = ({ct})({val});")
+            if (STREAM_STORES and not guarded and ct == "double"
+                    and getattr(self.spec, "mode", "") in ("march", "tile2")
+                    and m.container not in self.read_set):
+                # write-only output of a streaming sweep: evict-first store
+                self.emit(f"__stcs(&{target}, ({ct})({val}));")
+            else:
+                self.emit(f"{target} = ({ct})({val});")
         elif shared:
             self.emit(f"b2_atomic_{m.wcr}(&{target}, ({ct})({val}));")
         else:
@@ -983,10 +991,13 @@ class _Gen:
 
         # containers written anywhere in this group: the rest are read-only
         self.written = set()
+        self.read_set = set()
         for mem in grp.members:
             for a in self.pl.member_accesses(mem, grp.params):
                 if a[1]:
                     self.written.add(a[0])
+                else:
+                    self.read_set.add(a[0])
         self.cse = {}
         # batch the read-only loads of all `vec` points of a thread ahead of
         # their arithmetic: memory-level parallelism without extra warps
