@@ -99,3 +99,36 @@ def test_slab_runner_split_launch_bitwise(pg, N):
     out = r.gather({"A": A, "B": B})
     K.heat_3d_c(A, B, 5)
     assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_summa_single_rank_with_libb2_gemm(pg, dtype):
+    """dist.Summa on a 1x1 grid with the libb2 GEMMs the SUMMA bench uses
+    (DMMA f64 / tcgen05 3xTF32 f32), K cut into panels, C accumulated."""
+    import torch
+
+    from paper_2107_00555_b200 import dist, runtime as rt
+
+    rt.device(0)
+    L = rt.lib()
+    n = 1024
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    fn = L.b2_gemm_f64 if dtype == "f64" else L.b2_gemm_f32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.rand((n, n), dtype=tdt, device="cuda", generator=g) * 2 - 1
+    b = torch.rand((n, n), dtype=tdt, device="cuda", generator=g) * 2 - 1
+    c = torch.zeros((n, n), dtype=tdt, device="cuda")
+    s = dist.Summa(dist.ProcessGrid((1, 1)), 0, n, n, n)
+
+    def gemm(cc, pa, pb):
+        stream = torch.cuda.current_stream().cuda_stream
+        rt.check(fn(pa.shape[0], pb.shape[1], pa.shape[1], pa.data_ptr(), pa.stride(0), 1,
+                    pb.data_ptr(), pb.stride(0), 1, cc.data_ptr(), cc.stride(0), 1,
+                    rt.WCR_CODE["add"], stream))
+
+    s.run(a, b, c, gemm, lambda shape: torch.empty(shape, dtype=tdt, device="cuda"))
+    torch.cuda.synchronize()
+    ref = a.double().cpu().numpy() @ b.double().cpu().numpy()
+    got = c.double().cpu().numpy()
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert err <= (1e-12 if dtype == "f64" else 1e-5), err
