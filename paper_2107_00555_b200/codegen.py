@@ -43,6 +43,9 @@ FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min lo
 SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
+# shift the innermost tile origin down to a 128-byte line so a warp's row
+# access covers whole lines (march / tile2 with a constant unit-stride range)
+ALIGN_TILES = os.environ.get("B2_ALIGN_TILES", "0") == "1"  # measured neutral (heat, jacobi)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "6"))  # planes per thread, runtime dim-0 range
 STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 
@@ -65,6 +68,7 @@ class KernelSpec:
         self.params: list[str] = []
         self.vec = 1
         self.dyn0 = False  # range of the first parameter is a runtime argument
+        self.align = 0  # elements the innermost tile origin is shifted down by
         self.kernel = None  # runtime.Kernel
 
     def arg_index(self, desc) -> int:
@@ -984,6 +988,12 @@ class _Gen:
         if os.environ.get("B2_VEC"):
             vec = int(os.environ["B2_VEC"])
         spec.vec = vec
+        spec.align = 0
+        lastr = self.const_ranges[-1] if self.const_ranges else None
+        if (ALIGN_TILES and mode in ("tile2", "march") and k >= 2 and lastr is not None
+                and lastr[1] == 1):
+            esz = max([{"i32": 4, "bool": 1}.get(self.g.containers[n].dtype, 8) for n in spec.containers] or [8])
+            spec.align = lastr[0] % max(1, 128 // esz)
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, 8, 1), "march": (32, MARCH_BY, 1), "reduce": (256, 1, 1),
                       "rowred": (256, 1, 1),
@@ -1156,7 +1166,8 @@ class _Gen:
         elif mode == "tile2":
             x, y = k - 1, k - 2
             tw = 32 * vec
-            loop.append(f"  const b2_ll tiles_x = (rl{x} + {tw - 1}) / {tw};")
+            ax = spec.align
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + {ax + tw - 1}) / {tw};")
             loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
             outer = " * ".join(f"rl{i}" for i in range(k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({outer});")
@@ -1170,13 +1181,18 @@ class _Gen:
                     loop.append(f"    const b2_ll i{i} = rem;")
             loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
             loop.append(f"    if (i{y} >= rl{y}) continue;")
-            hdr = [f"    const b2_ll i{x} = tx * {tw} + v * 32 + threadIdx.x;",
-                   f"    if (i{x} >= rl{x}) break;"]
+            if ax:
+                hdr = [f"    const b2_ll i{x} = tx * {tw} + v * 32 + (b2_ll)threadIdx.x - {ax};",
+                       f"    if (i{x} >= rl{x}) break;",
+                       f"    if (i{x} < 0) continue;"]
+            else:
+                hdr = [f"    const b2_ll i{x} = tx * {tw} + v * 32 + threadIdx.x;",
+                       f"    if (i{x} >= rl{x}) break;"]
             for i, p in enumerate(grp.params):
                 hdr.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
             if MARCH_FULL and vec > 1:
-                loop.append(f"    if (tx * {tw} + {tw} <= rl{x}) {{")
-                loop += vloop([hdr[0]] + hdr[2:])
+                loop.append(f"    if (tx * {tw} >= {ax} && tx * {tw} + {tw - ax} <= rl{x}) {{")
+                loop += vloop([hdr[0]] + hdr[3 if ax else 2:])
                 loop.append("    } else {")
                 loop += vloop(hdr)
                 loop.append("    }")
@@ -1189,7 +1205,8 @@ class _Gen:
             # overlapping dim-0 neighbours of a stencil from registers
             x, y = k - 1, k - 2
             by = MARCH_BY
-            loop.append(f"  const b2_ll tiles_x = (rl{x} + 31) / 32;")
+            ax = spec.align
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + {ax + 31}) / 32;")
             loop.append(f"  const b2_ll tiles_y = (rl{y} + {by - 1}) / {by};")
             loop.append(f"  const b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
             mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
@@ -1202,8 +1219,12 @@ class _Gen:
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
             loop.append("    const b2_ll tz = rem;")
             loop.append(f"    const b2_ll i{y} = ty * {by} + threadIdx.y;")
-            loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
-            loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
+            if ax:
+                loop.append(f"    const b2_ll i{x} = tx * 32 + (b2_ll)threadIdx.x - {ax};")
+                loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x} || i{x} < 0) continue;")
+            else:
+                loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
+                loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
             for i in range(1, k):
                 loop.append(f"    const b2_ll p_{grp.params[i]} = rb{i} + rs{i} * i{i};")
             hdr = [f"    const b2_ll i0 = tz * {vec} + v;", "    if (i0 >= rl0) break;",
@@ -1663,7 +1684,7 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
         return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
     if spec.mode == "march":
-        nvb = -(-rl[k - 1] // 32) * -(-rl[k - 2] // MARCH_BY) * -(-rl[0] // spec.vec)
+        nvb = -(-(rl[k - 1] + spec.align) // 32) * -(-rl[k - 2] // MARCH_BY) * -(-rl[0] // spec.vec)
         for v in rl[1: k - 2]:
             nvb *= v
         blocks = max(1, min(nvb, MAX_BLOCKS * 8))
@@ -1671,7 +1692,7 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (32, MARCH_BY, 1)
     tw = 32 * spec.vec
-    tiles = ((rl[k - 1] + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
+    tiles = ((rl[k - 1] + spec.align + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:
         tiles *= v
     blocks = max(1, min(tiles, MAX_BLOCKS * 8))
