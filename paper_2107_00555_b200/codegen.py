@@ -46,6 +46,8 @@ MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in 
 # shift the innermost tile origin down to a 128-byte line so a warp's row
 # access covers whole lines (march / tile2 with a constant unit-stride range)
 ALIGN_TILES = os.environ.get("B2_ALIGN_TILES", "0") == "1"  # measured neutral (heat, jacobi)
+RED_UNROLL = int(os.environ.get("B2_RED_UNROLL", "0"))  # full-unroll innermost reduction trips <= this (neutral on conv2d)
+RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "6"))  # planes per thread, runtime dim-0 range
 STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 
@@ -158,6 +160,11 @@ class _Gen:
         full = self.red_full
         C = 1 if full else max(1, min(-(-148 * 512 // max(1, nout)), -(-nred // 16)))
         self.spec.red_threads = nout * C
+        if full and RED_BLOCK and len(pout) >= 2:
+            T = self.const_ranges[idx[pout[-1]]][2]
+            if (2 <= T <= RED_BLOCK and nout // T >= 148 * 256
+                    and all(t["exclusive"] for t in self.red.values())):
+                return self._reduce_loop_blocked(R, pout, reg_decls, body, nout, T)
         if not full and C <= 8:
             # few chunks per output: whole warps stay on one chunk of 32
             # consecutive outputs (coalesced / broadcast loads like the
@@ -181,9 +188,14 @@ class _Gen:
                     ident = "0"  # integer min/max: committed only when iterations ran
                 L.append(f"    {ct} {a} = ({ct})({ident});")
         if full:
-            for p in R:
+            for n, p in enumerate(R):
                 i = idx[p]
-                L.append(f"    for (b2_ll j{i} = 0; j{i} < rl{i}; ++j{i}) {{")
+                trip = self.const_ranges[i][2]
+                # short constant trips unroll (conv2d's ci/kj loops): the
+                # index arithmetic folds into load offsets; order unchanged
+                if n == len(R) - 1 and trip <= RED_UNROLL:
+                    L.append("#pragma unroll")
+                L.append(f"    for (int j{i} = 0; j{i} < (int)rl{i}; ++j{i}) {{")
                 L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         else:
             L.append("    const b2_ll lo = ch * NRED / NCH, hi = (ch + 1) * NRED / NCH;")
@@ -195,7 +207,10 @@ class _Gen:
             L.append("    b2_ll rr = rf;")
             for p in reversed(R):
                 i = idx[p]
-                L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
+                if len(R) == 1:
+                    L.append(f"    const b2_ll j{i} = rr;")  # lo..hi lies inside [0, rl)
+                else:
+                    L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
                 L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         L += reg_decls(4)
         L += body
@@ -223,6 +238,65 @@ class _Gen:
                 cond = "" if full else "if (lo < hi) "
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
         L.append("  }")
+        return L
+
+    def _reduce_loop_blocked(self, R, pout, reg_decls, body, nout, T) -> list:
+        """Full reductions whose innermost output parameter is short (conv2d's
+        output channel): each thread owns all T points of it, the reduction
+        loops outside and the T points unrolled inside, so reads that do not
+        depend on that parameter load once per T accumulations.  Per output
+        the reduction still runs in lexicographic order (bitwise equal to the
+        thread-per-output schedule)."""
+        grp = self.group
+        idx = {p: i for i, p in enumerate(grp.params)}
+        pc = pout[-1]
+        ic = idx[pc]
+        self.spec.red_threads = nout // T
+        accs = list(self.red.values())
+        L = [f"  constexpr b2_ll NOUTB = {nout // T}LL;",
+             "  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUTB; "
+             "f += (b2_ll)gridDim.x * blockDim.x) {",
+             "    b2_ll rem = f;"]
+        for p in reversed(pout[:-1]):
+            i = idx[p]
+            L.append(f"    const b2_ll q{i} = rem % rl{i}; rem /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * q{i};")
+        for t in accs:
+            L.append(f"    {t['ct']} {t['acc']}_v[{T}];")
+        L.append("#pragma unroll")
+        L.append(f"    for (int v = 0; v < {T}; ++v) {{")
+        L.append(f"      const b2_ll p_{pc} = rb{ic} + rs{ic} * v;")
+        for t in accs:
+            L.append(f"      {t['acc']}_v[v] = {t['target']};")
+        L.append("    }")
+        for n, p in enumerate(R):
+            i = idx[p]
+            if n == len(R) - 1 and self.const_ranges[i][2] <= RED_UNROLL:
+                L.append("#pragma unroll")
+            L.append(f"    for (int j{i} = 0; j{i} < (int)rl{i}; ++j{i}) {{")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
+        L.append("#pragma unroll")
+        L.append(f"    for (int v = 0; v < {T}; ++v) {{")
+        L.append(f"    const b2_ll p_{pc} = rb{ic} + rs{ic} * v;")
+        for t in accs:
+            L.append(f"    {t['ct']} {t['acc']} = {t['acc']}_v[v];")
+        L += reg_decls(4)
+        L += body
+        for t in accs:
+            L.append(f"    {t['acc']}_v[v] = {t['acc']};")
+        L.append("    }")
+        for _ in R:
+            L.append("    }")
+        L.append("#pragma unroll")
+        L.append(f"    for (int v = 0; v < {T}; ++v) {{")
+        L.append(f"      const b2_ll p_{pc} = rb{ic} + rs{ic} * v;")
+        for t in accs:
+            L.append(f"      {t['target']} = {t['acc']}_v[v];")
+        L.append("    }")
+        L.append("  }")
+        self.spec.red_fin = []
+        self.spec.red_nout, self.spec.red_nch = nout, 1
+        self.red_decode = []
         return L
 
     def _reduce_loop_inblock(self, R, pout, reg_decls, body, nout, nred, C) -> list:
@@ -258,7 +332,10 @@ class _Gen:
         L.append("    b2_ll rr = rf;")
         for p in reversed(R):
             i = idx[p]
-            L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
+            if len(R) == 1:
+                L.append(f"    const b2_ll j{i} = rr;")
+            else:
+                L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
             L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         L += reg_decls(4)
         L += body

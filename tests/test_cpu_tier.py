@@ -146,6 +146,14 @@ def test_kernel_mode_selection():
     m, _, _ = _modes("conv2d_bias.auto", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16,
                                           "K": 20, "HO": 237, "WO": 237})
     assert "reduce" in m.values()
+    # raw conv2d: the output channel (CO=16) is register-blocked per thread
+    from paper_2107_00555_b200 import codegen, plan as P, sdfg
+    syms = {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16, "K": 20, "HO": 237, "WO": 237}
+    g = sdfg.load(GOLDEN / "graphs" / "conv2d_bias.raw.json")
+    pl = P.Planner(g, syms).build()
+    srcs = [codegen.generate(pl, op, pl.shapes(syms), f"k{op.idx}").source
+            for op in pl.all_ops if isinstance(op, P.MapGroup)]
+    assert any("_v[16]" in s_ and "NOUTB = 449352LL" in s_ for s_ in srcs)
     m, _, _ = _modes("go_fast.pipe", {"N": 12000})
     assert "reduce" in m.values()
 

@@ -221,3 +221,24 @@ def test_dead_interior_inputs_upload_only_faces(name, syms, shape):
     (K.heat_3d_c if len(shape) == 3 else K.jacobi_2d_c)(A, B, syms["TSTEPS"])
     assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
     ex.close()
+
+
+def test_conv2d_register_blocked_reduction_bitwise(monkeypatch):
+    """conv2d_bias's 7-D WCR map with the output channel register-blocked
+    (each thread owns all CO accumulators, codegen._reduce_loop_blocked):
+    bitwise equal to the thread-per-output schedule, and to the oracle."""
+    from oracle import kernels_np as K
+    from paper_2107_00555_b200 import codegen
+
+    syms = {"NB": 2, "H": 160, "W": 160, "CI": 3, "CO": 16, "K": 20, "HO": 141, "WO": 141}
+    rng = np.random.default_rng(21)
+    x = {"inp": rng.uniform(-1, 1, (2, 160, 160, 3)), "w": rng.uniform(-1, 1, (20, 20, 3, 16)),
+         "bias": rng.uniform(-1, 1, 16), "out": np.zeros((2, 141, 141, 16))}
+    outs = {}
+    for rb in (16, 0):
+        monkeypatch.setattr(codegen, "RED_BLOCK", rb)
+        outs[rb] = _run("conv2d_bias.raw", syms, {k: v.copy() for k, v in x.items()})["out"]
+    assert np.array_equal(outs[16], outs[0])
+    ref = np.zeros_like(x["out"])
+    K.conv2d_bias(x["inp"], x["w"], x["bias"], ref)
+    assert rel_err(outs[16], ref) <= 1e-12
