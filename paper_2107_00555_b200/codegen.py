@@ -43,12 +43,16 @@ FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min lo
 SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
+MARCH_BX = int(os.environ.get("B2_MARCH_BX", "64"))  # tile columns (blockDim.x) in march mode
 # shift the innermost tile origin down to a 128-byte line so a warp's row
 # access covers whole lines (march / tile2 with a constant unit-stride range)
 ALIGN_TILES = os.environ.get("B2_ALIGN_TILES", "0") == "1"  # measured neutral (heat, jacobi)
 RED_UNROLL = int(os.environ.get("B2_RED_UNROLL", "0"))  # full-unroll innermost reduction trips <= this (neutral on conv2d)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
-SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "6"))  # planes per thread, runtime dim-0 range
+MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
+SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
+SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
+SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
 STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 
 
@@ -239,6 +243,66 @@ class _Gen:
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
         L.append("  }")
         return L
+
+    def _march_prefetch(self, vec, by, ax) -> list:
+        bx = self.spec.block[0]
+        """L2 bulk prefetch (cp.async.bulk.prefetch.L2) of the rows of every
+        read-only input the tile will touch, issued when the CTA picks the
+        tile up: the march's demand loads then find most lines in L2, so far
+        more bytes are in flight per SM than one load per thread allows."""
+        grp = self.group
+        out = []
+        for c in sorted(self.read_set - self.written):
+            if self.place(c) != "memory":
+                continue
+            shape = self.shapes[c]
+            if len(shape) != 3:
+                continue
+            offs = []
+            ok = True
+            for mem in grp.members:
+                for (cc, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                    if cc != c:
+                        continue
+                    if pt is None or len(pt) != 3:
+                        ok = False
+                        break
+                    o = []
+                    for d, (c0, co) in enumerate(pt):
+                        if co != ((grp.params[d], 1),):
+                            ok = False
+                            break
+                        o.append(c0)
+                    if not ok:
+                        break
+                    offs.append(o)
+                if not ok:
+                    break
+            if not ok or not offs:
+                continue
+            lo = [min(o[d] for o in offs) for d in range(3)]
+            hi = [max(o[d] for o in offs) for d in range(3)]
+            esz = 8 if self.g.containers[c].dtype in ("f64", "i64") else 4
+            out += [
+                "    {",
+                f"      const b2_ll z0 = b2_max_ll(rb0 + tz * {vec} + ({lo[0]}LL), 0LL);",
+                f"      const b2_ll z1 = b2_min_ll(rb0 + b2_min_ll(tz * {vec} + {vec - 1}, rl0 - 1) + ({hi[0]}LL), {shape[0] - 1}LL);",
+                f"      const b2_ll y0 = b2_max_ll(rb1 + ty * {by} + ({lo[1]}LL), 0LL);",
+                f"      const b2_ll y1 = b2_min_ll(rb1 + b2_min_ll(ty * {by} + {by - 1}, rl1 - 1) + ({hi[1]}LL), {shape[1] - 1}LL);",
+                f"      const b2_ll x0 = b2_max_ll(rb2 + tx * {bx} - {ax} + ({lo[2]}LL), 0LL);",
+                f"      const b2_ll x1 = b2_min_ll(rb2 + b2_min_ll(tx * {bx} - {ax} + {bx - 1}, rl2 - 1) + ({hi[2]}LL), {shape[2] - 1}LL);",
+                "      const int ny = (int)(y1 - y0 + 1), nrow = (int)(z1 - z0 + 1) * ny;",
+                f"      const b2_ll base = (b2_ll)(const char *)c_{c};",
+                "      for (int r = threadIdx.y * blockDim.x + threadIdx.x; r < nrow; r += blockDim.x * blockDim.y) {",
+                "        const int zz = r / ny, yy = r - zz * ny;",
+                f"        const b2_ll row = (z0 + zz) * st_{c}_0 + (y0 + yy) * st_{c}_1;",
+                f"        const b2_ll e0 = (row + x0) * {esz}LL, e1 = (row + x1 + 1) * {esz}LL;",
+                "        const b2_ll a0 = (base + e0) & ~15LL, a1 = (base + e1 + 15) & ~15LL;",
+                "        b2_prefetch_l2((const void *)a0, (unsigned)(a1 - a0));",
+                "      }",
+                "    }",
+            ]
+        return out
 
     def _reduce_loop_blocked(self, R, pout, reg_decls, body, nout, T) -> list:
         """Full reductions whose innermost output parameter is short (conv2d's
@@ -1050,7 +1114,8 @@ class _Gen:
             r0 = self.const_ranges[0]
             if self.dyn0:
                 # slab executors: measured per-rank times at P=2/4/8 (heat_3d
-                # N=400, scripts/scaling_projection.py) are best at 6 planes
+                # N=400, scripts/scaling_projection.py) with the L2 prefetch
+                # are best at 8 planes (6 without it)
                 vec = SLAB_VEC
             else:
                 vec = 16 if (r0 is not None and r0[2] >= 256) else 8
@@ -1072,7 +1137,7 @@ class _Gen:
             esz = max([{"i32": 4, "bool": 1}.get(self.g.containers[n].dtype, 8) for n in spec.containers] or [8])
             spec.align = lastr[0] % max(1, 128 // esz)
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1), "march": (32, MARCH_BY, 1), "reduce": (256, 1, 1),
+                      "tile2": (32, 8, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
                       "rowred": (256, 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
@@ -1283,7 +1348,8 @@ class _Gen:
             x, y = k - 1, k - 2
             by = MARCH_BY
             ax = spec.align
-            loop.append(f"  const b2_ll tiles_x = (rl{x} + {ax + 31}) / 32;")
+            bx = spec.block[0]
+            loop.append(f"  const b2_ll tiles_x = (rl{x} + {ax + bx - 1}) / {bx};")
             loop.append(f"  const b2_ll tiles_y = (rl{y} + {by - 1}) / {by};")
             loop.append(f"  const b2_ll tiles_z = (rl0 + {vec - 1}) / {vec};")
             mid = " * ".join(f"rl{i}" for i in range(1, k - 2)) or "1"
@@ -1295,12 +1361,14 @@ class _Gen:
             for i in reversed(range(1, k - 2)):
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
             loop.append("    const b2_ll tz = rem;")
+            if (SLAB_PREFETCH if self.dyn0 else MARCH_PREFETCH) and k == 3:
+                loop += self._march_prefetch(vec, by, spec.align)
             loop.append(f"    const b2_ll i{y} = ty * {by} + threadIdx.y;")
             if ax:
-                loop.append(f"    const b2_ll i{x} = tx * 32 + (b2_ll)threadIdx.x - {ax};")
+                loop.append(f"    const b2_ll i{x} = tx * {bx} + (b2_ll)threadIdx.x - {ax};")
                 loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x} || i{x} < 0) continue;")
             else:
-                loop.append(f"    const b2_ll i{x} = tx * 32 + threadIdx.x;")
+                loop.append(f"    const b2_ll i{x} = tx * {bx} + threadIdx.x;")
                 loop.append(f"    if (i{y} >= rl{y} || i{x} >= rl{x}) continue;")
             for i in range(1, k):
                 loop.append(f"    const b2_ll p_{grp.params[i]} = rb{i} + rs{i} * i{i};")
@@ -1761,13 +1829,14 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
         return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
     if spec.mode == "march":
-        nvb = -(-(rl[k - 1] + spec.align) // 32) * -(-rl[k - 2] // MARCH_BY) * -(-rl[0] // spec.vec)
+        bx, by = spec.block[0], spec.block[1]
+        nvb = -(-(rl[k - 1] + spec.align) // bx) * -(-rl[k - 2] // by) * -(-rl[0] // spec.vec)
         for v in rl[1: k - 2]:
             nvb *= v
         blocks = max(1, min(nvb, MAX_BLOCKS * 8))
         if spec.private:
             blocks = max(1, min(blocks, MAX_BLOCKS))
-        return (blocks, 1, 1), (32, MARCH_BY, 1)
+        return (blocks, 1, 1), (bx, by, 1)
     tw = 32 * spec.vec
     tiles = ((rl[k - 1] + spec.align + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
     for v in rl[: k - 2]:

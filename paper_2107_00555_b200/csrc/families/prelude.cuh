@@ -18,6 +18,10 @@ __device__ __forceinline__ b2_ll b2_floordiv_ll(b2_ll a, b2_ll b) {
 }
 __device__ __forceinline__ b2_ll b2_min_ll(b2_ll a, b2_ll b) { return a < b ? a : b; }
 __device__ __forceinline__ b2_ll b2_max_ll(b2_ll a, b2_ll b) { return a > b ? a : b; }
+// bulk L2 prefetch of [p, p + bytes) (16-byte aligned, bytes a multiple of 16)
+__device__ __forceinline__ void b2_prefetch_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ b2_ll b2_abs_ll(b2_ll a) { return a < 0 ? -a : a; }
 __device__ __forceinline__ b2_ll b2_ipow(b2_ll a, b2_ll e) {
   b2_ll r = 1;

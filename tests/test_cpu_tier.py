@@ -140,6 +140,14 @@ def test_kernel_mode_selection():
     go_fast's trace loop (pipe graph) is a register reduction."""
     m, _, _ = _modes("heat_3d.raw", {"N": 400, "TSTEPS": 100})
     assert set(m.values()) == {"march"}
+    # march tiles are 64 x 8 and bulk-prefetch their input rows into L2
+    from paper_2107_00555_b200 import codegen as CG, plan as P_, sdfg as S_
+    syms_h = {"N": 400, "TSTEPS": 100}
+    gh = S_.load(GOLDEN / "graphs" / "heat_3d.raw.json")
+    plh = P_.Planner(gh, syms_h).build()
+    sp = CG.generate(plh, next(o for o in plh.all_ops if isinstance(o, P_.MapGroup)),
+                     plh.shapes(syms_h), "h")
+    assert sp.block == (64, 8, 1) and "b2_prefetch_l2" in sp.source
     m, regs, _ = _modes("softmax.raw", {"N": 64, "H": 16, "SM": 512})
     assert "rowred" in m.values()
     assert len(regs) == 1 and regs[0].warp
