@@ -34,7 +34,8 @@ MAX_BLOCKS = 148 * 16
 STENCIL_MODE = os.environ.get("B2_STENCIL", "0") == "1"  # smem plane ring (slower on B200: off)
 STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
 STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
-HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads (slower: off)
+HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads in march mode (slower: off)
+HOIST_TILES = os.environ.get("B2_HOIST_TILES", "1") == "1"  # ... in flat / tile2 modes
 REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
@@ -52,6 +53,9 @@ RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a registe
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
+ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "4"))  # unroll of the warp-per-row loop
+ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowred kernels (softmax 1.11 -> 1.06 ms)
+ROWRED_HOIST = os.environ.get("B2_ROWRED_HOIST", "0") == "1"  # issue a lane's row loads first (slower: off)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
 STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 
@@ -540,8 +544,26 @@ class _Gen:
         for t in self.red.values():
             ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
             L.append(f"    {t['ct']} {t['acc']} = ({t['ct']})({ident});")
-        L.append(f"    for (int j{iL} = lane; j{iL} < (int)rl{iL}; j{iL} += 32) {{")
-        L.append(f"    const b2_ll p_{grp.params[-1]} = rb{iL} + rs{iL} * j{iL};")
+        pL = grp.params[-1]
+        if self.hoisted:
+            T = self.const_ranges[-1][2] // 32
+            for name, ct, expr in self.hoisted:
+                L.append(f"    {ct} {name}[{T}];")
+            L.append("#pragma unroll")
+            L.append(f"    for (int v = 0; v < {T}; ++v) {{")
+            L.append(f"    const int j{iL} = lane + 32 * v;")
+            L.append(f"    const b2_ll p_{pL} = rb{iL} + rs{iL} * j{iL};")
+            for name, _, expr in self.hoisted:
+                L.append(f"    {name}[v] = {expr};")
+            L.append("    }")
+            L.append("#pragma unroll")
+            L.append(f"    for (int v = 0; v < {T}; ++v) {{")
+            L.append(f"    const int j{iL} = lane + 32 * v;")
+        else:
+            if ROWRED_UNROLL > 1:
+                L.append(f"#pragma unroll {ROWRED_UNROLL}")
+            L.append(f"    for (int j{iL} = lane; j{iL} < (int)rl{iL}; j{iL} += 32) {{")
+        L.append(f"    const b2_ll p_{pL} = rb{iL} + rs{iL} * j{iL};")
         L += reg_decls(4)
         L += body
         L.append("    }")
@@ -1153,7 +1175,18 @@ class _Gen:
         self.cse = {}
         # batch the read-only loads of all `vec` points of a thread ahead of
         # their arithmetic: memory-level parallelism without extra warps
-        self.hoist = mode in ("flat", "tile2", "march") and vec > 1 and HOIST_LOADS
+        # flat / tile2: each thread's vec points issue their read-only loads
+        # before the math (softmax's divide map 0.78 -> 0.64 ms; neutral on
+        # jacobi_2d / go_fast).  march keeps program order: 16 planes x 7
+        # hoisted loads per thread tripled heat_3d's time.
+        self.hoist = ((mode in ("flat", "tile2") and vec > 1 and HOIST_TILES)
+                      or (mode == "march" and vec > 1 and HOIST_LOADS))
+        if mode == "rowred" and ROWRED_HOIST:
+            lastr = self.const_ranges[-1]
+            # constant trips per lane: every read-only load of the lane's row
+            # slice is issued before the math (exp/div latency otherwise
+            # leaves one load in flight per lane)
+            self.hoist = lastr is not None and lastr[2] % 32 == 0 and lastr[2] // 32 <= 32
         self.hoisted = []
 
         env = {p: f"p_{p}" for p in grp.params}
@@ -1170,7 +1203,8 @@ class _Gen:
 
         pro: list[str] = []
         nthr = spec.block[0] * spec.block[1] * spec.block[2]
-        pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}) '
+        minb = f", {ROWRED_MINB}" if mode == "rowred" and ROWRED_MINB else ""
+        pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}{minb}) '
                    f"{spec.name}(const __grid_constant__ B2Args a) {{")
         pro.append("  B2_PDL_ENTRY();")
         def _size(name):
@@ -1663,7 +1697,9 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         gen.ind -= 2
         gen.emit("}")
         gen.emit("__syncwarp();")
-        gen.emit(f"while ({cond}) s_{L.var} += {L.step};")
+        # the loop variable's exit value, in closed form (a counting loop
+        # here cost every lane `trip` serial iterations)
+        gen.emit(f"s_{L.var} = {fbase} + {trip} * {L.step};")
         gen.ind -= 2
         gen.emit("}")
 
