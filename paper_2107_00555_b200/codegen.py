@@ -49,6 +49,7 @@ MARCH_BX = int(os.environ.get("B2_MARCH_BX", "64"))  # tile columns (blockDim.x)
 # access covers whole lines (march / tile2 with a constant unit-stride range)
 ALIGN_TILES = os.environ.get("B2_ALIGN_TILES", "0") == "1"  # measured neutral (heat, jacobi)
 RED_UNROLL = int(os.environ.get("B2_RED_UNROLL", "0"))  # full-unroll innermost reduction trips <= this (neutral on conv2d)
+SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per chunk, small reductions (0: off)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
@@ -173,6 +174,13 @@ class _Gen:
             if (2 <= T <= RED_BLOCK and nout // T >= 148 * 256
                     and all(t["exclusive"] for t in self.red.values())):
                 return self._reduce_loop_blocked(R, pout, reg_decls, body, nout, T)
+        if not full and nout <= 4096 and nout * nred <= (1 << 22) and SMALL_RED_CHUNK:
+            # small latency-bound reductions (nbody's 100 x 100 pair forces,
+            # a pow per term): short chunks, folded in-block, one launch
+            C2 = min(-(-nred // SMALL_RED_CHUNK), 64)
+            if C2 > C:
+                self.spec.red_threads = nout * C2
+                return self._reduce_loop_inblock(R, pout, reg_decls, body, nout, nred, C2)
         if not full and C <= 8:
             # few chunks per output: whole warps stay on one chunk of 32
             # consecutive outputs (coalesced / broadcast loads like the

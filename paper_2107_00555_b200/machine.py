@@ -466,7 +466,7 @@ class GpuExecutor:
     def run_device(self, first_call: bool = True, counters=None):
         """Execute the whole state machine on the device (inputs already
         resident).  Returns after enqueueing; call ``sync()`` to wait."""
-        rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
+        self._reset_flags()
         self.zero_transients(first_call)
         if self.device_branching and self.graph_exec is None:
             try:
@@ -1097,6 +1097,10 @@ class GpuExecutor:
                                 external=external)
             child._external = external
             self.children[key] = child
+            # the child's error flag is cleared here once and then with the
+            # parent's at the start of every run (_reset_flags), not per call:
+            # one memset node fewer per nested call in the captured graph
+            rt.check(rt.lib().b2_memset(child.flag, 0, 8, self.stream), "memset")
         if dry:
             child._instantiate_children()
             return
@@ -1105,7 +1109,6 @@ class GpuExecutor:
             if conn in child._external:
                 continue
             self._copy_between(child, conn, e.memlet, sym, into_child=True)
-        rt.check(rt.lib().b2_memset(child.flag, 0, 8, self.stream), "memset")
         child.zero_transients(first_call=True)
         child._run_states(counters, eager=not self.capturable)
         self.launches += child.launches
@@ -1128,6 +1131,11 @@ class GpuExecutor:
         self.launches += 1
 
     # -- results --------------------------------------------------------------
+
+    def _reset_flags(self):
+        rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
+        for ch in self.children.values():
+            ch._reset_flags()
 
     def check_flag(self):
         v = np.zeros(2, dtype=np.int32)
