@@ -115,6 +115,7 @@ class _Gen:
         self.red_pout: list = []
         self.red_full = False
         self.ptr_override: dict[str, str] = {}  # container -> C pointer name
+        self.init_const: dict[str, str] = {}  # reduction target -> fused init constant
         self.read_set: set = set()
 
     def _wkey(self, m: sdfg.Memlet, env: dict):
@@ -122,6 +123,12 @@ class _Gen:
         keys = tuple(self.group.params) + tuple(sorted(self.pl.loopish))
         return (m.container, tuple(P.canon(P.rn(b, rename), keys, self.pl.fixed)
                                    for b, _, _ in m.subset))
+
+    def _old(self, t) -> str:
+        """The value a reduction target holds before this kernel: memory, or
+        the constant the executor's fused init map would have stored."""
+        lit = self.init_const.get(t.get("cont"))
+        return f"(({t['ct']})({lit}))" if lit is not None else t["target"]
 
     def _reduction_plan(self):
         """Reduction schedule for a parallel map whose only HBM writes are WCR
@@ -197,7 +204,7 @@ class _Gen:
         for t in self.red.values():
             a, ct = t["acc"], t["ct"]
             if full and t["exclusive"]:
-                L.append(f"    {ct} {a} = {t['target']};")
+                L.append(f"    {ct} {a} = {self._old(t)};")
             else:
                 ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
                 if ct != "double" and t["wcr"] in ("min", "max"):
@@ -343,7 +350,7 @@ class _Gen:
         L.append(f"    for (int v = 0; v < {T}; ++v) {{")
         L.append(f"      const b2_ll p_{pc} = rb{ic} + rs{ic} * v;")
         for t in accs:
-            L.append(f"      {t['acc']}_v[v] = {t['target']};")
+            L.append(f"      {t['acc']}_v[v] = {self._old(t)};")
         L.append("    }")
         for n, p in enumerate(R):
             i = idx[p]
@@ -429,7 +436,7 @@ class _Gen:
             L.append(f"      for (int c = 1; c < NCH; ++c) s{k} = b2_op_{op}(s{k}, "
                      f"red_sm[{k}][c * OPB + ol]);")
             if t["exclusive"]:
-                L.append(f"      {t['target']} = b2_op_{op}({t['target']}, s{k});")
+                L.append(f"      {t['target']} = b2_op_{op}({self._old(t)}, s{k});")
             else:
                 L.append(f"      b2_atomic_{op}(&{t['target']}, s{k});")
         L.append("    }")
@@ -477,13 +484,13 @@ class _Gen:
                       "    if (threadIdx.x == 0) {",
                       f"      double t = red[0];",
                       f"      for (int i = 1; i < 256; ++i) t = b2_op_{op}(t, red[i]);",
-                      f"      {t['target']} = b2_op_{op}({t['target']}, t);",
+                      f"      {t['target']} = b2_op_{op}({self._old(t)}, t);",
                       "    }",
                       "    __syncthreads();"]
             else:
                 L += [f"    double {acc} = {w}[f];",
                       f"    for (int c = 1; c < NCH; ++c) {acc} = b2_op_{op}({acc}, {w}[c * NOUT + f]);",
-                      f"    {t['target']} = b2_op_{op}({t['target']}, {acc});"]
+                      f"    {t['target']} = b2_op_{op}({self._old(t)}, {acc});"]
         L += ["  }", "}"]
         return L
 
@@ -582,7 +589,7 @@ class _Gen:
         L.append("    if (lane == 0) {")
         for t in self.red.values():
             if t["exclusive"]:
-                L.append(f"      {t['target']} = b2_op_{t['wcr']}({t['target']}, {t['acc']});")
+                L.append(f"      {t['target']} = b2_op_{t['wcr']}({self._old(t)}, {t['acc']});")
             else:
                 L.append(f"      b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
         L.append("    }")
@@ -880,7 +887,7 @@ class _Gen:
             if t is None:
                 idx = [symexpr.to_c(b, self.name_of(env)) for b, _, _ in m.subset]
                 self.spec.checks.append((m.container, m.subset, env))
-                t = {"acc": self.fresh("acc"), "ct": ct, "wcr": m.wcr,
+                t = {"acc": self.fresh("acc"), "ct": ct, "wcr": m.wcr, "cont": m.container,
                      "target": f"{self.ptr(m.container)}[{self.offset(m.container, idx)}]",
                      "exclusive": self.red_targets[key][1] == set(self.red_pout)}
                 self.red[key] = t
@@ -1827,10 +1834,20 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     return spec
 
 
-def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str) -> KernelSpec:
+def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
+             init_const: dict | None = None) -> KernelSpec:
     gen = _Gen(planner, group, shapes, name)
+    gen.init_const = dict(init_const or {})
     spec = gen.build()
     spec.params = list(group.params)
+    # reduction targets (container, point key) -> (exclusive, C type), for
+    # the executor's init-map fusion
+    spec.red_targets = {}
+    if gen.red:
+        for key, t in gen.red.items():
+            spec.red_targets[t["cont"]] = spec.red_targets.get(t["cont"], []) + [
+                (t["exclusive"], t["ct"])]
+        spec.red_points = list(gen.red_targets)
     # args block decoded positionally; fix the struct size after all args known
     spec.source = spec.source.replace(
         spec.source.splitlines()[1], "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)))

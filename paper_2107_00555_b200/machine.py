@@ -38,6 +38,9 @@ _NP = {"f64": np.float64, "i64": np.int64, "i32": np.int32, "bool": np.bool_}
 SHELL_UPLOAD = os.environ.get("B2_SHELL_UPLOAD", "1") == "1"
 # capture container-dependent branches as CUDA conditional nodes
 DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
+# a constant-fill map followed by a reduction over the same container starts
+# the reduction from the constant instead of launching the fill
+INIT_FUSION = os.environ.get("B2_INIT_FUSION", "1") == "1"
 
 
 class InterpreterError(RuntimeError):
@@ -196,12 +199,15 @@ class GpuExecutor:
             spec.kernel = rt.get_kernel(rt.family_source("prelude.cuh") + "\n" + spec.source, name)
             self.specs[reg.idx] = spec
             reg.spec = spec
+        self.init_skip: set[int] = set()
+        fused_init = self._init_fusions() if INIT_FUSION else {}
         for op in self.planner.all_ops:
             if op.idx in self.planner.in_region:
                 continue
             if isinstance(op, P.MapGroup):
                 name = f"b2_map_{self.g.name}_{op.idx}"
-                spec = codegen.generate(self.planner, op, self.buf.shape, name)
+                spec = codegen.generate(self.planner, op, self.buf.shape, name,
+                                        init_const=fused_init.get(op.idx))
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
                 spec.kernel = rt.get_kernel(src, name)
                 spec.fin_kernel = None
@@ -224,6 +230,66 @@ class GpuExecutor:
                 threads = codegen.MAX_BLOCKS * 256
                 self.scratch[n] = self.buf.alloc(per * threads)
                 self.buf.nbytes[n + "#scratch"] = per * threads
+
+    def _const_fill(self, op):
+        """(X, literal) when map group ``op`` only stores one constant into
+        every element of container X (``acc[:] = 0.0``), else None."""
+        pl = self.planner
+        if (not isinstance(op, P.MapGroup) or op.schedule != "parallel" or len(op.members) != 1
+                or op.idx in pl.in_region):
+            return None
+        mem = op.members[0]
+        accs = pl.member_accesses(mem, op.params)
+        if len(accs) != 1:
+            return None
+        c, w, wcr, depth, pt = accs[0]
+        if not w or wcr is not None or depth != 0 or pt is None or pl.placement.get(c) == "reg":
+            return None
+        shape = self.buf.shape.get(c)
+        if shape is None or len(pt) != len(op.params) or len(shape) != len(pt):
+            return None
+        for d, (c0, co) in enumerate(pt):
+            if c0 != 0 or co != ((op.params[d], 1),):
+                return None
+            r = codegen._const_range(pl, op.ranges[d])
+            if r is None or r != (0, 1, shape[d]):
+                return None
+        tasklets = ([mem.tasklet] if mem.tasklet is not None else
+                    [n for n in P._scope_children(mem.state, mem.entry)])
+        if len(tasklets) != 1 or not isinstance(tasklets[0], sdfg.Tasklet):
+            return None
+        code = tasklets[0].code
+        if len(code) != 1 or not isinstance(code[0][1], tuple) or code[0][1][0] != "num":
+            return None
+        v = code[0][1][1]
+        if not isinstance(v, (int, float)) or isinstance(v, bool):
+            return None
+        return c, repr(float(v)) if isinstance(v, float) else f"{int(v)}LL"
+
+    def _init_fusions(self) -> dict:
+        """Constant-fill map A directly followed (same state chain) by a
+        reduction B whose exclusive targets cover all of A's container: B
+        starts its folds from the constant and A is not launched (one kernel
+        fewer; nbody's ``acc[:] = 0.0`` + pair-force map).  {B.idx: {X: lit}}."""
+        pl = self.planner
+        out = {}
+        for ops in pl.ops.values():
+            for a, b in zip(ops, ops[1:]):
+                cf = self._const_fill(a)
+                if cf is None or not isinstance(b, P.MapGroup) or b.idx in pl.in_region:
+                    continue
+                X, lit = cf
+                spec = codegen.generate(pl, b, self.buf.shape, "probe")
+                # reduce mode: its plan already rejects plain reads of targets
+                if spec.mode != "reduce" or set(spec.red_targets) != {X}:
+                    continue
+                if not all(ex and ct == "double" for ex, ct in spec.red_targets[X]):
+                    continue
+                if not _covers(spec.red_points, X, b, self.buf.shape[X], pl):
+                    continue
+                out[b.idx] = {X: lit}
+                self.init_skip.add(a.idx)
+        return out
 
     def _compile_pairs(self):
         """Temporal pairs of stencil sweeps (temporal.py): one kernel for
@@ -892,6 +958,14 @@ class GpuExecutor:
         return True
 
     def _exec_map(self, op: P.MapGroup, sym, counters):
+        if op.idx in self.init_skip:
+            # constant fill folded into the next reduction's initial value
+            rvals = codegen.range_values(op, sym)
+            ok = self._check_bounds(self.specs[op.idx], rvals, sym, op.state.label,
+                                    f"map group {op.idx}")
+            if ok and counters is not None:
+                _count_map(self, op, rvals, counters, sym)
+            return
         spec = self.specs[op.idx]
         env = sym
         try:
@@ -1227,6 +1301,39 @@ def _complementary(a, b) -> bool:
         return b[2] == a
     return (isinstance(a, tuple) and isinstance(b, tuple) and a[0] == b[0] == "bin"
             and _NEGATED.get(a[1]) == b[1] and a[2:] == b[2:])
+
+
+def _covers(points, X, grp, shape, pl) -> bool:
+    """The reduction's target points on X (point keys: per dim a constant
+    plus parameter terms) write every element of X exactly once per output
+    point: each dim is either one full-range output parameter (same for all
+    targets) or a constant, and the constants enumerate the whole product."""
+    keys = [pt for (c, pt) in points if c == X]
+    if not keys or any(len(k) != len(shape) for k in keys):
+        return False
+    consts = []
+    for d in range(len(shape)):
+        forms = {k[d][1] for k in keys}
+        if forms == {()}:
+            consts.append(d)
+            continue
+        if len(forms) != 1:
+            return False
+        (co,) = forms
+        if len(co) != 1 or co[0][1] != 1 or any(k[d][0] != 0 for k in keys):
+            return False
+        p = co[0][0]
+        if p not in grp.params:
+            return False
+        r = codegen._const_range(pl, grp.ranges[grp.params.index(p)])
+        if r is None or r != (0, 1, shape[d]):
+            return False
+    want = 1
+    for d in consts:
+        want *= shape[d]
+    got = {tuple(k[d][0] for d in consts) for k in keys}
+    return len(got) == len(keys) == want and all(
+        0 <= v < shape[d] for t in got for v, d in zip(t, consts))
 
 
 def _add_counters(dst, src):

@@ -302,3 +302,25 @@ def test_rowpass_fusions_plan_and_compile():
                 src = rp.source(pl.shapes(), f"{g.name}_{op.idx}")
                 assert rt.get_cubin(src, f"b2_rp_{g.name}_{op.idx}")[0]
         assert got == kinds, (name, got)
+
+
+def test_init_fill_fusion_detected():
+    """machine._init_fusions: nbody's nested get_acc graph pairs its
+    constant fill (acc[:] = 0.0) with the following pair-force reduction,
+    whose targets acc[i, 0..2] cover the whole container."""
+    from paper_2107_00555_b200 import machine, plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / "nbody.raw.json")
+    pl = P.Planner(g, {"N": 100, "NT": 10}).build()
+    nested = [o for o in pl.all_ops if isinstance(o, P.NestedOp)][0]
+    pl2 = P.Planner(nested.node.sdfg, {"N": 100}).build()
+
+    class _Ex:
+        pass
+
+    ex = _Ex()
+    ex.planner, ex.buf, ex.init_skip = pl2, _Ex(), set()
+    ex.buf.shape = pl2.shapes({"N": 100})
+    ex._const_fill = machine.GpuExecutor._const_fill.__get__(ex)
+    fused = machine.GpuExecutor._init_fusions(ex)
+    assert fused == {1: {"acc": "0.0"}} and ex.init_skip == {0}
