@@ -32,6 +32,7 @@ transfer is issued.
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -175,6 +176,8 @@ class RankComm:
             self._bcast(ex, op, sym, counters)
         elif kind == "reduce":
             self._reduce(ex, op, sym, counters)
+        elif kind == "dist_matmul":
+            self._dist_matmul(ex, op, sym, counters)
         else:
             raise SimError(f"collective '{kind}' is not supported by the local-view runner")
 
@@ -295,6 +298,74 @@ class RankComm:
             counters.collective_calls += 1
             counters.comm_bytes += 8 * n if self.world > 1 else 0
 
+    # -- DIST_MATMUL: SUMMA over local blocks ------------------
+
+    def _dist_plan(self, ex, op, sym):
+        n = op.node
+        ins = {e.dst_conn: e for e in op.state.in_edges(n) if e.memlet is not None}
+        outs = [e for e in op.state.out_edges(n) if e.memlet is not None]
+        am, bm, om = ins["a"].memlet, ins["b"].memlet, outs[0].memlet
+        va, vb, vc = ex.view(am, sym), ex.view(bm, sym), ex.view(om, sym)
+        if any(v[2] != "f64" or len(v[3]) != 2 for v in (va, vb, vc)):
+            raise SimError("dist_matmul needs 2-D f64 blocks")
+        if om.wcr not in (None, "add"):
+            raise SimError(f"dist_matmul output WCR '{om.wcr}' is not supported")
+        dims = list(n.attrs.get("dist", {}).get("grid") or self._grid_dims())
+        if len(dims) == 1:
+            dims = [dims[0], 1]
+        Pr, Pc = (int(x) for x in dims)
+        if Pr * Pc != self.world:
+            raise SimError(f"dist_matmul grid {Pr}x{Pc} on {self.world} ranks")
+        (bm_, ka), (kb_, bn) = (va[3][0][0], va[3][1][0]), (vb[3][0][0], vb[3][1][0])
+        if vc[3][0][0] != bm_ or vc[3][1][0] != bn:
+            raise SimError("dist_matmul local C block does not match A / B blocks")
+        K = ka * Pc
+        if kb_ * Pr != K:
+            raise SimError(f"dist_matmul inner dimensions differ ({K} vs {kb_ * Pr})")
+        L = math.lcm(Pr, Pc)
+        if K % L:
+            raise SimError("uneven K panels (SPEC.md:588)")
+        return va, vb, vc, om, Pr, Pc, bm_, bn, K // L, L
+
+    def _dist_matmul(self, ex, op, sym, counters):
+        """C_local (=|+=) A @ B on a Pr x Pc grid: K in lcm(Pr, Pc) panels;
+        per panel the owner column of A's panel sends it along its grid row
+        and the owner row of B's panel along its grid column (one NCCL
+        send/recv group), then the local DMMA GEMM accumulates.  A 1x1 grid
+        is the local MATMUL with zero messages."""
+        va, vb, vc, om, Pr, Pc, am, bn, kb, L = self._dist_plan(ex, op, sym)
+        Lb = rt.lib()
+        i, j = divmod(self.rank, Pc)
+        pa = self._buffer((op.idx, "pa"), 8 * am * kb)
+        pb = self._buffer((op.idx, "pb"), 8 * kb * bn)
+        (ab, ao, _, ad), (bb, bo, _, bd), (cb, co, _, cd) = va, vb, vc
+        sent = 0
+        for l in range(L):
+            ca, la, rb, lb, ops = summa_panel_ops(Pr, Pc, i, j, l, pa, 8 * am * kb, pb, 8 * kb * bn)
+            if j == ca:
+                src = rt.make_view(ab, ao + la * kb * ad[1][1], "f64", [am, kb], [ad[0][1], ad[1][1]])
+                dst = rt.make_view(pa, 0, "f64", [am, kb], [kb, 1])
+                rt.check(Lb.b2_copy_view(ctypes.byref(dst), ctypes.byref(src), 0, ex.stream), "panel")
+                ex.launches += 1
+            if i == rb:
+                src = rt.make_view(bb, bo + lb * kb * bd[0][1], "f64", [kb, bn], [bd[0][1], bd[1][1]])
+                dst = rt.make_view(pb, 0, "f64", [kb, bn], [bn, 1])
+                rt.check(Lb.b2_copy_view(ctypes.byref(dst), ctypes.byref(src), 0, ex.stream), "panel")
+                ex.launches += 1
+            if ops:
+                sent += self.nccl.p2p(ops, ex.stream)
+            wcr = om.wcr if l == 0 else "add"
+            rt.check(Lb.b2_gemm_f64(am, bn, kb, pa, kb, 1, pb, bn, 1, cb + 8 * co, cd[0][1], cd[1][1],
+                                    rt.WCR_CODE[wcr], ex.stream), "dist gemm")
+            ex.launches += 1
+        if counters is not None:
+            counters.bytes_moved += 8 * (am * (kb * L // Pc) + (kb * L // Pr) * bn + am * bn)
+            if om.wcr is not None:
+                counters.wcr_commits += am * bn
+            if self.world > 1:
+                counters.collective_calls += 2 * L
+                counters.comm_bytes += sent
+
     # -- block collectives (root = rank 0 holds the global container) -----------
 
     def _grid_dims(self):
@@ -406,6 +477,11 @@ class RankComm:
             for q in range(self.world):
                 self._buffer((op.idx, "flat", q), c * sdfg.DTYPE_BYTES[gdt])
             self.colls.append((kind, c))
+        elif kind == "dist_matmul":
+            va, vb, vc, om, Pr, Pc, am_, bn, kb, L = self._dist_plan(ex, op, sym)
+            self._buffer((op.idx, "pa"), 8 * am_ * kb)
+            self._buffer((op.idx, "pb"), 8 * kb * bn)
+            self.colls.append((kind, Pr, Pc, kb * L))
         elif kind in ("bcast", "reduce"):
             am, _ = self._io(op)
             n = int(np.prod([len(r) for r in symexpr.eval_subset(am.subset, sym)]))
@@ -477,6 +553,29 @@ class RankComm:
         for p, _ in self._staging.values():
             rt.lib().b2_free(p)
         self._staging.clear()
+
+
+def summa_panel_ops(Pr, Pc, i, j, l, pa, abytes, pb, bbytes):
+    """Panel l of SUMMA on a Pr x Pc grid (rank = i * Pc + j, K cut into
+    lcm(Pr, Pc) panels): the grid column ``ca`` owning A's panel (its local
+    panel ``la``), the grid row ``rb`` owning B's (local panel ``lb``), and
+    this rank's NCCL ops [(send?, peer, ptr, bytes)] — the A panel travels
+    along grid row i, the B panel along grid column j."""
+    L = math.lcm(Pr, Pc)
+    ca, la = divmod(l, L // Pc)
+    rb, lb = divmod(l, L // Pr)
+    ops = []
+    if Pc > 1:
+        if j == ca:
+            ops += [(True, i * Pc + c, pa, abytes) for c in range(Pc) if c != ca]
+        else:
+            ops.append((False, i * Pc + ca, pa, abytes))
+    if Pr > 1:
+        if i == rb:
+            ops += [(True, r * Pc + j, pb, bbytes) for r in range(Pr) if r != rb]
+        else:
+            ops.append((False, rb * Pc + j, pb, bbytes))
+    return ca, la, rb, lb, ops
 
 
 def _nbytes(ex, m, sym):
