@@ -1,2 +1,8 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 600 python -m pytest tests/test_comm.py -q -m gpu -rf 2>&1 | tail -4
+run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only heat_3d --reps 10 --out gpurun_out/pf.json 2>&1 | grep -E "ms " | tail -1; }
+for i in 1 2; do
+run B2_MARCH_PF_LEAD=0
+run B2_MARCH_PF_LEAD=296
+run B2_MARCH_PF_LEAD=592
+run B2_MARCH_PF_LEAD=1184
+done
