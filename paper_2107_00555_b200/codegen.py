@@ -43,6 +43,7 @@ ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reduct
 FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min loop folds
 SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
+TILE_BY = int(os.environ.get("B2_TILE_BY", "8"))  # tile rows (blockDim.y) in tile2 mode
 MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in march mode
 MARCH_BX = int(os.environ.get("B2_MARCH_BX", "64"))  # tile columns (blockDim.x) in march mode
 # shift the innermost tile origin down to a 128-byte line so a warp's row
@@ -1174,7 +1175,7 @@ class _Gen:
             esz = max([{"i32": 4, "bool": 1}.get(self.g.containers[n].dtype, 8) for n in spec.containers] or [8])
             spec.align = lastr[0] % max(1, 128 // esz)
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
-                      "tile2": (32, 8, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
+                      "tile2": (32, TILE_BY, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
                       "rowred": (256, 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
@@ -1359,7 +1360,8 @@ class _Gen:
             tw = 32 * vec
             ax = spec.align
             loop.append(f"  const b2_ll tiles_x = (rl{x} + {ax + tw - 1}) / {tw};")
-            loop.append(f"  const b2_ll tiles_y = (rl{y} + 7) / 8;")
+            tby = spec.block[1]
+            loop.append(f"  const b2_ll tiles_y = (rl{y} + {tby - 1}) / {tby};")
             outer = " * ".join(f"rl{i}" for i in range(k - 2)) or "1"
             loop.append(f"  const b2_ll nvb = tiles_x * tiles_y * ({outer});")
             loop.append("  for (b2_ll vb = blockIdx.x; vb < nvb; vb += gridDim.x) {")
@@ -1370,7 +1372,7 @@ class _Gen:
                     loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
                 else:
                     loop.append(f"    const b2_ll i{i} = rem;")
-            loop.append(f"    const b2_ll i{y} = ty * 8 + threadIdx.y;")
+            loop.append(f"    const b2_ll i{y} = ty * {tby} + threadIdx.y;")
             loop.append(f"    if (i{y} >= rl{y}) continue;")
             if ax:
                 hdr = [f"    const b2_ll i{x} = tx * {tw} + v * 32 + (b2_ll)threadIdx.x - {ax};",
@@ -1899,13 +1901,14 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
             blocks = max(1, min(blocks, MAX_BLOCKS))
         return (blocks, 1, 1), (bx, by, 1)
     tw = 32 * spec.vec
-    tiles = ((rl[k - 1] + spec.align + tw - 1) // tw) * ((rl[k - 2] + 7) // 8)
+    tby = spec.block[1]
+    tiles = ((rl[k - 1] + spec.align + tw - 1) // tw) * ((rl[k - 2] + tby - 1) // tby)
     for v in rl[: k - 2]:
         tiles *= v
     blocks = max(1, min(tiles, MAX_BLOCKS * 8))
     if spec.private:
         blocks = max(1, min(blocks, MAX_BLOCKS))
-    return (blocks, 1, 1), (32, 8, 1)
+    return (blocks, 1, 1), (32, tby, 1)
 
 
 def pack_args(spec: KernelSpec, env: dict, rvals, ptrs: dict, strides: dict, sizes: dict,
