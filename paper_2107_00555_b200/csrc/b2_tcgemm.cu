@@ -17,8 +17,10 @@
 //   * warp 1 lane 0 issues tcgen05.mma (M=128, N=256, K=8) x 4 per stage into
 //     a 128 x 256 fp32 accumulator in TMEM and releases each stage with
 //     tcgen05.commit,
-//   * default: CTA pairs (tc_sgemm_pair, cta_group::2, 256 x 256 tiles, 6
-//     stages of 32 KB); B2_TC_PAIR=0 selects the single-CTA kernel,
+//   * default: CTA pairs (tc_sgemm_pair, cta_group::2, 256 x 256 tiles,
+//     two-segment operands A' = [lo|hi], B' = [hi|lo] per 32-wide k block so
+//     the three products lo.hi, hi.lo, hi.hi come from one stage; 3 stages of
+//     64 KB per CTA); B2_TC_PAIR=0 selects the single-CTA kernel,
 //   * long in-TMEM accumulations lose accuracy (the error grows with the
 //     accumulation length), so the MMA warp accumulates chunks of 128 k into
 //     two alternating 256-column TMEM buffers and eight epilogue warps drain
