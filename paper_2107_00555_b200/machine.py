@@ -287,6 +287,11 @@ class GpuExecutor:
                     continue
                 if not _covers(spec.red_points, X, b, self.buf.shape[X], pl):
                     continue
+                # B must launch whenever A would: every range constant and
+                # non-empty (an empty reduction range skips B's launch)
+                rng = [codegen._const_range(pl, r) for r in b.ranges]
+                if any(r is None or r[2] < 1 for r in rng):
+                    continue
                 out[b.idx] = {X: lit}
                 self.init_skip.add(a.idx)
         return out

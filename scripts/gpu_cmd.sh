@@ -1,6 +1,8 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only azimint_naive --reps 10 --out gpurun_out/j.json 2>&1 | grep -E "ms "; }
-run B2_RED_THREADS=606208
-run B2_RED_THREADS=1212416
-run B2_RED_THREADS=2424832
-B2_RED_THREADS=1212416 timeout -s KILL 900 python -m pytest tests -q -m gpu -rf -o faulthandler_timeout=300 2>&1 | grep -E "FAILED|passed|failed|Error" | head -8
+P="python scripts/probe_time.py"
+for w in gemver atax bicg; do
+  if [ $w = gemver ]; then S='{"N": 8000}'; else S='{"M": 8000, "N": 8000}'; fi
+  $P $w.raw "$S" 3 > gpurun_out/plain_$w.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/l_$w.csv $P $w.raw "$S" 3 > gpurun_out/ncu_$w.log 2>&1
+  tail -4 gpurun_out/plain_$w.log
+done
