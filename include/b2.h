@@ -114,6 +114,12 @@ B2_API int b2_func_set_max_smem(void *fn, int bytes);
 /* Launch `fn` whose single by-value parameter is the byte blob `args`. */
 B2_API int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by,
               unsigned bz, unsigned smem, void *stream, const void *args, size_t args_bytes);
+/* Same, always with programmatic stream serialization (PDL): the kernel may
+ * start before the previous one in the stream finishes and must open with
+ * griddepcontrol.wait (used for fold kernels right after their producer). */
+B2_API int b2_launch_pdl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+              unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
+              size_t args_bytes);
 /* Number of kernel launches issued through this library so far. */
 B2_API int64_t b2_launch_count(void);
 

@@ -31,6 +31,7 @@ from . import codegen, plan as P, runtime as rt, sdfg, symexpr
 
 TPB = 512
 MAX_CW = 8192
+RP_PDL = os.environ.get("B2_RP_PDL", "0") == "1"  # fold kernel as a programmatic dependent launch (neutral: off)
 TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpass.cuh)
 SMEM_BUDGET = 220 * 1024
 
@@ -361,6 +362,10 @@ class RowPass:
     def compile(self, ex):
         name = f"{ex.g.name}_{self.mvs[0].op.idx}"
         src = self.source(ex.buf.shape, name)
+        if RP_PDL:
+            # kernels open with griddepcontrol.wait: the fold kernel is
+            # launched programmatically and overlaps the row pass's tail
+            src = "#undef B2_NO_PDL\n" + src
         self.kmain = rt.get_kernel(src, f"b2_rp_{name}", max_smem=self.smem)
         self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
         ws = 0
@@ -410,7 +415,8 @@ class RowPass:
             if prof is not None:
                 ev = ex._prof_event_pair()
                 rt.lib().b2_event_record(ev[0], ex.stream)
-            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream)
+            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream,
+                      pdl=RP_PDL and prof is None)
             if prof is not None:
                 rt.lib().b2_event_record(ev[1], ex.stream)
                 prof.append((self.kfin.name, nfin, ev))

@@ -264,9 +264,9 @@ extern "C" int b2_func_set_max_smem(void *fn, int bytes) {
                   "cuFuncSetAttribute");
 }
 
-extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
-                         unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
-                         size_t args_bytes) {
+static int launch_impl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                       unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
+                       size_t args_bytes, bool pdl) {
   if (drv.status != 0) {
     int rc = load_driver();
     if (rc) return rc;
@@ -274,14 +274,6 @@ extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsign
   size_t sz = args_bytes;
   void *cfg[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void *>(args),
                  CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
-  // JIT kernels open with griddepcontrol.wait (prelude B2_PDL_ENTRY), so they
-  // may be launched programmatically: the launch overlaps the tail of the
-  // previous kernel in the stream (also as graph edges under capture)
-  static int pdl = -1;
-  if (pdl < 0) {  // opt-in, matching runtime.NVRTC_OPTS (-DB2_NO_PDL otherwise)
-    const char *e = getenv("B2_PDL");
-    pdl = e && e[0] == '1';
-  }
   CUresult r;
   if (pdl) {
     CUlaunchAttribute at[1];
@@ -306,6 +298,26 @@ extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsign
   if (r != CUDA_SUCCESS) return cu_check(r, "cuLaunchKernel");
   b2_count_launch();
   return B2_OK;
+}
+
+extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                         unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
+                         size_t args_bytes) {
+  // JIT kernels open with griddepcontrol.wait (prelude B2_PDL_ENTRY), so they
+  // may be launched programmatically: the launch overlaps the tail of the
+  // previous kernel in the stream (also as graph edges under capture)
+  static int pdl = -1;
+  if (pdl < 0) {  // opt-in, matching runtime.NVRTC_OPTS (-DB2_NO_PDL otherwise)
+    const char *e = getenv("B2_PDL");
+    pdl = e && e[0] == '1';
+  }
+  return launch_impl(fn, gx, gy, gz, bx, by, bz, smem, stream, args, args_bytes, pdl != 0);
+}
+
+extern "C" int b2_launch_pdl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                             unsigned by, unsigned bz, unsigned smem, void *stream,
+                             const void *args, size_t args_bytes) {
+  return launch_impl(fn, gx, gy, gz, bx, by, bz, smem, stream, args, args_bytes, true);
 }
 
 // ---------------------------------------------------------------------------

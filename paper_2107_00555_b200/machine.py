@@ -41,6 +41,7 @@ DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
 # a constant-fill map followed by a reduction over the same container starts
 # the reduction from the constant instead of launching the fill
 INIT_FUSION = os.environ.get("B2_INIT_FUSION", "1") == "1"
+FIN_PDL = os.environ.get("B2_FIN_PDL", "0") == "1"  # reduction fold kernels launched with PDL (neutral: off)
 
 
 class InterpreterError(RuntimeError):
@@ -209,6 +210,9 @@ class GpuExecutor:
                 spec = codegen.generate(self.planner, op, self.buf.shape, name,
                                         init_const=fused_init.get(op.idx))
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
+                if FIN_PDL and getattr(spec, "red_fin", None):
+                    # the fold kernel is a programmatic dependent launch
+                    src = "#undef B2_NO_PDL\n" + src
                 spec.kernel = rt.get_kernel(src, name)
                 spec.fin_kernel = None
                 if getattr(spec, "red_fin", None):
@@ -999,7 +1003,8 @@ class GpuExecutor:
         if spec.fin_kernel is not None:
             fg = spec.red_nout if spec.red_fin_block else -(-spec.red_nout // 256)
             fg = max(1, min(fg, codegen.MAX_BLOCKS * 8))
-            rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream)
+            rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream,
+                      pdl=FIN_PDL and self._prof is None)
             self.launches += 1
         if self._prof is not None:
             rt.lib().b2_event_record(ev[1], self.stream)

@@ -1,8 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-P="python scripts/probe_time.py"
-for w in gemver atax bicg; do
-  if [ $w = gemver ]; then S='{"N": 8000}'; else S='{"M": 8000, "N": 8000}'; fi
-  $P $w.raw "$S" 3 > gpurun_out/plain_$w.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/l_$w.csv $P $w.raw "$S" 3 > gpurun_out/ncu_$w.log 2>&1
-  tail -4 gpurun_out/plain_$w.log
-done
+run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only gemver,atax,bicg,azimint_naive,go_fast --reps 10 --out gpurun_out/j.json 2>&1 | grep -E "ms "; }
+run B2_RP_PDL=1 B2_FIN_PDL=1
+run B2_RP_PDL=0 B2_FIN_PDL=0
+run B2_RP_PDL=1 B2_FIN_PDL=1
+timeout -s KILL 900 python -m pytest tests -q -m gpu -rf -o faulthandler_timeout=300 2>&1 | grep -E "FAILED|passed|failed|Error" | head -8
