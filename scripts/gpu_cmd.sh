@@ -1,6 +1,6 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only gemver,atax,bicg,azimint_naive,go_fast --reps 10 --out gpurun_out/j.json 2>&1 | grep -E "ms "; }
-run B2_RP_PDL=1 B2_FIN_PDL=1
-run B2_RP_PDL=0 B2_FIN_PDL=0
-run B2_RP_PDL=1 B2_FIN_PDL=1
-timeout -s KILL 900 python -m pytest tests -q -m gpu -rf -o faulthandler_timeout=300 2>&1 | grep -E "FAILED|passed|failed|Error" | head -8
+B2_FORCE_SLAB=1 B2_SLAB_FORCE_SPLIT=1 timeout -s KILL 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 1 --steps 3 --warmup 3 > gpurun_out/slab1.json 2> gpurun_out/slab1.err; echo rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/slab1.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e'])"
+tail -3 gpurun_out/slab1.err
+timeout -s KILL 600 python -m pytest tests/test_gpu_dist.py -q 2>&1 | tail -2
