@@ -62,4 +62,35 @@ for name, syms in (("atax", {"M": 1001, "N": 999}), ("atax", {"M": 4000, "N": 40
     ok = err <= 1e-12 or nerr <= 1e-14
     fails += not ok
     print(name, syms, ok, err, nerr, flush=True)
+# NPBench sweep programs at odd sizes (reduction schedules: register-blocked,
+# short-chunk in-block, chunked + fold, row reductions, warp folds)
+npb = (("softmax", {"N": 3, "H": 5, "SM": 77}, ("x",), ("out",)),
+       ("softmax", {"N": 2, "H": 3, "SM": 512}, ("x",), ("out",)),
+       ("conv2d_bias", {"NB": 2, "H": 150, "W": 150, "CI": 3, "CO": 16, "K": 20, "HO": 131,
+                        "WO": 131}, ("inp", "w", "bias"), ("out",)),
+       ("conv2d_bias", {"NB": 1, "H": 37, "W": 41, "CI": 2, "CO": 5, "K": 3, "HO": 35,
+                        "WO": 39}, ("inp", "w", "bias"), ("out",)),
+       ("azimint_naive", {"N": 200001, "NPT": 997}, ("rmax", "data", "radius"), ("res",)),
+       ("go_fast", {"N": 3001}, ("a",), ("out",)),
+       ("nbody", {"N": 77, "NT": 9}, ("mass", "pos", "vel", "acc", "E", "G", "softening", "dt"),
+        ("pos", "vel", "acc", "E")))
+for name, syms, _, outs in npb:
+    g = sdfg.load(f"{GD}/{name}.raw.json")
+    ins = inputs_for(g, syms, 11)
+    if name == "azimint_naive":
+        ins["radius"] = np.abs(ins["radius"]) * ins["rmax"]
+    out = interpret(g, ExecContext(bindings=syms).bind_inputs(
+        {k: np.array(v, copy=True) for k, v in ins.items()}))
+    fn = getattr(K, name)
+    args = {k: (np.array(v, copy=True) if np.ndim(v) else v) for k, v in ins.items()}
+    params = list(inspect.signature(fn).parameters)
+    call = [args[p] if p in args else syms[p] for p in params]
+    ref = fn(*call)
+    if not isinstance(ref, dict):
+        ref = {o: args[o] for o in outs}
+    err = max(float(np.linalg.norm(out[k] - ref[k]) / max(np.linalg.norm(ref[k]), 1e-300))
+              for k in outs)
+    ok = err <= 1e-12
+    fails += not ok
+    print(name, syms, ok, err, flush=True)
 print("FAILS", fails)
