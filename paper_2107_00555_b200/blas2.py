@@ -368,9 +368,6 @@ class RowPass:
             src = "#undef B2_NO_PDL\n" + src
         self.kmain = rt.get_kernel(src, f"b2_rp_{name}", max_smem=self.smem)
         self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
-        ws = 0
-        if self.axpy is not None:
-            ws += self.G * self.N * 8
         self.ws_axpy = ex.buf.alloc(max(8, self.G * self.N * 8)) if self.axpy is not None else 0
         self.ws_dot = ex.buf.alloc(max(8, self.ctiles * self.M * 8)) if self.dot is not None else 0
 

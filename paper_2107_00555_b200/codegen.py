@@ -1847,7 +1847,7 @@ def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
     # the executor's init-map fusion
     spec.red_targets = {}
     if gen.red:
-        for key, t in gen.red.items():
+        for t in gen.red.values():
             spec.red_targets[t["cont"]] = spec.red_targets.get(t["cont"], []) + [
                 (t["exclusive"], t["ct"])]
         spec.red_points = list(gen.red_targets)

@@ -478,7 +478,7 @@ class RankComm:
                 self._buffer((op.idx, "flat", q), c * sdfg.DTYPE_BYTES[gdt])
             self.colls.append((kind, c))
         elif kind == "dist_matmul":
-            va, vb, vc, om, Pr, Pc, am_, bn, kb, L = self._dist_plan(ex, op, sym)
+            *_, Pr, Pc, am_, bn, kb, L = self._dist_plan(ex, op, sym)
             self._buffer((op.idx, "pa"), 8 * am_ * kb)
             self._buffer((op.idx, "pb"), 8 * kb * bn)
             self.colls.append((kind, Pr, Pc, kb * L))
