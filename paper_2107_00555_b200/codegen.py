@@ -54,6 +54,8 @@ RED_THREADS = int(os.environ.get("B2_RED_THREADS", str(148 * 8192)))  # chunked-
 SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per chunk, small reductions (0: off)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
+MARCH_PDL = os.environ.get("B2_MARCH_PDL", "1") == "1"  # march sweeps as programmatic dependent launches (heat 37.40 -> 37.24 ms)
+TILE_PDL = os.environ.get("B2_TILE_PDL", "0") == "1"  # ... tile2 sweeps (jacobi 1.74 -> 1.86 ms: off)
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
 ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "4"))  # unroll of the warp-per-row loop
@@ -1441,6 +1443,15 @@ class _Gen:
                f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
                "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
         fin = self._reduce_fin(pro) if mode == "reduce" and getattr(spec, "red_fin", None) else []
+        spec.pdl = ((MARCH_PDL and mode == "march") or (TILE_PDL and mode == "tile2")) \
+            and not self.dyn0
+        if spec.pdl:
+            # programmatic dependent launch: wait for the previous sweep's
+            # grid at entry, trigger our dependents only after this CTA's
+            # stores, so the next sweep launches into this one's tail
+            pro.insert(pro.index("  B2_PDL_ENTRY();") + 1,
+                       '  asm volatile("griddepcontrol.wait;" ::: "memory");')
+            loop.append('  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");')
         spec.source = "\n".join(src + pro + loop + ["}"] + fin) + "\n"
         return spec
 

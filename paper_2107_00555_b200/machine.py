@@ -999,7 +999,8 @@ class GpuExecutor:
         if self._prof is not None:
             ev = self._prof_event_pair()
             rt.lib().b2_event_record(ev[0], self.stream)
-        rt.launch(spec.kernel, grid, block, blob, self.stream)
+        rt.launch(spec.kernel, grid, block, blob, self.stream,
+                  pdl=getattr(spec, "pdl", False) and self._prof is None)
         if spec.fin_kernel is not None:
             fg = spec.red_nout if spec.red_fin_block else -(-spec.red_nout // 256)
             fg = max(1, min(fg, codegen.MAX_BLOCKS * 8))

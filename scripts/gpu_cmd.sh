@@ -1,3 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 900 python scripts/parity_sweep.py > gpurun_out/parity_sweep.log 2>&1; echo rc=$?
-tail -30 gpurun_out/parity_sweep.log
+run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only jacobi_2d,softmax,go_fast --reps 10 --out gpurun_out/pf.json 2>&1 | grep -E "ms "; }
+for i in 1 2; do run B2_TILE_PDL=0; run B2_TILE_PDL=1; done
+B2_TILE_PDL=1 B2_MARCH_PDL=1 timeout -s KILL 900 python -m pytest tests -q -m gpu -rf 2>&1 | grep -E "FAILED|passed|failed|Error" | head -8
