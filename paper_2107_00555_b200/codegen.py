@@ -55,6 +55,10 @@ SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per ch
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
 MARCH_PDL = os.environ.get("B2_MARCH_PDL", "1") == "1"  # march sweeps as programmatic dependent launches (heat 37.40 -> 37.24 ms)
+# ... small flat / reduce / scalar kernels, whose launch latency is a large
+# share of their time (nbody's per-step kernels: 5.32 -> 4.67 ms)
+SMALL_PDL = os.environ.get("B2_SMALL_PDL", "1") == "1"
+SMALL_PDL_POINTS = 1 << 16
 TILE_PDL = os.environ.get("B2_TILE_PDL", "0") == "1"  # ... tile2 sweeps (jacobi 1.74 -> 1.86 ms: off)
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
@@ -1443,8 +1447,12 @@ class _Gen:
                f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
                "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
         fin = self._reduce_fin(pro) if mode == "reduce" and getattr(spec, "red_fin", None) else []
-        spec.pdl = ((MARCH_PDL and mode == "march") or (TILE_PDL and mode == "tile2")) \
-            and not self.dyn0
+        npts = 1
+        for r in self.const_ranges:
+            npts *= r[2] if r is not None else 1 << 40
+        spec.pdl = ((MARCH_PDL and mode == "march") or (TILE_PDL and mode == "tile2")
+                    or (SMALL_PDL and mode in ("flat", "reduce", "scalar")
+                        and npts <= SMALL_PDL_POINTS)) and not self.dyn0
         if spec.pdl:
             # programmatic dependent launch: wait for the previous sweep's
             # grid at entry, trigger our dependents only after this CTA's
