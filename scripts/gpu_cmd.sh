@@ -1,3 +1,8 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
-timeout -s KILL 300 python scripts/bench_suite.py --only nbody,conv2d_bias,azimint_naive,go_fast --reps 10 --out gpurun_out/pf.json 2>&1 | grep -E "ms "
-timeout -s KILL 900 python -m pytest tests -q -m gpu -rf 2>&1 | grep -E "FAILED|passed|failed|Error" | head -8
+run() { echo "== $*"; env "$@" timeout -s KILL 300 python scripts/bench_suite.py --only heat_3d --reps 10 --out gpurun_out/pf.json 2>&1 | grep -E "ms " | tail -1; }
+for i in 1 2; do
+run B2_MARCH_BX=64
+run B2_MARCH_BX=64 B2_VEC=12
+run B2_MARCH_BX=128 B2_MARCH_BY=4
+run B2_MARCH_BX=32 B2_MARCH_BY=16
+done
