@@ -41,6 +41,7 @@ DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
 # a constant-fill map followed by a reduction over the same container starts
 # the reduction from the constant instead of launching the fill
 INIT_FUSION = os.environ.get("B2_INIT_FUSION", "1") == "1"
+ZERO_SKIP = os.environ.get("B2_ZERO_SKIP", "1") == "1"  # skip zeroing fully overwritten transients
 FIN_PDL = os.environ.get("B2_FIN_PDL", "0") == "1"  # reduction fold kernels launched with PDL (neutral: off)
 
 
@@ -449,6 +450,7 @@ class GpuExecutor:
         box [1, n-2]^d at one point per iteration without reading them: the
         interior input values are never observed (heat_3d / jacobi_2d's B),
         so only the 2d boundary faces need to reach the device."""
+        self.zero_skip = set()
         if not self.capturable or self.planner.regions:
             return set()
         first: dict = {}
@@ -462,6 +464,11 @@ class GpuExecutor:
             self._dry = False
             self._first_touch = None
         out = set()
+        for name, op in first.items():
+            c = self.g.containers[name]
+            if (c.transient and c.lifetime != "persistent" and ZERO_SKIP
+                    and self._overwrites(name, op)):
+                self.zero_skip.add(name)
         for name, op in first.items():
             c = self.g.containers[name]
             shape = self.buf.shape[name]
@@ -489,6 +496,46 @@ class GpuExecutor:
             if box_ok:
                 out.add(name)
         return out
+
+    def _overwrites(self, name: str, op) -> bool:
+        """``op`` (the first op of the trace touching transient ``name``)
+        writes every element of it without reading it: zeroing it per call
+        (interp.py:220-221) is then unobservable and is skipped."""
+        shape = self.buf.shape.get(name)
+        if not shape:
+            return False
+        if isinstance(op, P.MapGroup):
+            if name in self.planner.op_reads.get(op.idx, set()):
+                return False
+            sites = [st for st in self.planner.sites.get(name, []) if st.op == op.idx]
+            if (len(sites) != 1 or not sites[0].is_write or sites[0].wcr is not None
+                    or sites[0].depth != 0 or sites[0].point is None
+                    or len(sites[0].point) != len(shape) or len(op.params) != len(shape)):
+                return False
+            rng = [codegen._const_range(self.planner, r) for r in op.ranges]
+            for d, (c0, co) in enumerate(sites[0].point):
+                r = rng[d]
+                if r is None or r[1] != 1 or co != ((op.params[d], 1),):
+                    return False
+                if (r[0] + c0, r[0] + c0 + r[2] - 1) != (0, shape[d] - 1):
+                    return False
+            return True
+        if isinstance(op, P.LibOp) and op.kind == "matmul":
+            # the op's primary MATMUL runs first (fused row-pass partners
+            # consume its output afterwards); a prologue map runs before it
+            if op.prologue is not None:
+                return False
+            ins = [e for e in op.state.in_edges(op.node) if e.memlet is not None]
+            outs = [e for e in op.state.out_edges(op.node) if e.memlet is not None]
+            if any(e.memlet.container == name for e in ins):
+                return False
+            if len(outs) != 1 or outs[0].memlet.container != name or outs[0].memlet.wcr:
+                return False
+            try:
+                return _is_full(self, outs[0].memlet, dict(self.bindings))
+            except Exception:  # noqa: BLE001 - symbolic subset: keep zeroing
+                return False
+        return False
 
     def _upload_shell(self, name: str, arr: np.ndarray):
         """The 2d boundary faces of `arr` (host-packed into one pinned
@@ -530,6 +577,8 @@ class GpuExecutor:
                 continue
             if c.lifetime == "persistent" and not first_call:
                 continue  # persistent transients keep their contents (interp.py:216-219)
+            if name in self.zero_skip:
+                continue  # fully overwritten before any read (_overwrites)
             self.zero(name)
         for n, p in self.scratch.items():
             if n + "#scratch" in self.buf.nbytes:  # per-thread private scratch (not workspaces)

@@ -267,3 +267,22 @@ def test_init_fill_fused_into_reduction_bitwise(monkeypatch):
     for k in ("pos", "vel", "acc", "E"):
         assert np.array_equal(res[True][0][k], res[False][0][k]), k
     assert res[True][1] == res[False][1]
+
+
+def test_fully_overwritten_transients_not_zeroed():
+    """atax's tmp0 = A @ x is written in full by the row pass before anything
+    reads it, so the per-call zeroing (interp.py:220-221) is skipped; the
+    result still matches the port."""
+    from oracle import kernels_np as K
+    from paper_2107_00555_b200 import sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    g = sdfg.load(GOLDEN / "graphs" / "atax.raw.json")
+    ex = GpuExecutor(g, {"M": 300, "N": 200})
+    assert ex.zero_skip == {"tmp0"}
+    ex.close()
+    rng = np.random.default_rng(2)
+    A, x = rng.uniform(-1, 1, (300, 200)), rng.uniform(-1, 1, 200)
+    out = _run("atax.raw", {"M": 300, "N": 200}, {"A": A, "x": x, "y": np.zeros(200)})
+    ref = K.atax(A.copy(), x.copy(), np.zeros(200))
+    assert rel_err(out["y"], ref["y"]) <= 1e-12
