@@ -590,7 +590,6 @@ class GpuExecutor:
     def run_device(self, first_call: bool = True, counters=None):
         """Execute the whole state machine on the device (inputs already
         resident).  Returns after enqueueing; call ``sync()`` to wait."""
-        self._reset_flags()
         self.zero_transients(first_call)
         if self.device_branching and self.graph_exec is None:
             try:
@@ -616,6 +615,7 @@ class GpuExecutor:
                 counters.map_iterations += int(dc[1])
                 counters.bytes_moved += int(dc[2])
         else:
+            self._reset_flags()
             self._run_states(counters, eager=True)
 
     # -- device-side branches -------------------------------------------------------
@@ -792,6 +792,7 @@ class GpuExecutor:
         rt.check(L.b2_capture_begin(self.stream), "capture")
         tc = Counters()
         try:
+            self._reset_flags()  # error flags cleared by the graph itself
             self._run_states(tc, eager=False)
         except BaseException:
             ge = ctypes.c_void_p()
