@@ -62,7 +62,7 @@ SMALL_PDL_POINTS = 1 << 16
 TILE_PDL = os.environ.get("B2_TILE_PDL", "0") == "1"  # ... tile2 sweeps (jacobi 1.74 -> 1.86 ms: off)
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
-ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "4"))  # unroll of the warp-per-row loop
+ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "1"))  # unroll of the warp-per-row loop (4 spilled at 32 regs)
 ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowred kernels (softmax 1.11 -> 1.06 ms)
 ROWRED_HOIST = os.environ.get("B2_ROWRED_HOIST", "0") == "1"  # issue a lane's row loads first (slower: off)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
