@@ -120,6 +120,11 @@ B2_API int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned b
 B2_API int b2_launch_pdl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
               unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
               size_t args_bytes);
+/* Same, as a cooperative launch: every CTA co-resident (kernels with grid
+ * barriers, e.g. the row pass folding its partials in-kernel) or an error. */
+B2_API int b2_launch_coop(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+              unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
+              size_t args_bytes);
 /* Number of kernel launches issued through this library so far. */
 B2_API int64_t b2_launch_count(void);
 

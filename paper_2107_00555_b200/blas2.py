@@ -31,6 +31,7 @@ from . import codegen, plan as P, runtime as rt, sdfg, symexpr
 
 TPB = 512
 MAX_CW = 8192
+RP_COOP = os.environ.get("B2_RP_COOP", "0") == "1"  # fold inside the row pass (grid barrier)
 RP_PDL = os.environ.get("B2_RP_PDL", "0") == "1"  # fold kernel as a programmatic dependent launch (neutral: off)
 TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpass.cuh)
 SMEM_BUDGET = 220 * 1024
@@ -268,6 +269,9 @@ class RowPass:
         # register-prefetch kernel at 2-3 CTAs/SM: 184 vs 254 us)
         self.tma = (TMA_ROWS and self.prologue is None and rs % 2 == 0 and off % 2 == 0
                     and N % 2 == 0 and cw % 2 == 0 and ring_s >= 2)
+        # in-kernel fold after a grid barrier (cooperative launch): TMA
+        # variant (one CTA per SM, all co-resident), one column tile
+        self.coop = RP_COOP and self.tma and axpy is not None and self.ctiles == 1
         if self.tma:
             self.ring = min(4, ring_s)
             stage_base = 0
@@ -291,6 +295,7 @@ class RowPass:
                      ("RP_PROLOGUE", int(self.prologue is not None)),
                      ("RP_WRITEBACK", int(self.prologue is not None)),
                      ("RP_TMA", int(self.tma)), ("RP_S", max(1, self.ring)),
+                     ("RP_COOP", int(self.coop)),
                      ("RP_NSTAGED", nst)):
             L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")
         nbase = 8
@@ -370,6 +375,10 @@ class RowPass:
         self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
         self.ws_axpy = ex.buf.alloc(max(8, self.G * self.N * 8)) if self.axpy is not None else 0
         self.ws_dot = ex.buf.alloc(max(8, self.ctiles * self.M * 8)) if self.dot is not None else 0
+        self.bar = 0
+        if self.coop:  # grid-barrier state (count, sense), zero once
+            self.bar = ex.buf.alloc(16)
+            rt.check(rt.lib().b2_memset(self.bar, 0, 16, ex.stream), "memset")
 
     # -- run ---------------------------------------------------------------------
 
@@ -382,6 +391,7 @@ class RowPass:
         w[0] = ex.buf.ptr[cont] + 8 * off
         w[1] = self.ws_axpy
         w[2] = self.ws_dot
+        w[7] = self.bar
         if self.dot is not None:
             w[3] = self._ptr(ex, self.dot.vec)
             w[4] = self._ptr(ex, self.dot.out)
@@ -402,11 +412,11 @@ class RowPass:
             ev = ex._prof_event_pair()
             rt.lib().b2_event_record(ev[0], ex.stream)
         rt.launch(self.kmain, (self.G, self.ctiles, 1), (self.tpb, 1, 1), blob, ex.stream,
-                  self.smem)
+                  self.smem, coop=self.coop)
         if prof is not None:
             rt.lib().b2_event_record(ev[1], ex.stream)
             prof.append((self.kmain.name, self.M * self.N, ev))
-        nfin = max(self.N if self.axpy is not None else 0,
+        nfin = max(self.N if (self.axpy is not None and not self.coop) else 0,
                    self.M if (self.dot is not None and self.ctiles > 1) else 0)
         if nfin:
             if prof is not None:

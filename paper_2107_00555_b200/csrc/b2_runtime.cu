@@ -266,7 +266,7 @@ extern "C" int b2_func_set_max_smem(void *fn, int bytes) {
 
 static int launch_impl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
                        unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
-                       size_t args_bytes, bool pdl) {
+                       size_t args_bytes, bool pdl, bool coop = false) {
   if (drv.status != 0) {
     int rc = load_driver();
     if (rc) return rc;
@@ -275,10 +275,15 @@ static int launch_impl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned
   void *cfg[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void *>(args),
                  CU_LAUNCH_PARAM_BUFFER_SIZE, &sz, CU_LAUNCH_PARAM_END};
   CUresult r;
-  if (pdl) {
+  if (pdl || coop) {
     CUlaunchAttribute at[1];
-    at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
-    at[0].value.programmaticStreamSerializationAllowed = 1;
+    if (coop) {  // all CTAs co-resident (grid barriers), or the launch fails
+      at[0].id = CU_LAUNCH_ATTRIBUTE_COOPERATIVE;
+      at[0].value.cooperative = 1;
+    } else {
+      at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      at[0].value.programmaticStreamSerializationAllowed = 1;
+    }
     CUlaunchConfig lc = {};
     lc.gridDimX = gx;
     lc.gridDimY = gy;
@@ -290,7 +295,11 @@ static int launch_impl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned
     lc.hStream = (CUstream)stream;
     lc.attrs = at;
     lc.numAttrs = 1;
-    r = drv.launchKernelEx(&lc, (CUfunction)fn, nullptr, cfg);
+    // cooperative launches take kernelParams, not the packed-buffer `extra`:
+    // every kernel here has one by-value struct parameter, the blob itself
+    void *params[] = {const_cast<void *>(args)};
+    r = coop ? drv.launchKernelEx(&lc, (CUfunction)fn, params, nullptr)
+             : drv.launchKernelEx(&lc, (CUfunction)fn, nullptr, cfg);
   } else {
     r = drv.launchKernel((CUfunction)fn, gx, gy, gz, bx, by, bz, smem, (CUstream)stream,
                          nullptr, cfg);
@@ -312,6 +321,12 @@ extern "C" int b2_launch(void *fn, unsigned gx, unsigned gy, unsigned gz, unsign
     pdl = e && e[0] == '1';
   }
   return launch_impl(fn, gx, gy, gz, bx, by, bz, smem, stream, args, args_bytes, pdl != 0);
+}
+
+extern "C" int b2_launch_coop(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
+                              unsigned by, unsigned bz, unsigned smem, void *stream,
+                              const void *args, size_t args_bytes) {
+  return launch_impl(fn, gx, gy, gz, bx, by, bz, smem, stream, args, args_bytes, false, true);
 }
 
 extern "C" int b2_launch_pdl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,

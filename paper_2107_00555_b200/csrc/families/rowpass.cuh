@@ -32,6 +32,32 @@ __device__ __forceinline__ double rp_block_sum(double v, double *red, int parity
   return t;
 }
 
+#ifndef RP_COOP
+#define RP_COOP 0
+#endif
+#if RP_COOP
+// Grid barrier for a cooperative launch (every CTA co-resident): one
+// arrival counter and a sense word, both back to the start state after use,
+// so the same state serves every launch (and graph replay).
+__device__ __forceinline__ void rp_grid_sync(unsigned *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned *sense = bar + 1;
+    const unsigned s = *sense;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x * gridDim.y - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicExch(bar + 1, s ^ 1u);
+    } else {
+      while (*sense == s) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+#endif
+
 #if RP_TMA
 // TMA variant: rows stream through an RP_S-deep ring of shared-memory row
 // buffers filled by 1-D bulk copies (cp.async.bulk + mbarrier), so up to
@@ -123,6 +149,16 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
     const int j = tid + k * RP_TPB;
     if (j < cw) ws[(b2_ll)blockIdx.x * RP_N + c0 + j] = acc[k];
   }
+#if RP_COOP
+  // cooperative launch (one column tile): after the grid barrier every CTA
+  // folds a slice of the columns over the G partial rows in row order
+  rp_grid_sync((unsigned *)a.w[7]);
+  for (b2_ll i = (b2_ll)blockIdx.x * RP_TPB + tid; i < RP_N; i += (b2_ll)gridDim.x * RP_TPB) {
+    double t = 0.0;
+    for (int g = 0; g < RP_G; ++g) t += __ldcg(ws + (b2_ll)g * RP_N + i);
+    rp_store_axpy(a, i, t);
+  }
+#endif
 #endif
 }
 #else

@@ -78,7 +78,7 @@ EXPORTS = [
     "b2_stream_wait_event", "b2_capture_if_begin", "b2_capture_if_end", "b2_capture_body_begin",
     "b2_capture_body_end", "b2_counters_add",
     "b2_host_register", "b2_host_unregister", "b2_jit_compile", "b2_module_load",
-    "b2_module_unload", "b2_module_function", "b2_func_set_max_smem", "b2_launch", "b2_launch_pdl",
+    "b2_module_unload", "b2_module_function", "b2_func_set_max_smem", "b2_launch", "b2_launch_pdl", "b2_launch_coop",
     "b2_launch_count", "b2_capture_begin", "b2_capture_end", "b2_graph_launch",
     "b2_graph_destroy", "b2_copy_view", "b2_fill_view", "b2_gemm_f64", "b2_gemm_f32",
     "b2_reduce", "b2_nccl_unique_id", "b2_nccl_init", "b2_nccl_destroy", "b2_nccl_group_p2p",
@@ -139,6 +139,9 @@ _SIGS = {
     "b2_launch_pdl": ([_vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
                        ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _vp, _vp, ctypes.c_size_t],
                       ctypes.c_int),
+    "b2_launch_coop": ([_vp, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
+                        ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _vp, _vp, ctypes.c_size_t],
+                       ctypes.c_int),
     "b2_launch_count": ([], ctypes.c_int64),
     "b2_capture_begin": ([_vp], ctypes.c_int),
     "b2_capture_end": ([_vp, ctypes.POINTER(_vp)], ctypes.c_int),
@@ -295,12 +298,12 @@ def get_kernel(src: str, name: str, extra_opts=(), max_smem: int = 0) -> Kernel:
 
 
 def launch(k: Kernel, grid, block, args_blob: bytes, stream, smem: int = 0,
-           pdl: bool = False) -> None:
+           pdl: bool = False, coop: bool = False) -> None:
     """pdl: programmatic dependent launch (the kernel must open with
     griddepcontrol.wait, i.e. be compiled with B2_PDL_ENTRY enabled)."""
     gx, gy, gz = (tuple(grid) + (1, 1, 1))[:3]
     bx, by, bz = (tuple(block) + (1, 1, 1))[:3]
-    fn = lib().b2_launch_pdl if pdl else lib().b2_launch
+    fn = lib().b2_launch_coop if coop else (lib().b2_launch_pdl if pdl else lib().b2_launch)
     check(fn(k.fn, gx, gy, gz, bx, by, bz, smem, stream, args_blob, len(args_blob)),
           f"launch {k.name}")
 
