@@ -277,6 +277,8 @@ class RowPass:
             stage_base = 0
             self.smem = (nst * cw + 64 + self.ring * cw) * 8
             self.G = min(M, 148)
+            if self.coop and (-(-N // self.G) > 64 or tpb % 64 or self.ring * cw < tpb):
+                self.coop = False  # fold slices are at most 64 columns
         else:
             self.ring = 0
             stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64

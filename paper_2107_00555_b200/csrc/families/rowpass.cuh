@@ -153,10 +153,27 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
   // cooperative launch (one column tile): after the grid barrier every CTA
   // folds a slice of the columns over the G partial rows in row order
   rp_grid_sync((unsigned *)a.w[7]);
-  for (b2_ll i = (b2_ll)blockIdx.x * RP_TPB + tid; i < RP_N; i += (b2_ll)gridDim.x * RP_TPB) {
+  {
+    // this CTA's column slice; its threads split the G partial rows into
+    // RP_TPB / 64 strided groups, combined in group order (deterministic)
+    constexpr int CS = (int)((RP_N + RP_G - 1) / RP_G);
+    constexpr int NP = RP_TPB / 64;
+    static_assert(CS <= 64, "column slice wider than 64");
+    double *part = red;  // reuse the reduction scratch (64 doubles) + ring
+    const int col = tid & 63, grp = tid >> 6;
+    const b2_ll i = (b2_ll)blockIdx.x * CS + col;
     double t = 0.0;
-    for (int g = 0; g < RP_G; ++g) t += __ldcg(ws + (b2_ll)g * RP_N + i);
-    rp_store_axpy(a, i, t);
+    if (col < CS && i < RP_N)
+      for (int g = grp; g < RP_G; g += NP) t += __ldcg(ws + (b2_ll)g * RP_N + i);
+    __syncthreads();
+    ring[tid] = t;
+    __syncthreads();
+    if (grp == 0 && col < CS && i < RP_N) {
+      double u = ring[col];
+      for (int q = 1; q < NP; ++q) u += ring[q * 64 + col];
+      rp_store_axpy(a, i, u);
+    }
+    (void)part;
   }
 #endif
 #endif
