@@ -11,7 +11,9 @@
 // running CTAs stream neighbouring rows; grid.y tiles columns in RP_CW chunks
 // whose v / acc slices live in shared memory; the next row is prefetched into
 // registers while the current row's dot is block-reduced.  Column partials go
-// to a workspace reduced by rp_finalize in a fixed order (deterministic).
+// to a workspace reduced by rp_finalize in a fixed order (deterministic);
+// with RP_COOP (cooperative launch, opt-in) the TMA variant folds them itself
+// after a grid barrier.
 //
 // The including translation unit defines RP_* constants, struct RpArgs and
 // the hooks rp_row_setup / rp_elem / rp_dot_vec / rp_coef / rp_store_dot.
