@@ -54,6 +54,7 @@ RED_THREADS = int(os.environ.get("B2_RED_THREADS", str(148 * 8192)))  # chunked-
 SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per chunk, small reductions (0: off)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
+PF_EVICT_LAST = os.environ.get("B2_PF_EVICT_LAST", "0") == "1"  # evict_last policy on march prefetches
 MARCH_PDL = os.environ.get("B2_MARCH_PDL", "1") == "1"  # march sweeps as programmatic dependent launches (heat 37.40 -> 37.24 ms)
 # ... small flat / reduce / scalar kernels, whose launch latency is a large
 # share of their time (nbody's per-step kernels: 5.32 -> 4.67 ms)
@@ -325,7 +326,7 @@ class _Gen:
                 f"        const b2_ll row = (z0 + zz) * st_{c}_0 + (y0 + yy) * st_{c}_1;",
                 f"        const b2_ll e0 = (row + x0) * {esz}LL, e1 = (row + x1 + 1) * {esz}LL;",
                 "        const b2_ll a0 = (base + e0) & ~15LL, a1 = (base + e1 + 15) & ~15LL;",
-                "        b2_prefetch_l2((const void *)a0, (unsigned)(a1 - a0));",
+                f"        b2_prefetch_l2{'_last' if PF_EVICT_LAST else ''}((const void *)a0, (unsigned)(a1 - a0));",
                 "      }",
                 "    }",
             ]

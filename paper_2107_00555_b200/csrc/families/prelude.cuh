@@ -22,6 +22,13 @@ __device__ __forceinline__ b2_ll b2_max_ll(b2_ll a, b2_ll b) { return a > b ? a 
 __device__ __forceinline__ void b2_prefetch_l2(const void *p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
+// ... with an L2 evict_last policy on the prefetched lines
+__device__ __forceinline__ void b2_prefetch_l2_last(const void *p, unsigned bytes) {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p),
+               "r"(bytes), "l"(pol) : "memory");
+}
 __device__ __forceinline__ b2_ll b2_abs_ll(b2_ll a) { return a < 0 ? -a : a; }
 __device__ __forceinline__ b2_ll b2_ipow(b2_ll a, b2_ll e) {
   b2_ll r = 1;
