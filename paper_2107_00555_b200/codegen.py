@@ -1419,7 +1419,12 @@ class _Gen:
             loop.append("    const b2_ll ty = rem % tiles_y; rem /= tiles_y;")
             for i in reversed(range(1, k - 2)):
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
-            loop.append("    const b2_ll tz = rem;")
+            if getattr(self, "reverse", False):
+                # march the plane chunks last-to-first: the previous sweep's
+                # final (still L2-resident) planes are read first
+                loop.append("    const b2_ll tz = tiles_z - 1 - rem;")
+            else:
+                loop.append("    const b2_ll tz = rem;")
             if (SLAB_PREFETCH if self.dyn0 else MARCH_PREFETCH) and k == 3:
                 loop += self._march_prefetch(vec, by, spec.align)
             loop.append(f"    const b2_ll i{y} = ty * {by} + threadIdx.y;")
@@ -1451,6 +1456,7 @@ class _Gen:
         npts = 1
         for r in self.const_ranges:
             npts *= r[2] if r is not None else 1 << 40
+        spec.reverse = bool(getattr(self, "reverse", False)) and mode == "march"
         spec.pdl = ((MARCH_PDL and mode == "march") or (TILE_PDL and mode == "tile2")
                     or (SMALL_PDL and mode in ("flat", "reduce", "scalar")
                         and npts <= SMALL_PDL_POINTS)) and not self.dyn0
@@ -1858,9 +1864,10 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
 
 
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
-             init_const: dict | None = None) -> KernelSpec:
+             init_const: dict | None = None, reverse: bool = False) -> KernelSpec:
     gen = _Gen(planner, group, shapes, name)
     gen.init_const = dict(init_const or {})
+    gen.reverse = reverse
     spec = gen.build()
     spec.params = list(group.params)
     # reduction targets (container, point key) -> (exclusive, C type), for

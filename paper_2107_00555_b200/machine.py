@@ -41,6 +41,7 @@ DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
 # a constant-fill map followed by a reduction over the same container starts
 # the reduction from the constant instead of launching the fill
 INIT_FUSION = os.environ.get("B2_INIT_FUSION", "1") == "1"
+SWEEP_ALTERNATE = os.environ.get("B2_SWEEP_ALTERNATE", "0") == "1"  # alternate march direction (slower: off)
 ZERO_SKIP = os.environ.get("B2_ZERO_SKIP", "1") == "1"  # skip zeroing fully overwritten transients
 FIN_PDL = os.environ.get("B2_FIN_PDL", "0") == "1"  # reduction fold kernels launched with PDL (neutral: off)
 
@@ -203,13 +204,15 @@ class GpuExecutor:
             reg.spec = spec
         self.init_skip: set[int] = set()
         fused_init = self._init_fusions() if INIT_FUSION else {}
+        reverse = self._reverse_sweeps() if SWEEP_ALTERNATE else set()
         for op in self.planner.all_ops:
             if op.idx in self.planner.in_region:
                 continue
             if isinstance(op, P.MapGroup):
                 name = f"b2_map_{self.g.name}_{op.idx}"
                 spec = codegen.generate(self.planner, op, self.buf.shape, name,
-                                        init_const=fused_init.get(op.idx))
+                                        init_const=fused_init.get(op.idx),
+                                        reverse=op.idx in reverse)
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
                 if FIN_PDL and getattr(spec, "red_fin", None):
                     # the fold kernel is a programmatic dependent launch
@@ -235,6 +238,25 @@ class GpuExecutor:
                 threads = codegen.MAX_BLOCKS * 256
                 self.scratch[n] = self.buf.alloc(per * threads)
                 self.buf.nbytes[n + "#scratch"] = per * threads
+
+    def _reverse_sweeps(self) -> set:
+        """Every second march sweep of a state chain walks its plane chunks
+        last-to-first, so it starts on the planes the previous sweep wrote
+        last (still in L2); heat_3d's A->B / B->A pair alternates direction."""
+        pl = self.planner
+        out = set()
+        for ops in pl.ops.values():
+            k = 0
+            for op in ops:
+                if not isinstance(op, P.MapGroup) or op.idx in pl.in_region:
+                    continue
+                spec = codegen.generate(pl, op, self.buf.shape, "probe")
+                if spec.mode != "march" or spec.dyn0:
+                    continue
+                if k % 2:
+                    out.add(op.idx)
+                k += 1
+        return out
 
     def _const_fill(self, op):
         """(X, literal) when map group ``op`` only stores one constant into
