@@ -473,7 +473,7 @@ class GpuExecutor:
         interior input values are never observed (heat_3d / jacobi_2d's B),
         so only the 2d boundary faces need to reach the device."""
         self.zero_skip = set()
-        if not self.capturable or self.planner.regions:
+        if not self.capturable:
             return set()
         first: dict = {}
         self._first_touch = first
@@ -486,11 +486,18 @@ class GpuExecutor:
             self._dry = False
             self._first_touch = None
         out = set()
+        # ops inside device loop regions are not walked by the dry run: only
+        # containers no region touches have a reliable first touch
+        in_reg = set()
+        for idx in self.planner.in_region:
+            in_reg |= self.planner.op_reads.get(idx, set()) | self.planner.op_writes.get(idx, set())
         for name, op in first.items():
             c = self.g.containers[name]
-            if (c.transient and c.lifetime != "persistent" and ZERO_SKIP
+            if (c.transient and c.lifetime != "persistent" and ZERO_SKIP and name not in in_reg
                     and self._overwrites(name, op)):
                 self.zero_skip.add(name)
+        if self.planner.regions:
+            return out  # (dead-on-entry inputs: region-free programs only)
         for name, op in first.items():
             c = self.g.containers[name]
             shape = self.buf.shape[name]
@@ -527,12 +534,16 @@ class GpuExecutor:
         if not shape:
             return False
         if isinstance(op, P.MapGroup):
-            if name in self.planner.op_reads.get(op.idx, set()):
-                return False
+            # sites are in program order (members, then tasklets): the first
+            # access is the point write; later ones may only re-read that
+            # same point (softmax's ex, summed right after it is stored)
             sites = [st for st in self.planner.sites.get(name, []) if st.op == op.idx]
-            if (len(sites) != 1 or not sites[0].is_write or sites[0].wcr is not None
+            if (not sites or not sites[0].is_write or sites[0].wcr is not None
                     or sites[0].depth != 0 or sites[0].point is None
                     or len(sites[0].point) != len(shape) or len(op.params) != len(shape)):
+                return False
+            if any(st.is_write or st.depth != 0 or st.point != sites[0].point
+                   for st in sites[1:]):
                 return False
             rng = [codegen._const_range(self.planner, r) for r in op.ranges]
             for d, (c0, co) in enumerate(sites[0].point):
