@@ -324,3 +324,27 @@ def test_init_fill_fusion_detected():
     ex._const_fill = machine.GpuExecutor._const_fill.__get__(ex)
     fused = machine.GpuExecutor._init_fusions(ex)
     assert fused == {1: {"acc": "0.0"}} and ex.init_skip == {0}
+
+
+@pytest.mark.parametrize("name,syms,cont,expect", [
+    ("softmax.raw", {"N": 2, "H": 3, "SM": 64}, "ex", True),     # point write, same-point re-read
+    ("atax.raw", {"M": 30, "N": 20}, "tmp0", True),               # full MATMUL output
+    ("softmax.raw", {"N": 2, "H": 3, "SM": 64}, "sm", False),     # WCR target: needs its zeros
+])
+def test_transient_overwrite_analysis(name, syms, cont, expect):
+    """machine.GpuExecutor._overwrites: a scope transient whose first op
+    writes every element before any read is not zeroed per call."""
+    from paper_2107_00555_b200 import machine, plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+    pl = P.Planner(g, syms).build()
+
+    class _Ex:
+        pass
+
+    ex = _Ex()
+    ex.planner, ex.buf, ex.bindings = pl, _Ex(), dict(syms)
+    ex.buf.shape = pl.shapes(syms)
+    first = next(op for op in pl.all_ops
+                 if cont in pl.op_reads.get(op.idx, set()) | pl.op_writes.get(op.idx, set()))
+    assert machine.GpuExecutor._overwrites(ex, cont, first) is expect
