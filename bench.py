@@ -13,8 +13,9 @@ program run (99 iterations x 2 fused 7-point sweeps) through the executor.
 ``value`` = algorithmic HBM bytes of the whole run / device time, inputs
 resident in HBM; ``e2e`` = the same metric through the public
 ``interpret(g, ctx)`` with pinned host inputs, H2D + D2H inside the timed
-region.  ``--impl reference`` times the reference's CPU path (the numpy port
-of evaluate_program, oracle/kernels_np.py) on a bounded sample.
+region.  ``--impl reference`` times the reference's own CPU path (the
+unmodified ``sdfgkit.frontend.evaluate_program`` installed under
+baseline/_ref) on a bounded sample of the same config (2 sweeps).
 """
 
 from __future__ import annotations
@@ -184,16 +185,60 @@ def cpu_sample(workload, syms, sweeps=2):
             f"(evaluate_program port, planes split over {th} threads)", th)
 
 
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_sample(workload, syms):
+    """The UNMODIFIED reference's own CPU path on a bounded sample: the
+    reference package installed under baseline/_ref (pip --target, see
+    DESIGN.md), ``sdfgkit.frontend.evaluate_program`` (pkg/src/sdfgkit/
+    frontend/oracle.py:37-70) on the same DSL program at the full config size
+    with TSTEPS=2 (exactly 2 sweeps; one evaluate_program call, input copies
+    included as the reference makes them).  Returns (GB/s algorithmic,
+    seconds, description, threads) or None when the package is absent."""
+    if not (REF_DIR / "sdfgkit").is_dir():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    from sdfgkit import frontend
+
+    prog_file = {"heat_3d": ROOT / "programs" / "heat_3d.dpy"}.get(workload)
+    if prog_file is None:  # the reference corpus program (copied there by build())
+        prog_file = REF_DIR / "corpus" / f"{workload}.dpy"
+        if not prog_file.exists():
+            return None
+    program = frontend.parse(prog_file.read_text())
+    N = syms["N"]
+    s2 = dict(syms, TSTEPS=2)
+    rng = np.random.default_rng(0)
+    shape = (N, N, N) if workload == "heat_3d" else (N, N)
+    inputs = {"A": rng.uniform(-1, 1, shape), "B": rng.uniform(-1, 1, shape)}
+    t = time.perf_counter()
+    frontend.evaluate_program(program, s2, inputs)
+    dt = time.perf_counter() - t
+    byts = 2 * (_heat_bytes(N) if workload == "heat_3d" else _jac_bytes(N))
+    blas = os.environ.get("OPENBLAS_NUM_THREADS", "unset")
+    return (byts / dt / 1e9, dt,
+            f"reference sdfgkit.frontend.evaluate_program (baseline/_ref, unmodified) on "
+            f"{prog_file.name} N={N} TSTEPS=2 = 2 sweeps; numpy elementwise ops are "
+            f"single-threaded (OPENBLAS_NUM_THREADS={blas}, unused here)", 1)
+
+
 def run_reference(args, W):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     syms = W["syms"]
-    for _ in range(args.warmup):
-        cpu_sample(args.workload, syms, 2)
+    kind = "reference"
+    sample = lambda: reference_sample(args.workload, syms)  # noqa: E731
+    if sample() is None:  # not installed: the numpy port (kind "port")
+        kind = "port"
+        sample = lambda: cpu_sample(args.workload, syms, 2)  # noqa: E731
+    for _ in range(max(0, args.warmup - 1)):
+        sample()
     vals, ts = [], []
     for _ in range(args.steps):
-        v, dt, desc, th = cpu_sample(args.workload, syms, 2)
+        v, dt, desc, th = sample()
         vals.append(v)
         ts.append(dt)
     value = float(np.median(vals))
@@ -203,7 +248,7 @@ def run_reference(args, W):
         "ms_per_step": 1e3 * float(np.median(ts)), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": W["desc"], "sample": desc},
-        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": th, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": th, "kind": kind,
                          "sample": desc},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -306,7 +351,13 @@ def run_ours(args, W):
     h2d = getattr(ex, "last_h2d_bytes", None) or sum(v.nbytes for v in host.values())
     d2h = sum(np.asarray(v).nbytes for v in out.values())
 
-    cpu_v, cpu_dt, cpu_desc, cpu_th = cpu_sample(args.workload, syms, 2)
+    port_v, port_dt, port_desc, port_th = cpu_sample(args.workload, syms, 2)
+    refs = reference_sample(args.workload, syms)
+    if refs is not None:
+        cpu_v, cpu_dt, cpu_desc, cpu_th = refs
+        cpu_kind = "reference"
+    else:
+        cpu_v, cpu_dt, cpu_desc, cpu_th, cpu_kind = port_v, port_dt, port_desc, port_th, "port"
 
     line = {
         "metric": metric_name(args.workload), "value": value, "unit": "GB/s", "n_gpus": 1,
@@ -321,8 +372,10 @@ def run_ours(args, W):
                      "traffic": traffic_from_profiles(args.workload), "kernel": name,
                      "launch_ms": avg_ms, "launches_per_step": nl, "step_share": step_share,
                      "bytes_per_launch": per_launch},
-        "cpu_baseline": {"value": cpu_v, "unit": "GB/s", "cores": cpu_th, "kind": "port",
+        "cpu_baseline": {"value": cpu_v, "unit": "GB/s", "cores": cpu_th, "kind": cpu_kind,
                          "sample": cpu_desc, "seconds": cpu_dt},
+        "cpu_baseline_port": {"value": port_v, "unit": "GB/s", "cores": port_th, "kind": "port",
+                              "sample": port_desc, "seconds": port_dt},
         "e2e": {"value": run_bytes / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3},
         "gpu_launches": (launches_per_step or nl) * args.steps,
