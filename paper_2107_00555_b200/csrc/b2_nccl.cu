@@ -136,10 +136,17 @@ extern "C" int b2_nccl_bcast(void *comm, void *buf, size_t bytes, int root, void
 
 extern "C" int b2_nccl_allreduce_f64(void *comm, double *buf, size_t count, int wcr,
                                      void *stream) {
+  int op;
+  switch (wcr) {  // Wcr.ADD / MUL / MIN / MAX (ir.py:72-91); anything else is an error
+    case B2_WCR_ADD: op = kNcclSum; break;
+    case B2_WCR_MUL: op = kNcclProd; break;
+    case B2_WCR_MIN: op = kNcclMin; break;
+    case B2_WCR_MAX: op = kNcclMax; break;
+    default:
+      return b2_fail(B2_ERR_UNSUPPORTED, "b2_nccl_allreduce_f64: unsupported wcr code %d", wcr);
+  }
   int rc = load();
   if (rc) return rc;
-  int op = wcr == B2_WCR_MUL ? kNcclProd
-                             : (wcr == B2_WCR_MIN ? kNcclMin : (wcr == B2_WCR_MAX ? kNcclMax : kNcclSum));
   return nccl_check(nc.allReduce(buf, buf, count, kNcclFloat64, op, comm, (cudaStream_t)stream),
                     "ncclAllReduce");
 }

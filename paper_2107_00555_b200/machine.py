@@ -31,7 +31,7 @@ from typing import Mapping
 
 import numpy as np
 
-from . import codegen, plan as P, runtime as rt, scalar, sdfg, symexpr
+from . import codegen, plan as P, runtime as rt, scalar, sdfg, symexpr, validate
 
 _NP = {"f64": np.float64, "i64": np.int64, "i32": np.int32, "bool": np.bool_}
 # upload only the boundary faces of inputs whose interior is dead on entry
@@ -603,6 +603,36 @@ class GpuExecutor:
             rt.check(L.b2_copy_view(ctypes.byref(dv), ctypes.byref(sv), 0, self.stream), "shell")
             off += f.size
         return host
+
+    def persistent_names(self) -> list:
+        return [n for n, c in self.g.containers.items()
+                if c.transient and c.lifetime == "persistent" and n in self.buf.ptr]
+
+    def load_persistent(self, persistent: dict) -> list:
+        """PERSISTENT transients live in the caller's ``ctx.persistent``
+        (interp.py:216-219): zeros the first time a context sees one, its
+        saved contents afterwards."""
+        keep = []
+        for name in self.persistent_names():
+            if name in persistent:
+                arr = np.asarray(persistent[name], dtype=_NP[self.g.containers[name].dtype])
+                if arr.size != self.buf.size[name]:
+                    raise InterpreterError(
+                        f"persistent '{name}' has shape {arr.shape}, descriptor says "
+                        f"{self.buf.shape[name]}")
+                keep.append(self.upload(name, arr.reshape(self.buf.shape[name])))
+            else:
+                self.zero(name)
+        return keep
+
+    def store_persistent(self, persistent: dict):
+        """Copy the PERSISTENT transients back into ``ctx.persistent``."""
+        names = self.persistent_names()
+        if not names:
+            return
+        for name in names:
+            persistent[name] = self.download(name)
+        self.sync()
 
     def zero_transients(self, first_call: bool):
         for name, c in self.g.containers.items():
@@ -1518,22 +1548,34 @@ def _ctx_parts(ctx):
 _CACHE_MAX = 32
 
 
+def _opt_key(options) -> tuple:
+    """The InterpOptions fields that change what an executor does."""
+    o = options or InterpOptions()
+    return (bool(getattr(o, "reverse_maps", False)),
+            int(getattr(o, "max_transitions", 10_000_000)),
+            bool(getattr(o, "skip_validation", False)))
+
+
 def get_executor(g, bindings: dict, options=None, device: int = 0) -> GpuExecutor:
-    """Executors are cached per (graph, bindings, device): by identity for
-    Graph objects, by a hash of the schema-v1 document otherwise."""
+    """Executors are cached per (graph, bindings, options, device): by
+    identity for Graph objects, by a hash of the schema-v1 document
+    otherwise."""
     if isinstance(g, sdfg.Graph):
         graph, fkey = g, ("obj", id(g))
     else:
         graph = sdfg.as_graph(g)
         fkey = ("doc", hashlib.sha1(json.dumps(graph.doc, sort_keys=True).encode()).hexdigest())
-    missing = graph.free_symbols() - set(bindings)
-    if missing:
-        raise InterpreterError(f"missing symbol bindings: {sorted(missing)}")
-    key = (fkey, tuple(sorted((k, int(v)) for k, v in bindings.items())), device)
+    key = (fkey, tuple(sorted((k, int(v)) for k, v in bindings.items())), _opt_key(options),
+           device)
     ex = _exec_cache.get(key)
     if ex is not None and (fkey[0] != "obj" or ex.g is graph):
         return ex
-    _validate(graph)
+    # Machine.prepare order (interp.py:184-191): validate, then symbols
+    if not getattr(options, "skip_validation", False):
+        _validate(graph)
+    missing = graph.free_symbols() - set(bindings)
+    if missing:
+        raise InterpreterError(f"missing symbol bindings: {sorted(missing)}")
     try:
         ex = GpuExecutor(graph, bindings, device=device, options=options)
     except P.PlanError:
@@ -1547,41 +1589,29 @@ def get_executor(g, bindings: dict, options=None, device: int = 0) -> GpuExecuto
 
 
 def _validate(g: sdfg.Graph):
-    labels = {s.label for s in g.states}
-    if g.start not in labels:
-        raise InterpreterError("graph does not validate: start state missing")
-    for t in g.transitions:
-        if t.src not in labels or t.dst not in labels:
-            raise InterpreterError("graph does not validate: dangling transition")
-    for st in g.states:
-        try:
-            st.scope_parents()
-        except sdfg.SchemaError as ex:
-            raise InterpreterError(f"graph does not validate: {ex}") from None
-        for e in st.edges:
-            if e.memlet is not None:
-                c = g.containers.get(e.memlet.container)
-                if c is None:
-                    raise InterpreterError(
-                        f"graph does not validate: unknown container '{e.memlet.container}'")
-                if len(e.memlet.subset) != len(c.shape):
-                    raise InterpreterError(
-                        f"graph does not validate: memlet rank mismatch on '{c.name}'")
-        for n in st.nodes:
-            if isinstance(n, sdfg.Access) and n.container not in g.containers:
-                raise InterpreterError(f"graph does not validate: unknown container '{n.container}'")
+    """ir.validate restated (validate.py); any error diagnostic fails the
+    run like Machine.prepare (interp.py:184-189)."""
+    try:
+        errs = validate.errors(g)
+    except (KeyError, ValueError, sdfg.SchemaError) as ex:
+        raise InterpreterError(f"graph does not validate: {ex}") from None
+    if errs:
+        raise InterpreterError("graph does not validate: " + "; ".join(d.message for d in errs))
 
 
 def interpret(g, ctx, options: InterpOptions | None = None) -> dict[str, np.ndarray]:
     """Execute the graph on the B200; returns the non-transient containers."""
     bindings, store, counters = _ctx_parts(ctx)
     ex = get_executor(g, bindings, options)
-    first = not getattr(ex, "_ran", False)
     keep = ex.prepare_inputs(store)
+    persistent = getattr(ctx, "persistent", None)
+    if persistent is None:
+        persistent = {}
+    keep += ex.load_persistent(persistent)
     c = Counters() if counters is not None else None
-    ex.run_device(first_call=first, counters=c)
-    ex._ran = True
+    ex.run_device(first_call=False, counters=c)
     out = ex.outputs(pinned=bool(getattr(options, "pinned_outputs", False)))
+    ex.store_persistent(persistent)
     del keep
     ex.check_flag()
     if counters is not None and c is not None:

@@ -348,3 +348,32 @@ def test_transient_overwrite_analysis(name, syms, cont, expect):
     first = next(op for op in pl.all_ops
                  if cont in pl.op_reads.get(op.idx, set()) | pl.op_writes.get(op.idx, set()))
     assert machine.GpuExecutor._overwrites(ex, cont, first) is expect
+
+
+@pytest.mark.parametrize("name,syms,expect", [
+    # mx is touched by a device loop region (the max nest): never skipped;
+    # ex is written point-wise then re-read at the same point: skipped;
+    # sm is a WCR target that needs its zeros
+    ("softmax.raw", {"N": 2, "H": 3, "SM": 64}, {"ex"}),
+    # nbody: tmp0..2 (vel/pos update temporaries) are written point-wise
+    # over their whole [0:N-1, 0:2] box before any read: skipped
+    ("nbody.raw", {"N": 9, "NT": 2}, {"tmp0", "tmp1", "tmp2"}),
+])
+def test_zero_skip_set_from_dry_run(name, syms, expect):
+    """run the real dry-run analysis (_dead_on_entry) and pin the
+    exact zero-skip set, so region-touched containers stay zeroed."""
+    from paper_2107_00555_b200 import machine, plan as P, sdfg
+
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+    ex = object.__new__(machine.GpuExecutor)
+    ex.g, ex.bindings = g, dict(syms)
+    ex.opt = machine.InterpOptions()
+    ex.planner = P.Planner(g, ex.bindings).build()
+    ex.planner.dynamic_p0 = False
+    ex.comm, ex.capturable, ex.device_branching = None, True, False
+    ex.buf = machine._Buffers()
+    ex.buf.shape = ex.planner.shapes(syms)
+    ex._exec_nested = lambda op, sym, counters, dry=False: None
+    ex._dead_on_entry()
+    assert ex.zero_skip == expect
+    assert "mx" not in ex.zero_skip

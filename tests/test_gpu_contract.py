@@ -207,3 +207,85 @@ def test_device_branches_match_host_branches(monkeypatch, s0):
     for (xa, sa, ca), (xb, sb, cb) in zip(res[True], res[False]):
         assert np.array_equal(xa, xb) and sa == sb
         assert ca == cb
+
+
+def _azimint_inputs(seed, syms):
+    from paper_2107_00555_b200 import symexpr
+
+    g = _g("azimint_naive.auto")
+    rng = np.random.default_rng(seed)
+    out = {}
+    for n, c in g.containers.items():
+        if not c.transient:
+            shape = tuple(symexpr.evaluate(d, syms) for d in c.shape)
+            out[n] = rng.uniform(-1, 1, shape) if shape else float(rng.uniform(0.5, 1.5))
+    return out
+
+
+def test_persistent_transients_per_context():
+    """PERSISTENT transients belong to ctx.persistent
+    (interp.py:216-219).  Two fresh contexts on the SAME Graph object each
+    start from zeros; azimint_naive.auto's acc/cnt take only WCR-add writes,
+    so stale values would show."""
+    from oracle import interp_ref
+    from paper_2107_00555_b200 import interpret
+
+    g = _g("azimint_naive.auto")
+    syms = {"N": 301, "NPT": 7}
+    for seed in (0, 1):
+        inputs = _azimint_inputs(seed, syms)
+        ref = interp_ref.interpret(g, syms, {k: np.array(v) for k, v in inputs.items()})
+        ctx = _ctx(syms, inputs)
+        out = interpret(g, ctx)
+        for k in ref:
+            assert np.allclose(out[k], ref[k], rtol=1e-12, atol=1e-12, equal_nan=True), (seed, k)
+        assert set(ctx.persistent) == {"acc", "cnt"}
+
+
+def test_persistent_transients_kept_in_same_context():
+    """The same context twice: the second run starts from the persistent
+    values the first left in ctx.persistent (the reference's semantics),
+    and ctx.persistent holds the oracle's persistent arrays."""
+    from oracle import interp_ref
+    from paper_2107_00555_b200 import interpret
+
+    g = _g("azimint_naive.auto")
+    syms = {"N": 301, "NPT": 7}
+    inputs = _azimint_inputs(5, syms)
+    pers = {}
+    interp_ref.interpret(g, syms, {k: np.array(v) for k, v in inputs.items()}, persistent=pers)
+    ref = interp_ref.interpret(g, syms, {k: np.array(v) for k, v in inputs.items()},
+                               persistent=pers)
+    ctx = _ctx(syms, inputs)
+    interpret(g, ctx)
+    out = interpret(g, ctx)
+    for k in ref:
+        assert np.allclose(out[k], ref[k], rtol=1e-12, atol=1e-12, equal_nan=True), k
+    for k in ("acc", "cnt"):
+        assert np.allclose(ctx.persistent[k], pers[k], rtol=1e-12, atol=1e-12), k
+
+
+def test_options_are_part_of_executor_key():
+    from paper_2107_00555_b200 import InterpOptions
+    from paper_2107_00555_b200.machine import get_executor
+
+    g = _g("gemm.raw")
+    b = {"NI": 4, "NJ": 6, "NK": 8}
+    e1 = get_executor(g, b, InterpOptions())
+    e2 = get_executor(g, b, InterpOptions(skip_validation=True))
+    e3 = get_executor(g, b, InterpOptions(max_transitions=5))
+    assert e1 is get_executor(g, b, None)
+    assert len({id(e1), id(e2), id(e3)}) == 3
+
+
+def test_skip_validation_runs_racy_graph():
+    """With skip_validation the reference executes the racy graph (both
+    unordered writes store x into all of A); so do we."""
+    import json
+
+    from paper_2107_00555_b200 import InterpOptions, interpret
+
+    g = json.loads((GOLDEN / "validation_cases.json").read_text())["race_whole"]["graph"]
+    out = interpret(g, _ctx({"N": 8}, {"A": np.zeros(8), "x": 2.5}),
+                    InterpOptions(skip_validation=True))
+    assert np.array_equal(out["A"], np.full(8, 2.5))
