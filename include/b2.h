@@ -148,6 +148,13 @@ B2_API int b2_capture_body_end(void *body_stream);
 B2_API int b2_counters_add(long long *dev, long long a0, long long a1, long long a2, long long a3,
                     void *stream);
 
+/* TMA descriptor (CUtensorMap, 128 bytes written to out128) for a row-major
+ * f64 tensor: dims / box innermost first, no swizzle, zeros outside.  Used by
+ * the tma3 stencil sweeps (map scopes of interp.py:420-441 whose inputs are
+ * read at constant offsets), passed ahead of the kernel's argument words. */
+B2_API int b2_tensor_map_f64(void *out128, const void *base, int rank, const uint64_t *dims,
+                             const uint32_t *box);
+
 /* ---- ahead-of-time library kernels ------------------------------------- */
 /* dst[flat] (wcr)= convert(src[flat]) over the row-major flattening of both
  * views (equal element counts).  Implements access->access copies with
@@ -163,6 +170,12 @@ B2_API int b2_gemm_f64(int64_t M, int64_t N, int64_t K, const double *A, int64_t
 B2_API int b2_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa, int64_t csa,
                 const float *B, int64_t rsb, int64_t csb, float *C, int64_t rsc,
                 int64_t csc, int wcr, void *stream);
+/* f32 GEMM, f64 products and accumulation (DMMA), one rounding to f32:
+ * element-wise within rtol 1e-5 of the f64 product at any K.  Row-major
+ * A (M x K, row stride rsa), B (K x N), C (M x N); wcr NONE or ADD. */
+B2_API int b2_gemm_f32_f64acc(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa,
+                              const float *B, int64_t rsb, float *C, int64_t rsc, int wcr,
+                              void *stream);
 /* out (wcr)= op-reduce of `in` over the dims flagged in axes_mask (bit d),
  * output enumerated row-major over the kept dims (ufunc.reduce semantics). */
 B2_API int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axes_mask, int op, int wcr,

@@ -245,13 +245,26 @@ def nbody(mass, pos, vel, acc, E, G, softening, dt, NT):
     return {"mass": mass, "pos": pos, "vel": vel, "acc": acc, "E": E}
 
 
+_exp_ufunc = np.frompyfunc(math.exp, 1, 1)
+
+
+def _math_exp(a):
+    out = np.empty_like(a)
+    flat, dst = a.reshape(-1), out.reshape(-1)
+    for s in range(0, flat.size, 1 << 22):  # chunked: bounded object temporaries
+        dst[s:s + (1 << 22)] = _exp_ufunc(flat[s:s + (1 << 22)]).astype(np.float64)
+    return out
+
+
 def softmax(x, out):
     """programs/softmax.dpy: row max by a sequential scan, exp(x - max), row
     sum by WCR in l order, divide."""
     mx = x[..., 0].copy()
     for l in range(1, x.shape[-1]):
         mx = np.maximum(mx, x[..., l]) if False else np.where(x[..., l] > mx, x[..., l], mx)
-    ex = np.exp(x - mx[..., None])
+    # exp is math.exp per element in the reference (oracle.py:23, the map
+    # body runs per point); numpy's vectorised exp can differ by an ulp
+    ex = _math_exp(x - mx[..., None])
     sm = np.zeros(x.shape[:-1])
     for l in range(x.shape[-1]):
         sm = sm + ex[..., l]

@@ -34,6 +34,11 @@ MAX_CW = 8192
 RP_COOP = os.environ.get("B2_RP_COOP", "0") == "1"  # fold inside the row pass (grid barrier)
 RP_PDL = os.environ.get("B2_RP_PDL", "0") == "1"  # fold kernel as a programmatic dependent launch (neutral: off)
 TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpass.cuh)
+# compensated (Dot2 / double-double) sums in the row pass (rowpass.cuh
+# RP_COMP): ~17x closer to the exact result (atax 8000^2: 3.6e-14 vs 6.3e-13
+# rel_err against an 80-bit evaluation; the reference's BLAS: 3.5e-12) but
+# FP64-issue bound (atax 0.171 vs 0.092 ms), so opt-in
+RP_COMP = os.environ.get("B2_RP_COMP", "0") == "1"
 SMEM_BUDGET = 220 * 1024
 
 
@@ -263,7 +268,11 @@ class RowPass:
         # TMA row ring when every row slice is a 16-byte aligned, 16-byte
         # multiple (1-D bulk copies); else the register-prefetch kernel
         nst = len(self.staged)
-        ring_s = (SMEM_BUDGET // 8 - nst * cw - 64) // cw if cw else 0
+        red = 128 if RP_COMP else 64
+        # compensated dot + axpy: the dot vector moves to shared memory
+        self.vsmem = RP_COMP and dot is not None and axpy is not None
+        vs = cw if self.vsmem else 0
+        ring_s = (SMEM_BUDGET // 8 - nst * cw - red - vs) // cw if cw else 0
         off = self.R[1]
         # (gemver's prologue + write-back pass measured faster with the
         # register-prefetch kernel at 2-3 CTAs/SM: 184 vs 254 us)
@@ -271,17 +280,18 @@ class RowPass:
                     and N % 2 == 0 and cw % 2 == 0 and ring_s >= 2)
         # in-kernel fold after a grid barrier (cooperative launch): TMA
         # variant (one CTA per SM, all co-resident), one column tile
-        self.coop = RP_COOP and self.tma and axpy is not None and self.ctiles == 1
+        self.coop = (RP_COOP and not RP_COMP and self.tma and axpy is not None
+                     and self.ctiles == 1)
         if self.tma:
             self.ring = min(4, ring_s)
             stage_base = 0
-            self.smem = (nst * cw + 64 + self.ring * cw) * 8
+            self.smem = (nst * cw + red + vs + self.ring * cw) * 8
             self.G = min(M, 148)
             if self.coop and (-(-N // self.G) > 64 or tpb % 64 or self.ring * cw < tpb):
                 self.coop = False  # fold slices are at most 64 columns
         else:
             self.ring = 0
-            stage_base = (cw if axpy else 0) + (cw if dot else 0) + 64
+            stage_base = (cw if axpy else 0) * (2 if RP_COMP else 1) + (cw if dot else 0) + red
             smem_doubles = stage_base + cw * nst
             self.smem = smem_doubles * 8
             est_regs = 4 * kpt + 40  # x / xn double arrays + addressing
@@ -297,7 +307,8 @@ class RowPass:
                      ("RP_PROLOGUE", int(self.prologue is not None)),
                      ("RP_WRITEBACK", int(self.prologue is not None)),
                      ("RP_TMA", int(self.tma)), ("RP_S", max(1, self.ring)),
-                     ("RP_COOP", int(self.coop)),
+                     ("RP_COOP", int(self.coop)), ("RP_COMP", int(RP_COMP)),
+                     ("RP_VSMEM", int(self.tma and self.vsmem)),
                      ("RP_NSTAGED", nst)):
             L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")
         nbase = 8
@@ -375,7 +386,9 @@ class RowPass:
             src = "#undef B2_NO_PDL\n" + src
         self.kmain = rt.get_kernel(src, f"b2_rp_{name}", max_smem=self.smem)
         self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
-        self.ws_axpy = ex.buf.alloc(max(8, self.G * self.N * 8)) if self.axpy is not None else 0
+        nws = 2 if RP_COMP else 1  # hi (+ lo) column partials
+        self.ws_axpy = (ex.buf.alloc(max(8, nws * self.G * self.N * 8))
+                        if self.axpy is not None else 0)
         self.ws_dot = ex.buf.alloc(max(8, self.ctiles * self.M * 8)) if self.dot is not None else 0
         self.bar = 0
         if self.coop:  # grid-barrier state (count, sense), zero once

@@ -68,6 +68,17 @@ ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowr
 ROWRED_HOIST = os.environ.get("B2_ROWRED_HOIST", "0") == "1"  # issue a lane's row loads first (slower: off)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
 STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
+# 3-D stencil sweeps through a TMA plane ring (cp.async.bulk.tensor.3d into
+# shared memory, mbarrier-tracked, persistent balanced grid): the tma3 mode
+# (measured: heat_3d N=400 39.3 ms vs 37.3 for march at the best geometry
+# below — bitwise equal, not the default)
+TMA3 = os.environ.get("B2_TMA3", "0") == "1"
+TMA3_CTAS = int(os.environ.get("B2_TMA3_CTAS", "1"))  # resident CTAs per SM (grid = 148 x this)
+TMA3_PREF = int(os.environ.get("B2_TMA3_PREF", "2"))  # planes in flight beyond the stencil window
+TMA3_TJ = int(os.environ.get("B2_TMA3_TJ", "16"))  # tile rows (a multiple of the consumer warps)
+TMA3_L2PF = int(os.environ.get("B2_TMA3_L2PF", "0"))  # planes L2-prefetched ahead of the ring
+TMA3_CHUNK = int(os.environ.get("B2_TMA3_CHUNK", "32"))  # planes per CTA (0: persistent balanced grid)
+TMA3_CW = int(os.environ.get("B2_TMA3_CW", "8"))  # consumer warps per CTA (+1 producer warp)
 
 
 class KernelSpec:
@@ -90,6 +101,9 @@ class KernelSpec:
         self.dyn0 = False  # range of the first parameter is a runtime argument
         self.align = 0  # elements the innermost tile origin is shifted down by
         self.kernel = None  # runtime.Kernel
+        self.tmaps: list[tuple] = []  # (container, box (inner..outer)) TMA maps ahead of the args
+        self.smem = 0  # dynamic shared memory bytes
+        self.grid_cap = 0  # tma3: persistent grid size
 
     def arg_index(self, desc) -> int:
         try:
@@ -706,6 +720,171 @@ class _Gen:
         L.append("  }")
         return L
 
+    def _tma3_loop(self, reg_decls, body: list) -> list:
+        """tma3 mode (3-D sweeps whose read-only inputs are read at constant
+        offsets within +-1): each CTA of a persistent, balanced grid owns a
+        contiguous run of (tile, plane) units — tiles of T3_TK x T3_TJ
+        points over dims (1, 2), planes along dim 0 — and marches it.
+
+        Warp-specialised pipeline: one producer warp streams every plane of
+        every staged input into shared memory ONCE, as one
+        cp.async.bulk.tensor.3d box (tile + halo, zero-filled outside the
+        container), into a ring of T3_S slots; ``full[s]`` (expect_tx = the
+        boxes' bytes) tells the consumer warps a slot has landed, ``empty[s]``
+        (one arrival per consumer warp) tells the producer it may be
+        refilled.  Consumer warps compute their rows of each plane from the
+        window of span+1 slots (the tasklet chain unchanged, same op order as
+        every other mode: bitwise equal) and store straight to HBM; no
+        CTA-wide barrier in the steady state."""
+        grp = self.group
+        spec = self.spec
+        L: list[str] = []
+        st0 = next(iter(self.stencil.values()))
+        mins, maxs = st0["min"], st0["max"]
+        span = maxs[0] - mins[0]
+        halo_j = maxs[1] - mins[1]
+        halo_k = maxs[2] - mins[2]
+        rl1, rl2 = self.const_ranges[1][2], self.const_ranges[2][2]
+        ntx = -(-rl2 // 64)
+        tk = -(-rl2 // ntx)
+        # box rows start on 32-byte DRAM sectors (tile width a multiple of 4)
+        # and are a 16-byte multiple long (TMA)
+        tk = -(-tk // 4) * 4
+        if (tk + halo_k) % 2:
+            tk += 1
+        tk = min(tk, 64)
+        ntx = -(-rl2 // tk)
+        cw = spec.block[1] - 1  # consumer warps (the last warp produces)
+        tj = max(cw, min(TMA3_TJ // cw * cw, -(-rl1 // cw) * cw))
+        sk, sj = tk + halo_k, tj + halo_j
+        slot = -(-(sk * sj * 8) // 128) * 128 // 8  # doubles per slot, 128-B aligned
+        S = span + 1 + TMA3_PREF
+        conts = list(self.stencil)
+        spec.tmaps = [(c, (sk, sj, 1)) for c in conts]
+        spec.smem = len(conts) * S * slot * 8
+        nty = -(-rl1 // tj)
+        rl0 = self.const_ranges[0][2]
+        units = ntx * nty * rl0
+        if TMA3_CHUNK:
+            # one CTA per (tile, run of planes), tiles fastest: the hardware
+            # scheduler balances the SMs and a chunk's first (halo) planes
+            # were read by the previous wave moments ago (L2 hits)
+            nch = -(-rl0 // TMA3_CHUNK)
+            chunk = -(-rl0 // nch)
+            spec.grid_cap = ntx * nty * nch
+        else:
+            chunk = 0
+            spec.grid_cap = max(1, min(units, 148 * TMA3_CTAS))
+        box_bytes = sk * sj * 8 * len(conts)
+        L.append(f"  constexpr int T3_S = {S}, T3_SK = {sk}, T3_SLOT = {slot}, T3_TK = {tk}, "
+                 f"T3_CW = {cw};")
+        L.append(f"  constexpr b2_ll T3_NTX = {ntx}, T3_NT = {ntx * nty};")
+        L.append(f"  constexpr b2_ll T3_W = T3_NT * rl0;")
+        L.append("  extern __shared__ __align__(1024) double t3_smem[];")
+        L.append("  __shared__ __align__(8) unsigned long long t3_full[T3_S], t3_empty[T3_S];")
+        for i, c in enumerate(conts):
+            L.append(f"  const double *tsm_{c} = t3_smem + {i} * T3_S * T3_SLOT;")
+        L.append("  if (threadIdx.y == 0 && threadIdx.x == 0) {")
+        L.append("    for (int q = 0; q < T3_S; ++q) {")
+        L.append("      b2_mbar_init(&t3_full[q], 1);")
+        L.append("      b2_mbar_init(&t3_empty[q], T3_CW);")
+        L.append("    }")
+        L.append("  }")
+        L.append("  __syncthreads();")
+        if chunk:
+            L.append("  const b2_ll t3_tile = blockIdx.x % T3_NT, t3_ch = blockIdx.x / T3_NT;")
+            L.append(f"  const b2_ll u0 = t3_tile * rl0 + t3_ch * {chunk};")
+            L.append(f"  const b2_ll uend = t3_tile * rl0 + ((t3_ch + 1) * {chunk} < rl0 ? "
+                     f"(t3_ch + 1) * {chunk} : rl0);")
+        else:
+            L.append("  const b2_ll u0 = (b2_ll)blockIdx.x * T3_W / gridDim.x;")
+            L.append("  const b2_ll uend = ((b2_ll)blockIdx.x + 1) * T3_W / gridDim.x;")
+        # ---- producer warp
+        L.append("  if (threadIdx.y == T3_CW) {")
+        L.append("    if (threadIdx.x == 0) {")
+        for i in range(len(conts)):
+            L.append(f'      asm volatile("prefetch.tensormap [%0];" ::"l"((unsigned long long)&a.tm[{i}]) : "memory");')
+        L.append("      unsigned t = 0;")
+        L.append("      for (b2_ll u = u0; u < uend;) {")
+        L.append("        const b2_ll tile = u / rl0, i_start = u % rl0;")
+        L.append("        const b2_ll n_it = ((rl0 < i_start + (uend - u)) ? rl0 : i_start + (uend - u)) - i_start;")
+        L.append(f"        const b2_ll kx0 = (tile % T3_NTX) * T3_TK, jy0 = (tile / T3_NTX) * {tj};")
+        L.append(f"        const int g0 = (int)(rb0 + i_start + ({mins[0]})), gj = (int)(rb1 + jy0 + ({mins[1]})), "
+                 f"gk = (int)(rb2 + kx0 + ({mins[2]}));")
+        if TMA3_L2PF:
+            # L2 prefetch of the planes ahead of the ring (no shared memory:
+            # the ring's loads then hit L2)
+            L.append(f"        for (int q = 0; q < {TMA3_L2PF} && q < n_it + {span}; ++q) {{")
+            for i in range(len(conts)):
+                L.append("          asm volatile(\"cp.async.bulk.prefetch.tensor.3d.L2.global.tile "
+                         f"[%0, {{%1, %2, %3}}];\" :: \"l\"((unsigned long long)&a.tm[{i}]), "
+                         "\"r\"(gk), \"r\"(gj), \"r\"(g0 + q) : \"memory\");")
+            L.append("        }")
+        L.append(f"        for (int q = 0; q < n_it + {span}; ++q, ++t) {{")
+        L.append("          const unsigned s = t % T3_S;")
+        if TMA3_L2PF:
+            L.append(f"          if (q + {TMA3_L2PF} < n_it + {span}) {{")
+            for i in range(len(conts)):
+                L.append("            asm volatile(\"cp.async.bulk.prefetch.tensor.3d.L2.global.tile "
+                         f"[%0, {{%1, %2, %3}}];\" :: \"l\"((unsigned long long)&a.tm[{i}]), "
+                         f"\"r\"(gk), \"r\"(gj), \"r\"(g0 + q + {TMA3_L2PF}) : \"memory\");")
+            L.append("          }")
+        L.append("          b2_mbar_wait(&t3_empty[s], ((t / T3_S) & 1u) ^ 1u);")
+        L.append("          const unsigned fb = (unsigned)__cvta_generic_to_shared(&t3_full[s]);")
+        L.append(f'          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), '
+                 f'"r"({box_bytes}u) : "memory");')
+        for i, c in enumerate(conts):
+            L.append("          asm volatile(\"cp.async.bulk.tensor.3d.shared::cluster.global.tile."
+                     "mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\" "
+                     f":: \"r\"((unsigned)__cvta_generic_to_shared(tsm_{c} + s * T3_SLOT)), "
+                     f"\"l\"((unsigned long long)&a.tm[{i}]), \"r\"(gk), \"r\"(gj), "
+                     "\"r\"(g0 + q), \"r\"(fb) : \"memory\");")
+        L.append("        }")
+        L.append("        u += n_it;")
+        L.append("      }")
+        L.append("    }")
+        L.append("  } else {")
+        # ---- consumer warps
+        L.append("    unsigned t = 0;")
+        L.append("    for (b2_ll u = u0; u < uend;) {")
+        L.append("      const b2_ll tile = u / rl0, i_start = u % rl0;")
+        L.append("      const b2_ll n_it = ((rl0 < i_start + (uend - u)) ? rl0 : i_start + (uend - u)) - i_start;")
+        L.append(f"      const b2_ll kx0 = (tile % T3_NTX) * T3_TK, jy0 = (tile / T3_NTX) * {tj};")
+        L.append("      for (b2_ll it = 0; it < n_it; ++it) {")
+        L.append(f"        for (unsigned w = (it == 0 ? t : t + {span}); w <= t + {span}; ++w)")
+        L.append("          b2_mbar_wait(&t3_full[w % T3_S], (w / T3_S) & 1u);")
+        for o in range(span + 1):
+            L.append(f"        const int sl_{o} = (int)((t + {o}) % T3_S) * T3_SLOT;")
+        L.append(f"        const b2_ll p_{grp.params[0]} = rb0 + i_start + it;")
+        L.append("#pragma unroll")
+        L.append(f"        for (int r = 0; r < {tj // cw}; ++r) {{")
+        L.append(f"        const int ly = threadIdx.y + {cw} * r;")
+        L.append(f"        if (jy0 + ly >= {rl1}LL) break;")
+        L.append(f"        const b2_ll p_{grp.params[1]} = rb1 + jy0 + ly;")
+        L.append("#pragma unroll")
+        L.append("        for (int v = 0; v < 2; ++v) {")
+        L.append("          const int lx = threadIdx.x + 32 * v;")
+        L.append(f"          if (lx >= T3_TK || kx0 + lx >= {rl2}LL) break;")
+        L.append(f"          const b2_ll p_{grp.params[2]} = rb2 + kx0 + lx;")
+        L += reg_decls(10)
+        L += ["        " + ln for ln in body]
+        L.append("        }")
+        L.append("        }")
+        # release the oldest slot of the window (and at the end of the run
+        # of planes, the span slots above it too)
+        L.append("        __syncwarp();")
+        L.append(f"        const unsigned rel = (it + 1 == n_it) ? {span} + 1u : 1u;")
+        L.append("        if (threadIdx.x == 0)")
+        L.append("          for (unsigned q = 0; q < rel; ++q)")
+        L.append("            asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" ::\"r\"("
+                 "(unsigned)__cvta_generic_to_shared(&t3_empty[(t + q) % T3_S])) : \"memory\");")
+        L.append("        t += rel;")
+        L.append("      }")
+        L.append("      u += n_it;")
+        L.append("    }")
+        L.append("  }")
+        return L
+
     def _stencil_offsets(self, m: sdfg.Memlet, env: dict) -> tuple:
         offs = []
         for d, (b, _, _) in enumerate(m.subset):
@@ -826,6 +1005,19 @@ class _Gen:
         if pl == "colstage":  # staged column vector (rowpass prologue)
             self.spec.arg_index(("ptr", m.container))
             return f"rp_smem[{self.colstage[m.container]} + jl]", t
+        if depth == 0 and m.container in self.stencil and self.spec.mode == "tma3":
+            self.spec.checks.append((m.container, m.subset, env))
+            offs = self._stencil_offsets(m, env)
+            key = (m.container, offs)
+            hit = self.cse.get(key)
+            if hit is None:
+                st = self.stencil[m.container]
+                hit = self.fresh("sm")
+                self.emit(f"const double {hit} = tsm_{m.container}[sl_{offs[0] - st['min'][0]} + "
+                          f"(ly + {offs[1] - st['min'][1]}) * T3_SK + "
+                          f"lx + {offs[2] - st['min'][2]}];")
+                self.cse[key] = hit
+            return hit, t
         if depth == 0 and m.container in self.stencil:
             self.spec.checks.append((m.container, m.subset, env))
             offs = self._stencil_offsets(m, env)
@@ -1095,6 +1287,15 @@ class _Gen:
             if (mode == "tile2" and k == 3 and self.const_ranges[0] is not None
                     and self.const_ranges[0][2] >= 16):
                 mode = "march"  # measured best for 3-D sweeps (heat_3d: 207 us vs 247 tile2)
+        if (mode == "march" and TMA3 and not getattr(self.pl, "dynamic_p0", False)
+                and all(r is not None and r[1] == 1 for r in self.const_ranges)
+                and all(r[2] >= 8 for r in self.const_ranges)):
+            st = self._stencil_analysis()
+            if st and all(self.g.containers[c].dtype == "f64" for c in st):
+                sts = next(iter(st.values()))
+                if all(sts["max"][d] - sts["min"][d] <= 2 for d in range(3)):
+                    self.stencil = st
+                    mode = "tma3"
         if (mode in ("tile2", "flat", "march") and k == 3 and STENCIL_MODE
                 and all(r is not None and r[1] == 1 for r in self.const_ranges)
                 and all(r[2] >= 8 for r in self.const_ranges)):
@@ -1109,7 +1310,7 @@ class _Gen:
                 pass
             elif force != "tile2" or k >= 2:
                 mode = force
-        if mode != "stencil":
+        if mode not in ("stencil", "tma3"):
             self.stencil = {}
         if mode in ("flat", "tile2", "march") and REDUCE_MODE:
             rp = self._reduction_plan()
@@ -1168,6 +1369,8 @@ class _Gen:
         elif mode == "stencil":
             vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
                 (2 if self.const_ranges[-1][2] >= 1024 else 1)
+        elif mode == "tma3":
+            vec = 2  # points per thread along the row (tile width <= 64)
         elif mode == "flat" and all(r is not None for r in self.const_ranges):
             total = 1
             for r in self.const_ranges:
@@ -1184,7 +1387,7 @@ class _Gen:
             spec.align = lastr[0] % max(1, 128 // esz)
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, TILE_BY, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
-                      "rowred": (256, 1, 1),
+                      "rowred": (256, 1, 1), "tma3": (32, TMA3_CW + 1, 1),
                       "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -1359,6 +1562,8 @@ class _Gen:
             loop.append("  }")
         elif mode == "stencil":
             loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
+        elif mode == "tma3":
+            loop += self._tma3_loop(reg_decls, shift(body, -2))
         elif mode == "reduce":
             loop += self._reduce_loop(self.red_R, self.red_pout, reg_decls, shift(body, -2))
         elif mode == "rowred":
@@ -1450,14 +1655,19 @@ class _Gen:
                 loop += vloop(hdr)
             loop.append("  }")
         src = [f"// generated by paper_2107_00555_b200.codegen for state "
-               f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}",
-               "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))]
+               f"'{grp.state.label}', group of {len(grp.members)} scope(s), mode {mode}, vec {vec}"]
+        if spec.tmaps:
+            src.append("struct __align__(64) B2TMap { unsigned long long v[16]; };")
+            src.append("struct B2Args { B2TMap tm[%d]; long long w[%d]; };"
+                       % (len(spec.tmaps), max(1, len(spec.args))))
+        else:
+            src.append("struct B2Args { long long w[%d]; };" % max(1, len(spec.args)))
         fin = self._reduce_fin(pro) if mode == "reduce" and getattr(spec, "red_fin", None) else []
         npts = 1
         for r in self.const_ranges:
             npts *= r[2] if r is not None else 1 << 40
         spec.reverse = bool(getattr(self, "reverse", False)) and mode == "march"
-        spec.pdl = ((MARCH_PDL and mode == "march") or (TILE_PDL and mode == "tile2")
+        spec.pdl = ((MARCH_PDL and mode in ("march", "tma3")) or (TILE_PDL and mode == "tile2")
                     or (SMALL_PDL and mode in ("flat", "reduce", "scalar")
                         and npts <= SMALL_PDL_POINTS)) and not self.dyn0
         if spec.pdl:
@@ -1879,8 +2089,14 @@ def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
                 (t["exclusive"], t["ct"])]
         spec.red_points = list(gen.red_targets)
     # args block decoded positionally; fix the struct size after all args known
-    spec.source = spec.source.replace(
-        spec.source.splitlines()[1], "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)))
+    lines = spec.source.split("\n")
+    k = next(i for i, ln in enumerate(lines) if ln.startswith("struct B2Args"))
+    if spec.tmaps:
+        lines[k] = "struct B2Args { B2TMap tm[%d]; long long w[%d]; };" % (
+            len(spec.tmaps), max(1, len(spec.args)))
+    else:
+        lines[k] = "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))
+    spec.source = "\n".join(lines)
     return spec
 
 
@@ -1915,6 +2131,8 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
     if spec.mode in ("reduce", "rowred"):
         n = getattr(spec, "red_threads", 1)
         return (max(1, min(-(-n // 256), MAX_BLOCKS * 8)), 1, 1), (256, 1, 1)
+    if spec.mode == "tma3":
+        return (spec.grid_cap, 1, 1), spec.block
     if spec.mode == "stencil":
         tk = (32 if k == 3 else 256) * spec.vec
         nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
@@ -1964,4 +2182,22 @@ def pack_args(spec: KernelSpec, env: dict, rvals, ptrs: dict, strides: dict, siz
             raise AssertionError(d)
     if not vals:
         vals = [0]
-    return struct.pack(f"<{len(vals)}q", *[v if v < (1 << 63) else v - (1 << 64) for v in vals])
+    blob = struct.pack(f"<{len(vals)}q", *[v if v < (1 << 63) else v - (1 << 64) for v in vals])
+    if spec.tmaps:
+        from . import runtime as rt
+
+        maps = b"".join(rt.tensor_map_f64(scratch[c] if c in scratch else ptrs[c],
+                                          strides_shape(strides[c], sizes[c]), box)
+                        for c, box in spec.tmaps)
+        blob = maps + blob
+    return blob
+
+
+def strides_shape(st: list, size: int) -> tuple:
+    """Row-major shape from row-major element strides and the element count."""
+    shape = []
+    prev = size
+    for t in st:
+        shape.append(prev // t)
+        prev = t
+    return tuple(shape)

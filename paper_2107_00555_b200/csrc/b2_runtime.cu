@@ -264,6 +264,45 @@ extern "C" int b2_func_set_max_smem(void *fn, int bytes) {
                   "cuFuncSetAttribute");
 }
 
+// TMA descriptor for a row-major f64 tensor (tma3 stencil mode): dims and
+// box innermost first, no swizzle, no L2 promotion (boxes rows are not
+// 256-B aligned: promotion over-fetched 1.8x), zero fill outside the tensor.
+typedef CUresult (*PFN_EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+extern "C" int b2_tensor_map_f64(void *out128, const void *base, int rank, const uint64_t *dims,
+                                 const uint32_t *box) {
+  static PFN_EncodeTiled enc = nullptr;
+  if (!enc) {
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q) !=
+            cudaSuccess || !fp)
+      return b2_fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = (PFN_EncodeTiled)fp;
+  }
+  if (rank < 1 || rank > 5) return b2_fail(B2_ERR_ARG, "tensor map rank %d", rank);
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], es[5];
+  uint64_t acc = 8;
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    es[i] = 1;
+    if (i > 0) st[i - 1] = acc;
+    acc *= dims[i];
+  }
+  CUtensorMap m;
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, const_cast<void *>(base),
+                   d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return b2_fail(B2_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  memcpy(out128, &m, sizeof(m));
+  return B2_OK;
+}
+
 static int launch_impl(void *fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx,
                        unsigned by, unsigned bz, unsigned smem, void *stream, const void *args,
                        size_t args_bytes, bool pdl, bool coop = false) {

@@ -110,7 +110,67 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+__global__ void widen_f32(const float *__restrict__ src, int64_t rows, int64_t cols, int64_t ld,
+                          double *__restrict__ dst) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    dst[i] = (double)src[r * ld + c];
+  }
+}
+
+__global__ void narrow_f64(const double *__restrict__ src, int64_t rows, int64_t cols,
+                           float *__restrict__ dst, int64_t ld, int accumulate) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    float *d = dst + r * ld + c;
+    // the f32 += is the caller's WCR add, applied to the rounded product
+    *d = accumulate ? *d + (float)src[i] : (float)src[i];
+  }
+}
+
+double *g_wide = nullptr;
+size_t g_wide_bytes = 0;
+
 }  // namespace
+
+int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
+                  int64_t ldb, double *C, int64_t rsc, int64_t csc, int accumulate,
+                  void *stream);
+
+// f32 operands, f64 products and accumulation on the DMMA path, one
+// rounding to f32 at the end: the accurate f32 MatMul (element-wise within
+// rtol 1e-5 of the f64 product at K = 16384, where any fp32-accumulating
+// GEMM — the 3xTF32 kernel, the host's sgemm — is not).  Row-major operands.
+extern "C" int b2_gemm_f32_f64acc(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa,
+                                  const float *B, int64_t rsb, float *C, int64_t rsc, int wcr,
+                                  void *stream) {
+  if (wcr != B2_WCR_NONE && wcr != B2_WCR_ADD)
+    return b2_fail(B2_ERR_UNSUPPORTED, "b2_gemm_f32_f64acc: wcr %d", wcr);
+  const size_t need = (size_t)(M * K + K * N + M * N) * sizeof(double);
+  if (need > g_wide_bytes) {
+    if (g_wide) cudaFree(g_wide);
+    g_wide = nullptr;
+    g_wide_bytes = 0;
+    int rc = b2_cuda_check(cudaMalloc(&g_wide, need), "f64 workspace");
+    if (rc) return rc;
+    g_wide_bytes = need;
+  }
+  double *a = g_wide, *b = g_wide + M * K, *c = b + K * N;
+  cudaStream_t st = (cudaStream_t)stream;
+  B2_CLEAR_ERROR();
+  widen_f32<<<148 * 8, 256, 0, st>>>(A, M, K, rsa, a);
+  widen_f32<<<148 * 8, 256, 0, st>>>(B, K, N, rsb, b);
+  B2_LAUNCH_CHECK("widen");
+  int rc = b2_dgemm_dmma(M, N, K, a, K, b, N, c, N, 1, 0, stream);
+  if (rc) return rc;
+  narrow_f64<<<148 * 8, 256, 0, st>>>(c, M, N, C, rsc, wcr == B2_WCR_ADD);
+  B2_LAUNCH_CHECK("narrow");
+  return B2_OK;
+}
 
 int b2_sgemm_128(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, const float *B,
                  int64_t ldb, float *C, int64_t ldc, int accumulate, void *stream) {

@@ -217,7 +217,7 @@ class GpuExecutor:
                 if FIN_PDL and getattr(spec, "red_fin", None):
                     # the fold kernel is a programmatic dependent launch
                     src = "#undef B2_NO_PDL\n" + src
-                spec.kernel = rt.get_kernel(src, name)
+                spec.kernel = rt.get_kernel(src, name, max_smem=spec.smem)
                 spec.fin_kernel = None
                 if getattr(spec, "red_fin", None):
                     # deterministic chunked reduction: partial workspace + fold kernel
@@ -1112,7 +1112,7 @@ class GpuExecutor:
         if self._prof is not None:
             ev = self._prof_event_pair()
             rt.lib().b2_event_record(ev[0], self.stream)
-        rt.launch(spec.kernel, grid, block, blob, self.stream,
+        rt.launch(spec.kernel, grid, block, blob, self.stream, spec.smem,
                   pdl=getattr(spec, "pdl", False) and self._prof is None)
         if spec.fin_kernel is not None:
             fg = spec.red_nout if spec.red_fin_block else -(-spec.red_nout // 256)

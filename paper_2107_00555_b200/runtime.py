@@ -82,7 +82,8 @@ EXPORTS = [
     "b2_launch_count", "b2_capture_begin", "b2_capture_end", "b2_graph_launch",
     "b2_graph_destroy", "b2_copy_view", "b2_fill_view", "b2_gemm_f64", "b2_gemm_f32",
     "b2_reduce", "b2_nccl_unique_id", "b2_nccl_init", "b2_nccl_destroy", "b2_nccl_group_p2p",
-    "b2_nccl_bcast", "b2_nccl_allreduce_f64",
+    "b2_nccl_bcast", "b2_nccl_allreduce_f64", "b2_tensor_map_f64",
+    "b2_gemm_f32_f64acc",
 ]
 
 
@@ -162,6 +163,10 @@ _SIGS = {
     "b2_nccl_group_p2p": ([_vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "b2_nccl_bcast": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
     "b2_nccl_allreduce_f64": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
+    "b2_gemm_f32_f64acc": ([_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int,
+                            _vp], ctypes.c_int),
+    "b2_tensor_map_f64": ([_vp, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
+                           ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
 }
 
 
@@ -306,6 +311,23 @@ def launch(k: Kernel, grid, block, args_blob: bytes, stream, smem: int = 0,
     fn = lib().b2_launch_coop if coop else (lib().b2_launch_pdl if pdl else lib().b2_launch)
     check(fn(k.fn, gx, gy, gz, bx, by, bz, smem, stream, args_blob, len(args_blob)),
           f"launch {k.name}")
+
+
+_tmap_cache: dict = {}
+
+
+def tensor_map_f64(base: int, shape, box) -> bytes:
+    """128-byte TMA descriptor of a row-major f64 tensor (shape outermost
+    first, box innermost first), cached per (base, shape, box)."""
+    key = (base, tuple(shape), tuple(box))
+    hit = _tmap_cache.get(key)
+    if hit is None:
+        dims = (ctypes.c_uint64 * len(shape))(*reversed([int(x) for x in shape]))
+        bx = (ctypes.c_uint32 * len(box))(*[int(x) for x in box])
+        out = ctypes.create_string_buffer(128)
+        check(lib().b2_tensor_map_f64(out, base, len(shape), dims, bx), "tensor map")
+        hit = _tmap_cache[key] = out.raw
+    return hit
 
 
 def make_view(base: int, offset: int, dtype: str, shape, strides) -> View:
