@@ -26,6 +26,8 @@ ProcessGrid / block_indices mirror the reference dist API names (cli.py:
 from __future__ import annotations
 
 import copy
+import json
+import pathlib
 import math
 import os
 import time
@@ -761,6 +763,12 @@ class Summa:
         return c_local
 
 
+def measured_extra() -> dict:
+    """Compute / L2 ceilings measured on the box (scripts/peaks/)."""
+    p = pathlib.Path(__file__).resolve().parent.parent / "profiles" / "measured_peaks_extra.json"
+    return json.loads(p.read_text()) if p.exists() else {}
+
+
 def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     """bench.py --workload matmul[_f32]: SUMMA over all ranks (squarest grid),
     libb2 DMMA / f32 GEMM per panel, NCCL panel broadcasts.  Prints the JSON
@@ -844,21 +852,22 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     e2e_s = float(t.item())
     value = flop / (ms / 1e3) / 1e12
+    extra = measured_extra()
     if dtype == "f32":
-        # 3xTF32: three TF32 products per multiply-add; TF32 dense = half the
-        # measured bf16 rate (MEASURED_PEAKS.json)
-        from bench import ROOT as _R  # noqa: E402
-
-        pk = json.loads((_R / "MEASURED_PEAKS.json").read_text())["bf16_tflops"] / 2 \
-            if (_R / "MEASURED_PEAKS.json").exists() else 1100.0
+        # 3xTF32: three TF32 products per multiply-add, against the measured
+        # cuBLAS TF32 GEMM rate (profiles/measured_peaks_extra.json)
+        pk = extra.get("cublas_tf32_8192_tflops", 755.6)
         roof = {"bound": "tensor", "achieved": 3 * value / world, "peak": pk, "unit": "TFLOP/s",
-                "frac": 3 * value / world / pk, "traffic": None,
+                "frac": 3 * value / world / pk, "traffic": None, "peak_kind": "measured",
                 "note": "per-GPU TF32 tensor rate (3 products per fp32 MAC) incl. the operand "
-                        "split passes; peak = measured bf16 dense / 2"}
+                        "split passes; peak = measured cuBLAS TF32 8192^3"}
     else:
-        roof = {"bound": "tensor", "achieved": value / world, "peak": 37.0, "unit": "TFLOP/s",
-                "frac": value / world / 37.0, "traffic": None,
-                "note": "per-GPU DMMA rate; peak = nominal FP64 tensor (no measured figure)"}
+        pk = extra.get("dmma_f64_tflops", 37.13)
+        roof = {"bound": "tensor", "achieved": value / world, "peak": pk, "unit": "TFLOP/s",
+                "frac": value / world / pk, "traffic": None, "peak_kind": "measured",
+                "note": "per-GPU DMMA rate; peak = measured mma.sync f64 microbenchmark "
+                        "(cuBLAS DGEMM 16384^3: "
+                        f"{extra.get('cublas_dgemm_16384_tflops', 36.16):.2f} TFLOP/s)"}
     if rank == 0:
         print(json.dumps({
             "metric": f"summa_matmul_{dtype}_TFLOPs", "value": value,

@@ -145,6 +145,11 @@ class _P:
                 args.append(self.select())
             self.take(")")
             return ("call", t, tuple(args))
+        if t in ("inf", "nan"):
+            # the reference serialises float literals with repr(): a WCR
+            # identity TNum(inf) (autoopt.py:816-876) is written as "inf"
+            # (texpr.py:150-165) — a literal, not a name
+            return ("num", float(t))
         if re.fullmatch(r"[A-Za-z_][A-Za-z_0-9]*", t):
             return ("ref", t)
         raise ScalarSyntaxError(f"unexpected token {t!r}")

@@ -385,6 +385,77 @@ def from_dict(d: dict) -> Graph:
     except (KeyError, TypeError, IndexError) as ex:
         raise SchemaError(f"malformed graph document: {ex}") from ex
     g.doc = d
+    return inline_library_wrappers(g)
+
+
+WRAPPER_PREFIX = "b200_lib_"
+
+
+def _wrapped_library(n: Node):
+    """The library node held by a b200 expansion wrapper (expansions.py): a
+    nested graph named b200_lib_*, one state, one library node whose every
+    connector is a whole inner container.  None otherwise."""
+    if not isinstance(n, Nested) or not n.sdfg.name.startswith(WRAPPER_PREFIX):
+        return None
+    inner = n.sdfg
+    if len(inner.states) != 1 or inner.transitions:
+        return None
+    st = inner.states[0]
+    libs = [x for x in st.nodes if isinstance(x, Library)]
+    if len(libs) != 1 or len(st.nodes) != len(st.edges) + 1:
+        return None
+    lib = libs[0]
+    conn = {}
+    for e in st.edges:
+        acc = e.src if e.dst is lib else e.dst
+        if not isinstance(acc, Access) or e.memlet is None or e.memlet.container != acc.container:
+            return None
+        from .validate import normalize  # (validate imports this module)
+
+        c = inner.containers[acc.container]
+        if len(e.memlet.subset) != len(c.shape):
+            return None
+        for (b, en, st_), d in zip(e.memlet.subset, c.shape):
+            if (normalize(b) != {} or normalize(st_) != {(): 1}
+                    or normalize(en) != normalize(("-", d, ("c", 1)))):
+                return None
+        conn[acc.container] = (e.dst_conn if e.dst is lib else e.src_conn, e.dst is lib)
+    if any(symexpr.to_text(v) != k for k, v in n.symbol_map.items()):
+        return None
+    return lib, conn
+
+
+def inline_library_wrappers(g: Graph) -> Graph:
+    """Put library nodes the b200 registry wrapped (expansions.py) back onto
+    their outer memlets, in place: the wrapper's containers are exactly those
+    memlets' subsets, so the node reads and writes the same elements (the
+    outer write keeps its WCR)."""
+    for st in g.states:
+        for i, n in enumerate(list(st.nodes)):
+            hit = _wrapped_library(n)
+            if hit is None:
+                continue
+            lib, conn = hit
+            new = Library(n.id, lib.kind, lib.name, lib.attrs)
+            st.nodes[i] = new
+            edges = []
+            for e in st.edges:
+                if e.dst is n:
+                    c, _ = conn[e.dst_conn]
+                    e = Edge(e.src, new, e.memlet, e.src_conn, c)
+                elif e.src is n:
+                    c, _ = conn[e.src_conn]
+                    e = Edge(new, e.dst, e.memlet, c, e.dst_conn)
+                edges.append(e)
+            st.edges = []
+            st._in = {x.id: [] for x in st.nodes}
+            st._out = {x.id: [] for x in st.nodes}
+            st._topo = st._parents = None
+            for e in edges:
+                st.add_edge(e)
+        for n in st.nodes:
+            if isinstance(n, Nested):
+                inline_library_wrappers(n.sdfg)
     return g
 
 

@@ -62,7 +62,12 @@ CONFIGS = {
     "matmul_f32": ("matmul", "raw", {"M": 16384, "K": 16384, "N": 16384}, "reference",
                    ("A", "B")),
     "go_fast": ("go_fast", "pipe", {"N": 12000}, "reference", ()),
+    # nbody at the NPBench preset (N=100, dt=0.01, tEnd=10 -> 1000 steps) with
+    # NPBench's own initialisation (stored inputs, see npbench_nbody); the
+    # 1000-step trajectory is chaotic (a 1-ulp change of one coordinate moves
+    # every output by O(1)), so the 10-step run is the element-wise check
     "nbody": ("nbody", "raw", {"N": 100, "NT": 1000}, "reference", ()),
+    "nbody_short": ("nbody", "raw", {"N": 100, "NT": 10}, "reference", ()),
     "softmax": ("softmax", "raw", {"N": 64, "H": 16, "SM": 512}, "port", ()),
     "conv2d_bias": ("conv2d_bias", "raw", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16,
                                            "K": 20, "HO": 237, "WO": 237}, "port", ()),
@@ -184,6 +189,14 @@ def exact_matmul(inp, out, idx):
     return ex, te
 
 
+def npbench_nbody(N: int) -> dict:
+    """NPBench nbody initialisation: mass 20/N, positions and velocities
+    uniform [0, 1) from default_rng(42), G = 1, softening = 0.1, dt = 0.01."""
+    rng = np.random.default_rng(42)
+    return {"mass": np.full(N, 20.0 / N), "pos": rng.random((N, 3)), "vel": rng.random((N, 3)),
+            "acc": np.zeros((N, 3)), "E": np.zeros(2), "G": 1.0, "softening": 0.1, "dt": 0.01}
+
+
 # ---------------------------------------------------------------------------
 
 
@@ -192,7 +205,10 @@ def generate(name: str):
     program = frontend.parse(source(prog))
     order, shapes = shapes_of(program, syms)
     t = time.perf_counter()
-    inputs = CD.make_inputs(order, shapes, 0, round_f32=f32)
+    if prog == "nbody":
+        inputs = npbench_nbody(syms["N"])
+    else:
+        inputs = CD.make_inputs(order, shapes, 0, round_f32=f32)
     t_in = time.perf_counter() - t
     entry = {"program": prog, "graph": f"{prog}.{variant}", "symbols": syms, "seed": 0,
              "params": order, "shapes": {k: list(v) for k, v in shapes.items()},
@@ -209,6 +225,10 @@ def generate(name: str):
     print(f"[{name}] {engine} {entry['seconds']:.1f}s", flush=True)
     blob = {}
     outs = []
+    if prog == "nbody":  # inputs not drawn by make_inputs: stored with the digest
+        entry["inputs"] = "stored"
+        for k, v in inputs.items():
+            blob[f"in/{k}"] = np.asarray(v, dtype=np.float64)
     for k, v in out.items():
         v = np.asarray(v)
         if k in inputs and np.ndim(inputs[k]) and np.array_equal(v, inputs[k]):

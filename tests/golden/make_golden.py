@@ -14,7 +14,9 @@ Appendix B) — it writes:
   ``raw``  = frontend.compile_source (frontend/__init__.py:25-45),
   ``pipe`` = coarsen -> cleanup_maps -> subgraph_fusion (reverted when it
              breaks scope structure) -> transient_mitigation,
-  ``auto`` = autoopt.auto_optimize (autoopt.py:990), where it succeeds.
+  ``auto`` = autoopt.auto_optimize (autoopt.py:990), where it succeeds,
+  ``b2reg`` = auto_optimize with this repo's b200 library expansions ahead
+             of the CPU ones in the registry (expansions.py).
 * tests/golden/vectors/<kernel>.v<i>.s<seed>.npz — inputs drawn with the
   reference conftest's make_inputs semantics (pkg/tests/conftest.py:38-49),
   outputs of the reference oracle ``evaluate_program`` (frontend/oracle.py:37)
@@ -72,12 +74,63 @@ SIZES = {
                     {"NB": 1, "H": 9, "W": 8, "CI": 3, "CO": 5, "K": 2, "HO": 8, "WO": 7}],
     "nbody": [{"N": 5, "NT": 2}, {"N": 9, "NT": 1}],
     "matmul": [{"M": 4, "K": 6, "N": 5}, {"M": 67, "K": 45, "N": 129}],
+    # WCR mul / add-of-negated, sum(A, axis), negative floor division,
+    # NaN-ordered min / max (interp.py + texpr.py semantics)
+    "wcr_ops": [{"N": 7, "M": 5}, {"N": 33, "M": 70}],
+    # REDUCE mul / min / max / full, REDUCE into a WCR-add output, TRANSPOSE
+    # (library-node semantics of interp.py:462-480; see mutate_libops)
+    "libops": [{"N": 4, "M": 6}, {"N": 37, "M": 53}],
 }
 ONLY = sys.argv[1:]
 CORPUS = ["adi", "atax", "bicg", "doitgen", "fig4_loop", "gemm", "gemver", "gesummv",
           "jacobi_1d", "jacobi_2d", "k2mm", "k3mm", "mvt", "wcr_sum"]
 REPO_PROGRAMS = ["heat_3d", "go_fast", "softmax", "azimint_naive", "conv2d_bias", "nbody",
-                 "matmul"]
+                 "matmul", "wcr_ops", "libops"]
+
+
+def mutate_libops(g):
+    """The DSL only lowers ``sum`` (REDUCE add, lower.py:268-282) and has no
+    transpose, so the library-node variants the interpreter supports are
+    made here on the compiled graph: REDUCE op mul (s0) / min (s1) / max
+    (s2, s4 full), a WCR-add output (s3: u += row sums), and a TRANSPOSE
+    state B = A.T appended after s4.  Their expected values come from the
+    reference interpreter (interp.py:462-480), the oracle has no such ops."""
+    from sdfgkit.ir import AccessNode, InterstateEdge, LibKind, LibraryNode, Memlet, Wcr
+    from sdfgkit.symbolic import SubsetRange, Sym
+
+    ops = {"s0": "mul", "s1": "min", "s2": "max", "s4": "max"}
+    for st in g.states:
+        for n in st.nodes.values():
+            if isinstance(n, LibraryNode) and n.kind is LibKind.REDUCE:
+                if st.label in ops:
+                    n.attributes["op"] = ops[st.label]
+                if st.label == "s3":
+                    for e in st.out_edges(n):
+                        e.memlet.wcr = Wcr.ADD
+    last = g.states[-1].label
+    st = g.add_state("s_transpose")
+    a = st.add(AccessNode("A"))
+    tr = st.add(LibraryNode(LibKind.TRANSPOSE, "transpose", {}))
+    b = st.add(AccessNode("B"))
+    st.add_edge(a, tr, Memlet("A", SubsetRange.full((Sym("N"), Sym("M")))), dst_conn="a")
+    st.add_edge(tr, b, Memlet("B", SubsetRange.full((Sym("M"), Sym("N")))), src_conn="out")
+    g.transitions.append(InterstateEdge(last, "s_transpose"))
+    return g
+
+
+MUTATE = {"libops": mutate_libops}
+
+
+def b200_registry_variant(g):
+    """auto_optimize with the b200 library expansions first in the registry
+    (paper_2107_00555_b200/expansions.py): MATMUL / REDUCE / TRANSPOSE stay
+    device library nodes (inside single-node wrappers)."""
+    sys.path.insert(0, str(REPO))
+    from paper_2107_00555_b200 import expansions
+
+    with expansions.patched_cpu_registry(autoopt):
+        autoopt.auto_optimize(g)
+    return g
 SEEDS = (0, 1)
 
 
@@ -140,6 +193,8 @@ def main():
         program = frontend.parse(src)
         g, diags = frontend.compile_source(src)
         assert g is not None, [str(d) for d in diags]
+        if name in MUTATE:
+            g = MUTATE[name](g)
         variants = {"raw": copy.deepcopy(g)}
         gp, fused = pipeline(copy.deepcopy(g))
         variants["pipe"] = gp
@@ -149,6 +204,10 @@ def main():
             variants["auto"] = ga
         except Exception as ex:  # noqa: BLE001
             print(f"[{name}] auto_optimize failed: {ex}")
+        try:
+            variants["b2reg"] = b200_registry_variant(copy.deepcopy(g))
+        except Exception as ex:  # noqa: BLE001
+            print(f"[{name}] auto_optimize with the b200 registry failed: {ex}")
         for v, gg in variants.items():
             (gdir / f"{name}.{v}.json").write_text(json.dumps(to_dict(gg), indent=1) + "\n")
         entry = {
@@ -161,9 +220,16 @@ def main():
         for vi, syms in enumerate(SIZES[name]):
             for seed in SEEDS:
                 inputs = make_inputs(program, syms, seed)
-                ref = ref_oracle.evaluate_program(
-                    program, syms,
-                    {k: (np.array(v, copy=True) if hasattr(v, "shape") else v) for k, v in inputs.items()})
+                if name in MUTATE:  # library ops the oracle cannot express
+                    octx = ExecContext(bindings=dict(syms))
+                    octx.bind_inputs({k: np.array(v) if hasattr(v, "shape") else v
+                                      for k, v in inputs.items()})
+                    ref = interpret(copy.deepcopy(variants["raw"]), octx)
+                else:
+                    ref = ref_oracle.evaluate_program(
+                        program, syms,
+                        {k: (np.array(v, copy=True) if hasattr(v, "shape") else v)
+                         for k, v in inputs.items()})
                 blob = {}
                 for k, v in inputs.items():
                     blob[f"in/{k}"] = np.asarray(v, dtype=np.float64)
