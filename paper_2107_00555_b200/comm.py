@@ -57,6 +57,9 @@ def block_layout(shape, grid_dims, coords):
     (SPEC.md:532-534): grid dim d splits array dim d (a 1-D grid splits the
     first array dim); uneven extents are an error (no implicit padding).
     Returns (start, extent) per array dim for the rank at ``coords``."""
+    grid_dims = list(grid_dims)
+    while len(grid_dims) > len(shape) and grid_dims[-1] == 1:  # (P, 1) over a vector
+        grid_dims.pop()
     if len(grid_dims) > len(shape):
         raise SimError(f"grid {tuple(grid_dims)} has more dims than the array {tuple(shape)}")
     out = []
@@ -384,10 +387,17 @@ class RankComm:
         lm = (outs["out"] if scatter else ins["a"]).memlet  # local side
         gshape = [len(r) for r in symexpr.eval_subset(gm.subset, sym)]
         lshape = [len(r) for r in symexpr.eval_subset(lm.subset, sym)]
-        dims = self._grid_dims()
+        # the node's own distribution (distribute.py writes {"dist": {"grid"}}:
+        # a 1-D map over a 2-D machine uses a 1-D grid of all ranks)
+        ndims = (n.attrs.get("dist") or {}).get("grid")
+        dims = tuple(int(x) for x in ndims) if ndims else self._grid_dims()
         if int(np.prod(dims)) != self.world:
             raise SimError(f"grid {dims} does not have {self.world} ranks")
-        blocks = [block_layout(gshape, dims, self._coords(q)) for q in range(self.world)]
+
+        def coords(q):
+            return (q // dims[1], q % dims[1]) if len(dims) == 2 else (q,)
+
+        blocks = [block_layout(gshape, dims, coords(q)) for q in range(self.world)]
         if [e for _, e in blocks[self.rank]] != lshape:
             raise SimError(f"local view {lshape} does not match the block "
                            f"{[e for _, e in blocks[self.rank]]} of {gshape}")
@@ -447,8 +457,26 @@ class RankComm:
             counters.collective_calls += 1
             counters.comm_bytes += sum(x[3] for x in ops)
 
+    dry_errors: list = field(default_factory=list)
+
     def record_dry(self, ex, op, sym):
-        """State-machine walk without transfers: message keys only."""
+        """State-machine walk without transfers: message keys only.  A
+        collective whose layout does not work out is recorded as such and its
+        error deferred, so a rank-divergent collective sequence is reported
+        first (CollectiveOrderError)."""
+        try:
+            self._record_dry(ex, op, sym)
+        except SimError as exn:
+            if op.node.kind in ("isend", "irecv", "waitall"):
+                raise
+            self.colls.append((op.node.kind, op.state.label, op.node.id, "invalid"))
+            self.dry_errors.append(exn)
+
+    def raise_dry_errors(self):
+        if self.dry_errors:
+            raise self.dry_errors[0]
+
+    def _record_dry(self, ex, op, sym):
         kind = op.node.kind
         if kind in ("isend", "irecv"):
             peer, tag, ins, outs = self._args(ex, op, sym)
@@ -471,23 +499,24 @@ class RankComm:
             gm, lm, blocks, nbytes = self._block_plan(ex, op, sym, kind == "block_scatter")
             for q in range(self.world):
                 self._buffer((op.idx, "blk", q), nbytes)
-            self.colls.append((kind, tuple(e for _, e in blocks[0]), nbytes))
+            self.colls.append((kind, op.state.label, op.node.id,
+                               tuple(e for _, e in blocks[0]), nbytes))
         elif kind in ("scatter", "gather"):
             gm, lm, gb, goff, gdt, c = self._flat_plan(ex, op, sym, kind == "scatter")
             for q in range(self.world):
                 self._buffer((op.idx, "flat", q), c * sdfg.DTYPE_BYTES[gdt])
-            self.colls.append((kind, c))
+            self.colls.append((kind, op.state.label, op.node.id, c))
         elif kind == "dist_matmul":
             *_, Pr, Pc, am_, bn, kb, L = self._dist_plan(ex, op, sym)
             self._buffer((op.idx, "pa"), 8 * am_ * kb)
             self._buffer((op.idx, "pb"), 8 * kb * bn)
-            self.colls.append((kind, Pr, Pc, kb * L))
+            self.colls.append((kind, op.state.label, op.node.id, Pr, Pc, kb * L))
         elif kind in ("bcast", "reduce"):
             am, _ = self._io(op)
             n = int(np.prod([len(r) for r in symexpr.eval_subset(am.subset, sym)]))
             nb = n * sdfg.DTYPE_BYTES[ex.g.containers[am.container].dtype]
             self._buffer((op.idx, kind), 8 * n if kind == "reduce" else nb)
-            self.colls.append((kind, n))
+            self.colls.append((kind, op.state.label, op.node.id, n))
 
     def finish_dry(self):
         if self._cur:  # posted but never waited for
@@ -636,6 +665,7 @@ class LocalViewRunner:
             if recs[r][1] != recs[0][1]:
                 raise CollectiveOrderError(
                     f"rank {r} calls collectives {recs[r][1]}, rank 0 {recs[0][1]}")
+        self.comm.raise_dry_errors()
         check_matching([x[0] for x in recs])
         self.comm.nccl = NcclComm(rank, world)
 

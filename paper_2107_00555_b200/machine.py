@@ -162,6 +162,23 @@ class GpuExecutor:
         self._allocate(external or {})
         self._compile()
         self.shell_only = self._dead_on_entry()
+        self.root_only = self._root_only_ops()
+
+    def _root_only_ops(self) -> set:
+        """Ops of a distributed program that touch only global (root-resident)
+        containers: non-root ranks skip them (interp.py:343-359)."""
+        local = {n for n, c in self.g.containers.items() if c.storage == "distributed_local"}
+        if self.comm is None or not local:
+            return set()
+        out = set()
+        for op in self.planner.all_ops:
+            if isinstance(op, P.LibOp) and op.kind == "comm":
+                continue
+            touched = self.planner.op_reads.get(op.idx, set()) | \
+                self.planner.op_writes.get(op.idx, set())
+            if touched and not (touched & local):
+                out.add(op.idx)
+        return out
 
     # -- setup ------------------------------------------------------------------
 
@@ -944,6 +961,10 @@ class GpuExecutor:
 
     def _exec_region(self, reg, sym, counters):
         spec = reg.spec
+        if self.root_only and self.comm.rank != 0 and all(
+                op.idx in self.root_only for h in reg.heads for op in self.planner.ops[h]):
+            self._region_final(reg, sym)  # root-resident loop (interp.py:343-359)
+            return
         trips = self._region_trips(reg, sym) if reg.par else []
         npar = 1
         for _, _, vals in trips:
@@ -1021,6 +1042,8 @@ class GpuExecutor:
                   and self.comm.dry):
                 self.comm.record_dry(self, op, sym)
             return
+        if self.root_only and self.comm.rank != 0 and op.idx in self.root_only:
+            return  # root-resident data only (interp.py:343-359)
         if op.idx in self.pair_second:
             return  # ran inside the pair kernel of its predecessor
         if op.idx in self.pairs:

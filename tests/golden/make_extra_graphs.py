@@ -65,3 +65,45 @@ for name, src in CONTRACT.items():
     out = HERE / "graphs" / f"{name}.raw.json"
     out.write_text(json.dumps(to_dict(g), indent=1) + "\n")
     print("wrote", out)
+
+# Distribution-pipeline / rank-simulator programs (the cases of
+# pkg/tests/test_dist.py:41-95, 143-180, 264-282, 348-366, written here)
+DIST = {
+    "dist_flat": "def f(A: f64[N], B: f64[N]):\n    B[:] = A + 0.0\n",
+    "dist_alpha": "def f(alpha: f64, A: f64[N, M], T: f64[N, M]):\n    T[:] = alpha * A\n",
+    "dist_two_readers": ("def f(A: f64[N], B: f64[N], C: f64[N]):\n"
+                         "    T = zeros(N)\n"
+                         "    T[:] = A + 1.0\n"
+                         "    B[:] = T * 2.0\n"
+                         "    C[:] = T + 3.0\n"),
+    "dist_shifted": ("def f(A: f64[N], B: f64[N]):\n"
+                     "    T = zeros(N)\n"
+                     "    T[:] = A + 1.0\n"
+                     "    B[1:-1] = T[:-2] * 2.0\n"),
+    "dist_unmatched_send": ("def f(A: f64[lNx + 2, lNy + 2], peer: i32):\n"
+                            "    req = requests(1)\n"
+                            "    comm_isend(A[1:-1, 1], peer, 3, req[0])\n"
+                            "    comm_waitall(req)\n"),
+    "dist_missing_send": ("def f(A: f64[lNx + 2, lNy + 2], peer: i32):\n"
+                          "    req = requests(1)\n"
+                          "    comm_irecv(A[1:-1, 0], peer, 3, req[0])\n"
+                          "    comm_waitall(req)\n"),
+    "dist_waitall_empty": ("def f(A: f64[N]):\n"
+                           "    req = requests(4)\n"
+                           "    comm_waitall(req)\n"
+                           "    A[0] = 1.0\n"),
+    "dist_divergent": ("def f(A: f64[N], B: f64[N], C: f64[N], me: i32):\n"
+                       "    la = zeros(N // 2)\n"
+                       "    if me < 1:\n"
+                       "        la[:] = block_scatter(A)\n"
+                       "    else:\n"
+                       "        la[:] = block_scatter(B)\n"
+                       "    C[0:N // 2] = block_gather(la)\n"),
+}
+for name, src in DIST.items():
+    g, diags = frontend.compile_source(src)
+    errs = [d for d in diags if d.severity == "error"]
+    assert g is not None and not errs, (name, [str(d) for d in diags])
+    out = HERE / "graphs" / f"{name}.raw.json"
+    out.write_text(json.dumps(to_dict(g), indent=1) + "\n")
+    print("wrote", out)
