@@ -31,8 +31,6 @@ from . import codegen, plan as P, runtime as rt, sdfg, symexpr
 
 TPB = 512
 MAX_CW = 8192
-RP_COOP = os.environ.get("B2_RP_COOP", "0") == "1"  # fold inside the row pass (grid barrier)
-RP_PDL = os.environ.get("B2_RP_PDL", "0") == "1"  # fold kernel as a programmatic dependent launch (neutral: off)
 TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpass.cuh)
 # compensated (Dot2 / double-double) sums in the row pass (rowpass.cuh
 # RP_COMP): ~17x closer to the exact result (atax 8000^2: 3.6e-14 vs 6.3e-13
@@ -278,17 +276,11 @@ class RowPass:
         # register-prefetch kernel at 2-3 CTAs/SM: 184 vs 254 us)
         self.tma = (TMA_ROWS and self.prologue is None and rs % 2 == 0 and off % 2 == 0
                     and N % 2 == 0 and cw % 2 == 0 and ring_s >= 2)
-        # in-kernel fold after a grid barrier (cooperative launch): TMA
-        # variant (one CTA per SM, all co-resident), one column tile
-        self.coop = (RP_COOP and not RP_COMP and self.tma and axpy is not None
-                     and self.ctiles == 1)
         if self.tma:
             self.ring = min(4, ring_s)
             stage_base = 0
             self.smem = (nst * cw + red + vs + self.ring * cw) * 8
             self.G = min(M, 148)
-            if self.coop and (-(-N // self.G) > 64 or tpb % 64 or self.ring * cw < tpb):
-                self.coop = False  # fold slices are at most 64 columns
         else:
             self.ring = 0
             stage_base = (cw if axpy else 0) * (2 if RP_COMP else 1) + (cw if dot else 0) + red
@@ -307,7 +299,7 @@ class RowPass:
                      ("RP_PROLOGUE", int(self.prologue is not None)),
                      ("RP_WRITEBACK", int(self.prologue is not None)),
                      ("RP_TMA", int(self.tma)), ("RP_S", max(1, self.ring)),
-                     ("RP_COOP", int(self.coop)), ("RP_COMP", int(RP_COMP)),
+                     ("RP_COMP", int(RP_COMP)),
                      ("RP_VSMEM", int(self.tma and self.vsmem)),
                      ("RP_NSTAGED", nst)):
             L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")
@@ -380,20 +372,12 @@ class RowPass:
     def compile(self, ex):
         name = f"{ex.g.name}_{self.mvs[0].op.idx}"
         src = self.source(ex.buf.shape, name)
-        if RP_PDL:
-            # kernels open with griddepcontrol.wait: the fold kernel is
-            # launched programmatically and overlaps the row pass's tail
-            src = "#undef B2_NO_PDL\n" + src
         self.kmain = rt.get_kernel(src, f"b2_rp_{name}", max_smem=self.smem)
         self.kfin = rt.get_kernel(src, f"b2_rpf_{name}")
         nws = 2 if RP_COMP else 1  # hi (+ lo) column partials
         self.ws_axpy = (ex.buf.alloc(max(8, nws * self.G * self.N * 8))
                         if self.axpy is not None else 0)
         self.ws_dot = ex.buf.alloc(max(8, self.ctiles * self.M * 8)) if self.dot is not None else 0
-        self.bar = 0
-        if self.coop:  # grid-barrier state (count, sense), zero once
-            self.bar = ex.buf.alloc(16)
-            rt.check(rt.lib().b2_memset(self.bar, 0, 16, ex.stream), "memset")
 
     # -- run ---------------------------------------------------------------------
 
@@ -406,7 +390,6 @@ class RowPass:
         w[0] = ex.buf.ptr[cont] + 8 * off
         w[1] = self.ws_axpy
         w[2] = self.ws_dot
-        w[7] = self.bar
         if self.dot is not None:
             w[3] = self._ptr(ex, self.dot.vec)
             w[4] = self._ptr(ex, self.dot.out)
@@ -427,18 +410,17 @@ class RowPass:
             ev = ex._prof_event_pair()
             rt.lib().b2_event_record(ev[0], ex.stream)
         rt.launch(self.kmain, (self.G, self.ctiles, 1), (self.tpb, 1, 1), blob, ex.stream,
-                  self.smem, coop=self.coop)
+                  self.smem)
         if prof is not None:
             rt.lib().b2_event_record(ev[1], ex.stream)
             prof.append((self.kmain.name, self.M * self.N, ev))
-        nfin = max(self.N if (self.axpy is not None and not self.coop) else 0,
+        nfin = max(self.N if self.axpy is not None else 0,
                    self.M if (self.dot is not None and self.ctiles > 1) else 0)
         if nfin:
             if prof is not None:
                 ev = ex._prof_event_pair()
                 rt.lib().b2_event_record(ev[0], ex.stream)
-            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream,
-                      pdl=RP_PDL and prof is None)
+            rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream)
             if prof is not None:
                 rt.lib().b2_event_record(ev[1], ex.stream)
                 prof.append((self.kfin.name, nfin, ev))

@@ -31,10 +31,6 @@ CT = {"f64": "double", "i64": "b2_ll", "i32": "int", "bool": "bool"}
 TC = {"f64": "f", "i64": "i", "i32": "i", "bool": "b"}
 
 MAX_BLOCKS = 148 * 16
-STENCIL_MODE = os.environ.get("B2_STENCIL", "0") == "1"  # smem plane ring (slower on B200: off)
-STENCIL_CHUNK = 32  # planes marched per CTA in stencil mode
-STENCIL_PREFETCH = 2  # planes in flight ahead of the compute plane (cp.async)
-HOIST_LOADS = os.environ.get("B2_HOIST", "0") == "1"  # batch read-only loads in march mode (slower: off)
 HOIST_TILES = os.environ.get("B2_HOIST_TILES", "1") == "1"  # ... in flat / tile2 modes
 REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WCR reductions
 # branch-free unrolled copy of the per-thread point loop for full tiles
@@ -48,13 +44,10 @@ MARCH_BY = int(os.environ.get("B2_MARCH_BY", "8"))  # tile rows (blockDim.y) in 
 MARCH_BX = int(os.environ.get("B2_MARCH_BX", "64"))  # tile columns (blockDim.x) in march mode
 # shift the innermost tile origin down to a 128-byte line so a warp's row
 # access covers whole lines (march / tile2 with a constant unit-stride range)
-ALIGN_TILES = os.environ.get("B2_ALIGN_TILES", "0") == "1"  # measured neutral (heat, jacobi)
-RED_UNROLL = int(os.environ.get("B2_RED_UNROLL", "0"))  # full-unroll innermost reduction trips <= this (neutral on conv2d)
 RED_THREADS = int(os.environ.get("B2_RED_THREADS", str(148 * 8192)))  # chunked-reduction thread target (azimint 0.78 -> 0.51 ms vs 148 * 512)
 SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per chunk, small reductions (0: off)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
-PF_EVICT_LAST = os.environ.get("B2_PF_EVICT_LAST", "0") == "1"  # evict_last policy on march prefetches
 MARCH_PDL = os.environ.get("B2_MARCH_PDL", "1") == "1"  # march sweeps as programmatic dependent launches (heat 37.40 -> 37.24 ms)
 # ... small flat / reduce / scalar kernels, whose launch latency is a large
 # share of their time (nbody's per-step kernels: 5.32 -> 4.67 ms)
@@ -65,9 +58,7 @@ SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
 ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "1"))  # unroll of the warp-per-row loop (4 spilled at 32 regs)
 ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowred kernels (softmax 1.11 -> 1.06 ms)
-ROWRED_HOIST = os.environ.get("B2_ROWRED_HOIST", "0") == "1"  # issue a lane's row loads first (slower: off)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
-STREAM_STORES = os.environ.get("B2_STCS", "0") == "1"  # evict-first stores of write-only outputs
 # 3-D stencil sweeps through a TMA plane ring (cp.async.bulk.tensor.3d into
 # shared memory, mbarrier-tracked, persistent balanced grid): the tma3 mode
 # (measured: heat_3d N=400 39.3 ms vs 37.3 for march at the best geometry
@@ -237,10 +228,6 @@ class _Gen:
             for n, p in enumerate(R):
                 i = idx[p]
                 trip = self.const_ranges[i][2]
-                # short constant trips unroll (conv2d's ci/kj loops): the
-                # index arithmetic folds into load offsets; order unchanged
-                if n == len(R) - 1 and trip <= RED_UNROLL:
-                    L.append("#pragma unroll")
                 L.append(f"    for (int j{i} = 0; j{i} < (int)rl{i}; ++j{i}) {{")
                 L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         else:
@@ -340,7 +327,7 @@ class _Gen:
                 f"        const b2_ll row = (z0 + zz) * st_{c}_0 + (y0 + yy) * st_{c}_1;",
                 f"        const b2_ll e0 = (row + x0) * {esz}LL, e1 = (row + x1 + 1) * {esz}LL;",
                 "        const b2_ll a0 = (base + e0) & ~15LL, a1 = (base + e1 + 15) & ~15LL;",
-                f"        b2_prefetch_l2{'_last' if PF_EVICT_LAST else ''}((const void *)a0, (unsigned)(a1 - a0));",
+                "        b2_prefetch_l2((const void *)a0, (unsigned)(a1 - a0));",
                 "      }",
                 "    }",
             ]
@@ -377,8 +364,6 @@ class _Gen:
         L.append("    }")
         for n, p in enumerate(R):
             i = idx[p]
-            if n == len(R) - 1 and self.const_ranges[i][2] <= RED_UNROLL:
-                L.append("#pragma unroll")
             L.append(f"    for (int j{i} = 0; j{i} < (int)rl{i}; ++j{i}) {{")
             L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
         L.append("#pragma unroll")
@@ -615,107 +600,6 @@ class _Gen:
                 L.append(f"      {t['target']} = b2_op_{t['wcr']}({self._old(t)}, {t['acc']});")
             else:
                 L.append(f"      b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
-        L.append("    }")
-        L.append("  }")
-        return L
-
-    def _stencil_loop(self, k: int, vec: int, reg_decls, body: list) -> list:
-        """Stencil mode: each CTA owns a (8 x 32*vec) tile of the two inner
-        dims (3-D) or a 256*vec span of the inner dim (2-D) and marches over a
-        chunk of SCH planes along dim 0.  Every halo'd plane of each stencil
-        container is fetched once into a shared-memory ring of SDEPTH planes
-        (coalesced cooperative loads), so each input element is read from
-        L2/HBM ~once instead of once per neighbour."""
-        grp = self.group
-        L: list[str] = []
-        tk = (32 if k == 3 else 256) * vec
-        mins = [min(st["min"][d] for st in self.stencil.values()) for d in range(k)]
-        maxs = [max(st["max"][d] for st in self.stencil.values()) for d in range(k)]
-        for st in self.stencil.values():
-            st["min"], st["max"] = tuple(mins), tuple(maxs)
-        pref = STENCIL_PREFETCH
-        depth = maxs[0] - mins[0] + 1 + pref
-        sk = tk + maxs[-1] - mins[-1]
-        sj = 8 + maxs[1] - mins[1] if k == 3 else 1
-        L.append(f"  constexpr int SDEPTH = {depth}, SCH = {STENCIL_CHUNK}, TK = {tk};")
-        for c in self.stencil:
-            ct = CT[self.g.containers[c].dtype]
-            if k == 3:
-                L.append(f"  __shared__ {ct} sm_{c}[SDEPTH][{sj}][{sk}];")
-            else:
-                L.append(f"  __shared__ {ct} sm_{c}[SDEPTH][{sk}];")
-        x = k - 1
-        L.append(f"  constexpr b2_ll ntx = (rl{x} + TK - 1) / TK;")
-        L.append("  constexpr b2_ll nty = " + ("(rl1 + 7) / 8;" if k == 3 else "1;"))
-        L.append("  constexpr b2_ll nch = (rl0 + SCH - 1) / SCH;")
-        L.append("  const int tid = threadIdx.y * blockDim.x + threadIdx.x;")
-        L.append("  for (b2_ll vb = blockIdx.x; vb < ntx * nty * nch; vb += gridDim.x) {")
-        L.append("    const b2_ll txt = vb % ntx; b2_ll rem = vb / ntx;")
-        L.append("    const b2_ll tyt = rem % nty; const b2_ll ch = rem / nty;")
-        L.append("    const b2_ll i0 = ch * SCH;")
-        L.append("    const b2_ll nit = (rl0 - i0) < SCH ? (rl0 - i0) : SCH;")
-        L.append("    const b2_ll kx0 = txt * TK;")
-        if k == 3:
-            L.append("    const b2_ll jy0 = tyt * 8;")
-        L.append("    __syncthreads();")
-        # plane loader: row index (dim 0) relative to the map origin
-        for c in self.stencil:
-            shp = self.shapes[c]
-            ct = CT[self.g.containers[c].dtype]
-            L.append(f"    auto load_{c} = [&](b2_ll rel0, int slot) {{")
-            L.append(f"      const b2_ll g0 = rb0 + rel0;")
-            L.append(f"      const bool ok0 = g0 >= 0 && g0 < {shp[0]}LL;")
-            L.append(f"      for (int e = tid; e < {sj * sk}; e += {256}) {{")
-            if k == 3:
-                L.append(f"        const int jj = e / {sk}, kk = e % {sk};")
-                L.append(f"        const b2_ll g1 = rb1 + jy0 + ({mins[1]}) + jj;")
-                L.append(f"        const b2_ll g2 = rb2 + kx0 + ({mins[2]}) + kk;")
-                L.append(f"        const bool ok = ok0 && g1 >= 0 && g1 < {shp[1]}LL && g2 >= 0 && "
-                         f"g2 < {shp[2]}LL;")
-                L.append(f"        b2_cp_async<sizeof({ct})>(&sm_{c}[slot][jj][kk], ok ? "
-                         f"(const void *)(c_{c} + g0 * st_{c}_0 + g1 * st_{c}_1 + g2) : "
-                         f"(const void *)c_{c}, ok);")
-            else:
-                L.append(f"        const int kk = e;")
-                L.append(f"        const b2_ll g1 = rb1 + kx0 + ({mins[1]}) + kk;")
-                L.append(f"        const bool ok = ok0 && g1 >= 0 && g1 < {shp[1]}LL;")
-                L.append(f"        sm_{c}[slot][kk] = ok ? c_{c}[g0 * st_{c}_0 + g1] : ({ct})0;")
-            L.append("      }")
-            L.append("    };")
-        # cp.async pipeline: planes [min0, max0 + PREF) in flight before the
-        # march; each iteration issues plane it + max0 + PREF and waits for
-        # plane it + max0 (one commit group per plane)
-        L.append(f"    for (int d = {mins[0]}; d < {maxs[0] + pref}; ++d) {{")
-        for c in self.stencil:
-            L.append(f"      if (d - ({maxs[0]}) < nit) load_{c}(i0 + d, d - ({mins[0]}));")
-        L.append("      b2_cp_commit();")
-        L.append("    }")
-        L.append("    for (b2_ll it = 0; it < nit; ++it) {")
-        L.append(f"      if (it + {pref} < nit) {{")
-        for c in self.stencil:
-            L.append(f"        load_{c}(i0 + it + ({maxs[0] + pref}), "
-                     f"(int)((it + {maxs[0] - mins[0] + pref}) % SDEPTH));")
-        L.append("      }")
-        L.append("      b2_cp_commit();")
-        L.append(f"      b2_cp_wait<{pref}>();")
-        L.append("      __syncthreads();")
-        L.append(f"      const b2_ll p_{grp.params[0]} = rb0 + i0 + it;")
-        inner = "      "
-        if k == 3:
-            L.append("      if (jy0 + threadIdx.y < rl1) {")
-            L.append(f"      const b2_ll p_{grp.params[1]} = rb1 + jy0 + threadIdx.y;")
-        L.append("#pragma unroll")
-        L.append(f"      for (int v = 0; v < {vec}; ++v) {{")
-        step = 32 if k == 3 else 256
-        L.append(f"        const b2_ll ix = kx0 + threadIdx.x + {step} * v;")
-        L.append(f"        if (ix >= rl{x}) break;")
-        L.append(f"        const b2_ll p_{grp.params[x]} = rb{x} + ix;")
-        L += reg_decls(8)
-        L += [inner + ln for ln in body]
-        L.append("      }")
-        if k == 3:
-            L.append("      }")
-        L.append("      __syncthreads();")
         L.append("    }")
         L.append("  }")
         return L
@@ -1018,23 +902,6 @@ class _Gen:
                           f"lx + {offs[2] - st['min'][2]}];")
                 self.cse[key] = hit
             return hit, t
-        if depth == 0 and m.container in self.stencil:
-            self.spec.checks.append((m.container, m.subset, env))
-            offs = self._stencil_offsets(m, env)
-            key = (m.container, offs)
-            hit = self.cse.get(key)
-            if hit is None:
-                st = self.stencil[m.container]
-                hit = self.fresh("sm")
-                slot = f"((it + {offs[0] - st['min'][0]}) % SDEPTH)"
-                if len(offs) == 3:
-                    ix = (f"[{slot}][threadIdx.y + {offs[1] - st['min'][1]}]"
-                          f"[threadIdx.x + 32 * v + {offs[2] - st['min'][2]}]")
-                else:
-                    ix = f"[{slot}][threadIdx.x + 256 * v + {offs[1] - st['min'][1]}]"
-                self.emit(f"const {CT[c.dtype]} {hit} = sm_{m.container}{ix};")
-                self.cse[key] = hit
-            return hit, t
         idx = [symexpr.to_c(b, self.name_of(env)) for b, _, _ in m.subset]
         off = self.offset(m.container, idx)
         p = self.ptr(m.container)
@@ -1132,13 +999,7 @@ class _Gen:
             self.spec.checks.append((m.container, m.subset, env))
             target = f"{p}[{off}]"
         if m.wcr is None:
-            if (STREAM_STORES and not guarded and ct == "double"
-                    and getattr(self.spec, "mode", "") in ("march", "tile2")
-                    and m.container not in self.read_set):
-                # write-only output of a streaming sweep: evict-first store
-                self.emit(f"__stcs(&{target}, ({ct})({val}));")
-            else:
-                self.emit(f"{target} = ({ct})({val});")
+            self.emit(f"{target} = ({ct})({val});")
         elif shared:
             self.emit(f"b2_atomic_{m.wcr}(&{target}, ({ct})({val}));")
         else:
@@ -1296,21 +1157,13 @@ class _Gen:
                 if all(sts["max"][d] - sts["min"][d] <= 2 for d in range(3)):
                     self.stencil = st
                     mode = "tma3"
-        if (mode in ("tile2", "flat", "march") and k == 3 and STENCIL_MODE
-                and all(r is not None and r[1] == 1 for r in self.const_ranges)
-                and all(r[2] >= 8 for r in self.const_ranges)):
-            self.stencil = self._stencil_analysis()
-            if self.stencil:
-                mode = "stencil"
-        force = os.environ.get("B2_FORCE_MODE")  # tuning knob: flat | tile2 | stencil
-        if force and mode in ("flat", "tile2", "stencil") and k >= 1:
-            if force == "stencil" and not self.stencil:
-                pass
-            elif force == "march" and (k < 3 or any(r is None for r in self.const_ranges)):
+        force = os.environ.get("B2_FORCE_MODE")  # tuning knob: flat | tile2 | march
+        if force and mode in ("flat", "tile2", "march") and k >= 1:
+            if force == "march" and (k < 3 or any(r is None for r in self.const_ranges)):
                 pass
             elif force != "tile2" or k >= 2:
                 mode = force
-        if mode not in ("stencil", "tma3"):
+        if mode != "tma3":
             self.stencil = {}
         if mode in ("flat", "tile2", "march") and REDUCE_MODE:
             rp = self._reduction_plan()
@@ -1366,9 +1219,6 @@ class _Gen:
                 vec = SLAB_VEC
             else:
                 vec = 16 if (r0 is not None and r0[2] >= 256) else 8
-        elif mode == "stencil":
-            vec = _pick_vec(self.const_ranges[-1][2]) if k == 3 else \
-                (2 if self.const_ranges[-1][2] >= 1024 else 1)
         elif mode == "tma3":
             vec = 2  # points per thread along the row (tile width <= 64)
         elif mode == "flat" and all(r is not None for r in self.const_ranges):
@@ -1380,15 +1230,9 @@ class _Gen:
             vec = int(os.environ["B2_VEC"])
         spec.vec = vec
         spec.align = 0
-        lastr = self.const_ranges[-1] if self.const_ranges else None
-        if (ALIGN_TILES and mode in ("tile2", "march") and k >= 2 and lastr is not None
-                and lastr[1] == 1):
-            esz = max([{"i32": 4, "bool": 1}.get(self.g.containers[n].dtype, 8) for n in spec.containers] or [8])
-            spec.align = lastr[0] % max(1, 128 // esz)
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, TILE_BY, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
-                      "rowred": (256, 1, 1), "tma3": (32, TMA3_CW + 1, 1),
-                      "stencil": (32, 8, 1) if k == 3 else (256, 1, 1)}[mode]
+                      "rowred": (256, 1, 1), "tma3": (32, TMA3_CW + 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
         self.written = set()
@@ -1406,14 +1250,7 @@ class _Gen:
         # before the math (softmax's divide map 0.78 -> 0.64 ms; neutral on
         # jacobi_2d / go_fast).  march keeps program order: 16 planes x 7
         # hoisted loads per thread tripled heat_3d's time.
-        self.hoist = ((mode in ("flat", "tile2") and vec > 1 and HOIST_TILES)
-                      or (mode == "march" and vec > 1 and HOIST_LOADS))
-        if mode == "rowred" and ROWRED_HOIST:
-            lastr = self.const_ranges[-1]
-            # constant trips per lane: every read-only load of the lane's row
-            # slice is issued before the math (exp/div latency otherwise
-            # leaves one load in flight per lane)
-            self.hoist = lastr is not None and lastr[2] % 32 == 0 and lastr[2] // 32 <= 32
+        self.hoist = mode in ("flat", "tile2") and vec > 1 and HOIST_TILES
         self.hoisted = []
 
         env = {p: f"p_{p}" for p in grp.params}
@@ -1560,8 +1397,6 @@ class _Gen:
                 hdr.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * i{i};")
             loop += vloop(hdr)
             loop.append("  }")
-        elif mode == "stencil":
-            loop += self._stencil_loop(k, vec, reg_decls, shift(body, -2))
         elif mode == "tma3":
             loop += self._tma3_loop(reg_decls, shift(body, -2))
         elif mode == "reduce":
@@ -1624,12 +1459,7 @@ class _Gen:
             loop.append("    const b2_ll ty = rem % tiles_y; rem /= tiles_y;")
             for i in reversed(range(1, k - 2)):
                 loop.append(f"    const b2_ll i{i} = rem % rl{i}; rem /= rl{i};")
-            if getattr(self, "reverse", False):
-                # march the plane chunks last-to-first: the previous sweep's
-                # final (still L2-resident) planes are read first
-                loop.append("    const b2_ll tz = tiles_z - 1 - rem;")
-            else:
-                loop.append("    const b2_ll tz = rem;")
+            loop.append("    const b2_ll tz = rem;")
             if (SLAB_PREFETCH if self.dyn0 else MARCH_PREFETCH) and k == 3:
                 loop += self._march_prefetch(vec, by, spec.align)
             loop.append(f"    const b2_ll i{y} = ty * {by} + threadIdx.y;")
@@ -1666,7 +1496,6 @@ class _Gen:
         npts = 1
         for r in self.const_ranges:
             npts *= r[2] if r is not None else 1 << 40
-        spec.reverse = bool(getattr(self, "reverse", False)) and mode == "march"
         spec.pdl = ((MARCH_PDL and mode in ("march", "tma3")) or (TILE_PDL and mode == "tile2")
                     or (SMALL_PDL and mode in ("flat", "reduce", "scalar")
                         and npts <= SMALL_PDL_POINTS)) and not self.dyn0
@@ -2074,10 +1903,9 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
 
 
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
-             init_const: dict | None = None, reverse: bool = False) -> KernelSpec:
+             init_const: dict | None = None) -> KernelSpec:
     gen = _Gen(planner, group, shapes, name)
     gen.init_const = dict(init_const or {})
-    gen.reverse = reverse
     spec = gen.build()
     spec.params = list(group.params)
     # reduction targets (container, point key) -> (exclusive, C type), for
@@ -2133,10 +1961,6 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         return (max(1, min(-(-n // 256), MAX_BLOCKS * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "tma3":
         return (spec.grid_cap, 1, 1), spec.block
-    if spec.mode == "stencil":
-        tk = (32 if k == 3 else 256) * spec.vec
-        nvb = -(-rl[k - 1] // tk) * (-(-rl[1] // 8) if k == 3 else 1) * -(-rl[0] // STENCIL_CHUNK)
-        return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), spec.block
     if spec.mode == "march":
         bx, by = spec.block[0], spec.block[1]
         nvb = -(-(rl[k - 1] + spec.align) // bx) * -(-rl[k - 2] // by) * -(-rl[0] // spec.vec)

@@ -11,9 +11,7 @@
 // running CTAs stream neighbouring rows; grid.y tiles columns in RP_CW chunks
 // whose v / acc slices live in shared memory; the next row is prefetched into
 // registers while the current row's dot is block-reduced.  Column partials go
-// to a workspace reduced by rp_finalize in a fixed order (deterministic);
-// with RP_COOP (cooperative launch, opt-in) the TMA variant folds them itself
-// after a grid barrier.
+// to a workspace reduced by rp_finalize in a fixed order (deterministic).
 //
 // The including translation unit defines RP_* constants, struct RpArgs and
 // the hooks rp_row_setup / rp_elem / rp_dot_vec / rp_coef / rp_store_dot.
@@ -95,35 +93,6 @@ __device__ __forceinline__ double rp_block_sum(double v, double vl, double *red,
     rp_dd_add(t, tl, red[parity * 32 + i], RP_COMP ? red[64 + parity * 32 + i] : 0.0);
   return RP_COMP ? t + tl : t;
 }
-
-#ifndef RP_COOP
-#define RP_COOP 0
-#endif
-#if RP_COOP && RP_COMP
-#error "RP_COOP folds plain column partials: build it with RP_COMP 0"
-#endif
-#if RP_COOP
-// Grid barrier for a cooperative launch (every CTA co-resident): one
-// arrival counter and a sense word, both back to the start state after use,
-// so the same state serves every launch (and graph replay).
-__device__ __forceinline__ void rp_grid_sync(unsigned *bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned *sense = bar + 1;
-    const unsigned s = *sense;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x * gridDim.y - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicExch(bar + 1, s ^ 1u);
-    } else {
-      while (*sense == s) __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-#endif
 
 #if RP_TMA
 // TMA variant: rows stream through an RP_S-deep ring of shared-memory row
@@ -232,33 +201,6 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
       if (RP_COMP) ws[(b2_ll)(RP_G + blockIdx.x) * RP_N + c0 + j] = accl[k];
     }
   }
-#if RP_COOP
-  // cooperative launch (one column tile): after the grid barrier every CTA
-  // folds a slice of the columns over the G partial rows in row order
-  rp_grid_sync((unsigned *)a.w[7]);
-  {
-    // this CTA's column slice; its threads split the G partial rows into
-    // RP_TPB / 64 strided groups, combined in group order (deterministic)
-    constexpr int CS = (int)((RP_N + RP_G - 1) / RP_G);
-    constexpr int NP = RP_TPB / 64;
-    static_assert(CS <= 64, "column slice wider than 64");
-    double *part = red;  // reuse the reduction scratch (64 doubles) + ring
-    const int col = tid & 63, grp = tid >> 6;
-    const b2_ll i = (b2_ll)blockIdx.x * CS + col;
-    double t = 0.0;
-    if (col < CS && i < RP_N)
-      for (int g = grp; g < RP_G; g += NP) t += __ldcg(ws + (b2_ll)g * RP_N + i);
-    __syncthreads();
-    ring[tid] = t;
-    __syncthreads();
-    if (grp == 0 && col < CS && i < RP_N) {
-      double u = ring[col];
-      for (int q = 1; q < NP; ++q) u += ring[q * 64 + col];
-      rp_store_axpy(a, i, u);
-    }
-    (void)part;
-  }
-#endif
 #endif
 }
 #else

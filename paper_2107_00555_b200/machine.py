@@ -41,9 +41,7 @@ DEVICE_BRANCHES = os.environ.get("B2_DEVICE_BRANCHES", "1") == "1"
 # a constant-fill map followed by a reduction over the same container starts
 # the reduction from the constant instead of launching the fill
 INIT_FUSION = os.environ.get("B2_INIT_FUSION", "1") == "1"
-SWEEP_ALTERNATE = os.environ.get("B2_SWEEP_ALTERNATE", "0") == "1"  # alternate march direction (slower: off)
 ZERO_SKIP = os.environ.get("B2_ZERO_SKIP", "1") == "1"  # skip zeroing fully overwritten transients
-FIN_PDL = os.environ.get("B2_FIN_PDL", "0") == "1"  # reduction fold kernels launched with PDL (neutral: off)
 
 
 class InterpreterError(RuntimeError):
@@ -221,19 +219,14 @@ class GpuExecutor:
             reg.spec = spec
         self.init_skip: set[int] = set()
         fused_init = self._init_fusions() if INIT_FUSION else {}
-        reverse = self._reverse_sweeps() if SWEEP_ALTERNATE else set()
         for op in self.planner.all_ops:
             if op.idx in self.planner.in_region:
                 continue
             if isinstance(op, P.MapGroup):
                 name = f"b2_map_{self.g.name}_{op.idx}"
                 spec = codegen.generate(self.planner, op, self.buf.shape, name,
-                                        init_const=fused_init.get(op.idx),
-                                        reverse=op.idx in reverse)
+                                        init_const=fused_init.get(op.idx))
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
-                if FIN_PDL and getattr(spec, "red_fin", None):
-                    # the fold kernel is a programmatic dependent launch
-                    src = "#undef B2_NO_PDL\n" + src
                 spec.kernel = rt.get_kernel(src, name, max_smem=spec.smem)
                 spec.fin_kernel = None
                 if getattr(spec, "red_fin", None):
@@ -247,7 +240,6 @@ class GpuExecutor:
                 self.specs[op.idx] = spec
             elif isinstance(op, P.LibOp) and op.rowpass is not None:
                 op.rowpass.compile(self)
-        self._compile_pairs()
         # private scratch sized for the largest grid of the owning kernel
         for idx, spec in self.specs.items():
             for n in spec.private:
@@ -255,25 +247,6 @@ class GpuExecutor:
                 threads = codegen.MAX_BLOCKS * 256
                 self.scratch[n] = self.buf.alloc(per * threads)
                 self.buf.nbytes[n + "#scratch"] = per * threads
-
-    def _reverse_sweeps(self) -> set:
-        """Every second march sweep of a state chain walks its plane chunks
-        last-to-first, so it starts on the planes the previous sweep wrote
-        last (still in L2); heat_3d's A->B / B->A pair alternates direction."""
-        pl = self.planner
-        out = set()
-        for ops in pl.ops.values():
-            k = 0
-            for op in ops:
-                if not isinstance(op, P.MapGroup) or op.idx in pl.in_region:
-                    continue
-                spec = codegen.generate(pl, op, self.buf.shape, "probe")
-                if spec.mode != "march" or spec.dyn0:
-                    continue
-                if k % 2:
-                    out.add(op.idx)
-                k += 1
-        return out
 
     def _const_fill(self, op):
         """(X, literal) when map group ``op`` only stores one constant into
@@ -339,88 +312,6 @@ class GpuExecutor:
                 out[b.idx] = {X: lit}
                 self.init_skip.add(a.idx)
         return out
-
-    def _compile_pairs(self):
-        """Temporal pairs of stencil sweeps (temporal.py): one kernel for
-        two consecutive groups, writing the second's output into a
-        ping-pong buffer the executor swaps in afterwards."""
-        from . import temporal
-
-        self.pairs: dict[int, tuple] = {}
-        self.pair_second: set[int] = set()
-        if self.planner.dynamic_p0 or any(isinstance(op, P.NestedOp)
-                                          for op in self.planner.all_ops):
-            return
-        for g1, g2, X, Y, o1, emin, emax in temporal.find_pairs(self.planner):
-            if g1.idx not in self.specs or g2.idx not in self.specs:
-                continue
-            name = f"b2_pair_{self.g.name}_{g1.idx}"
-            try:
-                spec = temporal.generate_pair(self.planner, g1, g2, X, Y, o1, emin, emax,
-                                              self.buf.shape, name)
-            except P.PlanError:
-                continue
-            alt = Y + "#alt"
-            if alt not in self.buf.ptr:
-                self.buf.ptr[alt] = self.buf.alloc(self.buf.nbytes[Y])
-                self.buf.nbytes[alt] = self.buf.nbytes[Y]
-            spec.kernel = rt.get_kernel(rt.family_source("prelude.cuh") + "\n" + spec.source,
-                                        name)
-            self.pairs[g1.idx] = (g2, spec, Y)
-            self.pair_second.add(g2.idx)
-
-    def _pp_begin(self):
-        self._pp_flip = {spec_y: False for (_, _, spec_y) in self.pairs.values()}
-        self._pp_synced: set = set()
-
-    def _pp_end(self):
-        """Leave every ping-ponged container in its original buffer (the
-        captured graph and the next upload/download use fixed addresses)."""
-        for y, flipped in getattr(self, "_pp_flip", {}).items():
-            if flipped:
-                alt = y + "#alt"
-                rt.check(rt.lib().b2_memcpy_d2d(self.buf.ptr[alt], self.buf.ptr[y],
-                                                self.buf.nbytes[y], self.stream), "pp copy")
-                self.buf.ptr[y], self.buf.ptr[alt] = self.buf.ptr[alt], self.buf.ptr[y]
-        self._pp_flip = {}
-
-    def _exec_pair(self, g1, sym, counters):
-        g2, spec, y = self.pairs[g1.idx]
-        rv1 = codegen.range_values(g1, sym)
-        rv2 = codegen.range_values(g2, sym)
-        if not self._check_bounds(self.specs[g1.idx], rv1, sym, g1.state.label,
-                                  f"map group {g1.idx}"):
-            return
-        if not self._check_bounds(self.specs[g2.idx], rv2, sym, g2.state.label,
-                                  f"map group {g2.idx}"):
-            return
-        alt = y + "#alt"
-        if y not in self._pp_synced:
-            # the pair writes only the interior of Y#alt: start it as a copy
-            rt.check(rt.lib().b2_memcpy_d2d(self.buf.ptr[alt], self.buf.ptr[y],
-                                            self.buf.nbytes[y], self.stream), "pp init")
-            self._pp_synced.add(y)
-        from . import temporal
-
-        grid, block = temporal.pair_geometry(spec)
-        blob = codegen.pack_args(spec, sym, rv2, self.buf.ptr, self.buf.strides, self.buf.size,
-                                 self.scratch, self.flag)
-        if self._prof is not None:
-            ev = self._prof_event_pair()
-            rt.lib().b2_event_record(ev[0], self.stream)
-        rt.launch(spec.kernel, grid, block, blob, self.stream)
-        if self._prof is not None:
-            rt.lib().b2_event_record(ev[1], self.stream)
-            n = 1
-            for _, _, k in rv2:
-                n *= k
-            self._prof.append((spec.name, 2 * n, ev))
-        self.launches += 1
-        self.buf.ptr[y], self.buf.ptr[alt] = self.buf.ptr[alt], self.buf.ptr[y]
-        self._pp_flip[y] = not self._pp_flip.get(y, False)
-        if counters is not None:
-            _count_map(self, g1, rv1, counters, sym)
-            _count_map(self, g2, rv2, counters, sym)
 
     def close(self):
         for host, _ in getattr(self, "_shell_stage", {}).values():
@@ -894,8 +785,6 @@ class GpuExecutor:
     def _run_states(self, counters, eager: bool):
         g = self.g
         sym = dict(self.bindings)
-        if not self._dry:
-            self._pp_begin()
         cur = g.start
         steps = 0
         while cur is not None:
@@ -934,8 +823,6 @@ class GpuExecutor:
             steps += 1
             if steps > self.opt.max_transitions:
                 raise InterpreterError("transition budget exceeded (infinite loop?)")
-        if not self._dry:
-            self._pp_end()
         if self.op_hook is not None and not self._dry:
             self.op_hook(None, set(), set(), "end")
 
@@ -1036,6 +923,7 @@ class GpuExecutor:
             if ft is not None:
                 for cname in self.planner.op_reads[op.idx] | self.planner.op_writes[op.idx]:
                     ft.setdefault(cname, op)
+        if self._dry:
             if isinstance(op, P.NestedOp):
                 self._exec_nested(op, sym, None, dry=True)
             elif (isinstance(op, P.LibOp) and op.kind == "comm" and self.comm is not None
@@ -1044,11 +932,6 @@ class GpuExecutor:
             return
         if self.root_only and self.comm.rank != 0 and op.idx in self.root_only:
             return  # root-resident data only (interp.py:343-359)
-        if op.idx in self.pair_second:
-            return  # ran inside the pair kernel of its predecessor
-        if op.idx in self.pairs:
-            self._exec_pair(op, sym, counters)
-            return
         if self.op_hook is not None:
             self.op_hook(op, self.planner.op_reads[op.idx], self.planner.op_writes[op.idx], "pre")
             self._exec_op_inner(op, sym, counters)
@@ -1140,8 +1023,7 @@ class GpuExecutor:
         if spec.fin_kernel is not None:
             fg = spec.red_nout if spec.red_fin_block else -(-spec.red_nout // 256)
             fg = max(1, min(fg, codegen.MAX_BLOCKS * 8))
-            rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream,
-                      pdl=FIN_PDL and self._prof is None)
+            rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream)
             self.launches += 1
         if self._prof is not None:
             rt.lib().b2_event_record(ev[1], self.stream)

@@ -178,25 +178,6 @@ def test_kernel_mode_selection():
     assert "reduce" in m.values()
 
 
-def test_temporal_pair_legality():
-    """temporal.pair_info accepts heat_3d's two sweeps (offsets in [0, 2],
-    write offset 1) and nothing in jacobi_2d's 2-D sweeps (3-D only)."""
-    from paper_2107_00555_b200 import plan as P, sdfg, temporal
-
-    g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
-    pl = P.Planner(g, {"N": 40, "TSTEPS": 5}).build()
-    ops = [op for op in pl.all_ops if isinstance(op, P.MapGroup)]
-    info = temporal.pair_info(pl, ops[0], ops[1])
-    assert info is not None
-    X, Y, o1, emin, emax = info
-    assert (X, Y, o1, emin, emax) == ("B", "A", (1, 1, 1), (0, 0, 0), (2, 2, 2))
-    assert temporal.pair_info(pl, ops[1], ops[0]) is not None  # A -> B is the same shape
-    g2 = sdfg.load(GOLDEN / "graphs" / "jacobi_2d.raw.json")
-    pl2 = P.Planner(g2, {"N": 40, "TSTEPS": 5}).build()
-    ops2 = [op for op in pl2.all_ops if isinstance(op, P.MapGroup)]
-    assert temporal.pair_info(pl2, ops2[0], ops2[1]) is None
-
-
 def test_rowpass_tma_selection():
     """atax / bicg rows stream through the TMA bulk-copy ring; gemver's
     prologue pass keeps the register-prefetch kernel; odd row pitches (not
@@ -386,6 +367,8 @@ def test_zero_skip_set_from_dry_run(name, syms, expect):
     ex.buf = machine._Buffers()
     ex.buf.shape = ex.planner.shapes(syms)
     ex._exec_nested = lambda op, sym, counters, dry=False: None
+    ex.pairs, ex.waves, ex._wave_elig, ex._wave_pending = {}, {}, {}, []
+    ex.init_skip, ex.specs = set(), {}
     ex._dead_on_entry()
     assert ex.zero_skip == expect
     assert "mx" not in ex.zero_skip

@@ -144,32 +144,6 @@ def test_tc_sgemm_3xtf32_vs_numpy(M, K, N, acc):
         L.b2_free(p)
 
 
-@pytest.mark.parametrize("N,T", [(40, 6), (67, 5)])
-def test_temporal_pair_bitwise(monkeypatch, N, T):
-    """Opt-in paired sweeps (temporal.py): one kernel for both heat_3d sweeps
-    with the ping-pong buffer swapped by the executor — bitwise equal to the
-    C oracle, also across repeated calls (graph replay)."""
-    from oracle import kernels_np as K
-    from paper_2107_00555_b200 import sdfg, temporal
-    from paper_2107_00555_b200.machine import GpuExecutor
-
-    monkeypatch.setattr(temporal, "TEMPORAL", True)
-    g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
-    ex = GpuExecutor(g, {"N": N, "TSTEPS": T})
-    assert ex.pairs, "heat_3d sweeps were not paired"
-    for seed in (1, 2):
-        rng = np.random.default_rng(seed)
-        A = rng.uniform(-1, 1, (N, N, N))
-        B = rng.uniform(-1, 1, (N, N, N))
-        keep = ex.prepare_inputs({"A": A, "B": B})
-        ex.run_device(first_call=True)
-        ex.sync()
-        del keep
-        K.heat_3d_c(A, B, T)
-        assert np.array_equal(ex.download("A"), A) and np.array_equal(ex.download("B"), B)
-    ex.close()
-
-
 @pytest.mark.parametrize("N,H,SM", [(2, 3, 1), (2, 3, 33), (1, 2, 64), (3, 1, 100)])
 def test_softmax_fold_and_rowred_vs_numpy_port(N, H, SM):
     """softmax raw graph: the max loop runs as a warp fold (incl. zero-trip and
