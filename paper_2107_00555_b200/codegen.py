@@ -59,6 +59,10 @@ SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
 ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "1"))  # unroll of the warp-per-row loop (4 spilled at 32 regs)
 ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowred kernels (softmax 1.11 -> 1.06 ms)
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
+# out[m, n] += X[m, k] * Y[k, n] maps (affine gathers, e.g. conv2d's 7-D WCR
+# map) as an implicit GEMM on the FP64 tensor path (DMMA)
+CONTRACT_MODE = os.environ.get("B2_CONTRACT", "1") == "1"
+CONTRACT_MIN_FMA = 1 << 22
 # 3-D stencil sweeps through a TMA plane ring (cp.async.bulk.tensor.3d into
 # shared memory, mbarrier-tracked, persistent balanced grid): the tma3 mode
 # (measured: heat_3d N=400 39.3 ms vs 37.3 for march at the best geometry
@@ -143,6 +147,267 @@ class _Gen:
         the constant the executor's fused init map would have stored."""
         lit = self.init_const.get(t.get("cont"))
         return f"(({t['ct']})({lit}))" if lit is not None else t["target"]
+
+    def _contraction_plan(self):
+        """``O[m(p), n] (+)= X[a(p)] * Y[b(p)]``: one scope, one tasklet that
+        is the product of its two inputs, a WCR-add output indexed by one
+        parameter per dimension (the output parameters), X and Y affine in
+        the parameters.  The output parameter that only Y uses is the GEMM's
+        N; the other output parameters (used by X, not by Y) are M; the rest
+        are K.  Returns the address coefficients or None."""
+        grp = self.group
+        if grp.schedule != "parallel" or len(grp.members) != 1:
+            return None
+        if any(r is None or r[2] < 1 for r in self.const_ranges):
+            return None
+        mem = grp.members[0]
+        kids = ([mem.tasklet] if mem.tasklet is not None else
+                list(P._scope_children(mem.state, mem.entry)))
+        if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet):
+            return None
+        t = kids[0]
+        if len(t.code) != 1 or len(t.ins) != 2:
+            return None
+        code = t.code[0][1]
+        if code[0] != "bin" or code[1] != "*" or {code[2], code[3]} != \
+                {("ref", t.ins[0]), ("ref", t.ins[1])}:
+            return None
+        ins = {e.dst_conn: e.memlet for e in mem.state.in_edges(t) if e.memlet is not None}
+        outs = [e.memlet for e in mem.state.out_edges(t) if e.memlet is not None]
+        if len(outs) != 1 or outs[0].wcr != "add" or set(ins) != set(t.ins):
+            return None
+        acc = {(c, w): (wcr, depth, pt)
+               for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params)}
+        if len(acc) != 3:
+            return None
+        params = list(grp.params)
+
+        def coeffs(cont, pt):
+            if pt is None or self.place(cont) != "memory" or self.g.containers[cont].dtype != "f64":
+                return None
+            st = _row_major(self.shapes[cont])
+            if len(pt) != len(st):
+                return None
+            cst, co = 0, {}
+            for d, (c0, terms) in enumerate(pt):
+                cst += st[d] * c0
+                for q, cq in terms:
+                    co[q] = co.get(q, 0) + st[d] * cq
+            return cst, co
+
+        oc = outs[0].container
+        wcr, depth, opt = acc.get((oc, True), (None, 1, None))
+        if wcr != "add" or depth != 0 or opt is None:
+            return None
+        xs = [ins[c].container for c in t.ins]
+        if len(set(xs)) != 2 or oc in xs:
+            return None
+        ca = [coeffs(c, acc[(c, False)][2]) for c in xs]
+        co_ = coeffs(oc, opt)
+        if None in ca or co_ is None or any(acc[(c, False)][1] != 0 for c in xs):
+            return None
+        pout = []
+        for c0, terms in opt:
+            if len(terms) != 1 or terms[0][1] != 1:
+                return None
+            pout.append(terms[0][0])
+        if len(set(pout)) != len(pout):
+            return None
+        used = [set(q for q, v in c[1].items() if v) for c in ca]
+        outs_ = [set(pout) & u for u in used]
+        if outs_[0] & outs_[1] or (outs_[0] | outs_[1]) != set(pout):
+            return None
+        # the operand indexed by a single output parameter carries N
+        yi = 1 if len(outs_[1]) == 1 else (0 if len(outs_[0]) == 1 else None)
+        if yi is None:
+            return None
+        xi = 1 - yi
+        npar = next(iter(outs_[yi]))
+        M = [q for q in params if q in pout and q != npar]
+        K = [q for q in params if q not in pout]
+        if not M or not K or any(q in used[yi] for q in M):
+            return None
+        ext = {q: self.const_ranges[params.index(q)][2] for q in params}
+        fma = 1
+        for q in params:
+            fma *= ext[q]
+        if fma < CONTRACT_MIN_FMA:
+            return None
+        return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
+                "M": M, "N": npar, "K": K, "ext": ext,
+                "rng": {q: self.const_ranges[params.index(q)] for q in params}}
+
+    def _contract_kernel(self, cp):
+        """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 m x TN n,
+        8 warps of 16 m rows; K in 32-wide chunks staged in shared memory
+        through affine gathers (address = row part + k part, both
+        precomputed), double-buffered through registers.  The accumulators
+        start from O's current value (the WCR add) and store once.  FP64
+        tensor ops fuse multiply and add: within 1e-12 of the sequential
+        reference sum, not bitwise."""
+        spec = self.spec
+        X, Y, O = cp["X"], cp["Y"], cp["O"]
+        Mp, Kp, Np = cp["M"], cp["K"], cp["N"]
+        ext, rng = cp["ext"], cp["rng"]
+
+        def decode(names, cst_co, idx):
+            """C expression: address part of a flat index over ``names``
+            (mixed radix, last name fastest)."""
+            _, co = cst_co
+            rem = idx
+            out = []
+            for i, q in enumerate(reversed(names)):
+                e = ext[q]
+                v = f"(({rem}) % {e}u)" if i < len(names) - 1 else f"({rem})"
+                rem = f"(({rem}) / {e}u)"
+                val = f"({rng[q][0]}LL + {rng[q][1]}LL * (long long){v})"
+                c = co.get(q, 0)
+                if c:
+                    out.append(f"{c}LL * {val}")
+            return " + ".join(out) if out else "0LL"
+
+        Mtot = 1
+        for q in Mp:
+            Mtot *= ext[q]
+        Ktot = 1
+        for q in Kp:
+            Ktot *= ext[q]
+        Ntot = ext[Np]
+        TN = 8 * min(4, -(-Ntot // 8))
+        NF = TN // 8
+        ax, ay, ao = (self.arg(("ptr", X)), self.arg(("ptr", Y)), self.arg(("ptr", O)))
+        for c in (X, Y, O):
+            self.cont(c)
+        cyn = cp["cy"][1].get(Np, 0)
+        con = cp["co"][1].get(Np, 0)
+        L = [f"// generated by paper_2107_00555_b200.codegen: contraction (DMMA implicit GEMM) "
+             f"M={Mtot} N={Ntot} K={Ktot}",
+             "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)),
+             "namespace {",
+             "constexpr int TM = 128, BK = 16, TN = %d, NF = %d, APAD = 4, BPAD = 4;" % (TN, NF),
+             f"constexpr long long MT = {Mtot}LL, NT = {Ntot}LL, KT = {Ktot}LL;",
+             "__device__ __forceinline__ void b2c_dmma(double (&d)[4], double a0, double a1, "
+             "double b0) {",
+             '  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, '
+             '{%4,%5}, {%6}, {%0,%1,%2,%3};\\n" : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3]) '
+             ': "d"(a0), "d"(a1), "d"(b0));',
+             "}",
+             "__device__ __forceinline__ long long b2c_mx(unsigned m) { return "
+             + decode(Mp, cp["cx"], "m") + "; }",
+             "__device__ __forceinline__ long long b2c_kx(unsigned k) { return "
+             + decode(Kp, cp["cx"], "k") + "; }",
+             "__device__ __forceinline__ long long b2c_ky(unsigned k) { return "
+             + decode(Kp, cp["cy"], "k") + "; }",
+             "__device__ __forceinline__ long long b2c_mo(unsigned m) { return "
+             + decode(Mp, cp["co"], "m") + "; }",
+             "}  // namespace",
+             f'extern "C" __global__ void __launch_bounds__(256) {spec.name}'
+             f"(const __grid_constant__ B2Args a) {{",
+             "  B2_PDL_ENTRY();",
+             f"  const double *__restrict__ X = (const double *){ax} + {cp['cx'][0]}LL;",
+             f"  const double *__restrict__ Y = (const double *){ay} + {cp['cy'][0]}LL;",
+             f"  double *__restrict__ O = (double *){ao} + {cp['co'][0]}LL;",
+             "  __shared__ __align__(16) double As[2][TM][BK + APAD];",
+             "  __shared__ __align__(16) double Bs[2][BK][TN + BPAD];",
+             "  __shared__ long long sMX[TM];",
+             "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;",
+             "  const int g = lane >> 2, t = lane & 3;",
+             "  const long long ntiles = (NT + TN - 1) / TN;",
+             "  for (long long tile = blockIdx.x; tile < ((MT + TM - 1) / TM) * ntiles; "
+             "tile += gridDim.x) {",
+             "    const long long m0 = (tile / ntiles) * TM, n0 = (tile % ntiles) * TN;",
+             "    __syncthreads();",
+             "    if (tid < TM) sMX[tid] = (m0 + tid < MT) ? b2c_mx((unsigned)(m0 + tid)) : 0LL;",
+             "    __syncthreads();",
+             # staging: A element e = tid + 256 r: row e / BK, col e % BK
+             "    double ra[TM * BK / 256], rb[BK * TN / 256 > 0 ? BK * TN / 256 : 1];",
+             "    auto load = [&](long long k0) {",
+             "      // a thread stages one k column of A (8 rows) and one element of B",
+             "      const int acol = tid % BK;",
+             "      const long long ka = k0 + acol;",
+             "      const long long kx = ka < KT ? b2c_kx((unsigned)ka) : 0LL;",
+             "#pragma unroll",
+             "      for (int r = 0; r < TM * BK / 256; ++r) {",
+             "        const int row = tid / BK + (256 / BK) * r;",
+             "        ra[r] = (m0 + row < MT && ka < KT) ? X[sMX[row] + kx] : 0.0;",
+             "      }",
+             "#pragma unroll",
+             "      for (int r = 0; r < (BK * TN + 255) / 256; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        if (e < BK * TN) {",
+             "          const int row = e / TN, col = e % TN;",
+             "          const long long k = k0 + row, n = n0 + col;",
+             f"          rb[r] = (k < KT && n < NT) ? Y[b2c_ky((unsigned)k) + {cyn}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             "        }",
+             "      }",
+             "    };",
+             "    auto store = [&](int buf) {",
+             "#pragma unroll",
+             "      for (int r = 0; r < TM * BK / 256; ++r) {",
+             "        As[buf][tid / BK + (256 / BK) * r][tid % BK] = ra[r];",
+             "      }",
+             "#pragma unroll",
+             "      for (int r = 0; r < (BK * TN + 255) / 256; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        if (e < BK * TN) Bs[buf][e / TN][e % TN] = rb[r];",
+             "      }",
+             "    };",
+             # accumulators start from O (the WCR add)
+             "    double acc[NF][4];",
+             "    const int wm = warp * 16;",
+             "#pragma unroll",
+             "    for (int f = 0; f < NF; ++f)",
+             "#pragma unroll",
+             "      for (int h = 0; h < 2; ++h)",
+             "#pragma unroll",
+             "        for (int e2 = 0; e2 < 2; ++e2) {",
+             "          const long long m = m0 + wm + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
+             f"          acc[f][2 * h + e2] = (m < MT && n < NT) ? O[b2c_mo((unsigned)m) + {con}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             "        }",
+             "    load(0);",
+             "    store(0);",
+             "    __syncthreads();",
+             "    const long long nk = (KT + BK - 1) / BK;",
+             "    for (long long kc = 0; kc < nk; ++kc) {",
+             "      const int cur = (int)(kc & 1);",
+             "      if (kc + 1 < nk) load((kc + 1) * BK);",
+             "#pragma unroll",
+             "      for (int k4 = 0; k4 < BK; k4 += 4) {",
+             "        const double a0 = As[cur][wm + g][k4 + t], a1 = As[cur][wm + g + 8][k4 + t];",
+             "#pragma unroll",
+             "        for (int f = 0; f < NF; ++f) b2c_dmma(acc[f], a0, a1, Bs[cur][k4 + t][f * 8 + g]);",
+             "      }",
+             "      if (kc + 1 < nk) store(cur ^ 1);",
+             "      __syncthreads();",
+             "    }",
+             "#pragma unroll",
+             "    for (int f = 0; f < NF; ++f)",
+             "#pragma unroll",
+             "      for (int h = 0; h < 2; ++h)",
+             "#pragma unroll",
+             "        for (int e2 = 0; e2 < 2; ++e2) {",
+             "          const long long m = m0 + wm + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
+             f"          if (m < MT && n < NT) O[b2c_mo((unsigned)m) + {con}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] = acc[f][2 * h + e2];",
+             "        }",
+             "  }",
+             "}"]
+        # host-side bounds checks of the three memlets (as the generic body's)
+        mem = self.group.members[0]
+        menv = {mp: f"p_{gp}" for mp, gp in mem.rename.items()}
+        t = next(iter(P._scope_children(mem.state, mem.entry))) if mem.tasklet is None \
+            else mem.tasklet
+        for e in mem.state.in_edges(t) + mem.state.out_edges(t):
+            if e.memlet is not None:
+                spec.checks.append((e.memlet.container, e.memlet.subset, menv))
+        spec.source = "\n".join(L) + "\n"
+        spec.block = (256, 1, 1)
+        spec.vec = 1
+        spec.pdl = False
+        spec.contract = {"M": Mtot, "N": Ntot, "K": Ktot, "TN": TN}
+        return spec
 
     def _reduction_plan(self):
         """Reduction schedule for a parallel map whose only HBM writes are WCR
@@ -1165,6 +1430,11 @@ class _Gen:
                 mode = force
         if mode != "tma3":
             self.stencil = {}
+        if mode in ("flat", "tile2", "march") and CONTRACT_MODE and k >= 2:
+            cp = self._contraction_plan()
+            if cp is not None:
+                spec.mode = "contract"
+                return self._contract_kernel(cp)
         if mode in ("flat", "tile2", "march") and REDUCE_MODE:
             rp = self._reduction_plan()
             if rp is not None:
@@ -1961,6 +2231,10 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         return (max(1, min(-(-n // 256), MAX_BLOCKS * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "tma3":
         return (spec.grid_cap, 1, 1), spec.block
+    if spec.mode == "contract":
+        c = spec.contract
+        tiles = -(-c["M"] // 128) * -(-c["N"] // c["TN"])
+        return (max(1, min(tiles, 148 * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "march":
         bx, by = spec.block[0], spec.block[1]
         nvb = -(-(rl[k - 1] + spec.align) // bx) * -(-rl[k - 2] // by) * -(-rl[0] // spec.vec)

@@ -166,14 +166,23 @@ def test_kernel_mode_selection():
     m, _, _ = _modes("conv2d_bias.auto", {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16,
                                           "K": 20, "HO": 237, "WO": 237})
     assert "reduce" in m.values()
-    # raw conv2d: the output channel (CO=16) is register-blocked per thread
+    # raw conv2d: the 7-D WCR map is a contraction out[m, c] += inp[m, k] *
+    # w[k, c] -> implicit GEMM on DMMA (M = 8*237*237, N = 16, K = 20*20*3);
+    # with the contraction mode off, the output channel is register-blocked
     from paper_2107_00555_b200 import codegen, plan as P, sdfg
     syms = {"NB": 8, "H": 256, "W": 256, "CI": 3, "CO": 16, "K": 20, "HO": 237, "WO": 237}
     g = sdfg.load(GOLDEN / "graphs" / "conv2d_bias.raw.json")
     pl = P.Planner(g, syms).build()
-    srcs = [codegen.generate(pl, op, pl.shapes(syms), f"k{op.idx}").source
-            for op in pl.all_ops if isinstance(op, P.MapGroup)]
-    assert any("_v[16]" in s_ and "NOUTB = 449352LL" in s_ for s_ in srcs)
+    grp = [op for op in pl.all_ops if isinstance(op, P.MapGroup)][1]
+    sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")
+    assert sp.mode == "contract" and sp.contract == {"M": 449352, "N": 16, "K": 1200, "TN": 16}
+    assert "mma.sync.aligned.m16n8k4.row.col.f64" in sp.source
+    codegen.CONTRACT_MODE = False
+    try:
+        sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")
+    finally:
+        codegen.CONTRACT_MODE = True
+    assert sp.mode == "reduce" and "_v[16]" in sp.source and "NOUTB = 449352LL" in sp.source
     m, _, _ = _modes("go_fast.pipe", {"N": 12000})
     assert "reduce" in m.values()
 

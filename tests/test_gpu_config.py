@@ -7,8 +7,7 @@ NPBench programs use the bitwise-pinned numpy port, see the generator).
 Criteria, per output (tolerances written here, north_star: rtol 1e-12 f64,
 1e-5 f32):
 * BITWISE outputs (fixed op order on both sides: stencils, the elementwise
-  gemver update, conv2d's sequential accumulation): sha256 of the whole
-  array equal to the reference's.
+  gemver update): sha256 of the whole array equal to the reference's.
 * fixed-order outputs: rel_err (pkg/tests/conftest.py:85-93, floor 1) at
   the digest points <= rtol and row sums within rtol (relative to the row's
   sum of magnitudes).
@@ -36,8 +35,9 @@ pytestmark = pytest.mark.gpu
 CFG = GOLDEN / "config"
 CONFIGS = sorted(p.stem for p in CFG.glob("*.json")) if CFG.is_dir() else []
 
-BITWISE = {"jacobi_2d": {"A", "B"}, "heat_3d": {"A", "B"}, "gemver": {"A"},
-           "conv2d_bias": {"out"}}
+# (conv2d_bias runs on the FP64 tensor path since round 2: DMMA fuses the
+# multiply-adds, so its result is within rtol, no longer bitwise)
+BITWISE = {"jacobi_2d": {"A", "B"}, "heat_3d": {"A", "B"}, "gemver": {"A"}}
 F64_RTOL = 1e-12
 F32_RTOL = 1e-5
 
