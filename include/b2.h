@@ -176,6 +176,17 @@ B2_API int b2_gemm_f32(int64_t M, int64_t N, int64_t K, const float *A, int64_t 
 B2_API int b2_gemm_f32_f64acc(int64_t M, int64_t N, int64_t K, const float *A, int64_t rsa,
                               const float *B, int64_t rsb, float *C, int64_t rsc, int wcr,
                               void *stream);
+/* 3xTF32 operands split once (SUMMA f32): A' (M x Kp) / B'^T (N x Kp) in the
+ * CTA-pair kernel's two-segment layout, Kp = b2_tf32_split_cols(K); then
+ * C (=|+=) A @ B from the split operands.  A k-panel of a split operand is
+ * itself a split operand of the panel's K when panels are 32-aligned. */
+B2_API int64_t b2_tf32_split_cols(int64_t K);
+B2_API int b2_tf32_split_a(const float *A, int64_t lda, int64_t M, int64_t K, float *Ap,
+                           void *stream);
+B2_API int b2_tf32_split_bt(const float *B, int64_t ldb, int64_t K, int64_t N, float *Bt,
+                            void *stream);
+B2_API int b2_gemm_f32_presplit(int64_t M, int64_t N, int64_t K, const float *Ap, const float *Bt,
+                                float *C, int64_t ldc, int accumulate, void *stream);
 /* out (wcr)= op-reduce of `in` over the dims flagged in axes_mask (bit d),
  * output enumerated row-major over the kept dims (ufunc.reduce semantics). */
 B2_API int b2_reduce(const b2_view_t *out, const b2_view_t *in, unsigned axes_mask, int op, int wcr,

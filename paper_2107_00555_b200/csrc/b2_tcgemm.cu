@@ -628,6 +628,66 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
   return B2_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Pre-split operands (SUMMA f32: split each local block ONCE per call, then
+// broadcast and multiply the split panels).  Layouts are those the CTA-pair
+// kernel reads: A' = M x Kp, B'^T = N x Kp, Kp = ceil(K / 32) * 2 * 32,
+// per 32-wide k block [lo | hi] (A) and [hi | lo] (B).
+
+extern "C" int64_t b2_tf32_split_cols(int64_t K) { return (K + TK - 1) / TK * 2 * TK; }
+
+extern "C" int b2_tf32_split_a(const float *A, int64_t lda, int64_t M, int64_t K, float *Ap,
+                               void *stream) {
+  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * 2 * TK;
+  const unsigned ry = (unsigned)((M + 7) / 8 < 2048 ? (M + 7) / 8 : 2048);
+  B2_CLEAR_ERROR();
+  split_a<<<dim3((unsigned)nkb, ry), dim3(32, 8), 0, (cudaStream_t)stream>>>(A, lda, M, K, Kp, 2,
+                                                                             Ap);
+  B2_LAUNCH_CHECK("split_a");
+  return B2_OK;
+}
+
+extern "C" int b2_tf32_split_bt(const float *B, int64_t ldb, int64_t K, int64_t N, float *Bt,
+                                void *stream) {
+  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * 2 * TK;
+  B2_CLEAR_ERROR();
+  split_bt<<<dim3((unsigned)((N + 31) / 32), (unsigned)nkb), dim3(32, 8), 0,
+             (cudaStream_t)stream>>>(B, ldb, K, N, Kp, 2, Bt);
+  B2_LAUNCH_CHECK("split_bt");
+  return B2_OK;
+}
+
+// C (row stride ldc) (=|+=) A @ B from split operands (tcgen05 CTA pairs)
+extern "C" int b2_gemm_f32_presplit(int64_t M, int64_t N, int64_t K, const float *Ap,
+                                    const float *Bt, float *C, int64_t ldc, int accumulate,
+                                    void *stream) {
+  static int group_m = -1;
+  if (group_m < 0) {
+    const char *e = getenv("B2_TC_GROUP");
+    group_m = e ? atoi(e) : 4;
+    if (group_m < 1) group_m = 1;
+  }
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(tc_sgemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             P_SMEM_BYTES) != cudaSuccess)
+      return b2_fail(B2_ERR_CUDA, "tc sgemm smem attribute");
+    attr = true;
+  }
+  const int64_t nkb = (K + TK - 1) / TK, Kp = nkb * 2 * TK;
+  CUtensorMap pa, pb;
+  int rc = make_map(&pa, Ap, (uint64_t)Kp, (uint64_t)M, 128);
+  if (rc) return rc;
+  rc = make_map(&pb, Bt, (uint64_t)Kp, (uint64_t)N, 128);
+  if (rc) return rc;
+  const int pm = (int)((M + 255) / 256), pn = (int)((N + 255) / 256);
+  B2_CLEAR_ERROR();
+  tc_sgemm_pair<<<2 * pm * pn, THREADS, P_SMEM_BYTES, (cudaStream_t)stream>>>(
+      pa, pb, M, N, (int)nkb, (int)tc_chunk_kblocks(), C, ldc, accumulate, pm, pn, group_m);
+  B2_LAUNCH_CHECK("tc sgemm pair (presplit)");
+  return B2_OK;
+}
+
 int b2_sgemm_tc_enabled() {
   static int on = -1;
   if (on < 0) {

@@ -317,6 +317,10 @@ class GpuExecutor:
         for host, _ in getattr(self, "_shell_stage", {}).values():
             rt.lib().b2_host_unregister(host.ctypes.data)
         self._shell_stage = {}
+        for arr in (getattr(self, "_pinned_out", None) or {}).values():
+            if arr.nbytes:  # the arrays stay valid (pageable) for their holders
+                rt.lib().b2_host_unregister(arr.ctypes.data)
+        self._pinned_out = None
         if self.graph_exec is not None:
             rt.lib().b2_graph_destroy(self.graph_exec)
             self.graph_exec = None
@@ -723,26 +727,34 @@ class GpuExecutor:
         rt.check(rt.lib().b2_event_create(ctypes.byref(b)), "event")
         return a.value, b.value
 
-    def profile_launches(self) -> dict:
-        """One eager pass with a CUDA-event pair around every map-kernel
-        launch on the executor's stream.  Returns {kernel: (launches,
-        total_ms, points_per_launch)}."""
-        self._prof = []
-        try:
-            rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
-            self._run_states(None, eager=True)
-            self.sync()
-            out: dict = {}
-            for name, npts, (a, b) in self._prof:
-                ms = ctypes.c_float()
-                rt.check(rt.lib().b2_event_elapsed_ms(a, b, ctypes.byref(ms)), "elapsed")
-                n, tot, _ = out.get(name, (0, 0.0, npts))
-                out[name] = (n + 1, tot + ms.value, npts)
-                rt.lib().b2_event_destroy(a)
-                rt.lib().b2_event_destroy(b)
-            return out
-        finally:
-            self._prof = None
+    def profile_launches(self, passes: int = 3) -> dict:
+        """Eager passes with a CUDA-event pair around every kernel launch on
+        the executor's stream; per kernel the MEDIAN over the passes of its
+        per-pass total (the first pass after capture runs cold).  Returns
+        {kernel: (launches per pass, total_ms per pass, points_per_launch)}."""
+        runs = []
+        for _ in range(max(1, passes)):
+            self._prof = []
+            try:
+                rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
+                self._run_states(None, eager=True)
+                self.sync()
+                out: dict = {}
+                for name, npts, (a, b) in self._prof:
+                    ms = ctypes.c_float()
+                    rt.check(rt.lib().b2_event_elapsed_ms(a, b, ctypes.byref(ms)), "elapsed")
+                    n, tot, _ = out.get(name, (0, 0.0, npts))
+                    out[name] = (n + 1, tot + ms.value, npts)
+                    rt.lib().b2_event_destroy(a)
+                    rt.lib().b2_event_destroy(b)
+                runs.append(out)
+            finally:
+                self._prof = None
+        med = {}
+        for name, (n, _, npts) in runs[0].items():
+            tots = sorted(r[name][1] for r in runs if name in r)
+            med[name] = (n, tots[len(tots) // 2], npts)
+        return med
 
     def _instantiate_children(self):
         """Walk the state machine without launching anything so nested
@@ -1120,9 +1132,15 @@ class GpuExecutor:
         rsc, csc = _out_strides(cd, M, N)
         if rsc is None:
             raise P.PlanError("matmul output view is not an affine image of the result")
+        if self._prof is not None:
+            ev = self._prof_event_pair()
+            rt.lib().b2_event_record(ev[0], self.stream)
         rt.check(rt.lib().b2_gemm_f64(M, N, K, ab + 8 * ao, rsa, csa, bb + 8 * bo, rsb, csb,
                                       cb + 8 * co, rsc, csc, rt.WCR_CODE[om.wcr], self.stream),
                  "gemm")
+        if self._prof is not None:
+            rt.lib().b2_event_record(ev[1], self.stream)
+            self._prof.append((f"b2_gemm_f64[{M}x{N}x{K}]", M * N, ev))
         self.launches += 1
         if counters is not None:
             counters.bytes_moved += 8 * (M * K + K * N + M * N)

@@ -83,7 +83,8 @@ EXPORTS = [
     "b2_graph_destroy", "b2_copy_view", "b2_fill_view", "b2_gemm_f64", "b2_gemm_f32",
     "b2_reduce", "b2_nccl_unique_id", "b2_nccl_init", "b2_nccl_destroy", "b2_nccl_group_p2p",
     "b2_nccl_bcast", "b2_nccl_allreduce_f64", "b2_tensor_map_f64",
-    "b2_gemm_f32_f64acc",
+    "b2_gemm_f32_f64acc", "b2_tf32_split_cols", "b2_tf32_split_a", "b2_tf32_split_bt",
+    "b2_gemm_f32_presplit",
 ]
 
 
@@ -163,6 +164,11 @@ _SIGS = {
     "b2_nccl_group_p2p": ([_vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "b2_nccl_bcast": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
     "b2_nccl_allreduce_f64": ([_vp, _vp, ctypes.c_size_t, ctypes.c_int, _vp], ctypes.c_int),
+    "b2_tf32_split_cols": ([_i64], _i64),
+    "b2_tf32_split_a": ([_vp, _i64, _i64, _i64, _vp, _vp], ctypes.c_int),
+    "b2_tf32_split_bt": ([_vp, _i64, _i64, _i64, _vp, _vp], ctypes.c_int),
+    "b2_gemm_f32_presplit": ([_i64, _i64, _i64, _vp, _vp, _vp, _i64, ctypes.c_int, _vp],
+                             ctypes.c_int),
     "b2_gemm_f32_f64acc": ([_i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int,
                             _vp], ctypes.c_int),
     "b2_tensor_map_f64": ([_vp, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),

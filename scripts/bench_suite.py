@@ -152,6 +152,54 @@ def run_one(name, reps):
         res["frac_of_measured_hbm"] = rate / 1e9 / hbm
     elif unit == "flop":
         res["TFLOPs"] = rate / 1e12
+    res["step_share_top"] = top[1][1] / ms if ms else None
+    # roofline of the dominant kernel against the measured ceiling of its bound
+    extra = _extra_peaks()
+    if top[0] is not None and top[1][1] > 0:
+        npts = top[1][2] * top[1][0]
+        if bound == "hbm":
+            # the kernel's share of the run's algorithmic bytes (by points)
+            tot_pts = sum(n * pp for (n, _, pp) in prof.values()) or npts
+            kb = work * npts / tot_pts
+            ach = kb / (top[1][1] / 1e3) / 1e9
+            l2 = name == "jacobi_2d"  # 2 x 32 MB stay in the 126 MB L2 across sweeps
+            pk = extra.get("l2_read_gbs", 16190.1) if l2 else hbm
+            res["roofline"] = {"bound": "l2" if l2 else "hbm", "achieved": ach, "peak": pk,
+                               "unit": "GB/s", "frac": ach / pk, "peak_kind": "measured",
+                               "kernel": top[0]}
+        elif unit == "flop":
+            # (the run's flops are the dominant kernel's: matmul / conv2d)
+            pk = extra.get("dmma_f64_tflops", 37.13)
+            ach = work / (top[1][1] / 1e3) / 1e12
+            res["roofline"] = {"bound": "fp64_tensor", "achieved": ach, "peak": pk,
+                               "unit": "TFLOP/s", "frac": ach / pk, "peak_kind": "measured",
+                               "kernel": top[0]}
+    # end to end through interpret(): pinned host inputs, H2D + D2H timed
+    from paper_2107_00555_b200 import ExecContext, InterpOptions, interpret
+
+    host = {k: np.ascontiguousarray(v) if np.ndim(v) else v for k, v in inputs.items()}
+    for v in host.values():
+        if np.ndim(v) and v.nbytes:
+            L.b2_host_register(v.ctypes.data, v.nbytes)
+    ctx = ExecContext(bindings=dict(syms)).bind_inputs(host)
+    opts = InterpOptions(pinned_outputs=True)
+    out = interpret(g, ctx, opts)
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        out = interpret(g, ctx, opts)
+        ts.append(time.perf_counter() - t)
+    e2e_s = float(np.median(ts))
+    res["e2e"] = {"value": work / e2e_s / (1e9 if unit == "B" else 1.0), "unit":
+                  "GB/s" if unit == "B" else f"{unit}/s", "ms_per_run": e2e_s * 1e3,
+                  "d2h_bytes": int(sum(np.asarray(v).nbytes for v in out.values()))}
+    for v in host.values():
+        if np.ndim(v) and v.nbytes:
+            L.b2_host_unregister(v.ctypes.data)
+    from paper_2107_00555_b200 import machine as _m
+
+    while _m._exec_cache:
+        _m._exec_cache.popitem()[1].close()
     cpu = cpu_port(name, syms, inputs)
     if cpu is not None:
         res["cpu_port"] = {"rate": cpu[0], "seconds": cpu[1], "sample": cpu[2], "cores": 1,
@@ -159,6 +207,11 @@ def run_one(name, reps):
         res["speedup_vs_cpu_port"] = rate / cpu[0]
     ex.close()
     return res
+
+
+def _extra_peaks() -> dict:
+    p = ROOT / "profiles" / "measured_peaks_extra.json"
+    return json.loads(p.read_text()) if p.exists() else {}
 
 
 def main():

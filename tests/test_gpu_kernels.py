@@ -260,3 +260,40 @@ def test_fully_overwritten_transients_not_zeroed():
     out = _run("atax.raw", {"M": 300, "N": 200}, {"A": A, "x": x, "y": np.zeros(200)})
     ref = K.atax(A.copy(), x.copy(), np.zeros(200))
     assert rel_err(out["y"], ref["y"]) <= 1e-12
+
+
+def test_tf32_presplit_gemm_equals_gemm_f32():
+    """b2_tf32_split_a / _bt + b2_gemm_f32_presplit (SUMMA f32's split-once
+    path) is the same computation as b2_gemm_f32: bitwise equal output."""
+    import ctypes
+
+    from paper_2107_00555_b200 import runtime as rt
+
+    L = rt.lib()
+    M, N, K = 512, 768, 640
+    rng = np.random.default_rng(9)
+    A = rng.uniform(-1, 1, (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (K, N)).astype(np.float32)
+    kp = L.b2_tf32_split_cols(K)
+    sizes = (A.nbytes, B.nbytes, M * N * 4, M * N * 4, M * kp * 4, N * kp * 4)
+    ptr = [ctypes.c_void_p() for _ in sizes]
+    for p, nb in zip(ptr, sizes):
+        rt.check(L.b2_malloc(ctypes.byref(p), nb))
+    try:
+        rt.check(L.b2_memcpy_h2d(ptr[0], A.ctypes.data, A.nbytes, None))
+        rt.check(L.b2_memcpy_h2d(ptr[1], B.ctypes.data, B.nbytes, None))
+        rt.check(L.b2_gemm_f32(M, N, K, ptr[0], K, 1, ptr[1], N, 1, ptr[2], N, 1, 0, None))
+        rt.check(L.b2_tf32_split_a(ptr[0], K, M, K, ptr[4], None))
+        rt.check(L.b2_tf32_split_bt(ptr[1], N, K, N, ptr[5], None))
+        rt.check(L.b2_gemm_f32_presplit(M, N, K, ptr[4], ptr[5], ptr[3], N, 0, None))
+        c1 = np.empty((M, N), np.float32)
+        c2 = np.empty((M, N), np.float32)
+        rt.check(L.b2_memcpy_d2h(c1.ctypes.data, ptr[2], c1.nbytes, None))
+        rt.check(L.b2_memcpy_d2h(c2.ctypes.data, ptr[3], c2.nbytes, None))
+        rt.check(L.b2_device_sync())
+        assert np.array_equal(c1, c2)
+        ref = A.astype(np.float64) @ B.astype(np.float64)
+        assert np.linalg.norm(c2 - ref) / np.linalg.norm(ref) <= 1e-5
+    finally:
+        for p in ptr:
+            L.b2_free(p)
