@@ -227,7 +227,7 @@ class RankMachine(I.Machine):
 
 def sim_run(g, grid_dims, bindings, store, rank_bindings=None):
     """(rank 0's outputs, per-rank counters) of ``g`` on P logical ranks."""
-    from paper_2107_00555_b200 import distribute as DI
+    from paper_2107_00555_b200 import distribution as DI
 
     doc = g if isinstance(g, dict) else None
     g = sdfg.as_graph(g)

@@ -19,9 +19,20 @@ from .machine import (  # noqa: F401
 from .plan import PlanError  # noqa: F401
 from .runtime import BackendUnavailable  # noqa: F401
 from . import sdfg  # noqa: F401
+from . import validate  # noqa: F401  (validate.validate(g): ir.validate restated)
+from .dist import ProcessGrid  # noqa: F401
+from .distribution import (  # noqa: F401
+    distribute, distribute_elementwise, distribution_pipeline, expand_matmul_distributed,
+    remove_redundant_comm,
+)
+from .simrun import CollectiveOrderError, DeadlockError, RankSim, SimError, sim_run  # noqa: F401
+from .expansions import b200_registry, install as install_expansions  # noqa: F401
 
 __all__ = [
     "interpret", "ExecContext", "InterpOptions", "Counters", "InterpreterError",
     "OutOfBoundsError", "GpuExecutor", "get_executor", "PlanError", "BackendUnavailable", "sdfg",
-    "run_twice_determinism",
+    "run_twice_determinism", "validate", "ProcessGrid", "distribute", "distribute_elementwise",
+    "distribution_pipeline", "expand_matmul_distributed", "remove_redundant_comm", "sim_run",
+    "RankSim", "DeadlockError", "SimError", "CollectiveOrderError", "b200_registry",
+    "install_expansions",
 ]

@@ -29,7 +29,7 @@ import threading
 
 import numpy as np
 
-from . import comm as C, distribute as DI, runtime as rt, sdfg
+from . import comm as C, distribution as DI, runtime as rt, sdfg
 
 DeadlockError = C.DeadlockError
 SimError = C.SimError

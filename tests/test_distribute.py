@@ -60,7 +60,7 @@ def test_distribution_soundness(name, gdims):
     """test_dist.py:194-200: distributed == shared memory (<= 1e-12 here;
     the reference allows 1e-6)."""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D, sdfg
+    from paper_2107_00555_b200 import distribution as D, sdfg
 
     syms = DIST_SYMBOLS[name]
     ins = _inputs(sdfg.from_dict(_doc(name)), syms)
@@ -71,7 +71,7 @@ def test_distribution_soundness(name, gdims):
 
 
 def test_distributed_graphs_validate():
-    from paper_2107_00555_b200 import distribute as D, sdfg, validate
+    from paper_2107_00555_b200 import distribution as D, sdfg, validate
 
     for name in DIST_SYMBOLS:
         for gd in GRIDS:
@@ -82,7 +82,7 @@ def test_distributed_graphs_validate():
 def test_fig7_shape():
     """tmp0 = alpha*A on 2x2 -> Bcast(alpha), BlockScatter(A),
     local map, BlockGather(tmp0)."""
-    from paper_2107_00555_b200 import distribute as D
+    from paper_2107_00555_b200 import distribution as D
 
     doc, rep = D.distribute(_doc("dist_alpha"), (2, 2))
     kinds = sorted(n["kind"] for st in doc["states"] for n in st["nodes"]
@@ -96,7 +96,7 @@ def test_fig7_shape():
 def test_flat_scatter_chunks():
     """test_dist.py:43-52: a dense 1-D map scatters flat chunks."""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D
+    from paper_2107_00555_b200 import distribution as D
 
     doc, _ = D.distribution_pipeline(_doc("dist_flat"), (4, 1))
     kinds = {n["kind"] for st in doc["states"] for n in st["nodes"] if n["type"] == "library"}
@@ -108,7 +108,7 @@ def test_flat_scatter_chunks():
 
 def test_uneven_block_extent_fails():
     """test_dist.py:64-73: no implicit padding."""
-    from paper_2107_00555_b200 import distribute as D
+    from paper_2107_00555_b200 import distribution as D
 
     doc, _ = D.distribution_pipeline(_doc("dist_flat"), (4, 1))
     with pytest.raises(D.DistError, match="divisible|covered"):
@@ -127,7 +127,7 @@ def test_gemm_redundant_pairs_removed():
     flat-scattered statement never matches the 2-D product; here every
     2-D statement is block-distributed, so tmp0 / tmp1 / tmp2 all match.)"""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D, sdfg
+    from paper_2107_00555_b200 import distribution as D, sdfg
 
     syms = DIST_SYMBOLS["gemm"]
     full, _ = D.distribute(_doc("gemm"), (2, 2))
@@ -146,7 +146,7 @@ def test_gemm_redundant_pairs_removed():
 
 def test_global_read_elsewhere_not_removed():
     """test_dist.py:264-282: T read by two statements -> nothing removed."""
-    from paper_2107_00555_b200 import distribute as D
+    from paper_2107_00555_b200 import distribution as D
 
     doc, _ = D.distribute(_doc("dist_two_readers"), (2, 1))
     assert D.remove_redundant_comm(doc).get("remove_redundant_comm", 0) == 0
@@ -158,7 +158,7 @@ def test_mismatched_distribution_not_removed():
     frontend's dense temporary tmp0 (T[:-2] * 2.0, then copied into B[1:-1])
     is gathered and re-scattered flat with the same layout -> removed."""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D, sdfg
+    from paper_2107_00555_b200 import distribution as D, sdfg
 
     doc, rep = D.distribution_pipeline(_doc("dist_shifted"), (2, 1))
     assert rep.get("remove_redundant_comm", 0) == 1
@@ -177,7 +177,7 @@ def test_mismatched_distribution_not_removed():
 def test_single_rank_moves_no_bytes():
     """P = 1 -> every collective is a local copy."""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D, sdfg
+    from paper_2107_00555_b200 import distribution as D, sdfg
 
     syms = DIST_SYMBOLS["gemm"]
     doc, _ = D.distribution_pipeline(_doc("gemm"), (1, 1))

@@ -25,7 +25,7 @@ def _ctx(b, ins):
 def test_distributed_kernel_on_device(name, gdims):
     """test_dist.py:194-200: distribution_pipeline + sim_run == shared
     memory (the reference's bound is 1e-6; DIST_MATMUL re-associates)."""
-    from paper_2107_00555_b200 import distribute as D, sdfg, simrun
+    from paper_2107_00555_b200 import distribution as D, sdfg, simrun
 
     syms = DIST_SYMBOLS[name]
     ins = _inputs(sdfg.from_dict(_doc(name)), syms)
@@ -39,7 +39,7 @@ def test_distributed_kernel_on_device(name, gdims):
 def test_device_counters_match_oracle():
     """Per-rank collective calls, bytes and messages equal the oracle's."""
     from oracle import dist_ref
-    from paper_2107_00555_b200 import distribute as D, sdfg, simrun
+    from paper_2107_00555_b200 import distribution as D, sdfg, simrun
 
     syms = DIST_SYMBOLS["gemm"]
     ins = _inputs(sdfg.from_dict(_doc("gemm")), syms)
@@ -54,7 +54,7 @@ def test_device_counters_match_oracle():
 def test_redundant_comm_counter_drop():
     """test_dist.py:232-262: the collective-op count drops by two per removed
     pair; outputs bitwise unchanged."""
-    from paper_2107_00555_b200 import distribute as D, sdfg, simrun
+    from paper_2107_00555_b200 import distribution as D, sdfg, simrun
 
     syms = DIST_SYMBOLS["gemm"]
     ins = _inputs(sdfg.from_dict(_doc("gemm")), syms)
@@ -70,7 +70,7 @@ def test_redundant_comm_counter_drop():
 
 def test_scheduler_order_independence():
     """test_dist.py:208-214."""
-    from paper_2107_00555_b200 import distribute as D, sdfg, simrun
+    from paper_2107_00555_b200 import distribution as D, sdfg, simrun
 
     syms = DIST_SYMBOLS["gemm"]
     ins = _inputs(sdfg.from_dict(_doc("gemm")), syms)
@@ -83,7 +83,7 @@ def test_scheduler_order_independence():
 
 
 def test_single_rank_no_messages():
-    from paper_2107_00555_b200 import distribute as D, sdfg, simrun
+    from paper_2107_00555_b200 import distribution as D, sdfg, simrun
 
     syms = DIST_SYMBOLS["gemm"]
     ins = _inputs(sdfg.from_dict(_doc("gemm")), syms)
