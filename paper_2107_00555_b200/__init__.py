@@ -26,7 +26,9 @@ from .distribution import (  # noqa: F401
     remove_redundant_comm,
 )
 from .simrun import CollectiveOrderError, DeadlockError, RankSim, SimError, sim_run  # noqa: F401
-from .expansions import b200_registry, install as install_expansions  # noqa: F401
+from .expansions import (  # noqa: F401
+    b200_registry, install as install_expansions, patched_cpu_registry,
+)
 
 __all__ = [
     "interpret", "ExecContext", "InterpOptions", "Counters", "InterpreterError",
@@ -34,5 +36,5 @@ __all__ = [
     "run_twice_determinism", "validate", "ProcessGrid", "distribute", "distribute_elementwise",
     "distribution_pipeline", "expand_matmul_distributed", "remove_redundant_comm", "sim_run",
     "RankSim", "DeadlockError", "SimError", "CollectiveOrderError", "b200_registry",
-    "install_expansions",
+    "install_expansions", "patched_cpu_registry",
 ]
