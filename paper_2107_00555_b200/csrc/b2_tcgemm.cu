@@ -320,6 +320,11 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
       : "memory");
 }
 
+// Persistent: the grid holds one CTA pair per two SMs and each pair walks the
+// tiles pid, pid + pairs, ... (grouped rasterisation).  Stage and chunk
+// counters run on across tiles, so the TMA producer and the MMA warp start
+// the next tile while the epilogue warps still store the previous one (the
+// two TMEM chunk buffers decouple them); per tile the arithmetic is unchanged.
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_sgemm_pair(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                   int64_t M, int64_t N, int nk, int chunk, float *__restrict__ C, int64_t ldc,
@@ -336,12 +341,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
-  // tiles of 256 x 256 per pair, grouped rasterisation over pairs
-  const int pid = blockIdx.x >> 1, per_group = group_m * num_n;
-  const int first_m = (pid / per_group) * group_m;
-  const int gsize = num_m - first_m < group_m ? num_m - first_m : group_m;
-  const int m0 = (first_m + (pid % per_group) % gsize) * 256;
-  const int n0 = ((pid % per_group) / gsize) * 256;
+  const int num_tiles = num_m * num_n, pairs = (int)(gridDim.x >> 1);
+  const int per_group = group_m * num_n;
+  const int nchunks = (nk + chunk - 1) / chunk;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P_STAGES; ++s) {
@@ -367,76 +369,102 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    if (lane == 0) {
-      // TMA producer (both CTAs): this CTA's halves of A' and B'
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % P_STAGES;
-        if (kb >= P_STAGES) mbar_wait(&empty[s], ((kb / P_STAGES) + 1) & 1);
-        if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
-        const int ma = m0 + (int)rank * 128, nb = n0 + (int)rank * 128;
-        tma_load_2d_pair(sa + s * P_A_BYTES, &ta, &full[s], kb * 2 * TK, ma);
-        tma_load_2d_pair(sa + s * P_A_BYTES + P_SEG, &ta, &full[s], kb * 2 * TK + TK, ma);
-        tma_load_2d_pair(sb + s * P_B_BYTES, &tb, &full[s], kb * 2 * TK, nb);
-        tma_load_2d_pair(sb + s * P_B_BYTES + P_SEG, &tb, &full[s], kb * 2 * TK + TK, nb);
+  int tiles_done = 0;
+  for (int tile = (int)(blockIdx.x >> 1); tile < num_tiles; tile += pairs, ++tiles_done) {
+    const int first_m = (tile / per_group) * group_m;
+    const int gsize = num_m - first_m < group_m ? num_m - first_m : group_m;
+    const int m0 = (first_m + (tile % per_group) % gsize) * 256;
+    const int n0 = ((tile % per_group) / gsize) * 256;
+    const int g0 = tiles_done * nk;       // stage counter at this tile's first k block
+    const int j0 = tiles_done * nchunks;  // chunk counter at this tile's first chunk
+    if (warp == 0) {
+      if (lane == 0) {
+        // TMA producer (both CTAs): this CTA's halves of A' and B'
+        for (int kb = 0; kb < nk; ++kb) {
+          const int g = g0 + kb, s = g % P_STAGES;
+          if (g >= P_STAGES) mbar_wait(&empty[s], ((g / P_STAGES) + 1) & 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * P_STAGE_BYTES);
+          const int ma = m0 + (int)rank * 128, nb = n0 + (int)rank * 128;
+          tma_load_2d_pair(sa + s * P_A_BYTES, &ta, &full[s], kb * 2 * TK, ma);
+          tma_load_2d_pair(sa + s * P_A_BYTES + P_SEG, &ta, &full[s], kb * 2 * TK + TK, ma);
+          tma_load_2d_pair(sb + s * P_B_BYTES, &tb, &full[s], kb * 2 * TK, nb);
+          tma_load_2d_pair(sb + s * P_B_BYTES + P_SEG, &tb, &full[s], kb * 2 * TK + TK, nb);
+        }
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int j = kb / chunk, b = j & 1;
-        const bool first = kb - j * chunk == 0;
-        if (first && j >= 2) {
-          mbar_wait(&tempty[b], ((j >> 1) + 1) & 1);
+    } else if (warp == 1) {
+      if (lane == 0 && leader) {
+        for (int kb = 0; kb < nk; ++kb) {
+          const int jl = kb / chunk, J = j0 + jl, b = J & 1;
+          const bool first = kb - jl * chunk == 0;
+          if (first && J >= 2) {
+            mbar_wait(&tempty[b], ((J >> 1) + 1) & 1);
+            fence_after();
+          }
+          const int g = g0 + kb, s = g % P_STAGES;
+          mbar_wait(&full[s], (g / P_STAGES) & 1);
           fence_after();
+          const uint64_t a_lo = sw128_desc(smem_u32(sa + s * P_A_BYTES));
+          const uint64_t a_hi = sw128_desc(smem_u32(sa + s * P_A_BYTES + P_SEG));
+          const uint64_t b_hi = sw128_desc(smem_u32(sb + s * P_B_BYTES));
+          const uint64_t b_lo = sw128_desc(smem_u32(sb + s * P_B_BYTES + P_SEG));
+          const uint32_t d = tmem + (uint32_t)(b * 256);
+#pragma unroll
+          for (int k = 0; k < TK / 8; ++k) {  // small products first
+            mma_tf32_pair(d, a_lo + 2 * k, b_hi + 2 * k, !(first && k == 0));
+            mma_tf32_pair(d, a_hi + 2 * k, b_lo + 2 * k, 1);
+            mma_tf32_pair(d, a_hi + 2 * k, b_hi + 2 * k, 1);
+          }
+          mma_commit_pair(&empty[s]);
+          if (kb - jl * chunk == chunk - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
         }
-        const int s = kb % P_STAGES;
-        mbar_wait(&full[s], (kb / P_STAGES) & 1);
+      }
+    } else {
+      const int q = warp & 3, half = (warp - 2) >> 2;
+      float acc[128];
+#pragma unroll
+      for (int i = 0; i < 128; ++i) acc[i] = 0.f;
+      for (int jl = 0; jl < nchunks; ++jl) {
+        const int J = j0 + jl, b = J & 1;
+        mbar_wait(&tfull[b], (J >> 1) & 1);
         fence_after();
-        const uint64_t a_lo = sw128_desc(smem_u32(sa + s * P_A_BYTES));
-        const uint64_t a_hi = sw128_desc(smem_u32(sa + s * P_A_BYTES + P_SEG));
-        const uint64_t b_hi = sw128_desc(smem_u32(sb + s * P_B_BYTES));
-        const uint64_t b_lo = sw128_desc(smem_u32(sb + s * P_B_BYTES + P_SEG));
-        const uint32_t d = tmem + (uint32_t)(b * 256);
+        const uint32_t base =
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 256 + half * 128);
 #pragma unroll
-        for (int k = 0; k < TK / 8; ++k) {  // small products first
-          mma_tf32_pair(d, a_lo + 2 * k, b_hi + 2 * k, !(first && k == 0));
-          mma_tf32_pair(d, a_hi + 2 * k, b_lo + 2 * k, 1);
-          mma_tf32_pair(d, a_hi + 2 * k, b_hi + 2 * k, 1);
+        for (int c = 0; c < 128; c += 16) {
+          float v[16];
+          tmem_ld16(base + (uint32_t)c, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
         }
-        mma_commit_pair(&empty[s]);
-        if (kb - j * chunk == chunk - 1 || kb == nk - 1) mma_commit_pair(&tfull[b]);
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&tempty[b], 0);  // the leader's barrier
       }
-    }
-  } else {
-    const int q = warp & 3, half = (warp - 2) >> 2;
-    float acc[128];
+      // the TMEM buffers are released: the next tile's MMAs run during the stores
+      const int64_t row = m0 + (int64_t)rank * 128 + q * 32 + lane;
+      if (row < M) {
+        float *crow = C + row * ldc + n0 + half * 128;
+        const int64_t ncol = N - (n0 + half * 128);
+        if (ncol >= 128 && (((uintptr_t)crow) & 15) == 0) {
+          float4 *c4 = (float4 *)crow;
 #pragma unroll
-    for (int i = 0; i < 128; ++i) acc[i] = 0.f;
-    const int nchunks = (nk + chunk - 1) / chunk;
-    for (int j = 0; j < nchunks; ++j) {
-      const int b = j & 1;
-      mbar_wait(&tfull[b], (j >> 1) & 1);
-      fence_after();
-      const uint32_t base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 256 + half * 128);
+          for (int i = 0; i < 32; ++i) {
+            float4 o;
+            if (accumulate) {
+              const float4 x = c4[i];
+              o = make_float4(x.x + acc[4 * i], x.y + acc[4 * i + 1], x.z + acc[4 * i + 2],
+                              x.w + acc[4 * i + 3]);
+            } else {
+              o = make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+            }
+            c4[i] = o;
+          }
+        } else {
 #pragma unroll
-      for (int c = 0; c < 128; c += 16) {
-        float v[16];
-        tmem_ld16(base + (uint32_t)c, v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[c + i] += v[i];
+          for (int i = 0; i < 128; ++i)
+            if (i < ncol) crow[i] = accumulate ? crow[i] + acc[i] : acc[i];
+        }
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&tempty[b], 0);  // the leader's barrier
-    }
-    const int64_t row = m0 + (int64_t)rank * 128 + q * 32 + lane;
-    if (row < M) {
-      float *crow = C + row * ldc + n0 + half * 128;
-      const int64_t ncol = N - (n0 + half * 128);
-#pragma unroll
-      for (int i = 0; i < 128; ++i)
-        if (i < ncol) crow[i] = accumulate ? crow[i] + acc[i] : acc[i];
     }
   }
   fence_before();
@@ -546,6 +574,28 @@ int64_t tc_chunk_kblocks() {
   return c;
 }
 
+// Grid of the pair kernel.  Persistent (one pair per two SMs walking the
+// tiles) pays off for short K: the per-tile prologue and epilogue are then a
+// large share of a tile, and the persistent kernel overlaps them with the
+// next tile's MMAs (SUMMA panels, K <= 8192: measured 5-11 % faster).  For
+// long K one tile per pair is better: a wave of pairs starting together
+// walks the same k blocks of A' and B' at the same time, so they are shared
+// in L2 (16384^3 measured 6 % slower persistent, sustained).
+// B2_TC_PERSIST=0 / 1 forces either.
+int tc_pairs(int tiles, int nk) {
+  static int pairs = -1, mode = -1;
+  if (pairs < 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    pairs = sms / 2 > 0 ? sms / 2 : 1;
+    const char *e = getenv("B2_TC_PERSIST");
+    mode = e ? atoi(e) : 2;
+  }
+  const bool persist = mode == 1 || (mode == 2 && nk <= 256);
+  return persist && tiles > pairs ? pairs : tiles;
+}
+
 // split-operand workspace, grown on demand (one process drives one GPU)
 float *g_ws = nullptr;
 size_t g_ws_bytes = 0;
@@ -610,7 +660,7 @@ int b2_sgemm_tc(int64_t M, int64_t N, int64_t K, const float *A, int64_t lda, co
     if (rc) return rc;
     const int pm = (int)((M + 255) / 256), pn = (int)((N + 255) / 256);
     // one pipeline stage = one raw 32-wide k block (both segments)
-    tc_sgemm_pair<<<2 * pm * pn, THREADS, P_SMEM_BYTES, s>>>(
+    tc_sgemm_pair<<<2 * tc_pairs(pm * pn, (int)nkb), THREADS, P_SMEM_BYTES, s>>>(
         pa, pb, M, N, (int)nkb, (int)tc_chunk_kblocks(), C, ldc, accumulate, pm, pn, group_m);
     B2_LAUNCH_CHECK("tc sgemm pair");
     return B2_OK;
@@ -682,7 +732,7 @@ extern "C" int b2_gemm_f32_presplit(int64_t M, int64_t N, int64_t K, const float
   if (rc) return rc;
   const int pm = (int)((M + 255) / 256), pn = (int)((N + 255) / 256);
   B2_CLEAR_ERROR();
-  tc_sgemm_pair<<<2 * pm * pn, THREADS, P_SMEM_BYTES, (cudaStream_t)stream>>>(
+  tc_sgemm_pair<<<2 * tc_pairs(pm * pn, (int)nkb), THREADS, P_SMEM_BYTES, (cudaStream_t)stream>>>(
       pa, pb, M, N, (int)nkb, (int)tc_chunk_kblocks(), C, ldc, accumulate, pm, pn, group_m);
   B2_LAUNCH_CHECK("tc sgemm pair (presplit)");
   return B2_OK;

@@ -26,6 +26,7 @@ import itertools
 import json
 import os
 import struct
+import weakref
 from dataclasses import dataclass, field
 from typing import Mapping
 
@@ -314,12 +315,12 @@ class GpuExecutor:
         return out
 
     def close(self):
-        for host, _ in getattr(self, "_shell_stage", {}).values():
-            rt.lib().b2_host_unregister(host.ctypes.data)
+        # page-locked host buffers: unregistered now (the pinned output
+        # arrays stay valid, pageable, for their holders)
+        for fin in getattr(self, "_pins", []):
+            fin()
+        self._pins = []
         self._shell_stage = {}
-        for arr in (getattr(self, "_pinned_out", None) or {}).values():
-            if arr.nbytes:  # the arrays stay valid (pageable) for their holders
-                rt.lib().b2_host_unregister(arr.ctypes.data)
         self._pinned_out = None
         if self.graph_exec is not None:
             rt.lib().b2_graph_destroy(self.graph_exec)
@@ -482,6 +483,15 @@ class GpuExecutor:
                 return False
         return False
 
+    def _pin_host(self, arr: np.ndarray) -> None:
+        """Page-lock `arr`'s memory.  The registration ends at close() or,
+        for an executor dropped without close(), when `arr` is collected (its
+        weakref callbacks run before numpy frees the data), so a later
+        allocation at the same address never meets a stale registration."""
+        rt.check(rt.lib().b2_host_register(arr.ctypes.data, arr.nbytes), "pin")
+        self.__dict__.setdefault("_pins", []).append(
+            weakref.finalize(arr, rt.lib().b2_host_unregister, arr.ctypes.data))
+
     def _upload_shell(self, name: str, arr: np.ndarray):
         """The 2d boundary faces of `arr` (host-packed into one pinned
         staging buffer) scattered into the device container."""
@@ -495,7 +505,7 @@ class GpuExecutor:
         stg = getattr(self, "_shell_stage", {}).get(name)
         if stg is None:
             host = np.empty(total, dtype=np.float64)
-            rt.check(rt.lib().b2_host_register(host.ctypes.data, host.nbytes), "register")
+            self._pin_host(host)
             dev = self.buf.alloc(host.nbytes)
             stg = (host, dev)
             self.__dict__.setdefault("_shell_stage", {})[name] = stg
@@ -1284,7 +1294,7 @@ class GpuExecutor:
                 shape = self.buf.shape[n] if c.kind != "scalar" else ()
                 arr = np.empty(shape, dtype=_NP[c.dtype])
                 if arr.nbytes:
-                    rt.check(rt.lib().b2_host_register(arr.ctypes.data, arr.nbytes), "pin")
+                    self._pin_host(arr)
                 self._pinned_out[n] = arr
         for n, arr in self._pinned_out.items():
             rt.check(rt.lib().b2_memcpy_d2h(arr.ctypes.data, self.buf.ptr[n], arr.nbytes,
@@ -1493,6 +1503,11 @@ def get_executor(g, bindings: dict, options=None, device: int = 0) -> GpuExecuto
     ex = _exec_cache.get(key)
     if ex is not None and (fkey[0] != "obj" or ex.g is graph):
         return ex
+    if ex is not None:
+        # a collected Graph's id reused by a new one: release the stale
+        # executor (its HBM and page-locked staging buffers) before replacing it
+        del _exec_cache[key]
+        ex.close()
     # Machine.prepare order (interp.py:184-191): validate, then symbols
     if not getattr(options, "skip_validation", False):
         _validate(graph)

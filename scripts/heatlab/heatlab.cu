@@ -1,0 +1,754 @@
+// heatlab.cu — heat_3d sweep variants at N=400, timed back to back like the
+// program (A -> B, B -> A, programmatic dependent launches), each checked
+// bitwise against the baseline march after 4 sweeps.  Development tool for
+// the march mode of paper_2107_00555_b200/codegen.py; prints JSON lines.
+//
+// Build: nvcc -O3 -fmad=false -gencode arch=compute_100a,code=sm_100a -o heatlab heatlab.cu
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cuda_runtime.h>
+#include <nvml.h>
+#include <atomic>
+#include <thread>
+#include <vector>
+
+#define B2_NO_PDL
+#include "../../paper_2107_00555_b200/csrc/families/prelude.cuh"
+#include "gen_heat.cuh"
+
+#define CK(x)                                                                  \
+  do {                                                                         \
+    cudaError_t e = (x);                                                       \
+    if (e != cudaSuccess) {                                                    \
+      fprintf(stderr, "%s: %s\n", #x, cudaGetErrorString(e));                  \
+      exit(1);                                                                 \
+    }                                                                          \
+  } while (0)
+
+constexpr int N = 400, I = N - 2;
+constexpr long S0 = (long)N * N, S1 = N;
+constexpr double SWEEP_BYTES = 8.0 * N * N * N + 8.0 * I * I * I;
+
+__device__ __forceinline__ void pf_l2(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_go() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// same op order as the generated tasklet chain (heat_3d.raw, --fmad=false)
+__device__ __forceinline__ double pt(double c, double zp, double zm, double yp, double ym,
+                                     double xp, double xm) {
+  const double t3 = 0.125 * ((zp - 2.0 * c) + zm);
+  const double t7 = 0.125 * ((yp - 2.0 * c) + ym);
+  const double t12 = 0.125 * ((xp - 2.0 * c) + xm);
+  return ((t3 + t7) + t12) + c;
+}
+
+// prefetch the input rows of tile (tx, ty, tz) into L2
+template <int BX, int BY, int VEC>
+__device__ __forceinline__ void prefetch_tile(const double *A, int tx, int ty, int tz) {
+  const int z0 = tz * VEC, z1 = min(tz * VEC + VEC - 1, I - 1) + 2;
+  const int y0 = ty * BY, y1 = min(ty * BY + BY - 1, I - 1) + 2;
+  const int x0 = tx * BX, x1 = min(tx * BX + BX - 1, I - 1) + 2;
+  const int ny = y1 - y0 + 1, nrow = (z1 - z0 + 1) * ny;
+  const long base = (long)(const char *)A;
+  for (int r = threadIdx.y * blockDim.x + threadIdx.x; r < nrow; r += blockDim.x * blockDim.y) {
+    const int zz = r / ny, yy = r - zz * ny;
+    const long row = (z0 + zz) * S0 + (y0 + yy) * S1;
+    const long a0 = (base + (row + x0) * 8) & ~15L, a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+    pf_l2((const void *)a0, (unsigned)(a1 - a0));
+  }
+}
+
+// V-march: BX x BY tile of interior columns, VEC planes per thread.
+// PF: 0 none, 1 this tile at pickup, 2 persistent + next tile of this CTA
+template <int BX, int BY, int VEC, int PF, int MINB = 1>
+__global__ void __launch_bounds__(BX *BY, MINB) march(const double *__restrict__ A,
+                                                double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    if (PF == 1 || (PF == 2 && vb == (int)blockIdx.x)) prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    if (PF == 2 && vb + (int)gridDim.x < nvb) {
+      const int nb = vb + gridDim.x;
+      prefetch_tile<BX, BY, VEC>(A, nb % tiles_x, (nb / tiles_x) % tiles_y,
+                                 nb / (tiles_x * tiles_y));
+    }
+    const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+    if (i1 >= I || i2 >= I) continue;
+    const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+    if (tz * VEC + VEC <= I) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (tz * VEC + v >= I) break;
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    }
+  }
+  pdl_go();
+}
+
+// V-pair: each lane owns two array-aligned columns (2j, 2j+1) of a 64-column
+// tile aligned to the array (16-B loads and stores); x neighbours come from
+// the adjacent lanes by shuffle, z neighbours roll through registers.
+// Columns 0 and N-1 and rows / planes outside the interior are not written.
+template <int BY, int VEC, int PF>
+__global__ void __launch_bounds__(32 * BY) pairs(const double *__restrict__ A,
+                                                 double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (N + 63) / 64, tiles_y = (I + BY - 1) / BY, tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  const int lane = threadIdx.x;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    if (PF == 1) {
+      // rows z0-1 .. z1+1, y0-1 .. y1+1, columns of this tile (+-1)
+      const int z0 = tz * VEC, z1 = min(tz * VEC + VEC - 1, I - 1) + 2;
+      const int y0 = ty * BY, y1 = min(ty * BY + BY - 1, I - 1) + 2;
+      const int x0 = max(tx * 64 - 1, 0), x1 = min(tx * 64 + 64, N - 1);
+      const int ny = y1 - y0 + 1, nrow = (z1 - z0 + 1) * ny;
+      const long base = (long)(const char *)A;
+      for (int r = threadIdx.y * 32 + lane; r < nrow; r += 32 * BY) {
+        const int zz = r / ny, yy = r - zz * ny;
+        const long row = (z0 + zz) * S0 + (y0 + yy) * S1;
+        const long a0 = (base + (row + x0) * 8) & ~15L,
+                   a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+        pf_l2((const void *)a0, (unsigned)(a1 - a0));
+      }
+    }
+    const int i1 = ty * BY + threadIdx.y;
+    if (i1 >= I) continue;
+    const int c0 = tx * 64 + 2 * lane;  // array column of .x
+    const bool live = c0 < N;
+    const long row = (long)(i1 + 1) * S1;
+    const bool wx = c0 >= 1, wy = c0 + 1 <= N - 2;  // .x / .y interior columns
+    const int z0 = tz * VEC;
+    const int nz = min(VEC, I - z0);
+    double2 zm = make_double2(0, 0), c = zm;
+    if (live) {
+      zm = *(const double2 *)(A + (long)z0 * S0 + row + c0);
+      c = *(const double2 *)(A + (long)(z0 + 1) * S0 + row + c0);
+    }
+#pragma unroll 4
+    for (int v = 0; v < nz; ++v) {
+      const long p = (long)(z0 + v + 1) * S0 + row + c0;
+      double2 zp = make_double2(0, 0), yp = zp, ym = zp;
+      double el = 0, er = 0;
+      if (live) {
+        zp = *(const double2 *)(A + p + S0);
+        yp = *(const double2 *)(A + p + S1);
+        ym = *(const double2 *)(A + p - S1);
+        if (lane == 0 && c0 >= 1) el = A[p - 1];
+        if (lane == 31 && c0 + 2 < N) er = A[p + 2];
+      }
+      double xl = __shfl_up_sync(0xffffffffu, c.y, 1);
+      double xr = __shfl_down_sync(0xffffffffu, c.x, 1);
+      if (lane == 0) xl = el;
+      if (lane == 31) xr = er;
+      if (live) {
+        double2 o;
+        o.x = pt(c.x, zp.x, zm.x, yp.x, ym.x, c.y, xl);
+        o.y = pt(c.y, zp.y, zm.y, yp.y, ym.y, xr, c.x);
+        if (wx && wy)
+          *(double2 *)(B + p) = o;
+        else if (wx)
+          B[p] = o.x;
+        else if (wy)
+          B[p + 1] = o.y;
+      }
+      zm = c;
+      c = zp;
+    }
+  }
+  pdl_go();
+}
+
+
+// march with the next plane's loads issued before this plane's math
+// (registers roll along dim 0: zm <- c <- zp)
+template <int BX, int BY, int VEC, int PF, int MINB>
+__global__ void __launch_bounds__(BX *BY, MINB) march_sp(const double *__restrict__ A,
+                                                         double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    if (PF) prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+    if (i1 >= I || i2 >= I) continue;
+    const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+    const int nz = min(VEC, I - tz * VEC);
+    const double *a = A + (long)(tz * VEC + 1) * S0 + col;
+    double *b = B + (long)(tz * VEC + 1) * S0 + col;
+    double zm = a[-S0], c = a[0];
+    double zp = a[S0], yp = a[S1], ym = a[-S1], xp = a[1], xm = a[-1];
+#pragma unroll 4
+    for (int v = 0; v < nz; ++v) {
+      double nzp = 0, nyp = 0, nym = 0, nxp = 0, nxm = 0;
+      if (v + 1 < nz) {
+        const double *q = a + (long)(v + 1) * S0;
+        nzp = q[S0]; nyp = q[S1]; nym = q[-S1]; nxp = q[1]; nxm = q[-1];
+      }
+      b[(long)v * S0] = pt(c, zp, zm, yp, ym, xp, xm);
+      zm = c; c = zp; zp = nzp; yp = nyp; ym = nym; xp = nxp; xm = nxm;
+    }
+  }
+  pdl_go();
+}
+
+// march + prefetch.global.L1 of the z+1 row D planes ahead (no registers)
+template <int BX, int BY, int VEC, int D>
+__global__ void __launch_bounds__(BX *BY) march_l1(const double *__restrict__ A,
+                                                   double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+    if (i1 >= I || i2 >= I) continue;
+    const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+#pragma unroll
+    for (int d = 1; d <= D; ++d)
+      if (tz * VEC + d + 1 < N)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(A + (long)(tz * VEC + d + 1) * S0 + col));
+    if (tz * VEC + VEC <= I) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        if (v + D + 2 < VEC + 2 && tz * VEC + v + D + 2 < N)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(A + p + (long)(D + 1) * S0));
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (tz * VEC + v >= I) break;
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    }
+  }
+  pdl_go();
+}
+
+__device__ __forceinline__ void cpa8(void *smem, const void *g) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory"); }
+
+// march whose z+1 values arrive by cp.async into a per-thread shared-memory
+// ring D planes ahead (each thread reads only its own slots: no barriers)
+template <int BX, int BY, int VEC, int D>
+__global__ void __launch_bounds__(BX *BY) march_cpa(const double *__restrict__ A,
+                                                    double *__restrict__ B) {
+  pdl_wait();
+  constexpr int R = D + 1;
+  __shared__ double ring[R][BX * BY];
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+    if (i1 >= I || i2 >= I) continue;
+    const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+    const int nz = min(VEC, I - tz * VEC);
+    const double *a = A + (long)(tz * VEC + 1) * S0 + col;  // plane of v = 0
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (d < nz) cpa8(&ring[d % R][tid], a + (long)(d + 1) * S0);
+      cpa_commit();
+    }
+    double zm = a[-S0], c = a[0];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      if (v >= nz) break;
+      if (v + D < nz) cpa8(&ring[(v + D) % R][tid], a + (long)(v + D + 1) * S0);
+      cpa_commit();
+      cpa_wait<D>();
+      const double zp = ring[v % R][tid];
+      const double *q = a + (long)v * S0;
+      B[(q - A)] = pt(c, zp, zm, q[S1], q[-S1], q[1], q[-1]);
+      zm = c;
+      c = zp;
+    }
+    cpa_wait<0>();
+  }
+  pdl_go();
+}
+
+// march over array-aligned column tiles (array column = tx * BX + threadIdx.x;
+// columns 0 and N-1 idle), optional ty-fastest tile order, full-row tiles
+template <int BX, int BY, int VEC, bool YFAST>
+__global__ void __launch_bounds__(BX *BY) march_al(const double *__restrict__ A,
+                                                   double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (N + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    int tx, ty;
+    if (YFAST) {
+      ty = vb % tiles_y;
+      tx = (vb / tiles_y) % tiles_x;
+    } else {
+      tx = vb % tiles_x;
+      ty = (vb / tiles_x) % tiles_y;
+    }
+    const int tz = vb / (tiles_x * tiles_y);
+    {
+      const int z0 = tz * VEC, z1 = min(tz * VEC + VEC - 1, I - 1) + 2;
+      const int y0 = ty * BY, y1 = min(ty * BY + BY - 1, I - 1) + 2;
+      const int x0 = max(tx * BX - 1, 0), x1 = min(tx * BX + BX, N - 1);
+      const int ny = y1 - y0 + 1, nrow = (z1 - z0 + 1) * ny;
+      const long base = (long)(const char *)A;
+      for (int r = threadIdx.y * blockDim.x + threadIdx.x; r < nrow; r += blockDim.x * blockDim.y) {
+        const int zz = r / ny, yy = r - zz * ny;
+        const long row = (z0 + zz) * S0 + (y0 + yy) * S1;
+        const long a0 = (base + (row + x0) * 8) & ~15L,
+                   a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+        pf_l2((const void *)a0, (unsigned)(a1 - a0));
+      }
+    }
+    const int i1 = ty * BY + threadIdx.y, x = tx * BX + threadIdx.x;
+    if (i1 >= I || x < 1 || x > N - 2) continue;
+    const long col = (long)(i1 + 1) * S1 + x;
+    if (tz * VEC + VEC <= I) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        if (tz * VEC + v >= I) break;
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        B[p] = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+      }
+    }
+  }
+  pdl_go();
+}
+
+__device__ __forceinline__ void st_ef(double *p, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
+// aligned march with: REV — odd sweeps walk the plane chunks from the top
+// (the last-written chunks of the previous sweep are still in L2);
+// EF — evict_first L2 policy on the stores; PP — progressive L2 prefetch
+// PP planes ahead instead of the whole tile at pickup (0 = whole tile)
+template <int BX, int BY, int VEC, bool REV, bool EF, int PP>
+__global__ void __launch_bounds__(BX *BY) march_al2(const double *__restrict__ A,
+                                                    double *__restrict__ B, int odd) {
+  pdl_wait();
+  constexpr int tiles_x = (N + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  unsigned long long pol = 0;
+  if (EF) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y;
+    int tz = vb / (tiles_x * tiles_y);
+    if (REV && odd) tz = tiles_z - 1 - tz;
+    const int z0 = tz * VEC, z1 = min(tz * VEC + VEC - 1, I - 1) + 2;
+    const int y0 = ty * BY, y1 = min(ty * BY + BY - 1, I - 1) + 2;
+    const int x0 = max(tx * BX - 1, 0), x1 = min(tx * BX + BX, N - 1);
+    const int ny = y1 - y0 + 1;
+    const long base = (long)(const char *)A;
+    {
+      const int zl = PP ? min(z0 + PP + 1, z1) : z1;
+      const int nrow = (zl - z0 + 1) * ny;
+      for (int r = tid; r < nrow; r += BX * BY) {
+        const int zz = r / ny, yy = r - zz * ny;
+        const long row = (z0 + zz) * S0 + (y0 + yy) * S1;
+        const long a0 = (base + (row + x0) * 8) & ~15L,
+                   a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+        pf_l2((const void *)a0, (unsigned)(a1 - a0));
+      }
+    }
+    const int i1 = ty * BY + threadIdx.y, x = tx * BX + threadIdx.x;
+    const bool act = !(i1 >= I || x < 1 || x > N - 2);
+    const long col = (long)(i1 + 1) * S1 + x;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      if (tz * VEC + v >= I) break;
+      if (PP) {
+        const int zz = z0 + v + PP + 2;
+        if (tid < ny && zz <= z1) {
+          const long row = zz * S0 + (y0 + tid) * S1;
+          const long a0 = (base + (row + x0) * 8) & ~15L,
+                     a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+          pf_l2((const void *)a0, (unsigned)(a1 - a0));
+        }
+      }
+      if (act) {
+        const long p = (long)(tz * VEC + v + 1) * S0 + col;
+        const double o = pt(A[p], A[p + S0], A[p - S0], A[p + S1], A[p - S1], A[p + 1], A[p - 1]);
+        if (EF)
+          st_ef(B + p, o, pol);
+        else
+          B[p] = o;
+      }
+    }
+  }
+  pdl_go();
+}
+
+// energy decomposition: same tiling / prefetch as the generated march,
+// MODE 0: copy the centre (1 load, 1 store), 1: the 7 loads combined with
+// integer xor (no FP64), 2: the full FP64 stencil
+template <int MODE>
+__global__ void __launch_bounds__(512) dec(const double *__restrict__ A, double *__restrict__ B) {
+  pdl_wait();
+  constexpr int BX = 64, BY = 8, VEC = 16;
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY,
+                tiles_z = (I + VEC - 1) / VEC;
+  constexpr int nvb = tiles_x * tiles_y * tiles_z;
+  for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
+    const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
+    prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+    if (i1 >= I || i2 >= I) continue;
+    const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+    const double *a = A + (long)(tz * VEC + 1) * S0 + col;
+    double *b = B + (long)(tz * VEC + 1) * S0 + col;
+    const int nz = min(VEC, I - tz * VEC);
+    double zm = a[-S0], c = a[0];
+#pragma unroll 16
+    for (int v = 0; v < nz; ++v) {
+      const double *q = a + (long)v * S0;
+      const double zp = q[S0];
+      double o;
+      if (MODE == 0) {
+        o = c;
+      } else if (MODE == 1) {
+        const long long r = __double_as_longlong(c) ^ __double_as_longlong(zp) ^
+                            __double_as_longlong(zm) ^ __double_as_longlong(q[S1]) ^
+                            __double_as_longlong(q[-S1]) ^ __double_as_longlong(q[1]) ^
+                            __double_as_longlong(q[-1]);
+        o = __longlong_as_double(r);
+      } else {
+        o = pt(c, zp, zm, q[S1], q[-S1], q[1], q[-1]);
+      }
+      b[(long)v * S0] = o;
+      zm = c;
+      c = zp;
+    }
+  }
+  pdl_go();
+}
+
+__global__ void copy_u4(const double2 *__restrict__ a, double2 *__restrict__ b, long n) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const double2 x0 = a[i], x1 = a[i + stride], x2 = a[i + 2 * stride], x3 = a[i + 3 * stride];
+    b[i] = x0; b[i + stride] = x1; b[i + 2 * stride] = x2; b[i + 3 * stride] = x3;
+  }
+  for (; i < n; i += stride) b[i] = a[i];
+}
+
+__global__ void copy_flat(const double2 *__restrict__ a, double2 *__restrict__ b, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+__global__ void init(double *a, double *b, unsigned seed) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)N * N * N;
+       i += (long)gridDim.x * blockDim.x) {
+    unsigned long long h = (unsigned long long)i * 0x9E3779B97F4A7C15ull + seed;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    a[i] = (double)(h & 0xFFFFFF) / 16777216.0;
+    b[i] = a[i];
+  }
+}
+
+__global__ void ndiff(const double *a, const double *b, unsigned long long *cnt) {
+  unsigned long long c = 0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)N * N * N;
+       i += (long)gridDim.x * blockDim.x)
+    c += (__double_as_longlong(a[i]) != __double_as_longlong(b[i]));
+  atomicAdd(cnt, c);
+}
+
+typedef void (*KFn)(const double *, double *);
+typedef void (*KFn2)(const double *, double *, int);
+
+struct Var {
+  const char *name;
+  KFn fn;
+  dim3 block;
+  int grid;
+  KFn2 fn2 = nullptr;
+  bool gen = false;
+};
+static int *g_flag = nullptr;
+
+// NVML power / SM clock sampler (20 ms) around a timed region
+struct Sampler {
+  std::atomic<bool> on{false}, quit{false};
+  std::vector<double> pw, mhz;
+  std::thread th;
+  nvmlDevice_t dev;
+  Sampler() {
+    nvmlInit();
+    nvmlDeviceGetHandleByIndex(0, &dev);
+    th = std::thread([this] {
+      while (!quit) {
+        if (on) {
+          unsigned p = 0, c = 0;
+          nvmlDeviceGetPowerUsage(dev, &p);
+          nvmlDeviceGetClockInfo(dev, NVML_CLOCK_SM, &c);
+          pw.push_back(p / 1000.0);
+          mhz.push_back(c);
+        }
+        std::this_thread::sleep_for(std::chrono::milliseconds(20));
+      }
+    });
+  }
+  void start() { pw.clear(); mhz.clear(); on = true; }
+  void stop(double *p, double *c) {
+    on = false;
+    std::this_thread::sleep_for(std::chrono::milliseconds(30));
+    double sp = 0, sc = 0;
+    for (size_t i = 0; i < pw.size(); ++i) { sp += pw[i]; sc += mhz[i]; }
+    *p = pw.empty() ? 0 : sp / pw.size();
+    *c = mhz.empty() ? 0 : sc / mhz.size();
+  }
+  ~Sampler() { quit = true; th.join(); }
+};
+
+static void launch(const Var &v, const double *a, double *b, cudaStream_t s, int odd = 0) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(v.grid);
+  cfg.blockDim = v.block;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (v.gen) {
+    B2Args ar;
+    ar.w[0] = (long long)a;
+    ar.w[1] = (long long)b;
+    ar.w[2] = (long long)g_flag;
+    CK(cudaLaunchKernelEx(&cfg, gen_heat, ar));
+  } else if (v.fn2)
+    CK(cudaLaunchKernelEx(&cfg, v.fn2, a, b, odd));
+  else
+    CK(cudaLaunchKernelEx(&cfg, v.fn, a, b));
+}
+
+template <int BX, int BY, int VEC, int PF, int MINB = 1>
+Var mk_march(const char *name, int grid = 0) {
+  constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, march<BX, BY, VEC, PF, MINB>, dim3(BX, BY), grid ? grid : nvb};
+}
+template <int BX, int BY, int VEC, bool REV, bool EF, int PP>
+Var mk_al2(const char *name) {
+  constexpr int nvb = ((N + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  Var v{name, nullptr, dim3(BX, BY), nvb};
+  v.fn2 = march_al2<BX, BY, VEC, REV, EF, PP>;
+  return v;
+}
+template <int BX, int BY, int VEC, bool YF>
+Var mk_al(const char *name) {
+  constexpr int nvb = ((N + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, march_al<BX, BY, VEC, YF>, dim3(BX, BY), nvb};
+}
+template <int BX, int BY, int VEC, int D>
+Var mk_l1(const char *name) {
+  constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, march_l1<BX, BY, VEC, D>, dim3(BX, BY), nvb};
+}
+template <int BX, int BY, int VEC, int D>
+Var mk_cpa(const char *name) {
+  constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, march_cpa<BX, BY, VEC, D>, dim3(BX, BY), nvb};
+}
+template <int BX, int BY, int VEC, int PF, int MINB>
+Var mk_sp(const char *name) {
+  constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, march_sp<BX, BY, VEC, PF, MINB>, dim3(BX, BY), nvb};
+}
+template <int BY, int VEC, int PF>
+Var mk_pairs(const char *name, int grid = 0) {
+  constexpr int nvb = ((N + 63) / 64) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
+  return Var{name, pairs<BY, VEC, PF>, dim3(32, BY), grid ? grid : nvb};
+}
+
+int main(int argc, char **argv) {
+  const int reps = argc > 1 ? atoi(argv[1]) : 40;
+  const char *only = argc > 2 ? argv[2] : nullptr;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  const size_t bytes = (size_t)N * N * N * 8;
+  double *A, *B, *RA, *RB;
+  unsigned long long *cnt;
+  CK(cudaMalloc(&A, bytes));
+  CK(cudaMalloc(&B, bytes));
+  CK(cudaMalloc(&RA, bytes));
+  CK(cudaMalloc(&RB, bytes));
+  CK(cudaMalloc(&cnt, 8));
+  CK(cudaMalloc(&g_flag, 8));
+  cudaStream_t s;
+  CK(cudaStreamCreate(&s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+
+  // flat copy ceiling (same 512 MB buffers)
+  {
+    const long n2 = (long)N * N * N / 2;
+    for (int w = 0; w < 3; ++w) copy_flat<<<nsm * 8, 256, 0, s>>>((double2 *)A, (double2 *)B, n2);
+    CK(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r)
+      copy_flat<<<nsm * 8, 256, 0, s>>>((double2 *)(r & 1 ? B : A), (double2 *)(r & 1 ? A : B), n2);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    printf("{\"variant\": \"copy_flat\", \"us\": %.2f, \"GBps\": %.1f}\n", ms * 1e3 / reps,
+           2.0 * bytes / (ms / reps * 1e-3) / 1e9);
+  }
+  {
+    const long n2 = (long)N * N * N / 2;
+    for (int g : {nsm * 4, nsm * 8, nsm * 16}) {
+      for (int w = 0; w < 3; ++w) copy_u4<<<g, 256, 0, s>>>((double2 *)A, (double2 *)B, n2);
+      float best = 1e9, tot = 0;
+      for (int r = 0; r < reps; ++r) {
+        CK(cudaEventRecord(e0, s));
+        copy_u4<<<g, 256, 0, s>>>((double2 *)(r & 1 ? B : A), (double2 *)(r & 1 ? A : B), n2);
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        best = ms < best ? ms : best;
+        tot += ms;
+      }
+      printf("{\"variant\": \"copy_u4_g%d\", \"us\": %.2f, \"GBps\": %.1f, \"best_GBps\": %.1f}\n", g,
+             tot * 1e3 / reps, 2.0 * bytes / (tot / reps * 1e-3) / 1e9, 2.0 * bytes / (best * 1e-3) / 1e9);
+    }
+    float best = 1e9, tot = 0;
+    for (int r = 0; r < reps; ++r) {
+      CK(cudaEventRecord(e0, s));
+      CK(cudaMemcpyAsync(r & 1 ? A : B, r & 1 ? B : A, bytes, cudaMemcpyDeviceToDevice, s));
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      best = ms < best ? ms : best;
+      tot += ms;
+    }
+    printf("{\"variant\": \"memcpy_d2d\", \"us\": %.2f, \"GBps\": %.1f, \"best_GBps\": %.1f}\n",
+           tot * 1e3 / reps, 2.0 * bytes / (tot / reps * 1e-3) / 1e9, 2.0 * bytes / (best * 1e-3) / 1e9);
+  }
+
+  Var gv{"generated", nullptr, dim3(64, 8), 8750};
+  gv.gen = true;
+  Var vars[] = {
+      gv,
+      Var{"dec_centre", dec<0>, dim3(64, 8), 8750},
+      Var{"dec_loads_xor", dec<1>, dim3(64, 8), 8750},
+      Var{"dec_full", dec<2>, dim3(64, 8), 8750},
+      Var{"dec_centre2", dec<0>, dim3(64, 8), 8750},
+      gv,
+  };
+  const int nv = sizeof(vars) / sizeof(vars[0]);
+  Sampler smp;
+  {  // heat the part up to its power-capped steady state first
+    const long n2 = (long)N * N * N / 2;
+    for (int r = 0; r < 3000; ++r)
+      copy_u4<<<nsm * 16, 256, 0, s>>>((double2 *)(r & 1 ? B : A), (double2 *)(r & 1 ? A : B), n2);
+    CK(cudaStreamSynchronize(s));
+  }
+  // baseline result after 4 sweeps
+  init<<<nsm * 4, 256, 0, s>>>(RA, RB, 7);
+  for (int t = 0; t < 2; ++t) {
+    launch(vars[0], RA, RB, s);
+    launch(vars[0], RB, RA, s);
+  }
+  CK(cudaStreamSynchronize(s));
+  for (int k = 0; k < nv; ++k) {
+    const Var &v = vars[k];
+    if (only && !strstr(v.name, only)) continue;
+    init<<<nsm * 4, 256, 0, s>>>(A, B, 7);
+    for (int t = 0; t < 2; ++t) {
+      launch(v, A, B, s, 0);
+      launch(v, B, A, s, 1);
+    }
+    CK(cudaMemsetAsync(cnt, 0, 8, s));
+    ndiff<<<nsm * 4, 256, 0, s>>>(A, RA, cnt);
+    ndiff<<<nsm * 4, 256, 0, s>>>(B, RB, cnt);
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int w = 0; w < 4; ++w) launch(v, w & 1 ? B : A, w & 1 ? A : B, s, w & 1);
+    smp.start();
+    CK(cudaEventRecord(e0, s));
+    for (int r = 0; r < reps; ++r) launch(v, r & 1 ? B : A, r & 1 ? A : B, s, r & 1);
+    CK(cudaEventRecord(e1, s));
+    CK(cudaEventSynchronize(e1));
+    double watts, mhz;
+    smp.stop(&watts, &mhz);
+    CK(cudaGetLastError());
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    const double us = ms * 1e3 / reps;
+    // the same launches captured into one CUDA graph (as the executor runs them)
+    double gus = 0;
+    {
+      cudaGraph_t g;
+      cudaGraphExec_t ge;
+      CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+      for (int r = 0; r < reps; ++r) launch(v, r & 1 ? B : A, r & 1 ? A : B, s, r & 1);
+      CK(cudaStreamEndCapture(s, &g));
+      CK(cudaGraphInstantiate(&ge, g, 0));
+      CK(cudaGraphLaunch(ge, s));
+      CK(cudaEventRecord(e0, s));
+      CK(cudaGraphLaunch(ge, s));
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      float gms;
+      CK(cudaEventElapsedTime(&gms, e0, e1));
+      gus = gms * 1e3 / reps;
+      CK(cudaGraphExecDestroy(ge));
+      CK(cudaGraphDestroy(g));
+    }
+    printf("{\"variant\": \"%s\", \"grid\": %d, \"block\": [%d, %d], \"us\": %.2f, \"GBps\": %.1f, "
+           "\"mismatches\": %llu, \"graph_us\": %.2f, \"W\": %.0f, \"sm_mhz\": %.0f, \"uJ_per_sweep\": %.0f}\n",
+           v.name, v.grid, v.block.x, v.block.y, us, SWEEP_BYTES / (us * 1e-6) / 1e9, h, gus, watts, mhz, watts * us);
+    fflush(stdout);
+  }
+  return 0;
+}

@@ -6,7 +6,9 @@ f64: libb2 DMMA DGEMM per panel.  f32: the local blocks are split into
 3xTF32 hi/lo operands ONCE per call (b2_tf32_split_a / _bt, panel-major so a
 panel is one contiguous broadcast buffer), then one b2_gemm_f32_presplit per
 panel.  T1 = the same call on one GPU (b2_gemm_f64 / b2_gemm_f32 16384^3).
-Compute-side efficiency = T1 / (P * T_rank); the panel broadcasts overlap the
+Compute-side efficiency = T1 / (P * T_rank), both timed sustained (1.5 s of
+back-to-back calls each, T1 re-timed next to every grid: the GEMMs run
+power-capped); the panel broadcasts overlap the
 previous panel's GEMM in the multi-GPU runner and are not part of this
 projection."""
 import ctypes
@@ -44,14 +46,22 @@ L.b2_event_create(ctypes.byref(e0))
 L.b2_event_create(ctypes.byref(e1))
 
 
-def timed(fn, reps=2):
-    for _ in range(reps):  # warm, then timed
+def timed(fn, secs=1.5):
+    """Sustained time of one call: fn repeated for `secs` seconds (the part
+    settles at its power-capped clocks), median of the second half of the
+    per-call CUDA-event times."""
+    import time
+
+    ts = []
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < secs or len(ts) < 4:
         L.b2_event_record(e0, s)
         fn()
         L.b2_event_record(e1, s)
         ms = ctypes.c_float()
         rt.check(L.b2_event_elapsed_ms(e0, e1, ctypes.byref(ms)))
-    return ms.value
+        ts.append(ms.value)
+    return float(np.median(ts[len(ts) // 2:]))
 
 
 rng = np.random.default_rng(0)
@@ -62,9 +72,12 @@ for dtype in WHICH:
     B = alloc(n * n * esz, "rand", npd, (n, n), rng)
     C = alloc(n * n * esz)
     if dtype == "f64":
-        t1 = timed(lambda: rt.check(L.b2_gemm_f64(n, n, n, A, n, 1, B, n, 1, C, n, 1, 1, s)))
+        def full():
+            rt.check(L.b2_gemm_f64(n, n, n, A, n, 1, B, n, 1, C, n, 1, 1, s))
     else:
-        t1 = timed(lambda: rt.check(L.b2_gemm_f32(n, n, n, A, n, 1, B, n, 1, C, n, 1, 1, s)))
+        def full():
+            rt.check(L.b2_gemm_f32(n, n, n, A, n, 1, B, n, 1, C, n, 1, 1, s))
+    t1 = None
     res = {"T1_ms": t1}
     for (pr, pc) in ((2, 1), (2, 2), (4, 2)):
         P = pr * pc
@@ -89,8 +102,11 @@ for dtype in WHICH:
                 for l in range(Lp):
                     rt.check(L.b2_gemm_f32_presplit(am, bn, kb, pa[l % len(pa)],
                                                     pb[l % len(pb)], C, bn, 1, s))
+        # T1 re-timed right before each grid: both sides see the same
+        # (power-capped) clocks
+        t1 = timed(full)
         t = timed(rank)
-        res[f"{pr}x{pc}"] = {"rank_ms": t, "efficiency": t1 / (P * t)}
+        res[f"{pr}x{pc}"] = {"rank_ms": t, "T1_ms": t1, "efficiency": t1 / (P * t)}
         print(json.dumps({"dtype": dtype, "grid": f"{pr}x{pc}", "rank_ms": t, "T1_ms": t1,
                           "projected_efficiency": t1 / (P * t)}), flush=True)
         if dtype == "f32":
