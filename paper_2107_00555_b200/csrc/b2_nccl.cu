@@ -30,7 +30,8 @@ typedef int (*PFN_CommDestroy)(NcclComm);
 typedef int (*PFN_Group)(void);
 typedef int (*PFN_Send)(const void *, size_t, int, int, NcclComm, cudaStream_t);
 typedef int (*PFN_Recv)(void *, size_t, int, int, NcclComm, cudaStream_t);
-typedef int (*PFN_Bcast)(void *, size_t, int, int, NcclComm, cudaStream_t);
+// ncclBroadcast(sendbuff, recvbuff, count, datatype, root, comm, stream)
+typedef int (*PFN_Bcast)(const void *, void *, size_t, int, int, NcclComm, cudaStream_t);
 typedef int (*PFN_AllReduce)(const void *, void *, size_t, int, int, NcclComm, cudaStream_t);
 typedef const char *(*PFN_ErrStr)(int);
 
@@ -130,7 +131,7 @@ extern "C" int b2_nccl_group_p2p(void *comm, int n, const b2_p2p_t *ops, void *s
 extern "C" int b2_nccl_bcast(void *comm, void *buf, size_t bytes, int root, void *stream) {
   int rc = load();
   if (rc) return rc;
-  return nccl_check(nc.bcast(buf, bytes, kNcclInt8, root, comm, (cudaStream_t)stream),
+  return nccl_check(nc.bcast(buf, buf, bytes, kNcclInt8, root, comm, (cudaStream_t)stream),
                     "ncclBroadcast");
 }
 

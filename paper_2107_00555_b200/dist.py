@@ -451,7 +451,10 @@ class NcclComm:
     captured into the same CUDA graph as the kernels.  The unique id is
     bootstrapped over the torch.distributed process group."""
 
-    def __init__(self, rank: int, world: int):
+    def __init__(self, rank: int, world: int, group=None, root_global: int = 0):
+        """rank / world within `group` (a torch.distributed group; None = the
+        default group); the unique id travels from the group member whose
+        global rank is `root_global` (group rank 0)."""
         import ctypes
 
         import torch.distributed as tdist
@@ -464,7 +467,8 @@ class NcclComm:
         if rank == 0:
             rt.check(rt.lib().b2_nccl_unique_id(idbuf), "nccl id")
         obj = [idbuf.raw if rank == 0 else None]
-        tdist.broadcast_object_list(obj, src=0)
+        if world > 1 or group is None:
+            tdist.broadcast_object_list(obj, src=root_global, group=group)
         idbuf = ctypes.create_string_buffer(obj[0], 128)
         comm = ctypes.c_void_p()
         rt.check(rt.lib().b2_nccl_init(world, rank, idbuf, ctypes.byref(comm)), "nccl init")
@@ -727,40 +731,214 @@ class Summa:
         return (A[self.i * am:(self.i + 1) * am, self.j * ak:(self.j + 1) * ak],
                 B[self.i * bk:(self.i + 1) * bk, self.j * bn:(self.j + 1) * bn])
 
+    def schedule(self) -> list:
+        """summa_schedule for this rank."""
+        return summa_schedule(self.grid.dims, (self.i, self.j), self.L)
+
     def run(self, a_local, b_local, c_local, gemm, new_buffer):
         """a_local/b_local/c_local: torch tensors (device or host); gemm(c, a,
         b) accumulates; new_buffer(shape) returns an uninitialised tensor."""
-        Pr, Pc = self.grid.dims
-        per_a = self.L // Pc  # panels per A column block
-        per_b = self.L // Pr  # panels per B row block
         kb = self.kb
-        am = self.M // Pr
-        bn = self.N // Pc
+        am = self.M // self.grid.dims[0]
+        bn = self.N // self.grid.dims[1]
         bufs = [(new_buffer((am, kb)), new_buffer((kb, bn))) for _ in range(2)]
+        steps = self.schedule()
 
-        def issue(l, slot):
-            pa, pb = bufs[slot]
-            ca, la = divmod(l, per_a)  # owner grid column of A's panel, local panel
-            rb, lb = divmod(l, per_b)  # owner grid row of B's panel
-            if self.j == ca:
-                pa.copy_(a_local[:, la * kb:(la + 1) * kb])
-            if self.i == rb:
-                pb.copy_(b_local[lb * kb:(lb + 1) * kb, :])
-            w1 = self.td.broadcast(pa, self.grid.rank_of((self.i, ca)),
+        def issue(st):
+            pa, pb = bufs[st.slot]
+            if st.a_local is not None:
+                pa.copy_(a_local[:, st.a_local * kb:(st.a_local + 1) * kb])
+            if st.b_local is not None:
+                pb.copy_(b_local[st.b_local * kb:(st.b_local + 1) * kb, :])
+            w1 = self.td.broadcast(pa, self.grid.rank_of((self.i, st.a_root)),
                                    group=self.row_groups[self.i], async_op=True)
-            w2 = self.td.broadcast(pb, self.grid.rank_of((rb, self.j)),
+            w2 = self.td.broadcast(pb, self.grid.rank_of((st.b_root, self.j)),
                                    group=self.col_groups[self.j], async_op=True)
             return w1, w2
 
-        pending = issue(0, 0)
-        for l in range(self.L):
-            nxt = issue(l + 1, (l + 1) % 2) if l + 1 < self.L else None
+        pending = issue(steps[0])
+        for n, st in enumerate(steps):
+            nxt = issue(steps[n + 1]) if n + 1 < len(steps) else None
             for w in pending:
                 w.wait()
-            pa, pb = bufs[l % 2]
+            pa, pb = bufs[st.slot]
             gemm(c_local, pa, pb)
             pending = nxt
         return c_local
+
+
+@dataclass(frozen=True)
+class SummaStep:
+    """Panel l of SUMMA on one rank: A's panel comes from grid column
+    `a_root` of this rank's grid row (its local panel `a_local` when this
+    rank is the root, else None), B's from grid row `b_root` of its grid
+    column (`b_local` likewise); both land in double-buffer slot `slot`."""
+    l: int
+    slot: int
+    a_root: int
+    a_local: int | None
+    b_root: int
+    b_local: int | None
+
+
+def summa_schedule(dims, coords, L: int) -> list:
+    """The broadcast schedule of SUMMA: K in L = lcm(Pr,
+    Pc) panels; A's column block j holds panels j*L/Pc .. (j+1)*L/Pc - 1, B's
+    row block i holds panels i*L/Pr ...  Shared by the torch (CPU / gloo)
+    runner and the libb2 device runner, so the multi-rank exchange logic is
+    the one the gloo tests check."""
+    Pr, Pc = dims
+    i, j = coords
+    per_a, per_b = L // Pc, L // Pr
+    out = []
+    for l in range(L):
+        ca, la = divmod(l, per_a)
+        rb, lb = divmod(l, per_b)
+        out.append(SummaStep(l, l % 2, ca, la if j == ca else None, rb, lb if i == rb else None))
+    return out
+
+
+class SummaDevice:
+    """The SUMMA data plane on libb2 for one rank on its GPU.
+
+    * f32: this rank's A and B blocks are split ONCE per call into 3xTF32
+      operands, panel by panel (b2_tf32_split_a / _bt: each panel one
+      contiguous buffer); f64: A's column panels are packed contiguous once
+      (b2_copy_view), B's row panels already are.
+    * Panels are broadcast with libb2 NCCL (b2_nccl_bcast, in place from the
+      root's own panel) on row / column sub-communicators, on a comm stream;
+      the GEMM of panel l (b2_gemm_f32_presplit / b2_gemm_f64, C += A_l B_l)
+      runs on the compute stream.  Two buffer slots: the broadcast of panel
+      l + 1 (and l + 2 once slot l % 2 is released by its GEMM's event)
+      overlaps the GEMM of panel l.
+    * The whole call — memset of C, splits, broadcasts, GEMMs, both streams —
+      is captured once into a CUDA graph (``capture``) and replayed
+      (``launch``)."""
+
+    def __init__(self, grid: ProcessGrid, rank: int, M: int, N: int, K: int, dtype: str = "f64",
+                 stream=None):
+        import ctypes
+
+        from . import runtime as rt
+
+        if dtype not in ("f64", "f32"):
+            raise DistError(f"SUMMA dtype {dtype!r}")
+        self.rt, self.ct = rt, ctypes
+        self.L_ = rt.lib()
+        self.geo = Summa(grid, rank, M, N, K)
+        g = self.geo
+        Pr, Pc = grid.dims
+        self.dtype, self.esz = dtype, (8 if dtype == "f64" else 4)
+        (self.am, self.ak), (self.bk, self.bn), _ = g.local_shapes()
+        self.kb = g.kb
+        self.kp = self.L_.b2_tf32_split_cols(self.kb) if dtype == "f32" else self.kb
+        self.steps = g.schedule()
+        # row / column communicators (libb2 NCCL), bootstrapped over the
+        # torch groups Summa created
+        self.row = NcclComm(g.j, Pc, g.row_groups[g.i], grid.rank_of((g.i, 0)))
+        self.col = NcclComm(g.i, Pr, g.col_groups[g.j], grid.rank_of((0, g.j)))
+        self._bufs = []
+        abytes = self.am * self.kp * self.esz
+        bbytes = (self.bn * self.kp if dtype == "f32" else self.kb * self.bn) * self.esz
+        self.a_bytes, self.b_bytes = abytes, bbytes
+        self.own_a = [self._alloc(abytes) for _ in range(g.L // Pc)]
+        self.own_b = [self._alloc(bbytes) for _ in range(g.L // Pr)] if dtype == "f32" else []
+        self.slot_a = [self._alloc(abytes) for _ in range(2)]
+        self.slot_b = [self._alloc(bbytes) for _ in range(2)]
+        self.sc = stream or self._new(self.L_.b2_stream_create)
+        self.sm = self._new(self.L_.b2_stream_create)
+        self.ev = {k: self._new(self.L_.b2_event_create)
+                   for k in ("fork", "join", "r0", "r1", "f0", "f1")}
+        self.gexec = None
+        self.kernels_per_call = 0
+
+    def _new(self, fn):
+        p = self.ct.c_void_p()
+        self.rt.check(fn(self.ct.byref(p)), "create")
+        return p.value
+
+    def _alloc(self, n):
+        p = self.ct.c_void_p()
+        self.rt.check(self.L_.b2_malloc(self.ct.byref(p), max(1, n)), "summa alloc")
+        self._bufs.append(p.value)
+        return p.value
+
+    def enqueue(self, a: int, b: int, c: int) -> None:
+        """One SUMMA call on this rank's device blocks (row-major, contiguous):
+        a (am x ak), b (bk x bn), c (am x bn) = the local block of A @ B."""
+        rt, L, g = self.rt, self.L_, self.geo
+        chk = rt.check
+        sc, sm, ev = self.sc, self.sm, self.ev
+        am, ak, bn, kb, esz = self.am, self.ak, self.bn, self.kb, self.esz
+        nk = 0
+        chk(L.b2_memset(c, 0, am * bn * esz, sc), "summa C")
+        if self.dtype == "f32":
+            for la, p in enumerate(self.own_a):
+                chk(L.b2_tf32_split_a(a + esz * la * kb, ak, am, kb, p, sc), "split a")
+            for lb, p in enumerate(self.own_b):
+                chk(L.b2_tf32_split_bt(b + esz * lb * kb * bn, bn, kb, bn, p, sc), "split b")
+            nk += len(self.own_a) + len(self.own_b)
+        else:
+            for la, p in enumerate(self.own_a):
+                dv = rt.make_view(p, 0, "f64", [am, kb], [kb, 1])
+                sv = rt.make_view(a, la * kb, "f64", [am, kb], [ak, 1])
+                chk(L.b2_copy_view(self.ct.byref(dv), self.ct.byref(sv), 0, sc), "pack a")
+            nk += len(self.own_a)
+        chk(L.b2_event_record(ev["fork"], sc), "fork")
+        chk(L.b2_stream_wait_event(sm, ev["fork"]), "fork")
+        for st in self.steps:
+            ready, free = ev[f"r{st.slot}"], ev[f"f{st.slot}"]
+            if st.l >= 2:
+                chk(L.b2_stream_wait_event(sm, free), "slot free")
+            pa = self.own_a[st.a_local] if st.a_local is not None else self.slot_a[st.slot]
+            if self.dtype == "f32":
+                pb = self.own_b[st.b_local] if st.b_local is not None else self.slot_b[st.slot]
+            else:
+                pb = (b + esz * st.b_local * kb * bn) if st.b_local is not None \
+                    else self.slot_b[st.slot]
+            self.row.bcast(pa, self.a_bytes, st.a_root, sm)
+            self.col.bcast(pb, self.b_bytes, st.b_root, sm)
+            chk(L.b2_event_record(ready, sm), "ready")
+            chk(L.b2_stream_wait_event(sc, ready), "ready")
+            if self.dtype == "f32":
+                chk(L.b2_gemm_f32_presplit(am, bn, kb, pa, pb, c, bn, 1, sc), "panel gemm")
+            else:
+                chk(L.b2_gemm_f64(am, bn, kb, pa, kb, 1, pb, bn, 1, c, bn, 1,
+                                  rt.WCR_CODE["add"], sc), "panel gemm")
+            nk += 1
+            chk(L.b2_event_record(free, sc), "free")
+        chk(L.b2_event_record(ev["join"], sm), "join")
+        chk(L.b2_stream_wait_event(sc, ev["join"]), "join")
+        self.kernels_per_call = nk
+
+    def capture(self, a: int, b: int, c: int) -> None:
+        """Capture one call (both streams) into a CUDA graph."""
+        L = self.L_
+        self.rt.check(L.b2_capture_begin(self.sc), "capture")
+        try:
+            self.enqueue(a, b, c)
+        finally:
+            gx = self.ct.c_void_p()
+            rc = L.b2_capture_end(self.sc, self.ct.byref(gx))
+        self.rt.check(rc, "capture end")
+        self.gexec = gx.value
+
+    def launch(self) -> None:
+        self.rt.check(self.L_.b2_graph_launch(self.gexec, self.sc), "summa graph")
+
+    def close(self):
+        L = self.L_
+        if self.gexec:
+            L.b2_graph_destroy(self.gexec)
+            self.gexec = None
+        for p in self._bufs:
+            L.b2_free(p)
+        self._bufs = []
+        for e in self.ev.values():
+            L.b2_event_destroy(e)
+        L.b2_stream_destroy(self.sm)
+        self.row.close()
+        self.col.close()
 
 
 def measured_extra() -> dict:
@@ -773,6 +951,7 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     """bench.py --workload matmul[_f32]: SUMMA over all ranks (squarest grid),
     libb2 DMMA / f32 GEMM per panel, NCCL panel broadcasts.  Prints the JSON
     line from rank 0 (TFLOP/s of the whole job, max-over-ranks time)."""
+    import ctypes
     import json
 
     import torch
@@ -791,49 +970,46 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
                                  device_id=torch.device("cuda", local))
     rt.device(local)
     grid = ProcessGrid.squarest(world)
-    s = Summa(grid, rank, n, n, n)
+    sd = SummaDevice(grid, rank, n, n, n, dtype)
+    s = sd.geo
     tdt = torch.float64 if dtype == "f64" else torch.float32
     (am, ak), (bk, bn), (cm, cn) = s.local_shapes()
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     a = torch.rand((am, ak), dtype=tdt, device="cuda", generator=gen) * 2 - 1
     b = torch.rand((bk, bn), dtype=tdt, device="cuda", generator=gen) * 2 - 1
     c = torch.zeros((cm, cn), dtype=tdt, device="cuda")
+    torch.cuda.synchronize()
     L = rt.lib()
-    fn = L.b2_gemm_f64 if dtype == "f64" else L.b2_gemm_f32
-
-    def gemm(cc, pa, pb):
-        stream = torch.cuda.current_stream().cuda_stream
-        rt.check(fn(pa.shape[0], pb.shape[1], pa.shape[1], pa.data_ptr(), pa.stride(0), 1,
-                    pb.data_ptr(), pb.stride(0), 1, cc.data_ptr(), cc.stride(0), 1,
-                    rt.WCR_CODE["add"], stream), "summa gemm")
-
-    def buf(shape):
-        return torch.empty(shape, dtype=tdt, device="cuda")
+    # one call (C = 0, operand splits / packs, panel broadcasts on the comm
+    # stream, panel GEMMs on the compute stream) captured as one CUDA graph
+    sd.capture(a.data_ptr(), b.data_ptr(), c.data_ptr())
+    ev0, ev1 = ctypes.c_void_p(), ctypes.c_void_p()
+    rt.check(L.b2_event_create(ctypes.byref(ev0)))
+    rt.check(L.b2_event_create(ctypes.byref(ev1)))
 
     from bench import ClockSampler  # noqa: E402
 
     for _ in range(args.warmup):
-        s.run(a, b, c, gemm, buf)
-    torch.cuda.synchronize()
+        sd.launch()
+    rt.check(L.b2_stream_sync(sd.sc))
     tdist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    n_launch0 = L.b2_launch_count()
+    rt.check(L.b2_stream_sync(sd.sc))
     with ClockSampler(local) as clk:
-        e0.record()
+        rt.check(L.b2_event_record(ev0, sd.sc))
         for _ in range(args.steps):
-            s.run(a, b, c, gemm, buf)
-        e1.record()
-        torch.cuda.synchronize()
-    launches = L.b2_launch_count() - n_launch0
-    ms = e0.elapsed_time(e1) / args.steps
+            sd.launch()
+        rt.check(L.b2_event_record(ev1, sd.sc))
+        rt.check(L.b2_stream_sync(sd.sc))
+    launches = sd.kernels_per_call * args.steps
+    fms = ctypes.c_float()
+    rt.check(L.b2_event_elapsed_ms(ev0, ev1, ctypes.byref(fms)))
+    ms = fms.value / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     flop = 2.0 * n ** 3
     # end to end: this rank's A and B blocks from pinned host memory, the
-    # SUMMA run, C block back to pinned host memory
+    # SUMMA graph, C block back to pinned host memory
     ha = a.cpu().pin_memory()
     hb = b.cpu().pin_memory()
     hc = torch.empty_like(c, device="cpu").pin_memory()
@@ -842,11 +1018,14 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        a.copy_(ha, non_blocking=True)
-        b.copy_(hb, non_blocking=True)
-        s.run(a, b, c, gemm, buf)
-        hc.copy_(c, non_blocking=True)
-        torch.cuda.synchronize()
+        rt.check(L.b2_memcpy_h2d(a.data_ptr(), ha.data_ptr(), ha.numel() * ha.element_size(),
+                                 sd.sc))
+        rt.check(L.b2_memcpy_h2d(b.data_ptr(), hb.data_ptr(), hb.numel() * hb.element_size(),
+                                 sd.sc))
+        sd.launch()
+        rt.check(L.b2_memcpy_d2h(hc.data_ptr(), c.data_ptr(), hc.numel() * hc.element_size(),
+                                 sd.sc))
+        rt.check(L.b2_stream_sync(sd.sc))
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -876,6 +1055,9 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
             "vs_baseline": None, "dtype": dtype, "data": "synthetic uniform(-1,1)",
             "config": {"workload": f"SUMMA M=N=K={n} {dtype} (BASELINE configs[3])",
                        "grid": str(grid), "panels": s.L,
+                       "data_plane": "libb2: operands split / packed once per call, panel "
+                                     "broadcasts (NCCL row / column communicators) on a comm "
+                                     "stream overlapping the panel GEMMs, one CUDA graph per call",
                        "parallelism": f"summa{grid}"},
             "roofline": roof,
             "e2e": {"value": flop / e2e_s / 1e12, "unit": "TFLOP/s",
@@ -885,6 +1067,7 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
             "gpu_launches": int(launches),
             "clocks": clk.summary()}), flush=True)
     tdist.barrier()
+    sd.close()
     tdist.destroy_process_group()
 
 

@@ -275,3 +275,28 @@ def test_summa_matches_shared_memory_matmul(dims):
     for i, j, c in parts:
         C[i * bm:(i + 1) * bm, j * bn:(j + 1) * bn] = c
     assert np.max(np.abs(C - A @ B)) <= 1e-12 * max(1.0, np.max(np.abs(A @ B)))
+
+
+@pytest.mark.parametrize("dims", [(1, 1), (2, 1), (1, 2), (2, 2), (4, 2), (2, 4), (3, 2)])
+def test_summa_schedule_covers_every_panel_once(dims):
+    """summa_schedule (shared by the torch runner and the libb2 device runner):
+    on every rank each of the L panels arrives once from the rank that owns
+    it; the root uses its own panel; slots alternate."""
+    import math
+
+    Pr, Pc = dims
+    L = math.lcm(Pr, Pc)
+    for i in range(Pr):
+        for j in range(Pc):
+            steps = dist.summa_schedule(dims, (i, j), L)
+            assert [st.l for st in steps] == list(range(L))
+            assert [st.slot for st in steps] == [l % 2 for l in range(L)]
+            for st in steps:
+                # A's panel l lives in grid column l // (L / Pc) as local panel l % (L / Pc)
+                assert st.a_root == st.l // (L // Pc) and st.b_root == st.l // (L // Pr)
+                assert (st.a_local is not None) == (j == st.a_root)
+                assert (st.b_local is not None) == (i == st.b_root)
+                if st.a_local is not None:
+                    assert st.a_local == st.l % (L // Pc)
+                if st.b_local is not None:
+                    assert st.b_local == st.l % (L // Pr)
