@@ -2,7 +2,7 @@
 // np.matmul semantics, pkg/src/sdfgkit/interp.py:450-460) on sm_100a.
 //
 // Blackwell has no tcgen05 kind for f64, so the FP64 tensor
-// path is DMMA: mma.sync.m16n8k4.f64.  CTA tile 128x128x16, 8 warps (2 x 4),
+// path is DMMA: mma.sync.m16n8k4.f64.  CTA tile 128x128xBK (BK = 32, B2_DGEMM_BK=16 for the 16-deep stages), 8 warps (2 x 4),
 // warp tile 64x32 (4 x 4 m16n8 accumulators = 64 doubles per thread), operand
 // tiles staged through a 3-stage cp.async shared-memory ring.  Shared layouts
 // are padded so every fragment load is exactly two wavefronts (conflict-free):
@@ -20,13 +20,18 @@
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+constexpr int BM = 128, BN = 128, STAGES = 3;
 constexpr int APAD = 4, BPAD = 8;
-constexpr int AS_STRIDE = BK + APAD;   // 20 doubles
 constexpr int BS_STRIDE = BN + BPAD;   // 136 doubles
-constexpr int AS_TILE = BM * AS_STRIDE;
-constexpr int BS_TILE = BK * BS_STRIDE;
-constexpr int SMEM_BYTES = STAGES * (AS_TILE + BS_TILE) * 8;
+// k depth of one pipeline stage: BK = 16 (113 KB of stages) or 32 (215 KB;
+// half the barriers per flop)
+template <int BK>
+struct Tile {
+  static constexpr int AS_STRIDE = BK + APAD;
+  static constexpr int AS_TILE = BM * AS_STRIDE;
+  static constexpr int BS_TILE = BK * BS_STRIDE;
+  static constexpr int SMEM_BYTES = STAGES * (AS_TILE + BS_TILE) * 8;
+};
 
 __device__ __forceinline__ void cp8(double *smem, const double *g, bool ok) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -49,25 +54,26 @@ __device__ __forceinline__ void dmma(double (&d)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <bool VEC>
+template <bool VEC, int BK>
 __device__ __forceinline__ void load_tiles(double *As, double *Bs, const double *A, int64_t lda,
                                            const double *B, int64_t ldb, int64_t M, int64_t N,
                                            int64_t K, int64_t m0, int64_t n0, int64_t k0) {
+  constexpr int AS_STRIDE = Tile<BK>::AS_STRIDE;
   const int tid = threadIdx.x;
   if (VEC) {
-    // A: 128 rows x 16 k = 1024 chunks of 2 doubles, 4 per thread
+    // A: 128 rows x BK k in chunks of 2 doubles
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < BK / 4; ++i) {
       const int c = tid + i * 256;
-      const int r = c >> 3, kk = (c & 7) * 2;
+      const int r = c / (BK / 2), kk = (c % (BK / 2)) * 2;
       const int64_t gm = m0 + r, gk = k0 + kk;
       int bytes = 0;
       if (gm < M) bytes = gk + 1 < K ? 16 : (gk < K ? 8 : 0);
       cp16(As + r * AS_STRIDE + kk, bytes ? A + gm * lda + gk : A, bytes);
     }
-    // B: 16 k x 128 cols = 1024 chunks, 4 per thread
+    // B: BK k x 128 cols in chunks of 2 doubles
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < BK / 4; ++i) {
       const int c = tid + i * 256;
       const int kk = c >> 6, nn = (c & 63) * 2;
       const int64_t gk = k0 + kk, gn = n0 + nn;
@@ -77,15 +83,15 @@ __device__ __forceinline__ void load_tiles(double *As, double *Bs, const double 
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < BK / 2; ++i) {
       const int c = tid + i * 256;
-      const int r = c >> 4, kk = c & 15;
+      const int r = c / BK, kk = c % BK;
       const int64_t gm = m0 + r, gk = k0 + kk;
       const bool ok = gm < M && gk < K;
       cp8(As + r * AS_STRIDE + kk, ok ? A + gm * lda + gk : A, ok);
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < BK / 2; ++i) {
       const int c = tid + i * 256;
       const int kk = c >> 7, nn = c & 127;
       const int64_t gk = k0 + kk, gn = n0 + nn;
@@ -95,11 +101,13 @@ __device__ __forceinline__ void load_tiles(double *As, double *Bs, const double 
   }
 }
 
-template <bool VEC>
+template <bool VEC, int BK>
 __global__ void __launch_bounds__(256, 1)
     dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *__restrict__ A, int64_t lda,
                const double *__restrict__ B, int64_t ldb, double *__restrict__ C, int64_t rsc,
                int64_t csc, int accumulate, int num_m, int num_n, int group_m) {
+  constexpr int AS_STRIDE = Tile<BK>::AS_STRIDE, AS_TILE = Tile<BK>::AS_TILE,
+                BS_TILE = Tile<BK>::BS_TILE;
   extern __shared__ __align__(16) double smem[];
   double *As = smem;
   double *Bs = smem + STAGES * AS_TILE;
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles)
-      load_tiles<VEC>(As + s * AS_TILE, Bs + s * BS_TILE, A, lda, B, ldb, M, N, K, m0, n0,
+      load_tiles<VEC, BK>(As + s * AS_TILE, Bs + s * BS_TILE, A, lda, B, ldb, M, N, K, m0, n0,
                       (int64_t)s * BK);
     commit();
   }
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(256, 1)
     const int pre = kt + STAGES - 1;
     if (pre < ktiles) {
       const int ps = pre % STAGES;
-      load_tiles<VEC>(As + ps * AS_TILE, Bs + ps * BS_TILE, A, lda, B, ldb, M, N, K, m0, n0,
+      load_tiles<VEC, BK>(As + ps * AS_TILE, Bs + ps * BS_TILE, A, lda, B, ldb, M, N, K, m0, n0,
                       (int64_t)pre * BK);
     }
     commit();
@@ -185,13 +193,18 @@ __global__ void __launch_bounds__(256, 1)
 int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda, const double *B,
                   int64_t ldb, double *C, int64_t rsc, int64_t csc, int accumulate,
                   void *stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(dgemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    cudaFuncSetAttribute(dgemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
-    configured = true;
+  static int bk = -1;
+  if (bk < 0) {
+    const char *e = getenv("B2_DGEMM_BK");
+    bk = e && atoi(e) == 16 ? 16 : 32;
+    cudaFuncSetAttribute(dgemm_dmma<true, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tile<16>::SMEM_BYTES);
+    cudaFuncSetAttribute(dgemm_dmma<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tile<16>::SMEM_BYTES);
+    cudaFuncSetAttribute(dgemm_dmma<true, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tile<32>::SMEM_BYTES);
+    cudaFuncSetAttribute(dgemm_dmma<false, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Tile<32>::SMEM_BYTES);
   }
   const bool vec = (lda % 2 == 0) && (ldb % 2 == 0) && (((uintptr_t)A & 15) == 0) &&
                    (((uintptr_t)B & 15) == 0);
@@ -203,13 +216,23 @@ int b2_dgemm_dmma(int64_t M, int64_t N, int64_t K, const double *A, int64_t lda,
     if (group_m < 1) group_m = 1;
   }
   const unsigned grid = (unsigned)(num_m * num_n);
+  cudaStream_t st = (cudaStream_t)stream;
   B2_CLEAR_ERROR();
-  if (vec)
-    dgemm_dmma<true><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(
-        M, N, K, A, lda, B, ldb, C, rsc, csc, accumulate, num_m, num_n, group_m);
-  else
-    dgemm_dmma<false><<<grid, 256, SMEM_BYTES, (cudaStream_t)stream>>>(
-        M, N, K, A, lda, B, ldb, C, rsc, csc, accumulate, num_m, num_n, group_m);
+#define B2_DG(V, K_)                                                                   \
+  dgemm_dmma<V, K_><<<grid, 256, Tile<K_>::SMEM_BYTES, st>>>(M, N, K, A, lda, B, ldb, C, rsc, \
+                                                            csc, accumulate, num_m, num_n, group_m)
+  if (bk == 32) {
+    if (vec)
+      B2_DG(true, 32);
+    else
+      B2_DG(false, 32);
+  } else {
+    if (vec)
+      B2_DG(true, 16);
+    else
+      B2_DG(false, 16);
+  }
+#undef B2_DG
   B2_LAUNCH_CHECK("dgemm launch");
   return B2_OK;
 }
