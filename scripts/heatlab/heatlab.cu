@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(BX *BY) march_al2(const double *__restrict__ A
 // energy decomposition: same tiling / prefetch as the generated march,
 // MODE 0: copy the centre (1 load, 1 store), 1: the 7 loads combined with
 // integer xor (no FP64), 2: the full FP64 stencil
-template <int MODE>
+template <int MODE, bool DPF = true>
 __global__ void __launch_bounds__(512) dec(const double *__restrict__ A, double *__restrict__ B) {
   pdl_wait();
   constexpr int BX = 64, BY = 8, VEC = 16;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(512) dec(const double *__restrict__ A, double 
   constexpr int nvb = tiles_x * tiles_y * tiles_z;
   for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {
     const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, tz = vb / (tiles_x * tiles_y);
-    prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
+    if (DPF) prefetch_tile<BX, BY, VEC>(A, tx, ty, tz);
     const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
     if (i1 >= I || i2 >= I) continue;
     const long col = (long)(i1 + 1) * S1 + (i2 + 1);
@@ -627,6 +627,86 @@ __global__ void __launch_bounds__(TX *TY) pair3(const double *__restrict__ A,
   pdl_go();
 }
 
+__global__ void copy8_u4(const double *__restrict__ a, double *__restrict__ b, long n) {
+  const long stride = (long)gridDim.x * blockDim.x;
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    const double x0 = a[i], x1 = a[i + stride], x2 = a[i + 2 * stride], x3 = a[i + 3 * stride];
+    b[i] = x0; b[i + stride] = x1; b[i + 2 * stride] = x2; b[i + 3 * stride] = x3;
+  }
+  for (; i < n; i += stride) b[i] = a[i];
+}
+// flat copy in CTA-sized contiguous blocks, each block L2-prefetched in bulk
+// at pickup (isolates the cost of cp.async.bulk.prefetch.L2)
+__global__ void copy_blk_pf(const double *__restrict__ a, double *__restrict__ b, long n) {
+  constexpr int BLK = 8192;  // doubles per block (64 KB)
+  for (long blk = blockIdx.x; blk * BLK < n; blk += gridDim.x) {
+    const long base = blk * BLK;
+    if (threadIdx.x < 16) pf_l2(a + base + threadIdx.x * (BLK / 16), BLK / 16 * 8);
+    for (int i = threadIdx.x; i < BLK && base + i < n; i += blockDim.x) b[base + i] = a[base + i];
+  }
+}
+__global__ void copy_blk(const double *__restrict__ a, double *__restrict__ b, long n) {
+  constexpr int BLK = 8192;
+  for (long blk = blockIdx.x; blk * BLK < n; blk += gridDim.x) {
+    const long base = blk * BLK;
+    for (int i = threadIdx.x; i < BLK && base + i < n; i += blockDim.x) b[base + i] = a[base + i];
+  }
+}
+
+// lockstep z march: every CTA owns a BX x BY column tile and one of ZS
+// z segments and walks it plane by plane (registers roll zm <- c <- zp), so
+// at any moment the whole GPU reads a few planes (DRAM-page friendly).
+// D > 0: each step prefetches the tile's rows of plane z + D into L2.
+template <int BX, int BY, int ZS, int D>
+__global__ void __launch_bounds__(BX *BY) zmarch(const double *__restrict__ A, double *__restrict__ B) {
+  pdl_wait();
+  constexpr int tiles_x = (I + BX - 1) / BX, tiles_y = (I + BY - 1) / BY;
+  constexpr int SEG = (I + ZS - 1) / ZS;
+  const int vb = blockIdx.x;
+  const int tx = vb % tiles_x, ty = (vb / tiles_x) % tiles_y, zseg = vb / (tiles_x * tiles_y);
+  const int i1 = ty * BY + threadIdx.y, i2 = tx * BX + threadIdx.x;
+  const int z0 = zseg * SEG, z1 = min(z0 + SEG, I);
+  const int tid = threadIdx.y * BX + threadIdx.x;
+  const long base = (long)(const char *)A;
+  const int y0 = ty * BY, x0 = tx * BX, x1 = min(tx * BX + BX - 1, I - 1) + 2;
+  const int ny = min(BY, I - y0) + 2;
+  if (D > 0) {
+    for (int r = tid; r < ny * (D + 2); r += BX * BY) {
+      const int zz = z0 + r / ny, yy = y0 + r % ny;
+      if (zz <= N - 1) {
+        const long row = (long)zz * S0 + (long)yy * S1;
+        const long a0 = (base + (row + x0) * 8) & ~15L, a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+        pf_l2((const void *)a0, (unsigned)(a1 - a0));
+      }
+    }
+  }
+  const bool act = i1 < I && i2 < I;
+  const long col = (long)(i1 + 1) * S1 + (i2 + 1);
+  const double *a = A + (long)(z0 + 1) * S0 + col;
+  double *b = B + (long)(z0 + 1) * S0 + col;
+  double zm = act ? a[-S0] : 0, c = act ? a[0] : 0;
+#pragma unroll 4
+  for (int v = 0; v < z1 - z0; ++v) {
+    if (D > 0 && tid < ny) {
+      const int zz = z0 + v + D + 2;
+      if (zz <= N - 1) {
+        const long row = (long)zz * S0 + (long)(y0 + tid) * S1;
+        const long a0 = (base + (row + x0) * 8) & ~15L, a1 = (base + (row + x1 + 1) * 8 + 15) & ~15L;
+        pf_l2((const void *)a0, (unsigned)(a1 - a0));
+      }
+    }
+    if (act) {
+      const double *q = a + (long)v * S0;
+      const double zp = q[S0];
+      b[(long)v * S0] = pt(c, zp, zm, q[S1], q[-S1], q[1], q[-1]);
+      zm = c;
+      c = zp;
+    }
+  }
+  pdl_go();
+}
+
 __global__ void copy_u4(const double2 *__restrict__ a, double2 *__restrict__ b, long n) {
   const long stride = (long)gridDim.x * blockDim.x;
   long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
@@ -748,6 +828,11 @@ Var mk_al(const char *name) {
   constexpr int nvb = ((N + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
   return Var{name, march_al<BX, BY, VEC, YF>, dim3(BX, BY), nvb};
 }
+template <int BX, int BY, int ZS, int D>
+Var mk_zm(const char *name) {
+  constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ZS;
+  return Var{name, zmarch<BX, BY, ZS, D>, dim3(BX, BY), nvb};
+}
 template <int BX, int BY, int VEC, int D>
 Var mk_l1(const char *name) {
   constexpr int nvb = ((I + BX - 1) / BX) * ((I + BY - 1) / BY) * ((I + VEC - 1) / VEC);
@@ -789,6 +874,40 @@ int main(int argc, char **argv) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
 
+  Sampler smp0;
+  if (getenv("COPYPOWER")) {  // sustained copies with power: heat up first
+    const long n2 = (long)N * N * N / 2;
+    for (int r = 0; r < 3000; ++r)
+      copy_u4<<<nsm * 16, 256, 0, s>>>((double2 *)(r & 1 ? B : A), (double2 *)(r & 1 ? A : B), n2);
+    CK(cudaStreamSynchronize(s));
+    const long n1 = (long)N * N * N;
+    const char *mname[] = {"copy_u4_g2368", "memcpy_d2d", "copy8_u4_g2368", "copy_blk_pf_g1184", "copy_blk_g1184"};
+    for (int mode = 0; mode < 5; ++mode) {
+      smp0.start();
+      CK(cudaEventRecord(e0, s));
+      for (int r = 0; r < 2000; ++r) {
+        if (mode == 0)
+          copy_u4<<<nsm * 16, 256, 0, s>>>((double2 *)(r & 1 ? B : A), (double2 *)(r & 1 ? A : B), n2);
+        else if (mode == 1)
+          CK(cudaMemcpyAsync(r & 1 ? A : B, r & 1 ? B : A, bytes, cudaMemcpyDeviceToDevice, s));
+        else if (mode == 2)
+          copy8_u4<<<nsm * 16, 256, 0, s>>>(r & 1 ? B : A, r & 1 ? A : B, n1);
+        else if (mode == 3)
+          copy_blk_pf<<<nsm * 8, 256, 0, s>>>(r & 1 ? B : A, r & 1 ? A : B, n1);
+        else
+          copy_blk<<<nsm * 8, 256, 0, s>>>(r & 1 ? B : A, r & 1 ? A : B, n1);
+      }
+      CK(cudaEventRecord(e1, s));
+      CK(cudaEventSynchronize(e1));
+      double w, c;
+      smp0.stop(&w, &c);
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      const double us = ms * 1e3 / 2000;
+      printf("{\"variant\": \"sustained_%s\", \"us\": %.2f, \"GBps\": %.1f, \"W\": %.0f, \"sm_mhz\": %.0f, \"mJ_per_GB\": %.1f}\n",
+             mname[mode], us, 2.0 * bytes / (us * 1e-6) / 1e9, w, c, w * us * 1e-3 / (2.0 * bytes / 1e9));
+    }
+  }
   // flat copy ceiling (same 512 MB buffers)
   {
     const long n2 = (long)N * N * N / 2;
@@ -840,10 +959,14 @@ int main(int argc, char **argv) {
   gv.gen = true;
   Var vars[] = {
       gv,
-      Var{"dec_centre", dec<0>, dim3(64, 8), 8750},
-      Var{"dec_loads_xor", dec<1>, dim3(64, 8), 8750},
-      Var{"dec_full", dec<2>, dim3(64, 8), 8750},
-      Var{"dec_centre2", dec<0>, dim3(64, 8), 8750},
+      mk_zm<64, 8, 2, 0>("zm_64x8_s2"),
+      mk_zm<64, 8, 2, 4>("zm_64x8_s2_pf4"),
+      mk_zm<64, 8, 2, 8>("zm_64x8_s2_pf8"),
+      mk_zm<64, 8, 4, 4>("zm_64x8_s4_pf4"),
+      mk_zm<64, 4, 2, 4>("zm_64x4_s2_pf4"),
+      mk_zm<32, 8, 2, 4>("zm_32x8_s2_pf4"),
+      mk_zm<64, 8, 8, 4>("zm_64x8_s8_pf4"),
+      mk_zm<64, 8, 4, 8>("zm_64x8_s4_pf8"),
       gv,
   };
   const int nv = sizeof(vars) / sizeof(vars[0]);

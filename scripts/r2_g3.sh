@@ -1,1 +1,2 @@
-PAIR=1 ./scripts/heatlab/jaclab 400
+./scripts/heatlab/heatlab 40 2>&1 | grep -E "zm_|generated"
+./scripts/heatlab/heatlab 2500 2>&1 | grep -E "zm_|generated"
