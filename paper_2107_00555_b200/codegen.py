@@ -63,6 +63,10 @@ SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime
 # map) as an implicit GEMM on the FP64 tensor path (DMMA)
 CONTRACT_MODE = os.environ.get("B2_CONTRACT", "1") == "1"
 CONTRACT_MIN_FMA = 1 << 22
+# m16 fragments per warp (CTA tile TM = 128 MF rows): conv2d_bias 0.760 ms at
+# MF = 1, 0.705 at 2 (each B fragment feeds two DMMAs); BK = 32 is slower
+CONTRACT_MF = int(os.environ.get("B2_CONTRACT_MF", "2"))
+CONTRACT_BK = int(os.environ.get("B2_CONTRACT_BK", "16"))  # k chunk staged per barrier
 # 3-D stencil sweeps through a TMA plane ring (cp.async.bulk.tensor.3d into
 # shared memory, mbarrier-tracked, persistent balanced grid): the tma3 mode
 # (measured: heat_3d N=400 39.3 ms vs 37.3 for march at the best geometry
@@ -238,8 +242,8 @@ class _Gen:
                 "rng": {q: self.const_ranges[params.index(q)] for q in params}}
 
     def _contract_kernel(self, cp):
-        """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 m x TN n,
-        8 warps of 16 m rows; K in 32-wide chunks staged in shared memory
+        """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 MF m x TN
+        n, 8 warps of 16 MF m rows; K in BK-wide chunks staged in (dynamic) shared memory
         through affine gathers (address = row part + k part, both
         precomputed), double-buffered through registers.  The accumulators
         start from O's current value (the WCR add) and store once.  FP64
@@ -275,6 +279,7 @@ class _Gen:
         Ntot = ext[Np]
         TN = 8 * min(4, -(-Ntot // 8))
         NF = TN // 8
+        MF, BK = CONTRACT_MF, CONTRACT_BK  # m16 fragments per warp, k chunk
         ax, ay, ao = (self.arg(("ptr", X)), self.arg(("ptr", Y)), self.arg(("ptr", O)))
         for c in (X, Y, O):
             self.cont(c)
@@ -284,7 +289,8 @@ class _Gen:
              f"M={Mtot} N={Ntot} K={Ktot}",
              "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)),
              "namespace {",
-             "constexpr int TM = 128, BK = 16, TN = %d, NF = %d, APAD = 4, BPAD = 4;" % (TN, NF),
+             "constexpr int MF = %d, TM = 128 * MF, BK = %d, TN = %d, NF = %d, APAD = 4, BPAD = 4;"
+             % (MF, BK, TN, NF),
              f"constexpr long long MT = {Mtot}LL, NT = {Ntot}LL, KT = {Ktot}LL;",
              "__device__ __forceinline__ void b2c_dmma(double (&d)[4], double a0, double a1, "
              "double b0) {",
@@ -307,9 +313,12 @@ class _Gen:
              f"  const double *__restrict__ X = (const double *){ax} + {cp['cx'][0]}LL;",
              f"  const double *__restrict__ Y = (const double *){ay} + {cp['cy'][0]}LL;",
              f"  double *__restrict__ O = (double *){ao} + {cp['co'][0]}LL;",
-             "  __shared__ __align__(16) double As[2][TM][BK + APAD];",
-             "  __shared__ __align__(16) double Bs[2][BK][TN + BPAD];",
-             "  __shared__ long long sMX[TM];",
+             "  extern __shared__ __align__(16) double b2c_smem[];",
+             "  double (*As)[TM][BK + APAD] = reinterpret_cast<double (*)[TM][BK + APAD]>(b2c_smem);",
+             "  double (*Bs)[BK][TN + BPAD] = reinterpret_cast<double (*)[BK][TN + BPAD]>("
+             "b2c_smem + 2 * TM * (BK + APAD));",
+             "  long long *sMX = reinterpret_cast<long long *>("
+             "b2c_smem + 2 * TM * (BK + APAD) + 2 * BK * (TN + BPAD));",
              "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;",
              "  const int g = lane >> 2, t = lane & 3;",
              "  const long long ntiles = (NT + TN - 1) / TN;",
@@ -354,16 +363,18 @@ class _Gen:
              "      }",
              "    };",
              # accumulators start from O (the WCR add)
-             "    double acc[NF][4];",
-             "    const int wm = warp * 16;",
+             "    double acc[MF][NF][4];",
+             "    const int wm = warp * 16 * MF;",
+             "#pragma unroll",
+             "    for (int mf = 0; mf < MF; ++mf)",
              "#pragma unroll",
              "    for (int f = 0; f < NF; ++f)",
              "#pragma unroll",
              "      for (int h = 0; h < 2; ++h)",
              "#pragma unroll",
              "        for (int e2 = 0; e2 < 2; ++e2) {",
-             "          const long long m = m0 + wm + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
-             f"          acc[f][2 * h + e2] = (m < MT && n < NT) ? O[b2c_mo((unsigned)m) + {con}LL * "
+             "          const long long m = m0 + wm + 16 * mf + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
+             f"          acc[mf][f][2 * h + e2] = (m < MT && n < NT) ? O[b2c_mo((unsigned)m) + {con}LL * "
              f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
              "        }",
              "    load(0);",
@@ -375,22 +386,31 @@ class _Gen:
              "      if (kc + 1 < nk) load((kc + 1) * BK);",
              "#pragma unroll",
              "      for (int k4 = 0; k4 < BK; k4 += 4) {",
-             "        const double a0 = As[cur][wm + g][k4 + t], a1 = As[cur][wm + g + 8][k4 + t];",
+             "        double bf[NF];",
              "#pragma unroll",
-             "        for (int f = 0; f < NF; ++f) b2c_dmma(acc[f], a0, a1, Bs[cur][k4 + t][f * 8 + g]);",
+             "        for (int f = 0; f < NF; ++f) bf[f] = Bs[cur][k4 + t][f * 8 + g];",
+             "#pragma unroll",
+             "        for (int mf = 0; mf < MF; ++mf) {",
+             "          const double a0 = As[cur][wm + 16 * mf + g][k4 + t], "
+             "a1 = As[cur][wm + 16 * mf + g + 8][k4 + t];",
+             "#pragma unroll",
+             "          for (int f = 0; f < NF; ++f) b2c_dmma(acc[mf][f], a0, a1, bf[f]);",
+             "        }",
              "      }",
              "      if (kc + 1 < nk) store(cur ^ 1);",
              "      __syncthreads();",
              "    }",
+             "#pragma unroll",
+             "    for (int mf = 0; mf < MF; ++mf)",
              "#pragma unroll",
              "    for (int f = 0; f < NF; ++f)",
              "#pragma unroll",
              "      for (int h = 0; h < 2; ++h)",
              "#pragma unroll",
              "        for (int e2 = 0; e2 < 2; ++e2) {",
-             "          const long long m = m0 + wm + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
+             "          const long long m = m0 + wm + 16 * mf + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
              f"          if (m < MT && n < NT) O[b2c_mo((unsigned)m) + {con}LL * "
-             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] = acc[f][2 * h + e2];",
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] = acc[mf][f][2 * h + e2];",
              "        }",
              "  }",
              "}"]
@@ -406,7 +426,8 @@ class _Gen:
         spec.block = (256, 1, 1)
         spec.vec = 1
         spec.pdl = False
-        spec.contract = {"M": Mtot, "N": Ntot, "K": Ktot, "TN": TN}
+        spec.contract = {"M": Mtot, "N": Ntot, "K": Ktot, "TN": TN, "TM": 128 * MF}
+        spec.smem = 8 * (2 * 128 * MF * (BK + 4) + 2 * BK * (TN + 4) + 128 * MF)
         return spec
 
     def _reduction_plan(self):
@@ -2233,7 +2254,7 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         return (spec.grid_cap, 1, 1), spec.block
     if spec.mode == "contract":
         c = spec.contract
-        tiles = -(-c["M"] // 128) * -(-c["N"] // c["TN"])
+        tiles = -(-c["M"] // c.get("TM", 128)) * -(-c["N"] // c["TN"])
         return (max(1, min(tiles, 148 * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "march":
         bx, by = spec.block[0], spec.block[1]

@@ -24,6 +24,16 @@ sys.path.insert(0, str(ROOT))
 from bench import ClockSampler, make_inputs, peaks  # noqa: E402
 
 
+# algorithmic bytes per launch of kernels whose run-level share is not their
+# share of points (N = 8000, f64): gemver's row pass 0 reads and writes A and
+# reads u1 v1 u2 v2 y, writes x partials; row pass 2 reads A and x
+_N = 8000
+KERNEL_BYTES = {
+    "gemver": {"b2_rp_gemver_0": 16 * _N * _N + 6 * 8 * _N,
+               "b2_rp_gemver_2": 8 * _N * _N + 2 * 8 * _N},
+}
+
+
 def _b(*shapes):
     return 8 * sum(int(np.prod(s)) for s in shapes)
 
@@ -163,9 +173,18 @@ def run_one(name, reps):
     if top[0] is not None and top[1][1] > 0:
         npts = top[1][2] * top[1][0]
         if bound == "hbm":
-            # the kernel's share of the run's algorithmic bytes (by points)
-            tot_pts = sum(n * pp for (n, _, pp) in prof.values()) or npts
-            kb = work * npts / tot_pts
+            # the kernel's share of the run's algorithmic bytes: explicit per
+            # kernel where kernels of one run move different bytes per point
+            # (gemver's first row pass reads and writes A, the second only
+            # reads it), else by points
+            model = KERNEL_BYTES.get(name, {}).get(top[0])
+            if model is not None:
+                kb = model * top[1][0]
+                res["bytes_model"] = "per-kernel algorithmic bytes (KERNEL_BYTES)"
+            else:
+                tot_pts = sum(n * pp for (n, _, pp) in prof.values()) or npts
+                kb = work * npts / tot_pts
+                res["bytes_model"] = "run bytes x the kernel's share of points"
             ach = kb / (top[1][1] / 1e3) / 1e9
             l2 = name == "jacobi_2d"  # 2 x 32 MB stay in the 126 MB L2 across sweeps
             pk = extra.get("l2_read_gbs", 16190.1) if l2 else hbm

@@ -175,7 +175,9 @@ def test_kernel_mode_selection():
     pl = P.Planner(g, syms).build()
     grp = [op for op in pl.all_ops if isinstance(op, P.MapGroup)][1]
     sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")
-    assert sp.mode == "contract" and sp.contract == {"M": 449352, "N": 16, "K": 1200, "TN": 16}
+    assert sp.mode == "contract" and sp.contract == {"M": 449352, "N": 16, "K": 1200, "TN": 16,
+                                                     "TM": 256}
+    assert sp.smem > 48 * 1024  # dynamic shared memory (two 256 x 20 A stages)
     assert "mma.sync.aligned.m16n8k4.row.col.f64" in sp.source
     codegen.CONTRACT_MODE = False
     try:
