@@ -1,6 +1,4 @@
-for cfg in "1 16" "1 32" "2 16" "2 32"; do
-  set -- $cfg
-  echo "== MF=$1 BK=$2"
-  B2_CONTRACT_MF=$1 B2_CONTRACT_BK=$2 timeout 600 python -m pytest tests/test_gpu_config.py tests/test_gpu_contract.py tests/test_gpu_parity.py -m gpu -q -x -k "conv2d" 2>&1 | tail -1
-  B2_CONTRACT_MF=$1 B2_CONTRACT_BK=$2 timeout 300 python scripts/bench_suite.py --only conv2d_bias --reps 10 --out gpurun_out/c.json 2>&1 | grep conv2d
-done
+echo "256 thr BK32"; timeout 300 python scripts/probe_dgemm.py
+echo "512 thr BK32"; B2_DGEMM_THREADS=512 timeout 300 python scripts/probe_dgemm.py
+echo "512 thr BK16"; B2_DGEMM_THREADS=512 B2_DGEMM_BK=16 timeout 300 python scripts/probe_dgemm.py
+B2_DGEMM_THREADS=512 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_config.py -m gpu -q -x -k "gemm or dgemm or matmul" 2>&1 | tail -1
