@@ -37,6 +37,12 @@ TMA_ROWS = os.environ.get("B2_RP_TMA", "1") == "1"  # bulk-copy row ring (rowpas
 # rel_err against an 80-bit evaluation; the reference's BLAS: 3.5e-12) but
 # FP64-issue bound (atax 0.171 vs 0.092 ms), so opt-in
 RP_COMP = os.environ.get("B2_RP_COMP", "0") == "1"
+# dot-only passes walk the rows bottom-up: a pass that follows another over
+# the same matrix (gemver's w = A x after the A update) starts on the rows the
+# previous pass left in L2.  Row dots are independent of the row order, so the
+# results are bitwise the same; passes with column partials (AXPY) keep the
+# forward order their fold relies on.
+RP_REV_DOT = os.environ.get("B2_RP_REV", "1") == "1"
 SMEM_BUDGET = 220 * 1024
 
 
@@ -300,6 +306,7 @@ class RowPass:
                      ("RP_WRITEBACK", int(self.prologue is not None)),
                      ("RP_TMA", int(self.tma)), ("RP_S", max(1, self.ring)),
                      ("RP_COMP", int(RP_COMP)),
+                     ("RP_REV", int(RP_REV_DOT and axpy is None and self.tma)),
                      ("RP_VSMEM", int(self.tma and self.vsmem)),
                      ("RP_NSTAGED", nst)):
             L.append(f"#define {k} {v}LL" if k in ("RP_M", "RP_N", "RP_RS") else f"#define {k} {v}")

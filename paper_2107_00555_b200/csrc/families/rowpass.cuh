@@ -94,6 +94,12 @@ __device__ __forceinline__ double rp_block_sum(double v, double vl, double *red,
   return RP_COMP ? t + tl : t;
 }
 
+#ifndef RP_REV
+#define RP_REV 0
+#endif
+// row of step index mi (bottom-up for RP_REV passes; see blas2.RP_REV_DOT)
+#define RP_ROW(mi) (RP_REV ? (RP_M - 1 - (mi)) : (mi))
+
 #if RP_TMA
 // TMA variant: rows stream through an RP_S-deep ring of shared-memory row
 // buffers filled by 1-D bulk copies (cp.async.bulk + mbarrier), so up to
@@ -139,12 +145,13 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
   if (tid == 0) {
     for (int s = 0; s < RP_S; ++s) {
       const b2_ll m = blockIdx.x + (b2_ll)s * gridDim.x;
-      if (m < RP_M) b2_bulk_load(ring + s * RP_CW, R + m * RP_RS + c0, bytes, &rp_bar[s]);
+      if (m < RP_M) b2_bulk_load(ring + s * RP_CW, R + RP_ROW(m) * RP_RS + c0, bytes, &rp_bar[s]);
     }
   }
   int parity = 0;
   int it = 0;
-  for (b2_ll m = blockIdx.x; m < RP_M; m += gridDim.x, ++it) {
+  for (b2_ll mi = blockIdx.x; mi < RP_M; mi += gridDim.x, ++it) {
+    const b2_ll m = RP_ROW(mi);  // the row this step processes
     const int s = it % RP_S;
     b2_mbar_wait(&rp_bar[s], (unsigned)((it / RP_S) & 1));
     double x[RP_KPT];
@@ -181,8 +188,8 @@ extern "C" __global__ void __launch_bounds__(RP_TPB) RP_NAME(const __grid_consta
     __syncthreads();  // every thread has read slot s
 #endif
     if (tid == 0) {
-      const b2_ll mn = m + (b2_ll)RP_S * gridDim.x;
-      if (mn < RP_M) b2_bulk_load(ring + s * RP_CW, R + mn * RP_RS + c0, bytes, &rp_bar[s]);
+      const b2_ll mn = mi + (b2_ll)RP_S * gridDim.x;
+      if (mn < RP_M) b2_bulk_load(ring + s * RP_CW, R + RP_ROW(mn) * RP_RS + c0, bytes, &rp_bar[s]);
     }
 #if RP_AXPY
     const double c = rp_coef(a, m, d);
