@@ -53,6 +53,15 @@ MARCH_PDL = os.environ.get("B2_MARCH_PDL", "1") == "1"  # march sweeps as progra
 # share of their time (nbody's per-step kernels: 5.32 -> 4.67 ms)
 SMALL_PDL = os.environ.get("B2_SMALL_PDL", "1") == "1"
 SMALL_PDL_POINTS = 1 << 16
+# 2-D sweeps small enough to stay mostly in L2 (<= 2^24 points): each thread
+# walks MARCH2_V consecutive rows of a 64-column tile and reuses the
+# north / centre rows from registers (scripts/heatlab/jaclab.cu: jacobi_2d
+# N=2000 8.03 vs 8.54 us per sweep for tile2; in the program with
+# programmatic dependent launch 1.572 ms vs 1.735 for tile2, 1.670 without PDL)
+MARCH2 = os.environ.get("B2_MARCH2", "1") == "1"
+MARCH2_V = int(os.environ.get("B2_MARCH2_V", "16"))
+MARCH2_BY = int(os.environ.get("B2_MARCH2_BY", "4"))
+MARCH2_PDL = os.environ.get("B2_MARCH2_PDL", "1") == "1"
 TILE_PDL = os.environ.get("B2_TILE_PDL", "0") == "1"  # ... tile2 sweeps (jacobi 1.74 -> 1.86 ms: off)
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
 SLAB_BX = int(os.environ.get("B2_SLAB_BX", "32"))  # tile columns of slab sweeps
@@ -1434,6 +1443,7 @@ class _Gen:
             if (mode == "tile2" and k == 3 and self.const_ranges[0] is not None
                     and self.const_ranges[0][2] >= 16):
                 mode = "march"  # measured best for 3-D sweeps (heat_3d: 207 us vs 247 tile2)
+
         if (mode == "march" and TMA3 and not getattr(self.pl, "dynamic_p0", False)
                 and all(r is not None and r[1] == 1 for r in self.const_ranges)
                 and all(r[2] >= 8 for r in self.const_ranges)):
@@ -1482,6 +1492,11 @@ class _Gen:
                 self.red_pout = pout
                 self.red_full = False
                 self.red_R = R
+        if (mode == "tile2" and k == 2 and MARCH2
+                and not getattr(self.pl, "dynamic_p0", False)
+                and self.const_ranges[0][2] >= 4 * MARCH2_V
+                and self.const_ranges[0][2] * self.const_ranges[1][2] <= (1 << 24)):
+            mode = "march2"  # (reductions / row reductions / contractions keep theirs)
         spec.mode = mode
         # slab executors launch a map's chunk in pieces (boundary rows first,
         # interior overlapped with the halo exchange): keep dim 0's range a
@@ -1510,6 +1525,8 @@ class _Gen:
                 vec = SLAB_VEC
             else:
                 vec = 16 if (r0 is not None and r0[2] >= 256) else 8
+        elif mode == "march2":
+            vec = MARCH2_V  # rows per thread
         elif mode == "tma3":
             vec = 2  # points per thread along the row (tile width <= 64)
         elif mode == "flat" and all(r is not None for r in self.const_ranges):
@@ -1523,6 +1540,7 @@ class _Gen:
         spec.align = 0
         spec.block = {"scalar": (1, 1, 1), "seq": (1, 1, 1), "flat": (256, 1, 1),
                       "tile2": (32, TILE_BY, 1), "march": (SLAB_BX if self.dyn0 else MARCH_BX, MARCH_BY, 1), "reduce": (256, 1, 1),
+                      "march2": (64, MARCH2_BY, 1),
                       "rowred": (256, 1, 1), "tma3": (32, TMA3_CW + 1, 1)}[mode]
 
         # containers written anywhere in this group: the rest are read-only
@@ -1731,6 +1749,30 @@ class _Gen:
             else:
                 loop += vloop(hdr)
             loop.append("  }")
+        elif mode == "march2":
+            # 64-column tiles of MARCH2_BY x vec rows: each thread walks `vec`
+            # consecutive rows (unrolled), so a stencil's north / centre rows
+            # come from the previous iterations' registers
+            rows = spec.block[1] * vec
+            loop.append("  const b2_ll tiles_x = (rl1 + 63) / 64;")
+            loop.append(f"  const b2_ll tiles_y = (rl0 + {rows - 1}) / {rows};")
+            loop.append("  for (b2_ll vb = blockIdx.x; vb < tiles_x * tiles_y; vb += gridDim.x) {")
+            loop.append("    const b2_ll tx = vb % tiles_x, ty = vb / tiles_x;")
+            loop.append("    const b2_ll i1 = tx * 64 + threadIdx.x;")
+            loop.append("    if (i1 >= rl1) continue;")
+            loop.append(f"    const b2_ll p_{grp.params[1]} = rb1 + rs1 * i1;")
+            loop.append(f"    const b2_ll r0 = (ty * {spec.block[1]} + threadIdx.y) * {vec};")
+            hdr = ["    const b2_ll i0 = r0 + v;", "    if (i0 >= rl0) break;",
+                   f"    const b2_ll p_{grp.params[0]} = rb0 + rs0 * i0;"]
+            if MARCH_FULL:
+                loop.append(f"    if (r0 + {vec} <= rl0) {{")
+                loop += vloop([hdr[0], hdr[2]])
+                loop.append("    } else {")
+                loop += vloop(hdr)
+                loop.append("    }")
+            else:
+                loop += vloop(hdr)
+            loop.append("  }")
         elif mode == "march":
             # 32 x 8 tiles over dims (k-2, k-1); each thread walks `vec`
             # consecutive indices of dim 0 (unrolled) so the compiler reuses the
@@ -1788,6 +1830,7 @@ class _Gen:
         for r in self.const_ranges:
             npts *= r[2] if r is not None else 1 << 40
         spec.pdl = ((MARCH_PDL and mode in ("march", "tma3")) or (TILE_PDL and mode == "tile2")
+                    or (MARCH2_PDL and mode == "march2")
                     or (SMALL_PDL and mode in ("flat", "reduce", "scalar")
                         and npts <= SMALL_PDL_POINTS)) and not self.dyn0
         if spec.pdl:
@@ -2256,6 +2299,10 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         c = spec.contract
         tiles = -(-c["M"] // c.get("TM", 128)) * -(-c["N"] // c["TN"])
         return (max(1, min(tiles, 148 * 8)), 1, 1), (256, 1, 1)
+    if spec.mode == "march2":
+        rows = spec.block[1] * spec.vec
+        nvb = -(-rl[1] // 64) * -(-rl[0] // rows)
+        return (max(1, min(nvb, MAX_BLOCKS * 8)), 1, 1), (64, spec.block[1], 1)
     if spec.mode == "march":
         bx, by = spec.block[0], spec.block[1]
         nvb = -(-(rl[k - 1] + spec.align) // bx) * -(-rl[k - 2] // by) * -(-rl[0] // spec.vec)
