@@ -95,6 +95,9 @@ B2_API int b2_device_sync(void);
 B2_API int b2_event_create(void **ev);
 B2_API int b2_event_destroy(void *ev);
 B2_API int b2_event_record(void *ev, void *stream);
+/* Inside a stream capture: an event-record node timestamped when the graph
+ * replays (per-kernel timing of a captured trace, Machine.profile_launches). */
+B2_API int b2_event_record_external(void *ev, void *stream);
 B2_API int b2_event_elapsed_ms(void *start, void *end, float *ms);
 /* `stream` waits for `ev` (fork/join of side streams, also inside capture). */
 B2_API int b2_stream_wait_event(void *stream, void *ev);

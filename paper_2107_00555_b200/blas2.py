@@ -415,21 +415,21 @@ class RowPass:
         prof = ex._prof
         if prof is not None:
             ev = ex._prof_event_pair()
-            rt.lib().b2_event_record(ev[0], ex.stream)
+            ex._prof_record(ev[0])
         rt.launch(self.kmain, (self.G, self.ctiles, 1), (self.tpb, 1, 1), blob, ex.stream,
                   self.smem)
         if prof is not None:
-            rt.lib().b2_event_record(ev[1], ex.stream)
+            ex._prof_record(ev[1])
             prof.append((self.kmain.name, self.M * self.N, ev))
         nfin = max(self.N if self.axpy is not None else 0,
                    self.M if (self.dot is not None and self.ctiles > 1) else 0)
         if nfin:
             if prof is not None:
                 ev = ex._prof_event_pair()
-                rt.lib().b2_event_record(ev[0], ex.stream)
+                ex._prof_record(ev[0])
             rt.launch(self.kfin, ((nfin + 31) // 32, 1, 1), (32, 32, 1), blob, ex.stream)
             if prof is not None:
-                rt.lib().b2_event_record(ev[1], ex.stream)
+                ex._prof_record(ev[1])
                 prof.append((self.kfin.name, nfin, ev))
             ex.launches += 1
         ex.launches += 1

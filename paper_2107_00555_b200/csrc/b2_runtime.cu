@@ -181,6 +181,13 @@ extern "C" int b2_event_destroy(void *ev) {
 extern "C" int b2_event_record(void *ev, void *s) {
   return b2_cuda_check(cudaEventRecord((cudaEvent_t)ev, (cudaStream_t)s), "event record");
 }
+// inside a stream capture: an event record NODE (timestamped at replay), not
+// a capture-internal dependency
+extern "C" int b2_event_record_external(void *ev, void *s) {
+  return b2_cuda_check(
+      cudaEventRecordWithFlags((cudaEvent_t)ev, (cudaStream_t)s, cudaEventRecordExternal),
+      "event record external");
+}
 extern "C" int b2_event_elapsed_ms(void *a, void *b, float *ms) {
   int rc = b2_cuda_check(cudaEventSynchronize((cudaEvent_t)b), "event sync");
   if (rc) return rc;

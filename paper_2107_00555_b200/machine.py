@@ -731,34 +731,67 @@ class GpuExecutor:
     _dry = False
     _prof = None
 
+    def _prof_record(self, ev):
+        """Record a profiling event: an event-record node when capturing."""
+        fn = (rt.lib().b2_event_record_external if getattr(self, "_capturing", False)
+              else rt.lib().b2_event_record)
+        rt.check(fn(ev, self.stream), "prof event")
+
     def _prof_event_pair(self):
         a, b = ctypes.c_void_p(), ctypes.c_void_p()
         rt.check(rt.lib().b2_event_create(ctypes.byref(a)), "event")
         rt.check(rt.lib().b2_event_create(ctypes.byref(b)), "event")
         return a.value, b.value
 
-    def profile_launches(self, passes: int = 3) -> dict:
-        """Eager passes with a CUDA-event pair around every kernel launch on
-        the executor's stream; per kernel the MEDIAN over the passes of its
-        per-pass total (the first pass after capture runs cold).  Returns
-        {kernel: (launches per pass, total_ms per pass, points_per_launch)}."""
+    def profile_launches(self, passes: int = 3, graph: bool | None = None) -> dict:
+        """Per-kernel device times: a CUDA-event pair around every kernel
+        launch on the executor's stream; per kernel the MEDIAN over `passes`
+        of its per-pass total (the first pass after capture runs cold).
+
+        graph (default when the trace has no device-side branches): each pass
+        is the state machine captured WITH the event pairs and replayed as one
+        graph, so short kernels are timed without the host's launch gaps (an
+        eager pass times jacobi_2d's 8 us sweeps at ~10 us); programmatic
+        dependent launch is off between the event pairs.  Otherwise eager
+        passes.  Returns {kernel: (launches per pass, total_ms per pass,
+        points_per_launch)}."""
+        L = rt.lib()
+        if graph is None:
+            graph = not self.device_branching
         runs = []
         for _ in range(max(1, passes)):
             self._prof = []
+            ge = ctypes.c_void_p()
             try:
-                rt.check(rt.lib().b2_memset(self.flag, 0, 8, self.stream), "memset")
-                self._run_states(None, eager=True)
+                rt.check(L.b2_memset(self.flag, 0, 8, self.stream), "memset")
+                if graph:
+                    self._instantiate_children()
+                    self._capturing = True
+                    rt.check(L.b2_capture_begin(self.stream), "capture")
+                    try:
+                        self._reset_flags()
+                        self._run_states(Counters(), eager=False)
+                    finally:
+                        self._capturing = False
+                        rc = L.b2_capture_end(self.stream, ctypes.byref(ge))
+                    rt.check(rc, "capture end")
+                    rt.check(L.b2_graph_launch(ge.value, self.stream), "graph launch")
+                else:
+                    self._run_states(None, eager=True)
                 self.sync()
                 out: dict = {}
                 for name, npts, (a, b) in self._prof:
                     ms = ctypes.c_float()
-                    rt.check(rt.lib().b2_event_elapsed_ms(a, b, ctypes.byref(ms)), "elapsed")
+                    rt.check(L.b2_event_elapsed_ms(a, b, ctypes.byref(ms)), "elapsed")
                     n, tot, _ = out.get(name, (0, 0.0, npts))
                     out[name] = (n + 1, tot + ms.value, npts)
-                    rt.lib().b2_event_destroy(a)
-                    rt.lib().b2_event_destroy(b)
                 runs.append(out)
             finally:
+                for _, _, (a, b) in self._prof or []:
+                    L.b2_event_destroy(a)
+                    L.b2_event_destroy(b)
+                if ge.value:
+                    L.b2_graph_destroy(ge.value)
                 self._prof = None
         med = {}
         for name, (n, _, npts) in runs[0].items():
@@ -1039,7 +1072,7 @@ class GpuExecutor:
                                  self.scratch, self.flag)
         if self._prof is not None:
             ev = self._prof_event_pair()
-            rt.lib().b2_event_record(ev[0], self.stream)
+            self._prof_record(ev[0])
         rt.launch(spec.kernel, grid, block, blob, self.stream, spec.smem,
                   pdl=getattr(spec, "pdl", False) and self._prof is None)
         if spec.fin_kernel is not None:
@@ -1048,7 +1081,7 @@ class GpuExecutor:
             rt.launch(spec.fin_kernel, (fg, 1, 1), (256, 1, 1), blob, self.stream)
             self.launches += 1
         if self._prof is not None:
-            rt.lib().b2_event_record(ev[1], self.stream)
+            self._prof_record(ev[1])
             self._prof.append((spec.name, npts, ev))
         self.launches += 1
         if counters is not None:
@@ -1144,12 +1177,12 @@ class GpuExecutor:
             raise P.PlanError("matmul output view is not an affine image of the result")
         if self._prof is not None:
             ev = self._prof_event_pair()
-            rt.lib().b2_event_record(ev[0], self.stream)
+            self._prof_record(ev[0])
         rt.check(rt.lib().b2_gemm_f64(M, N, K, ab + 8 * ao, rsa, csa, bb + 8 * bo, rsb, csb,
                                       cb + 8 * co, rsc, csc, rt.WCR_CODE[om.wcr], self.stream),
                  "gemm")
         if self._prof is not None:
-            rt.lib().b2_event_record(ev[1], self.stream)
+            self._prof_record(ev[1])
             self._prof.append((f"b2_gemm_f64[{M}x{N}x{K}]", M * N, ev))
         self.launches += 1
         if counters is not None:

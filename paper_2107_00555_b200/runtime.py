@@ -74,7 +74,8 @@ EXPORTS = [
     "b2_version", "b2_last_error", "b2_init", "b2_device_count", "b2_device_info",
     "b2_malloc", "b2_free", "b2_memcpy_h2d", "b2_memcpy_d2h", "b2_memcpy_d2d", "b2_memset",
     "b2_stream_create", "b2_stream_destroy", "b2_stream_sync", "b2_device_sync",
-    "b2_event_create", "b2_event_destroy", "b2_event_record", "b2_event_elapsed_ms",
+    "b2_event_create", "b2_event_destroy", "b2_event_record", "b2_event_record_external",
+    "b2_event_elapsed_ms",
     "b2_stream_wait_event", "b2_capture_if_begin", "b2_capture_if_end", "b2_capture_body_begin",
     "b2_capture_body_end", "b2_counters_add",
     "b2_host_register", "b2_host_unregister", "b2_jit_compile", "b2_module_load",
@@ -117,6 +118,7 @@ _SIGS = {
     "b2_event_create": ([ctypes.POINTER(_vp)], ctypes.c_int),
     "b2_event_destroy": ([_vp], ctypes.c_int),
     "b2_event_record": ([_vp, _vp], ctypes.c_int),
+    "b2_event_record_external": ([_vp, _vp], ctypes.c_int),
     "b2_event_elapsed_ms": ([_vp, _vp, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
     "b2_stream_wait_event": ([_vp, _vp], ctypes.c_int),
     "b2_capture_if_begin": ([_vp, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp),

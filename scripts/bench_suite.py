@@ -162,16 +162,19 @@ def run_one(name, reps):
         res["frac_of_measured_hbm"] = rate / 1e9 / hbm
     elif unit == "flop":
         res["TFLOPs"] = rate / 1e12
-    # eager per-launch events include each launch's issue gap, so for
-    # launch-bound programs (nbody: 10 µs kernels) their sum exceeds the
-    # captured graph's run time; the share is taken against the larger of the two
-    eager_ms = sum(tot for (_, tot, _) in prof.values())
-    res["eager_kernel_ms_total"] = eager_ms
-    res["step_share_top"] = top[1][1] / max(ms, eager_ms) if ms else None
+    # the event pairs between kernels add small gaps, so the kernels' sum can
+    # exceed the plain graph's run time; the share is taken against the larger
+    kern_ms = sum(tot for (_, tot, _) in prof.values())
+    res["kernel_ms_total"] = kern_ms
+    res["step_share_top"] = top[1][1] / max(ms, kern_ms) if ms else None
     # roofline of the dominant kernel against the measured ceiling of its bound
     extra = _extra_peaks()
     if top[0] is not None and top[1][1] > 0:
         npts = top[1][2] * top[1][0]
+        res["kernel_time_basis"] = ("CUDA-event pairs around every launch, captured and "
+                                    "replayed as one graph (median of 3)"
+                                    if not ex.device_branching else
+                                    "eager per-launch CUDA events (median of 3)")
         if bound == "hbm":
             # the kernel's share of the run's algorithmic bytes: explicit per
             # kernel where kernels of one run move different bytes per point

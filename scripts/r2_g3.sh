@@ -1,4 +1,8 @@
-timeout 1800 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-for v in "1 0" "1 1" "0 0"; do set -- $v
-  B2_MARCH2=$1 B2_MARCH2_PDL=$2 timeout 300 python scripts/bench_suite.py --only jacobi_2d --reps 20 --out gpurun_out/j.json 2>&1 | grep jacobi | sed "s/^/march2=$1 pdl=$2 /"
-done
+timeout 900 python bench.py --steps 10 --warmup 3 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline'])"
+timeout 1800 python scripts/bench_suite.py --reps 10 --out gpurun_out/bench_suite_r02d.json > gpurun_out/f_suite_d.log 2>&1; tail -12 gpurun_out/f_suite_d.log
+python - <<'PY'
+import json
+d = json.load(open("gpurun_out/bench_suite_r02d.json"))
+for k, x in d.items():
+    print(k, round(x["ms_per_run"], 4), x.get("roofline") and round(x["roofline"]["frac"], 3), round(x.get("step_share_top") or 0, 3), x.get("kernel_time_basis"))
+PY
