@@ -103,6 +103,13 @@ B2_API int b2_event_elapsed_ms(void *start, void *end, float *ms);
 B2_API int b2_stream_wait_event(void *stream, void *ev);
 B2_API int b2_host_register(void *p, size_t bytes);
 B2_API int b2_host_unregister(void *p);
+/* CUDA IPC for peer-store halos (dist.PeerHalo): the 64-byte handle of an
+ * allocation, its mapping in another process on a peer GPU, unmapping.
+ * Replaces the reference's simulated ISEND/IRECV copies
+ * (interp.py:443-447, 483-489) when B2_SLAB_PEER=1. */
+B2_API int b2_ipc_handle(void *p, void *out64);
+B2_API int b2_ipc_open(const void *h64, void **p);
+B2_API int b2_ipc_close(void *p);
 
 /* ---- JIT of kernel families with inlined tasklet functors (NVRTC) ------ */
 /* Compile CUDA C++ `src` for sm_100a.  On success *cubin_size is the image

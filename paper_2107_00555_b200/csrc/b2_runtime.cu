@@ -203,6 +203,24 @@ extern "C" int b2_host_register(void *p, size_t n) {
 extern "C" int b2_host_unregister(void *p) {
   return b2_cuda_check(cudaHostUnregister(p), "host unregister");
 }
+// CUDA IPC: a peer process maps this allocation (peer-store halos)
+extern "C" int b2_ipc_handle(void *p, void *out64) {
+  cudaIpcMemHandle_t h;
+  int rc = b2_cuda_check(cudaIpcGetMemHandle(&h, p), "ipc get handle");
+  if (rc) return rc;
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out64, &h, sizeof(h));
+  return B2_OK;
+}
+extern "C" int b2_ipc_open(const void *h64, void **p) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h64, sizeof(h));
+  return b2_cuda_check(cudaIpcOpenMemHandle(p, h, cudaIpcMemLazyEnablePeerAccess),
+                       "ipc open handle");
+}
+extern "C" int b2_ipc_close(void *p) {
+  return b2_cuda_check(cudaIpcCloseMemHandle(p), "ipc close handle");
+}
 
 // ---------------------------------------------------------------------------
 // NVRTC JIT

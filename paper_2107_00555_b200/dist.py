@@ -498,6 +498,92 @@ class NcclComm:
         self.rt.lib().b2_nccl_destroy(self.comm)
 
 
+def peer_copy_plan(plan: SlabPlan, rank: int, ops, row_elems: dict, esz: int = 8) -> list:
+    """The peer stores of a halo exchange: for every send op (True, peer, c,
+    lo, hi) — global rows [lo, hi) of container c, owned here and read by
+    `peer` — (peer, c, src_byte_offset in this rank's buffer, dst_byte_offset
+    in the peer's buffer, bytes).  A rank's buffer of c holds global rows
+    plan.window[rank][c][0] ... contiguously, rows of row_elems[c] elements."""
+    out = []
+    for send, peer, c, lo, hi in ops:
+        if not send:
+            continue
+        row = row_elems[c] * esz
+        out.append((peer, c, (lo - plan.window[rank][c][0]) * row,
+                    (lo - plan.window[peer][c][0]) * row, (hi - lo) * row))
+    return out
+
+
+class PeerHalo:
+    """Peer-store halo exchange (B2_SLAB_PEER=1; NVLink P2P on a multi-GPU
+    node): every rank maps its neighbours' buffers of the distributed
+    containers through CUDA IPC (b2_ipc_handle / b2_ipc_open) and writes the
+    rows they read straight into their halos with a copy kernel on the
+    exchange stream (SM stores over NVLink — no NCCL data movement); then
+    each pair of neighbours trades an 8-byte token (``sync``: NCCL send/recv
+    on the same stream by default), so a rank's next use of its halo is
+    ordered after its neighbours' stores, and a neighbour's next store after
+    this rank's last read of the halo (the halo rows are read only by the
+    boundary launch, which precedes this rank's token in stream order).
+    Unmeasured in this environment (one GPU); the data path and the offsets
+    are tested with two processes sharing one GPU and a host-side sync."""
+
+    def __init__(self, plan: SlabPlan, rank: int, ptrs: dict, row_elems: dict, sync=None,
+                 group=None):
+        import ctypes
+
+        import torch.distributed as tdist
+
+        from . import runtime as rt
+
+        self.rt, self.ct = rt, ctypes
+        self.plan, self.rank = plan, rank
+        self.ptrs, self.row_elems = dict(ptrs), dict(row_elems)
+        L = rt.lib()
+        mine = {}
+        for c in sorted(plan.dist):
+            h = ctypes.create_string_buffer(64)
+            rt.check(L.b2_ipc_handle(ptrs[c], h), "ipc handle")
+            mine[c] = h.raw
+        allh = [None] * plan.P
+        tdist.all_gather_object(allh, mine, group=group)
+        self.peer_ptr = {}
+        peers = {peer for c in plan.dist for peer, _, _ in plan.transfers(c, rank)[0]}
+        for peer in sorted(peers):
+            for c in sorted(plan.dist):
+                p = ctypes.c_void_p()
+                rt.check(L.b2_ipc_open(ctypes.create_string_buffer(allh[peer][c], 64),
+                                       ctypes.byref(p)), "ipc open")
+                self.peer_ptr[(peer, c)] = p.value
+        self.sync = sync
+        self.bytes_stored = 0
+
+    def store(self, ops, stream) -> int:
+        """Peer stores of one exchange on `stream`; returns bytes stored."""
+        rt, ct, L = self.rt, self.ct, self.rt.lib()
+        n = 0
+        for peer, c, so, do, nb in peer_copy_plan(self.plan, self.rank, ops, self.row_elems):
+            dv = rt.make_view(self.peer_ptr[(peer, c)], do // 8, "f64", [nb // 8], [1])
+            sv = rt.make_view(self.ptrs[c], so // 8, "f64", [nb // 8], [1])
+            rt.check(L.b2_copy_view(ct.byref(dv), ct.byref(sv), 0, stream), "peer store")
+            n += nb
+        self.bytes_stored += n
+        return n
+
+    def exchange(self, ops, stream) -> int:
+        n = self.store(ops, stream)
+        peers = sorted({peer for _, peer, *_ in ops})
+        if peers and self.sync is not None:
+            self.sync(peers, stream)
+        return n
+
+    def close(self):
+        L = self.rt.lib()
+        for p in self.peer_ptr.values():
+            L.b2_ipc_close(p)
+        self.peer_ptr = {}
+
+
 class SlabGpuRunner:
     """One rank of a slab-distributed program on its own GPU: the local graph
     runs through a normal GpuExecutor (fused kernels, CUDA-graph capture of
@@ -505,12 +591,15 @@ class SlabGpuRunner:
     NCCL group send/recv on the same stream — one graph launch per run."""
 
     def __init__(self, g, bindings: dict, rank: int, world: int, device: int,
-                 overlap: bool | None = None, force_split: bool = False):
+                 overlap: bool | None = None, force_split: bool = False,
+                 peer: bool | None = None):
         import ctypes
         import os
 
         if overlap is None:
             overlap = os.environ.get("B2_SLAB_OVERLAP", "1") != "0"
+        if peer is None:
+            peer = os.environ.get("B2_SLAB_PEER", "0") == "1"
 
         import torch
 
@@ -525,6 +614,15 @@ class SlabGpuRunner:
         self.ex = GpuExecutor(self.lg, bindings, device=device, options=InterpOptions(),
                               dynamic_p0=overlap)
         self.nccl = NcclComm(rank, world) if world > 1 else None
+        self.peer = None
+        if peer and world > 1 and all(self.lg.containers[c].dtype == "f64" for c in self.plan.dist):
+            rows = {c: int(np.prod(self.ex.buf.shape[c][1:])) for c in self.plan.dist}
+            self.peer = PeerHalo(self.plan, rank, {c: self.ex.buf.ptr[c] for c in self.plan.dist},
+                                 rows, sync=self._tokens)
+            # token buffers allocated up front (no cudaMalloc inside a capture)
+            nbrs = {peer for c in self.plan.dist for lst in self.plan.transfers(c, rank)
+                    for peer, _, _ in lst}
+            self._tok = {p: (self.ex.buf.alloc(8), self.ex.buf.alloc(8)) for p in sorted(nbrs)}
         self.xchg = HaloExchanger(self.plan, rank, self._rows_of, transport=self._transport)
         self.ex.op_hook = self._hook
         self._exchanged: set[str] = set()
@@ -572,9 +670,7 @@ class SlabGpuRunner:
                 ops += [(True, peer, c, lo, hi) for peer, lo, hi in sends]
                 ops += [(False, peer, c, lo, hi) for peer, lo, hi in recvs]
             if ops:
-                self.xchg.bytes_sent += self.nccl.p2p(
-                    [(sd, peer) + self._rows_ptr(c, lo, hi) for sd, peer, c, lo, hi in ops],
-                    self.side)
+                self.xchg.bytes_sent += self._p2p(ops, self.side)
                 self.xchg.exchanges += 1
         rt.check(L.b2_event_record(self.ev_join, self.side), "event")
         ex.launch_map_rows(op, rvals, env, n_lo, n - n_hi, ex.stream)
@@ -598,8 +694,20 @@ class SlabGpuRunner:
             return 0
         if self.nccl is None:
             raise DistError("halo exchange without a communicator")
+        return self._p2p(ops, self.ex.stream)
+
+    def _p2p(self, ops, stream) -> int:
+        """One halo exchange on `stream`: NCCL send/recv of the rows, or (peer
+        mode) stores into the neighbours' halos plus a token exchange."""
+        if self.peer is not None:
+            return self.peer.exchange(ops, stream)
         return self.nccl.p2p([(s, peer) + self._rows_ptr(c, lo, hi) for s, peer, c, lo, hi in ops],
-                             self.ex.stream)
+                             stream)
+
+    def _tokens(self, peers, stream):
+        """8-byte NCCL send + recv with every neighbour of the exchange."""
+        self.nccl.p2p([(True, p, self._tok[p][0], 8) for p in peers]
+                      + [(False, p, self._tok[p][1], 8) for p in peers], stream)
 
     def _rows_of(self, c, lo, hi):
         """torch view of global rows [lo, hi) of container c's local buffer."""

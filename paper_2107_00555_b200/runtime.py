@@ -78,7 +78,8 @@ EXPORTS = [
     "b2_event_elapsed_ms",
     "b2_stream_wait_event", "b2_capture_if_begin", "b2_capture_if_end", "b2_capture_body_begin",
     "b2_capture_body_end", "b2_counters_add",
-    "b2_host_register", "b2_host_unregister", "b2_jit_compile", "b2_module_load",
+    "b2_host_register", "b2_host_unregister", "b2_ipc_handle", "b2_ipc_open", "b2_ipc_close",
+    "b2_jit_compile", "b2_module_load",
     "b2_module_unload", "b2_module_function", "b2_func_set_max_smem", "b2_launch", "b2_launch_pdl", "b2_launch_coop",
     "b2_launch_count", "b2_capture_begin", "b2_capture_end", "b2_graph_launch",
     "b2_graph_destroy", "b2_copy_view", "b2_fill_view", "b2_gemm_f64", "b2_gemm_f32",
@@ -129,6 +130,9 @@ _SIGS = {
     "b2_counters_add": ([_vp, ctypes.c_longlong, ctypes.c_longlong, ctypes.c_longlong,
                          ctypes.c_longlong, _vp], ctypes.c_int),
     "b2_host_register": ([_vp, ctypes.c_size_t], ctypes.c_int),
+    "b2_ipc_handle": ([_vp, _vp], ctypes.c_int),
+    "b2_ipc_open": ([_vp, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "b2_ipc_close": ([_vp], ctypes.c_int),
     "b2_host_unregister": ([_vp], ctypes.c_int),
     "b2_jit_compile": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p),
                         ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_size_t), ctypes.c_char_p,

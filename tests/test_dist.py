@@ -300,3 +300,40 @@ def test_summa_schedule_covers_every_panel_once(dims):
                     assert st.a_local == st.l % (L // Pc)
                 if st.b_local is not None:
                     assert st.b_local == st.l % (L // Pr)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("name,syms", [("heat_3d", {"N": 12, "TSTEPS": 2}),
+                                       ("jacobi_2d", {"N": 14, "TSTEPS": 2})])
+def test_peer_copy_plan_fills_every_needed_row(name, syms, P):
+    """dist.peer_copy_plan (B2_SLAB_PEER): replaying every rank's peer
+    stores on host copies of the rank windows leaves every row a rank reads
+    equal to the owner's row — the same rows the NCCL path receives."""
+    g = sdfg.load(GOLDEN / "graphs" / f"{name}.raw.json")
+    plan = dist.slab_decompose(g, syms, P)
+    rng = np.random.default_rng(P)
+    for c in plan.dist:
+        full = rng.uniform(-1, 1, (syms["N"],) * (3 if name == "heat_3d" else 2))
+        row = int(np.prod(full.shape[1:]))
+        local = []
+        for r in range(P):
+            # the window as load_inputs leaves it, with every row another
+            # rank owns poisoned: only the exchange may fill those
+            lo, hi = plan.window[r][c]
+            buf = np.array(full[lo:hi], copy=True)
+            for s_ in range(P):
+                if s_ != r:
+                    for row_i in plan.owned[s_][c] & set(range(lo, hi)):
+                        buf[row_i - lo] = np.nan
+            local.append(buf.reshape(-1))
+        for r in range(P):
+            sends, recvs = plan.transfers(c, r)
+            ops = [(True, p, c, lo, hi) for p, lo, hi in sends]
+            for peer, cc, so, do, nb in dist.peer_copy_plan(plan, r, ops, {c: row}):
+                local[peer][do // 8:(do + nb) // 8] = local[r][so // 8:(so + nb) // 8]
+        for r in range(P):
+            lo = plan.window[r][c][0]
+            for row_i in plan.needed[r][c] | plan.owned[r][c]:
+                assert plan.window[r][c][0] <= row_i < plan.window[r][c][1]
+                got = local[r][(row_i - lo) * row:(row_i - lo + 1) * row]
+                assert np.array_equal(got, full[row_i].reshape(-1)), (c, r, row_i)

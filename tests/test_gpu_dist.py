@@ -167,3 +167,83 @@ def test_summa_device_data_plane_single_rank(pg, dtype, n):
     got = c.double().cpu().numpy()
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert err <= (1e-12 if dtype == "f64" else 1e-5), err
+
+
+def _peer_worker(rank, port, q):
+    import ctypes
+
+    import torch.distributed as tdist
+
+    from paper_2107_00555_b200 import dist, runtime as rt, sdfg
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        rt.device(0)
+        L = rt.lib()
+        syms = {"N": 12, "TSTEPS": 2}
+        g = sdfg.load(GOLDEN / "graphs" / "heat_3d.raw.json")
+        plan = dist.slab_decompose(g, syms, 2)
+        rng = np.random.default_rng(3)
+        ptrs, rows, want = {}, {}, {}
+        for c in sorted(plan.dist):
+            full = rng.uniform(-1, 1, (12, 12, 12))
+            lo, hi = plan.window[rank][c]
+            buf = np.array(full[lo:hi], copy=True)
+            for row_i in plan.owned[1 - rank][c] & set(range(lo, hi)):
+                buf[row_i - lo] = np.nan  # only the peer's stores may fill these
+            p = ctypes.c_void_p()
+            rt.check(L.b2_malloc(ctypes.byref(p), buf.nbytes))
+            rt.check(L.b2_memcpy_h2d(p, buf.ctypes.data, buf.nbytes, None))
+            ptrs[c], rows[c], want[c] = p.value, 144, full[lo:hi]
+        s = ctypes.c_void_p()
+        rt.check(L.b2_stream_create(ctypes.byref(s)))
+
+        def host_sync(peers, stream):
+            rt.check(L.b2_stream_sync(stream))
+            tdist.barrier()
+
+        ph = dist.PeerHalo(plan, rank, ptrs, rows, sync=host_sync)
+        ops = []
+        for c in sorted(plan.dist):
+            sends, recvs = plan.transfers(c, rank)
+            ops += [(True, p_, c, lo, hi) for p_, lo, hi in sends]
+            ops += [(False, p_, c, lo, hi) for p_, lo, hi in recvs]
+        n = ph.exchange(ops, s.value)
+        ok = n > 0
+        for c in sorted(plan.dist):
+            got = np.empty_like(want[c])
+            rt.check(L.b2_memcpy_d2h(got.ctypes.data, ptrs[c], got.nbytes, None))
+            ok = ok and np.array_equal(got, want[c])
+        tdist.barrier()
+        ph.close()
+        tdist.barrier()
+        for p in ptrs.values():
+            L.b2_free(p)
+        q.put((rank, bool(ok), n))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_peer_halo_two_processes_one_gpu():
+    """dist.PeerHalo's data path: two processes on the same GPU map each
+    other's slab buffers through CUDA IPC and store the halo rows the other
+    reads (host-side sync instead of the NCCL tokens, which need two GPUs);
+    afterwards every window equals the global array."""
+    import torch.multiprocessing as mp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
