@@ -60,7 +60,7 @@ SMALL_PDL_POINTS = 1 << 16
 # programmatic dependent launch 1.572 ms vs 1.735 for tile2, 1.670 without PDL)
 MARCH2 = os.environ.get("B2_MARCH2", "1") == "1"
 MARCH2_V = int(os.environ.get("B2_MARCH2_V", "16"))
-MARCH2_BY = int(os.environ.get("B2_MARCH2_BY", "4"))
+MARCH2_BY = int(os.environ.get("B2_MARCH2_BY", "2"))  # 1.550 ms vs 1.57 at 4, 2.01 at 1
 MARCH2_PDL = os.environ.get("B2_MARCH2_PDL", "1") == "1"
 TILE_PDL = os.environ.get("B2_TILE_PDL", "0") == "1"  # ... tile2 sweeps (jacobi 1.74 -> 1.86 ms: off)
 SLAB_PREFETCH = os.environ.get("B2_SLAB_PF", "1") == "1"  # ... in slab (runtime dim-0) sweeps
