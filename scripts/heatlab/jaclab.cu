@@ -91,6 +91,116 @@ __global__ void __launch_bounds__(NTH) pair2d(const double *__restrict__ A, doub
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+
+// two sweeps per launch in registers: warp w owns B columns 30 w .. 30 w + 31
+// (lanes) and A' columns 30 w + 1 .. 30 w + 30 (lanes 1..30); each thread
+// marches V output rows keeping A rows i-1, i, i+1 and B rows i-2, i-1, i
+// in registers, x neighbours by shuffle (edge lanes load theirs).  Same op
+// order as two sweeps, so bitwise.  SB: store B's owned points (needed only
+// after the last pass).
+template <int WARPS, int V, bool SB>
+__global__ void __launch_bounds__(32 * WARPS) jac2reg(const double *__restrict__ A,
+                                                     double *__restrict__ B,
+                                                     double *__restrict__ An) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int strips = (I + 29) / 30, chunks = (I + V - 1) / V;
+  for (int vb = blockIdx.x; vb < ((strips + WARPS - 1) / WARPS) * chunks; vb += gridDim.x) {
+    const int st = (vb % ((strips + WARPS - 1) / WARPS)) * WARPS + w;
+    const int ch = vb / ((strips + WARPS - 1) / WARPS);
+    if (st >= strips) continue;
+    const int cb = 30 * st + lane;          // this lane's B column (global)
+    const bool live = cb <= N - 1;
+    const bool bint = cb >= 1 && cb <= N - 2;  // B evaluated here (else boundary value)
+    const bool aout = lane >= 1 && lane <= 30 && cb >= 1 && cb <= N - 2;
+    const int i0 = 1 + ch * V;               // first A' row of this chunk
+    const int i1 = min(i0 + V, N - 1);       // one past the last
+    // A rows i0-2 .. i0 (to evaluate B row i0-1 we need A rows i0-2, i0-1, i0)
+    auto ld = [&](int r, int c) -> double { return (live && r >= 0 && r <= N - 1 && c >= 0 && c <= N - 1) ? A[(long)r * N + c] : 0.0; };
+    double am = ld(i0 - 2, cb), ac = ld(i0 - 1, cb), ap;
+    double bm2 = 0.0, bm1 = 0.0;  // B rows (i - 2), (i - 1) at cb
+    for (int i = i0 - 1; i <= i1; ++i) {  // B row i
+      ap = ld(i + 1, cb);
+      // x neighbours of A row i
+      double aw = __shfl_up_sync(0xffffffffu, ac, 1), ae = __shfl_down_sync(0xffffffffu, ac, 1);
+      if (lane == 0) aw = ld(i, cb - 1);
+      if (lane == 31) ae = ld(i, cb + 1);
+      double b;
+      if (i >= 1 && i <= N - 2 && bint) {
+        b = 0.2 * ((((ac + aw) + ae) + ap) + am);
+        if (SB && i >= i0 && i < i1 && aout) B[(long)i * N + cb] = b;
+      } else {
+        b = live && i >= 0 && i <= N - 1 ? B[(long)i * N + cb] : 0.0;
+      }
+      // A' row i - 1 from B rows i - 2, i - 1, i
+      if (i - 1 >= i0) {
+        double bw = __shfl_up_sync(0xffffffffu, bm1, 1), be = __shfl_down_sync(0xffffffffu, bm1, 1);
+        if (aout) An[(long)(i - 1) * N + cb] = 0.2 * ((((bm1 + bw) + be) + b) + bm2);
+      }
+      bm2 = bm1;
+      bm1 = b;
+      am = ac;
+      ac = ap;
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+
+// jac2reg with every A row of the chunk loaded up front (registers, fully
+// unrolled) so the loads overlap; full chunks only take this path
+template <int WARPS, int V, bool SB>
+__global__ void __launch_bounds__(32 * WARPS) jac2u(const double *__restrict__ A,
+                                                   double *__restrict__ B,
+                                                   double *__restrict__ An) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int strips = (I + 29) / 30, chunks = (I + V - 1) / V, sw = (strips + WARPS - 1) / WARPS;
+  for (int vb = blockIdx.x; vb < sw * chunks; vb += gridDim.x) {
+    const int st = (vb % sw) * WARPS + w, ch = vb / sw;
+    if (st >= strips) continue;
+    const int cb = 30 * st + lane;
+    const bool live = cb <= N - 1;
+    const bool bint = cb >= 1 && cb <= N - 2;
+    const bool aout = lane >= 1 && lane <= 30 && bint;
+    const int i0 = 1 + ch * V, i1 = min(i0 + V, N - 1);
+    auto ld = [&](int r, int c) -> double {
+      return (live && r >= 0 && r <= N - 1 && c >= 0 && c <= N - 1) ? A[(long)r * N + c] : 0.0;
+    };
+    double a[V + 3], ax[V + 1];  // A rows i0-2 .. i0+V at cb; edge lanes' outer neighbour
+#pragma unroll
+    for (int k = 0; k < V + 3; ++k) a[k] = ld(i0 - 2 + k, cb);
+#pragma unroll
+    for (int k = 0; k < V + 1; ++k)  // rows i0-1 .. i0+V-1 (B rows): lane 0 west, lane 31 east
+      ax[k] = lane == 0 ? ld(i0 - 1 + k, cb - 1) : (lane == 31 ? ld(i0 - 1 + k, cb + 1) : 0.0);
+    double bm2 = 0.0, bm1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < V + 2; ++k) {  // B row i = i0 - 1 + k
+      const int i = i0 - 1 + k;
+      double b = 0.0;
+      if (k <= V) {
+        const double ac = a[k + 1];
+        double aw = __shfl_up_sync(0xffffffffu, ac, 1), ae = __shfl_down_sync(0xffffffffu, ac, 1);
+        if (lane == 0) aw = ax[k];
+        if (lane == 31) ae = ax[k];
+        if (i >= 1 && i <= N - 2 && i <= i1 && bint) {
+          b = 0.2 * ((((ac + aw) + ae) + a[k + 2]) + a[k]);
+          if (SB && i >= i0 && i < i1 && aout) B[(long)i * N + cb] = b;
+        } else if (live && i >= 0 && i <= N - 1) {
+          b = B[(long)i * N + cb];
+        }
+      }
+      if (k >= 2 && i - 1 < i1) {  // A' row i - 1 from B rows i - 2 .. i
+        double bw = __shfl_up_sync(0xffffffffu, bm1, 1), be = __shfl_down_sync(0xffffffffu, bm1, 1);
+        if (aout) An[(long)(i - 1) * N + cb] = 0.2 * ((((bm1 + bw) + be) + b) + bm2);
+      }
+      bm2 = bm1;
+      bm1 = b;
+    }
+  }
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __global__ void init(double *a, double *b) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)N * N; i += (long)gridDim.x * blockDim.x) {
     unsigned long long h = (unsigned long long)i * 0x9E3779B97F4A7C15ull;
@@ -139,7 +249,9 @@ int main(int argc, char **argv) {
     for (int t = 0; t < 4; ++t) { launch(gv0, RA, RB, s); launch(gv0, RB, RA, s); }
     struct PV { const char *name; void (*f)(const double *, double *, double *); void (*fsb)(const double *, double *, double *); int nth; int grid; };
 #define PVM(TX, TY, NT) PV{"pair2d_" #TX "x" #TY "_t" #NT, pair2d<TX, TY, NT, false>, pair2d<TX, TY, NT, true>, NT, ((I + TX - 1) / TX) * ((I + TY - 1) / TY)}
-    PV pvs[] = {PVM(64, 32, 256), PVM(64, 16, 256), PVM(32, 32, 256), PVM(128, 16, 256), PVM(64, 32, 512), PVM(128, 16, 512), PVM(32, 16, 128)};
+#define JRM(WW, VV) PV{"jac2reg_w" #WW "_v" #VV, jac2reg<WW, VV, false>, jac2reg<WW, VV, true>, 32 * WW, (((I + 29) / 30 + WW - 1) / WW) * ((I + VV - 1) / VV)}
+#define JUM(WW, VV) PV{"jac2u_w" #WW "_v" #VV, jac2u<WW, VV, false>, jac2u<WW, VV, true>, 32 * WW, (((I + 29) / 30 + WW - 1) / WW) * ((I + VV - 1) / VV)}
+    PV pvs[] = {JRM(8, 8), JUM(4, 8), JUM(8, 8), JUM(4, 16), JUM(8, 16), JUM(2, 16), JUM(4, 12), JUM(8, 4)};
     auto pl = [&](void (*f)(const double *, double *, double *), int nth, int grid, const double *a, double *b, double *an) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid); cfg.blockDim = dim3(nth); cfg.stream = s;
