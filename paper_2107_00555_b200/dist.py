@@ -758,6 +758,25 @@ class SlabGpuRunner:
     def run(self):
         self.ex.run_device(first_call=True)
 
+    def close(self):
+        """Release the peer mappings, the side stream and its events, the
+        executor's HBM and the NCCL communicator."""
+        from . import runtime as rt
+
+        L = rt.lib()
+        if self.peer is not None:
+            self.peer.close()
+            self.peer = None
+        if getattr(self, "side", None):
+            L.b2_event_destroy(self.ev_fork)
+            L.b2_event_destroy(self.ev_join)
+            L.b2_stream_destroy(self.side)
+            self.side = None
+        self.ex.close()
+        if self.nccl is not None:
+            self.nccl.close()
+            self.nccl = None
+
     def gather(self, full_inputs: dict) -> dict | None:
         """Owned rows of every non-transient distributed container to rank 0."""
         import torch.distributed as tdist
@@ -1308,5 +1327,6 @@ def bench_slab(args, W):
         }
         print(json.dumps(line), flush=True)
     tdist.barrier()
+    runner.close()
     tdist.destroy_process_group()
     _ = rt

@@ -75,6 +75,7 @@ def test_slab_runner_single_rank_matches_oracle(pg):
     r.load_inputs({"A": A, "B": B})
     r.run()
     out = r.gather({"A": A, "B": B})
+    r.close()
     K.heat_3d_c(A, B, 6)
     assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
 
@@ -97,6 +98,7 @@ def test_slab_runner_split_launch_bitwise(pg, N):
     r.run()
     assert r.splits > 0
     out = r.gather({"A": A, "B": B})
+    r.close()
     K.heat_3d_c(A, B, 5)
     assert np.array_equal(out["A"], A) and np.array_equal(out["B"], B)
 
