@@ -1,1 +1,2 @@
-PAIR=1 ./scripts/heatlab/jaclab 400
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
