@@ -66,17 +66,44 @@ class _Hub:
             return dict(self.slots[key])
 
 
-def _blocks(gshape, gdims, coords):
+def _owned(extent, griddim, coord, block):
+    """Indices of one dim owned by ``coord``: blocks of ``block`` dealt
+    round-robin (block = extent / griddim is the plain block layout)."""
+    idx = []
+    for start in range(coord * block, extent, griddim * block):
+        idx.extend(range(start, min(start + block, extent)))
+    return idx
+
+
+def _blocks(gshape, gdims, coords, scheme="block", blocks=None):
+    """np.ix_ index of the rank's part (block needs
+    divisible extents, block-cyclic does not)."""
+    gdims = list(gdims)
+    while len(gdims) > len(gshape) and gdims[-1] == 1:
+        gdims.pop()
     out = []
     for d, n in enumerate(gshape):
         if d < len(gdims):
-            if n % gdims[d]:
-                raise SimError(f"extent {n} not covered by grid dim {gdims[d]} (divisible)")
-            b = n // gdims[d]
-            out.append(slice(coords[d] * b, coords[d] * b + b))
+            if scheme == "block":
+                if n % gdims[d]:
+                    raise SimError(f"extent {n} not covered by grid dim {gdims[d]} (divisible)")
+                b = n // gdims[d]
+            else:
+                b = int(blocks[d]) if blocks else -(-n // gdims[d])
+            out.append(_owned(n, gdims[d], coords[d], b))
         else:
-            out.append(slice(0, n))
-    return tuple(out)
+            out.append(list(range(n)))
+    return np.ix_(*out)
+
+
+def _dist_of(n, env, gdims):
+    a = n.attrs.get("dist") or {}
+    dims = tuple(a.get("grid") or gdims)
+    scheme = a.get("scheme", "block")
+    blocks = None
+    if scheme == "block_cyclic" and a.get("block"):
+        blocks = [symexpr.evaluate(symexpr.parse(str(b)), env) for b in a["block"]]
+    return dims, scheme, blocks
 
 
 class RankMachine(I.Machine):
@@ -168,8 +195,8 @@ class RankMachine(I.Machine):
                 c = flat.size // self.P
                 v = flat[self.rank * c:(self.rank + 1) * c]
             else:
-                dims = tuple(n.attrs.get("dist", {}).get("grid") or self.gdims)
-                v = G[_blocks(G.shape, dims, self._coords(dims, self.rank))]
+                dims, scheme, blocks = _dist_of(n, env, self.gdims)
+                v = G[_blocks(G.shape, dims, self._coords(dims, self.rank), scheme, blocks)]
             ranges = symexpr.eval_subset(o_e.memlet.subset, env)
             self.write(o_e.memlet, np.asarray(v).reshape(tuple(len(r) for r in ranges)), env,
                        st.label, n.id)
@@ -186,9 +213,9 @@ class RankMachine(I.Machine):
                 if k == "gather":
                     G = np.concatenate([parts[r].reshape(-1) for r in range(self.P)]).reshape(gshape)
                 else:
-                    dims = tuple(n.attrs.get("dist", {}).get("grid") or self.gdims)
+                    dims, scheme, blocks = _dist_of(n, env, self.gdims)
                     for r in range(self.P):
-                        sl = _blocks(gshape, dims, self._coords(dims, r))
+                        sl = _blocks(gshape, dims, self._coords(dims, r), scheme, blocks)
                         G[sl] = parts[r].reshape(G[sl].shape)
                 self.write(o_e.memlet, G, env, st.label, n.id)
             if self.P > 1:

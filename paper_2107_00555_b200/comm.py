@@ -32,6 +32,7 @@ transfer is issued.
 from __future__ import annotations
 
 import ctypes
+import itertools
 import math
 from dataclasses import dataclass, field
 
@@ -50,6 +51,14 @@ class SimError(RuntimeError):
 
 class CollectiveOrderError(RuntimeError):
     pass
+
+
+def _row_major(shape) -> list:
+    st, acc = [1] * len(shape), 1
+    for d in range(len(shape) - 1, -1, -1):
+        st[d] = acc
+        acc *= shape[d]
+    return st
 
 
 def block_layout(shape, grid_dims, coords):
@@ -380,6 +389,11 @@ class RankComm:
         return self.grid.coords(r)
 
     def _block_plan(self, ex, op, sym, scatter):
+        """Global / local memlets, per-rank runs of the node's distribution
+        (block or block-cyclic, dist/layout.py), per-rank local shapes and
+        bytes."""
+        from .dist import layout as LY
+
         n = op.node
         ins = {e.dst_conn: e for e in op.state.in_edges(n) if e.memlet is not None}
         outs = {e.src_conn: e for e in op.state.out_edges(n) if e.memlet is not None}
@@ -387,72 +401,90 @@ class RankComm:
         lm = (outs["out"] if scatter else ins["a"]).memlet  # local side
         gshape = [len(r) for r in symexpr.eval_subset(gm.subset, sym)]
         lshape = [len(r) for r in symexpr.eval_subset(lm.subset, sym)]
-        # the node's own distribution (distribute.py writes {"dist": {"grid"}}:
-        # a 1-D map over a 2-D machine uses a 1-D grid of all ranks)
-        ndims = (n.attrs.get("dist") or {}).get("grid")
+        # the node's own distribution (distribution.py writes {"dist": {"grid",
+        # "block", "scheme"}}: a 1-D map over a 2-D machine uses a 1-D grid)
+        attr = n.attrs.get("dist") or {}
+        ndims = attr.get("grid")
         dims = tuple(int(x) for x in ndims) if ndims else self._grid_dims()
         if int(np.prod(dims)) != self.world:
             raise SimError(f"grid {dims} does not have {self.world} ranks")
+        scheme = attr.get("scheme", LY.SCHEME_BLOCK)
+        bsz = None
+        if scheme == LY.SCHEME_BLOCK_CYCLIC and attr.get("block"):
+            bsz = [symexpr.evaluate(symexpr.parse(str(b)), sym)
+                   for b in attr["block"]]
 
         def coords(q):
             return (q // dims[1], q % dims[1]) if len(dims) == 2 else (q,)
 
-        blocks = [block_layout(gshape, dims, coords(q)) for q in range(self.world)]
-        if [e for _, e in blocks[self.rank]] != lshape:
+        try:
+            runs = [LY.block_runs(gshape, dims, coords(q), scheme, bsz) for q in range(self.world)]
+        except LY.LayoutError as exn:
+            raise SimError(str(exn)) from exn
+        lshapes = [LY.local_shape(r) for r in runs]
+        if lshapes[self.rank] != lshape:
             raise SimError(f"local view {lshape} does not match the block "
-                           f"{[e for _, e in blocks[self.rank]]} of {gshape}")
+                           f"{lshapes[self.rank]} of {gshape}")
         esz = sdfg.DTYPE_BYTES[ex.g.containers[gm.container].dtype]
-        return gm, lm, blocks, int(np.prod(lshape)) * esz
+        nbytes = [int(np.prod(ls)) * esz for ls in lshapes]
+        return gm, lm, runs, lshapes, nbytes
 
     def _block(self, ex, op, sym, counters, scatter):
-        gm, lm, blocks, nbytes = self._block_plan(ex, op, sym, scatter)
+        gm, lm, runs, lshapes, nbytes = self._block_plan(ex, op, sym, scatter)
         L = rt.lib()
         gb, goff, gdt, gdims = ex.view(gm, sym)
         lb, loff, ldt, ldims = ex.view(lm, sym)
         lview = rt.make_view(lb, loff, ldt, [d[0] for d in ldims], [d[1] for d in ldims])
-        n_el = nbytes // sdfg.DTYPE_BYTES[gdt]
+        stg = [self._buffer((op.idx, "blk", q), nbytes[q]) for q in range(self.world)]
 
-        def gblock(q):  # view of rank q's block inside the root's global view
-            off = goff + sum(st * gd[1] for (st, _), gd in zip(blocks[q], gdims))
-            return rt.make_view(gb, off, gdt, [e for _, e in blocks[q]], [d[1] for d in gdims])
+        def staged(q):  # rank q's local array, row-major, in its staging buffer
+            return rt.make_view(stg[q], 0, gdt, lshapes[q], _row_major(lshapes[q]))
 
-        stg = [self._buffer((op.idx, "blk", q), nbytes) for q in range(self.world)]
-
-        def flat(q):
-            return rt.make_view(stg[q], 0, gdt, [n_el], [1])
+        def pieces(q):
+            """(global sub-box view, staging sub-box view) per product of runs."""
+            lst = _row_major(lshapes[q])
+            for combo in itertools.product(*runs[q]):
+                shape = [n for _, n, _ in combo]
+                if not all(shape):
+                    continue
+                goff_q = goff + sum(g0 * gd[1] for (g0, _, _), gd in zip(combo, gdims))
+                loff_q = sum(l0 * st for (_, _, l0), st in zip(combo, lst))
+                yield (rt.make_view(gb, goff_q, gdt, shape, [d[1] for d in gdims]),
+                       rt.make_view(stg[q], loff_q, gdt, shape, lst))
 
         ops = []
         if scatter:
             if self.rank == 0:
                 for q in range(self.world):
-                    v, f = gblock(q), flat(q)
-                    rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(v), 0, ex.stream), "scatter")
-                    ex.launches += 1
+                    for v, f in pieces(q):
+                        rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(v), 0, ex.stream),
+                                 "scatter")
+                        ex.launches += 1
                     if q:
-                        ops.append((True, q, stg[q], nbytes))
+                        ops.append((True, q, stg[q], nbytes[q]))
             else:
-                ops.append((False, 0, stg[self.rank], nbytes))
+                ops.append((False, 0, stg[self.rank], nbytes[self.rank]))
             if ops:
                 self.nccl.p2p(ops, ex.stream)
-            f = flat(self.rank)
+            f = staged(self.rank)
             rt.check(L.b2_copy_view(ctypes.byref(lview), ctypes.byref(f), 0, ex.stream), "scatter")
             ex.launches += 1
         else:
-            f = flat(self.rank)
+            f = staged(self.rank)
             rt.check(L.b2_copy_view(ctypes.byref(f), ctypes.byref(lview), 0, ex.stream), "gather")
             ex.launches += 1
             if self.rank == 0:
-                ops = [(False, q, stg[q], nbytes) for q in range(1, self.world)]
+                ops = [(False, q, stg[q], nbytes[q]) for q in range(1, self.world)]
             else:
-                ops = [(True, 0, stg[self.rank], nbytes)]
+                ops = [(True, 0, stg[self.rank], nbytes[self.rank])]
             if ops:
                 self.nccl.p2p(ops, ex.stream)
             if self.rank == 0:
                 for q in range(self.world):
-                    v, fq = gblock(q), flat(q)
-                    rt.check(L.b2_copy_view(ctypes.byref(v), ctypes.byref(fq), 0, ex.stream),
-                             "gather")
-                    ex.launches += 1
+                    for v, fq in pieces(q):
+                        rt.check(L.b2_copy_view(ctypes.byref(v), ctypes.byref(fq), 0, ex.stream),
+                                 "gather")
+                        ex.launches += 1
         if counters is not None:
             counters.collective_calls += 1
             counters.comm_bytes += sum(x[3] for x in ops)
@@ -496,11 +528,10 @@ class RankComm:
             self.records.append([x[:4] for x in self._cur])
             self._cur = []
         elif kind in ("block_scatter", "block_gather"):
-            gm, lm, blocks, nbytes = self._block_plan(ex, op, sym, kind == "block_scatter")
+            gm, lm, runs, lshapes, nbytes = self._block_plan(ex, op, sym, kind == "block_scatter")
             for q in range(self.world):
-                self._buffer((op.idx, "blk", q), nbytes)
-            self.colls.append((kind, op.state.label, op.node.id,
-                               tuple(e for _, e in blocks[0]), nbytes))
+                self._buffer((op.idx, "blk", q), nbytes[q])
+            self.colls.append((kind, op.state.label, op.node.id, tuple(lshapes[0]), nbytes[0]))
         elif kind in ("scatter", "gather"):
             gm, lm, gb, goff, gdt, c = self._flat_plan(ex, op, sym, kind == "scatter")
             for q in range(self.world):

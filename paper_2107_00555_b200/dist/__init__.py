@@ -35,7 +35,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import plan as P, sdfg, symexpr
+from .. import plan as P, sdfg, symexpr
 
 
 class DistError(ValueError):
@@ -86,17 +86,9 @@ class ProcessGrid:
         return "x".join(map(str, self.dims))
 
 
-def block_indices(extent: int, griddim: int, coord: int, block: int | None = None) -> range:
-    """Indices of ``extent`` owned by ``coord`` of ``griddim``: contiguous
-    near-equal blocks (block=None) or block-cyclic with block size ``block``."""
-    if block is None:
-        lo = extent * coord // griddim
-        hi = extent * (coord + 1) // griddim
-        return range(lo, hi)
-    idx = []
-    for start in range(coord * block, extent, griddim * block):
-        idx.extend(range(start, min(start + block, extent)))
-    return idx  # type: ignore[return-value]
+from .layout import (  # noqa: E402,F401  (reference API: sdfgkit.dist.layout)
+    SCHEME_BLOCK, SCHEME_BLOCK_CYCLIC, block_indices,
+)
 
 
 # ---------------------------------------------------------------------------
@@ -459,7 +451,7 @@ class NcclComm:
 
         import torch.distributed as tdist
 
-        from . import runtime as rt
+        from .. import runtime as rt
 
         self.rt = rt
         self.rank, self.world = rank, world
@@ -534,7 +526,7 @@ class PeerHalo:
 
         import torch.distributed as tdist
 
-        from . import runtime as rt
+        from .. import runtime as rt
 
         self.rt, self.ct = rt, ctypes
         self.plan, self.rank = plan, rank
@@ -603,8 +595,8 @@ class SlabGpuRunner:
 
         import torch
 
-        from . import runtime as rt
-        from .machine import GpuExecutor, InterpOptions
+        from .. import runtime as rt
+        from ..machine import GpuExecutor, InterpOptions
 
         self.torch = torch
         self.g = sdfg.as_graph(g)
@@ -647,7 +639,7 @@ class SlabGpuRunner:
         """Boundary iterations and the halo exchange of their rows on the side
         stream, the interior on the executor stream, joined before the next
         op: the exchange hides behind the interior sweep."""
-        from . import runtime as rt
+        from .. import runtime as rt
 
         if ex.specs[op.idx].private:
             return False  # per-thread scratch cannot be shared by concurrent launches
@@ -761,7 +753,7 @@ class SlabGpuRunner:
     def close(self):
         """Release the peer mappings, the side stream and its events, the
         executor's HBM and the NCCL communicator."""
-        from . import runtime as rt
+        from .. import runtime as rt
 
         L = rt.lib()
         if self.peer is not None:
@@ -946,7 +938,7 @@ class SummaDevice:
                  stream=None):
         import ctypes
 
-        from . import runtime as rt
+        from .. import runtime as rt
 
         if dtype not in ("f64", "f32"):
             raise DistError(f"SUMMA dtype {dtype!r}")
@@ -1070,7 +1062,7 @@ class SummaDevice:
 
 def measured_extra() -> dict:
     """Compute / L2 ceilings measured on the box (scripts/peaks/)."""
-    p = pathlib.Path(__file__).resolve().parent.parent / "profiles" / "measured_peaks_extra.json"
+    p = pathlib.Path(__file__).resolve().parents[2] / "profiles" / "measured_peaks_extra.json"
     return json.loads(p.read_text()) if p.exists() else {}
 
 
@@ -1084,7 +1076,7 @@ def bench_summa(args, n: int = 16384, dtype: str = "f64"):
     import torch
     import torch.distributed as tdist
 
-    from . import runtime as rt
+    from .. import runtime as rt
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -1206,7 +1198,7 @@ def bench_slab(args, W):
     import torch
     import torch.distributed as tdist
 
-    from . import runtime as rt
+    from .. import runtime as rt
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -1216,7 +1208,7 @@ def bench_slab(args, W):
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import pathlib
 
-    root = pathlib.Path(__file__).resolve().parent.parent
+    root = pathlib.Path(__file__).resolve().parents[2]
     syms = W["syms"]
     g = sdfg.load(root / "tests" / "golden" / "graphs" / f"{W['graph']}.json")
     from bench import make_inputs, peaks  # noqa: E402

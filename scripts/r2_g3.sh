@@ -1,2 +1,1 @@
-timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -3
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 900 python -m pytest tests/test_gpu_simrun.py -m gpu -q -x 2>&1 | tail -15

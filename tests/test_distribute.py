@@ -184,3 +184,75 @@ def test_single_rank_moves_no_bytes():
     ins = _inputs(sdfg.from_dict(_doc("gemm")), syms)
     _, cnt = dist_ref.sim_run(doc, (1, 1), syms, ins)
     assert cnt[0]["comm_bytes"] == 0 and cnt[0]["messages_posted"] == 0
+
+
+def _cyclic_doc(extent, dims, bs):
+    """A -> BLOCK_SCATTER -> L (lr x lc, distributed local) -> BLOCK_GATHER -> B
+    with a block-cyclic distribution (pkg/tests/test_dist.py:328-376)."""
+    attr = {"dist": {"grid": list(dims), "block": [str(bs), str(bs)], "scheme": "block_cyclic"}}
+    full = f"[0:{extent - 1}:1, 0:{extent - 1}:1]"
+    lfull = "[0:(lr - 1):1, 0:(lc - 1):1]"
+    c = lambda n, shape, tr, st: {"name": n, "dtype": "f64", "shape": shape, "kind": "array",  # noqa: E731
+                                  "transient": tr, "lifetime": "scope", "storage": st}
+    return {"version": 1, "name": "cyc",
+            "symbols": [{"name": "lr", "min": 0}, {"name": "lc", "min": 0}],
+            "containers": [c("A", [str(extent)] * 2, False, "heap"),
+                           c("B", [str(extent)] * 2, False, "heap"),
+                           c("L", ["lr", "lc"], True, "distributed_local")],
+            "states": [{"label": "s0", "nodes": [
+                {"id": 0, "type": "access", "container": "A"},
+                {"id": 1, "type": "library", "kind": "block_scatter", "name": "scatter", "attrs": attr},
+                {"id": 2, "type": "access", "container": "L"},
+                {"id": 3, "type": "library", "kind": "block_gather", "name": "gather", "attrs": attr},
+                {"id": 4, "type": "access", "container": "B"}],
+                "edges": [{"src": 0, "dst": 1, "dst_conn": "a", "memlet": "A" + full},
+                          {"src": 1, "dst": 2, "src_conn": "out", "memlet": "L" + lfull},
+                          {"src": 2, "dst": 3, "dst_conn": "a", "memlet": "L" + lfull},
+                          {"src": 3, "dst": 4, "src_conn": "out", "memlet": "B" + full}]}],
+            "transitions": [], "start": "s0"}
+
+
+def _cyclic_bindings(extent, dims, bs):
+    from paper_2107_00555_b200.dist import ProcessGrid, block_indices
+
+    grid = ProcessGrid(dims)
+    out = []
+    for r in range(grid.size):
+        co = grid.coords(r)
+        i, j = co[0], (co[1] if len(co) == 2 else 0)
+        out.append({"lr": len(block_indices(extent, dims[0], i, bs)),
+                    "lc": len(block_indices(extent, dims[1], j, bs))})
+    return out
+
+
+@pytest.mark.parametrize("gdims", [(1, 1), (2, 1), (2, 2)])
+@pytest.mark.parametrize("scheme_block", [1, 2, None])
+def test_block_indices_cover_every_cell_once(gdims, scheme_block):
+    """pkg/tests/test_dist.py:66-85: ownership covers every cell exactly once."""
+    from paper_2107_00555_b200.dist import ProcessGrid, block_indices
+
+    grid, extent = ProcessGrid(gdims), 4
+    blocks = [scheme_block or -(-extent // d) for d in gdims]
+    owned = np.zeros((extent, extent), dtype=int)
+    for r in range(grid.size):
+        i, j = grid.coords(r)
+        for x in block_indices(extent, gdims[0], i, blocks[0]):
+            for y in block_indices(extent, gdims[1], j, blocks[1]):
+                owned[x, y] += 1
+    assert np.all(owned == 1)
+
+
+@pytest.mark.parametrize("gdims", [(1, 1), (2, 1), (1, 2), (2, 2)])
+@pytest.mark.parametrize("bs", [1, 2, 3, 4])
+def test_block_cyclic_roundtrip_oracle(gdims, bs):
+    """pkg/tests/test_dist.py:328-376: block_gather(block_scatter(A)) == A for
+    block-cyclic layouts (block sizes 1, 2, 3 — uneven — and the extent) in
+    the CPU rank-simulator oracle."""
+    from oracle import dist_ref
+
+    extent = 4
+    A = np.random.default_rng(bs).uniform(-1, 1, (extent, extent))
+    out, _ = dist_ref.sim_run(_cyclic_doc(extent, gdims, bs), gdims, {},
+                              {"A": A, "B": np.zeros_like(A)},
+                              rank_bindings=_cyclic_bindings(extent, gdims, bs))
+    assert np.array_equal(out["B"], A)

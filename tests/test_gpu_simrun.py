@@ -193,3 +193,21 @@ def test_local_view_jacobi2d_equals_global(P):
                 assert np.array_equal(got[1:-1, :], ref[k][lo + 1:hi - 1, :]), (r, k)
     finally:
         sim.close()
+
+
+@pytest.mark.parametrize("gdims", [(1, 1), (2, 1), (1, 2), (2, 2)])
+@pytest.mark.parametrize("bs", [1, 2, 3, 4])
+def test_block_cyclic_roundtrip_on_device(gdims, bs):
+    """pkg/tests/test_dist.py:328-376 on the B200 rank simulator:
+    block_gather(block_scatter(A)) == A for block-cyclic layouts (uneven
+    block size 3 included); each block of a rank moves by its own copy."""
+    from test_distribute import _cyclic_bindings, _cyclic_doc
+
+    from paper_2107_00555_b200 import simrun
+
+    extent = 4
+    A = np.random.default_rng(bs).uniform(-1, 1, (extent, extent))
+    out, _ = simrun.sim_run(_cyclic_doc(extent, gdims, bs), gdims,
+                            _ctx({}, {"A": A, "B": np.zeros_like(A)}),
+                            _cyclic_bindings(extent, gdims, bs))
+    assert np.array_equal(out["B"], A)
