@@ -150,6 +150,9 @@ class RankMachine(I.Machine):
             peer = int(symexpr.evaluate(n.attrs["peer"], env))
             tag = int(symexpr.evaluate(n.attrs["tag"], env))
             m = (ins if k == "isend" else outs)["buf"].memlet
+            if peer == -1:  # MPI_PROC_NULL: posted, nothing moves
+                C.messages_posted += k == "isend"
+                return
             if k == "isend":
                 data = np.array(self.read(m, env, st.label, n.id))
                 self.pending.append(("s", peer, tag, data))
@@ -252,8 +255,11 @@ class RankMachine(I.Machine):
         raise SimError(f"collective '{k}' not supported")
 
 
-def sim_run(g, grid_dims, bindings, store, rank_bindings=None):
-    """(rank 0's outputs, per-rank counters) of ``g`` on P logical ranks."""
+def sim_run(g, grid_dims, bindings, store, rank_bindings=None, rank_stores=None,
+            all_outputs=False):
+    """(rank 0's outputs, per-rank counters) of ``g`` on P logical ranks
+    (``rank_stores``: per-rank inputs of local-view programs; ``all_outputs``:
+    every rank's outputs as a list)."""
     from paper_2107_00555_b200 import distribution as DI
 
     doc = g if isinstance(g, dict) else None
@@ -266,8 +272,8 @@ def sim_run(g, grid_dims, bindings, store, rank_bindings=None):
         b = DI.local_bindings(doc, grid_dims, dict(bindings), r)
         if rank_bindings is not None:
             b.update(rank_bindings[r])
-        st = dict(store)
-        if r:  # root-resident containers: placeholders this rank never reads
+        st = dict(rank_stores[r]) if rank_stores is not None else dict(store)
+        if r and rank_stores is None:  # root-resident containers: placeholders
             for name, c in g.containers.items():
                 if not c.transient and name not in st:
                     st[name] = np.zeros(tuple(symexpr.evaluate(d, b) for d in c.shape))
@@ -293,4 +299,5 @@ def sim_run(g, grid_dims, bindings, store, rank_bindings=None):
     e = next((x for x in errs if x is not None), None)
     if e is not None:
         raise e
-    return ms[0].outputs(), {r: dict(ms[r].counters.__dict__) for r in range(P)}
+    outs = [m.outputs() for m in ms] if all_outputs else ms[0].outputs()
+    return outs, {r: dict(ms[r].counters.__dict__) for r in range(P)}

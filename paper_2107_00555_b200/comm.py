@@ -41,6 +41,11 @@ import numpy as np
 from . import runtime as rt, sdfg, symexpr
 
 
+# peer of a send / receive that has no partner (a rank on the grid boundary):
+# the post completes at waitall without moving data, like MPI_PROC_NULL
+PROC_NULL = -1
+
+
 class DeadlockError(RuntimeError):
     pass
 
@@ -512,6 +517,8 @@ class RankComm:
         kind = op.node.kind
         if kind in ("isend", "irecv"):
             peer, tag, ins, outs = self._args(ex, op, sym)
+            if peer == PROC_NULL:
+                return
             m = (ins if kind == "isend" else outs)["buf"].memlet
             nbytes = _nbytes(ex, m, sym)
             if kind == "irecv":  # race diagnostic, before any transfer
@@ -558,6 +565,10 @@ class RankComm:
 
     def _post(self, ex, op, sym, counters, send):
         peer, tag, ins, outs = self._args(ex, op, sym)
+        if peer == PROC_NULL:  # MPI_PROC_NULL: posted, nothing moves
+            if send and counters is not None:
+                counters.messages_posted += 1
+            return
         m = (ins if send else outs)["buf"].memlet
         base, off, dt, dims = ex.view(m, sym)
         esz = sdfg.DTYPE_BYTES[dt]

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_simrun.py -m gpu -q -x 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_simrun.py tests/test_gpu_dist.py -m gpu -q -x 2>&1 | tail -15

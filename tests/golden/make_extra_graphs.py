@@ -28,13 +28,18 @@ sys.path.insert(0, str(REF / "src"))
 from sdfgkit import frontend  # noqa: E402
 from sdfgkit.serialize import to_dict  # noqa: E402
 
-for name in ("halo_pair", "jacobi2d_local", "overlap_recv", "block_roundtrip"):
+for name in ("halo_pair", "jacobi2d_local", "overlap_recv", "block_roundtrip",
+             "jacobi2d_local_view"):
     g, diags = frontend.compile_source((REPO / "programs" / f"{name}.dpy").read_text())
     errs = [d for d in diags if d.severity == "error"]
     assert not errs, errs
     out = HERE / "graphs" / f"{name}.raw.json"
     out.write_text(json.dumps(to_dict(g), indent=1) + "\n")
     print("wrote", out)
+    if name == "jacobi2d_local_view":  # dist.benchmark's program graph (package data)
+        pkg = REPO / "paper_2107_00555_b200" / "dist" / "jacobi2d_local_view.json"
+        pkg.write_text(json.dumps(to_dict(g), indent=1) + "\n")
+        print("wrote", pkg)
 
 # Interpreter-contract programs (the cases of pkg/tests/test_interp.py:52-121,
 # written here; compiled by the reference frontend, tile_wcr by its autoopt)

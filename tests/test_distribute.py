@@ -256,3 +256,51 @@ def test_block_cyclic_roundtrip_oracle(gdims, bs):
                               {"A": A, "B": np.zeros_like(A)},
                               rank_bindings=_cyclic_bindings(extent, gdims, bs))
     assert np.array_equal(out["B"], A)
+
+
+def test_benchmark_program_text_is_the_compiled_one():
+    from conftest import GOLDEN as _G  # noqa: F401
+    import pathlib
+
+    from paper_2107_00555_b200.dist import benchmark as BM
+
+    root = pathlib.Path(__file__).resolve().parent.parent
+    assert BM.JACOBI2D_LOCAL_VIEW == (root / "programs" / "jacobi2d_local_view.dpy").read_text()
+    pkg = json.loads((root / "paper_2107_00555_b200" / "dist" / "jacobi2d_local_view.json").read_text())
+    gold = json.loads((GOLDEN / "graphs" / "jacobi2d_local_view.raw.json").read_text())
+    assert pkg == gold
+
+
+@pytest.mark.parametrize("gdims", [(1, 1), (2, 1), (1, 2), (2, 2)])
+def test_local_view_benchmark_oracle(gdims):
+    """pkg/tests/test_dist.py:288-306 on the CPU rank-simulator oracle: the
+    local-view jacobi_2d (dist.benchmark) equals the shared-memory program
+    bitwise, and a 2x2 grid posts exactly 8 sends per rank per step (four
+    directions, PROC_NULL on the global boundary)."""
+    from oracle import dist_ref, interp_ref
+    from paper_2107_00555_b200.dist import benchmark as BM
+
+    n, tsteps = 8, 4
+    rng = np.random.default_rng(5)
+    A, B = rng.uniform(-1, 1, (n, n)), rng.uniform(-1, 1, (n, n))
+    ref = interp_ref.interpret(sdfg_load("jacobi_2d"), {"N": n, "TSTEPS": tsteps},
+                               {"A": A.copy(), "B": B.copy()})
+    wins = BM.windows(n, gdims)
+    stores = [{"A": A[w].copy(), "B": B[w].copy()} for w in wins]
+    outs, cnt = dist_ref.sim_run(BM.build_graph(), gdims, {"TSTEPS": tsteps}, {},
+                                 rank_bindings=BM.rank_bindings(n, gdims, tsteps),
+                                 rank_stores=stores, all_outputs=True)
+    gotA, gotB = A.copy(), B.copy()
+    for r, (rs, cs) in enumerate(wins):
+        inner = (slice(rs.start + 1, rs.stop - 1), slice(cs.start + 1, cs.stop - 1))
+        gotA[inner] = outs[r]["A"][1:-1, 1:-1]
+        gotB[inner] = outs[r]["B"][1:-1, 1:-1]
+    assert np.array_equal(gotA, ref["A"]) and np.array_equal(gotB, ref["B"])
+    for c in cnt.values():
+        assert c["messages_posted"] == 8 * (tsteps - 1)
+
+
+def sdfg_load(name):
+    from paper_2107_00555_b200 import sdfg
+
+    return sdfg.load(GOLDEN / "graphs" / f"{name}.raw.json")

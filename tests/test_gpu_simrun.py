@@ -211,3 +211,23 @@ def test_block_cyclic_roundtrip_on_device(gdims, bs):
                             _ctx({}, {"A": A, "B": np.zeros_like(A)}),
                             _cyclic_bindings(extent, gdims, bs))
     assert np.array_equal(out["B"], A)
+
+
+@pytest.mark.parametrize("gdims", [(1, 1), (2, 1), (1, 2), (2, 2)])
+def test_local_view_benchmark_on_device(gdims):
+    """pkg/tests/test_dist.py:288-306 / test_acceptance.py:285-317 through
+    dist.benchmark.run on the B200: equal to the shared-memory jacobi_2d
+    (bitwise: same op order), 8 posted sends per rank per step on 2x2."""
+    from oracle import interp_ref
+    from paper_2107_00555_b200 import sdfg
+    from paper_2107_00555_b200.dist import ProcessGrid, benchmark as BM
+
+    n, tsteps = 8, 4
+    rng = np.random.default_rng(13)
+    A, B = rng.uniform(-1, 1, (n, n)), rng.uniform(-1, 1, (n, n))
+    ref = interp_ref.interpret(sdfg.load(GOLDEN / "graphs" / "jacobi_2d.raw.json"),
+                               {"N": n, "TSTEPS": tsteps}, {"A": A.copy(), "B": B.copy()})
+    out, instr = BM.run(n, tsteps, ProcessGrid(gdims), A.copy(), B.copy())
+    assert np.array_equal(out["A"], ref["A"]) and np.array_equal(out["B"], ref["B"])
+    for c in instr["per_rank"].values():
+        assert c["messages_posted"] == 8 * (tsteps - 1)
