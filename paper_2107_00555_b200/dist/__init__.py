@@ -87,8 +87,26 @@ class ProcessGrid:
 
 
 from .layout import (  # noqa: E402,F401  (reference API: sdfgkit.dist.layout)
-    SCHEME_BLOCK, SCHEME_BLOCK_CYCLIC, block_indices,
+    SCHEME_BLOCK, SCHEME_BLOCK_CYCLIC, Distribution, block_indices,
 )
+
+_PASSES = ("distribute", "distribute_elementwise", "distribution_pipeline",
+           "expand_matmul_distributed", "remove_redundant_comm")
+_SIM = ("sim_run", "RankSim", "DeadlockError", "SimError", "CollectiveOrderError")
+
+
+def __getattr__(name):
+    """The rest of the reference's ``sdfgkit.dist`` surface (passes, the rank
+    simulator and its errors), resolved lazily: those modules import this one."""
+    if name in _PASSES:
+        from .. import distribution as _D
+
+        return getattr(_D, name)
+    if name in _SIM:
+        from .. import simrun as _S
+
+        return getattr(_S, name)
+    raise AttributeError(name)
 
 
 # ---------------------------------------------------------------------------

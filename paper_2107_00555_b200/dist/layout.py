@@ -74,3 +74,26 @@ def block_runs(shape, grid_dims, coords, scheme: str = SCHEME_BLOCK, blocks=None
 
 def local_shape(runs) -> list:
     return [sum(n for _, n, _ in r) for r in runs]
+
+
+class Distribution:
+    """A container's distribution: grid, per-dimension
+    block sizes (None = ceil(extent / grid dim)) and scheme.  ``attr()`` is
+    the {"dist": ...} attribute of the BlockScatter / BlockGather nodes."""
+
+    def __init__(self, grid, blocks=None, scheme: str = SCHEME_BLOCK):
+        dims = getattr(grid, "dims", grid)
+        self.grid = tuple(int(d) for d in dims)
+        self.blocks = None if blocks is None else [str(b) for b in blocks]
+        if scheme not in (SCHEME_BLOCK, SCHEME_BLOCK_CYCLIC):
+            raise LayoutError(f"unknown distribution scheme {scheme!r}")
+        self.scheme = scheme
+
+    def attr(self) -> dict:
+        return {"grid": list(self.grid), "block": self.blocks, "scheme": self.scheme}
+
+    def __eq__(self, other):
+        return isinstance(other, Distribution) and self.attr() == other.attr()
+
+    def __repr__(self):
+        return f"Distribution({self.grid}, {self.blocks}, {self.scheme!r})"

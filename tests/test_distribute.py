@@ -304,3 +304,20 @@ def sdfg_load(name):
     from paper_2107_00555_b200 import sdfg
 
     return sdfg.load(GOLDEN / "graphs" / f"{name}.raw.json")
+
+
+def test_reference_dist_import_surface():
+    """Every name pkg/tests/test_dist.py:5-10 imports from sdfgkit.dist,
+    .dist.benchmark and .dist.layout exists under paper_2107_00555_b200.dist."""
+    from paper_2107_00555_b200.dist import (  # noqa: F401
+        DeadlockError, Distribution, ProcessGrid, RankSim, distribute,
+        distribution_pipeline, remove_redundant_comm, sim_run,
+    )
+    from paper_2107_00555_b200.dist.benchmark import (  # noqa: F401
+        JACOBI2D_LOCAL_VIEW, build_graph, rank_bindings, run,
+    )
+    from paper_2107_00555_b200.dist.layout import (  # noqa: F401
+        SCHEME_BLOCK, SCHEME_BLOCK_CYCLIC, block_indices,
+    )
+    d = Distribution(ProcessGrid((2, 2)), [2, 2], SCHEME_BLOCK_CYCLIC)
+    assert d.attr() == {"grid": [2, 2], "block": ["2", "2"], "scheme": "block_cyclic"}
