@@ -36,6 +36,9 @@ REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WC
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
 ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reductions
+# the next map of a row reduction fused as its epilogue (softmax: ex / sm)
+ROWRED_EPILOGUE = os.environ.get("B2_ROWRED_EPILOGUE", "1") == "1"
+ROWRED_EPI_MINB = int(os.environ.get("B2_ROWRED_EPI_MINB", "3"))  # softmax 1.231 ms (2: 1.391, 4: 1.314, 8: spills)
 FOLD_MODE = os.environ.get("B2_FOLD", "1") == "1"  # warp-cooperative max/min loop folds
 SMALL_PRIVATE = 16  # elements: thread-private transients up to this size stay in registers
 FOLD_UNROLL = int(os.environ.get("B2_FOLD_UNROLL", "4"))
@@ -112,6 +115,7 @@ class KernelSpec:
         self.tmaps: list[tuple] = []  # (container, box (inner..outer)) TMA maps ahead of the args
         self.smem = 0  # dynamic shared memory bytes
         self.grid_cap = 0  # tma3: persistent grid size
+        self.epilogue = None  # index of the map group run as this kernel's epilogue
 
     def arg_index(self, desc) -> int:
         try:
@@ -148,6 +152,10 @@ class _Gen:
         self.ptr_override: dict[str, str] = {}  # container -> C pointer name
         self.init_const: dict[str, str] = {}  # reduction target -> fused init constant
         self.read_set: set = set()
+        self.redirect: dict[str, str] = {}  # container -> C expression (register copies)
+        self.epi_group = None  # a map fused as the epilogue of a row reduction
+        self.epi = None
+        self.rowred_pointw: dict = {}
 
     def _wkey(self, m: sdfg.Memlet, env: dict):
         rename = {mp: v[2:] for mp, v in env.items() if isinstance(v, str) and v.startswith("p_")}
@@ -840,7 +848,72 @@ class _Gen:
         for c, pt in pointw.items():  # a written container is only re-read at its own point
             if reads.get(c, {pt}) != {pt}:
                 return None
+        self.rowred_pointw = dict(pointw)
         return [last], list(grp.params[:-1]), targets
+
+    def _epilogue_plan(self, B):
+        """Map group ``B`` (the next op) runs as the epilogue of this row
+        reduction when it iterates the same space, reads this group's
+        point-written transients T only at their point and the reduction
+        targets R only at the row's point, writes full points of containers
+        this group does not touch, and no other op reads T: each warp keeps
+        its row of T in registers (T never reaches HBM) and evaluates B from
+        them and the reduced R (softmax: ex / sm).  Same tasklets, same
+        values: bitwise equal to the two launches."""
+        A = self.group
+        if (not isinstance(B, P.MapGroup) or B.schedule != "parallel"
+                or len(B.params) != len(A.params) or B.idx in self.pl.in_region):
+            return None
+        rb = [_const_range(self.pl, r) for r in B.ranges]
+        if rb != self.const_ranges:
+            return None
+        TV = -(-self.const_ranges[-1][2] // 32)
+        if TV > 32:
+            return None
+        ren = dict(zip(B.params, A.params))
+
+        def rn(pt):
+            return tuple((c0, tuple((ren.get(p, p), k) for p, k in co)) for c0, co in pt)
+
+        Ts = {c: pt for c, pt in self.rowred_pointw.items() if self.g.containers[c].transient
+              and self.g.containers[c].lifetime != "persistent"}
+        if not Ts or set(Ts) != set(self.rowred_pointw):
+            return None
+        R = {c: pt for (c, pt) in self.red_targets}
+        # every reduction target must be exclusive to its row (one warp
+        # commits it), so the warp holds the final value
+        if any(deps != set(self.red_pout) for (_, deps) in self.red_targets.values()):
+            return None
+        written_A = set(Ts) | set(R)
+        touched_A = set()
+        for mem in A.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, A.params):
+                touched_A.add(c)
+        for mem in B.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, B.params):
+                if depth != 0 or pt is None:
+                    return None
+                if not w:
+                    if c in Ts:
+                        if rn(pt) != Ts[c]:
+                            return None
+                    elif c in R:
+                        if rn(pt) != R[c]:
+                            return None
+                    elif c in written_A:
+                        return None
+                    continue
+                if wcr is not None or c in touched_A:
+                    return None
+                deps = {p for key in pt for (p, _) in key[1]}
+                if deps != set(B.params):
+                    return None
+        for op in self.pl.all_ops:
+            if op.idx in (A.idx, B.idx):
+                continue
+            if set(self.pl.op_reads.get(op.idx, set())) & set(Ts):
+                return None
+        return {"B": B, "T": sorted(Ts), "TV": TV}
 
     def _rowred_loop(self, pout, reg_decls, body) -> list:
         grp = self.group
@@ -863,7 +936,15 @@ class _Gen:
             ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
             L.append(f"    {t['ct']} {t['acc']} = ({t['ct']})({ident});")
         pL = grp.params[-1]
-        if self.hoisted:
+        if self.epi is not None:
+            TV = self.epi["TV"]
+            for T in self.epi["T"]:
+                L.append(f"    {CT[self.g.containers[T].dtype]} tb_{T}[{TV}];")
+            L.append("#pragma unroll")
+            L.append(f"    for (int v = 0; v < {TV}; ++v) {{")
+            L.append(f"    const int j{iL} = lane + 32 * v;")
+            L.append(f"    if (j{iL} >= (int)rl{iL}) break;")
+        elif self.hoisted:
             T = self.const_ranges[-1][2] // 32
             for name, ct, expr in self.hoisted:
                 L.append(f"    {ct} {name}[{T}];")
@@ -889,13 +970,33 @@ class _Gen:
             a = t["acc"]
             L.append(f"    for (int o = 16; o > 0; o >>= 1) {a} = b2_op_{t['wcr']}({a}, "
                      f"__shfl_xor_sync(0xffffffffu, {a}, o));")
-        L.append("    if (lane == 0) {")
-        for t in self.red.values():
-            if t["exclusive"]:
-                L.append(f"      {t['target']} = b2_op_{t['wcr']}({self._old(t)}, {t['acc']});")
-            else:
-                L.append(f"      b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
-        L.append("    }")
+        if self.epi is not None:
+            # the xor tree left every lane with the reduced value: every lane
+            # forms the committed value (old (+) acc, exclusive targets only),
+            # lane 0 stores it, the epilogue reads it from the register
+            for t in self.red.values():
+                L.append(f"    {t['acc']} = b2_op_{t['wcr']}({self._old(t)}, {t['acc']});")
+            L.append("    if (lane == 0) {")
+            for t in self.red.values():
+                L.append(f"      {t['target']} = {t['acc']};")
+            L.append("    }")
+        else:
+            L.append("    if (lane == 0) {")
+            for t in self.red.values():
+                if t["exclusive"]:
+                    L.append(f"      {t['target']} = b2_op_{t['wcr']}({self._old(t)}, {t['acc']});")
+                else:
+                    L.append(f"      b2_atomic_{t['wcr']}(&{t['target']}, {t['acc']});")
+            L.append("    }")
+        if self.epi is not None:
+            L.append("#pragma unroll")
+            L.append(f"    for (int v = 0; v < {self.epi['TV']}; ++v) {{")
+            L.append(f"    const int j{iL} = lane + 32 * v;")
+            L.append(f"    if (j{iL} >= (int)rl{iL}) break;")
+            L.append(f"    const b2_ll p_{pL} = rb{iL} + rs{iL} * j{iL};")
+            L += reg_decls(4)
+            L += [ln[2:] if ln.startswith("  ") else ln for ln in self.epi_body]
+            L.append("    }")
         L.append("  }")
         return L
 
@@ -1176,6 +1277,8 @@ class _Gen:
     # -- reads / writes ---------------------------------------------------------
 
     def read(self, m: sdfg.Memlet, env: dict, depth: int) -> tuple[str, str]:
+        if m.container in self.redirect:
+            return self.redirect[m.container], TC[self.g.containers[m.container].dtype]
         c = self.cont(m.container)
         t = TC[c.dtype]
         pl = self.place(m.container)
@@ -1230,6 +1333,10 @@ class _Gen:
         return self.group.idx * 4096 + len(self.spec.sites) - 1
 
     def write(self, m: sdfg.Memlet, code: str, vt: str, env: dict, depth: int):
+        if m.container in self.redirect and m.wcr is None:
+            want = TC[self.g.containers[m.container].dtype]
+            self.emit(f"{self.redirect[m.container]} = {scalar.cast(code, vt, want)};")
+            return
         c = self.cont(m.container)
         ct = CT[c.dtype]
         want = TC[c.dtype]
@@ -1492,6 +1599,8 @@ class _Gen:
                 self.red_pout = pout
                 self.red_full = False
                 self.red_R = R
+                if self.epi_group is not None and ROWRED_EPILOGUE:
+                    self.epi = self._epilogue_plan(self.epi_group)
         if (mode == "tile2" and k == 2 and MARCH2
                 and not getattr(self.pl, "dynamic_p0", False)
                 and self.const_ranges[0][2] >= 4 * MARCH2_V
@@ -1563,6 +1672,8 @@ class _Gen:
         self.hoisted = []
 
         env = {p: f"p_{p}" for p in grp.params}
+        if self.epi is not None:
+            self.redirect = {T: f"tb_{T}[v]" for T in self.epi["T"]}
         body_lines_start = len(self.lines)
         self.ind = 6
         for mem in grp.members:
@@ -1573,10 +1684,36 @@ class _Gen:
                 self.scope(mem.state, mem.entry, menv, 0)
         body = self.lines[body_lines_start:]
         self.lines = self.lines[:body_lines_start]
+        self.epi_body = []
+        if self.epi is not None:
+            # the epilogue map: reads of T from the row registers, of the
+            # reduction targets from the (warp-reduced) accumulators
+            B = self.epi["B"]
+            for t in self.red.values():
+                self.redirect[t["cont"]] = t["acc"]
+            for mem in B.members:
+                for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, B.params):
+                    (self.written if w else self.read_set).add(c)
+            benv = {bp: f"p_{ap}" for bp, ap in zip(B.params, grp.params)}
+            start = len(self.lines)
+            self.ind = 6
+            for mem in B.members:
+                menv = {mp: benv[gp] for mp, gp in mem.rename.items()}
+                if mem.tasklet is not None:
+                    self.tasklet(mem.state, mem.tasklet, menv, 0)
+                else:
+                    self.scope(mem.state, mem.entry, menv, 0)
+            self.epi_body = self.lines[start:]
+            self.lines = self.lines[:start]
+            self.redirect = {}
+            spec.epilogue = B.idx
 
         pro: list[str] = []
         nthr = spec.block[0] * spec.block[1] * spec.block[2]
         minb = f", {ROWRED_MINB}" if mode == "rowred" and ROWRED_MINB else ""
+        if mode == "rowred" and self.epi is not None:
+            # the row lives in registers (tb_*): fewer resident CTAs, no spills
+            minb = f", {ROWRED_EPI_MINB}"
         pro.append(f'extern "C" __global__ void __launch_bounds__({max(256, nthr)}{minb}) '
                    f"{spec.name}(const __grid_constant__ B2Args a) {{")
         pro.append("  B2_PDL_ENTRY();")
@@ -2237,9 +2374,10 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
 
 
 def generate(planner: P.Planner, group: P.MapGroup, shapes: dict, name: str,
-             init_const: dict | None = None) -> KernelSpec:
+             init_const: dict | None = None, epilogue=None) -> KernelSpec:
     gen = _Gen(planner, group, shapes, name)
     gen.init_const = dict(init_const or {})
+    gen.epi_group = epilogue
     spec = gen.build()
     spec.params = list(group.params)
     # reduction targets (container, point key) -> (exclusive, C type), for

@@ -219,14 +219,26 @@ class GpuExecutor:
             self.specs[reg.idx] = spec
             reg.spec = spec
         self.init_skip: set[int] = set()
+        self.epi_skip: set[int] = set()  # maps run as the epilogue of the previous op
         fused_init = self._init_fusions() if INIT_FUSION else {}
+        nxt = {}
+        for ops in self.planner.ops.values():
+            for a, b in zip(ops, ops[1:]):
+                if isinstance(a, P.MapGroup) and isinstance(b, P.MapGroup):
+                    nxt[a.idx] = b
         for op in self.planner.all_ops:
             if op.idx in self.planner.in_region:
                 continue
             if isinstance(op, P.MapGroup):
                 name = f"b2_map_{self.g.name}_{op.idx}"
+                epi = nxt.get(op.idx)
+                if epi is not None and (epi.idx in self.init_skip or op.idx in self.epi_skip
+                                        or op.idx in self.init_skip):
+                    epi = None
                 spec = codegen.generate(self.planner, op, self.buf.shape, name,
-                                        init_const=fused_init.get(op.idx))
+                                        init_const=fused_init.get(op.idx), epilogue=epi)
+                if getattr(spec, "epilogue", None) is not None:
+                    self.epi_skip.add(spec.epilogue)
                 src = rt.family_source("prelude.cuh") + "\n" + spec.source
                 spec.kernel = rt.get_kernel(src, name, max_smem=spec.smem)
                 spec.fin_kernel = None
@@ -1041,8 +1053,9 @@ class GpuExecutor:
         return True
 
     def _exec_map(self, op: P.MapGroup, sym, counters):
-        if op.idx in self.init_skip:
-            # constant fill folded into the next reduction's initial value
+        if op.idx in self.init_skip or op.idx in self.epi_skip:
+            # constant fill folded into the next reduction's initial value, or
+            # a map the previous row reduction ran as its epilogue
             rvals = codegen.range_values(op, sym)
             ok = self._check_bounds(self.specs[op.idx], rvals, sym, op.state.label,
                                     f"map group {op.idx}")
