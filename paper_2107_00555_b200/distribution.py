@@ -35,6 +35,7 @@ hard error ("no implicit padding").
 from __future__ import annotations
 
 import copy
+import importlib
 import json
 import math
 
@@ -474,7 +475,28 @@ def _same_subset(a, b) -> bool:
         _norm(x) == _norm(y) for da, db in zip(a, b) for x, y in zip(da, db))
 
 
-def remove_redundant_comm(doc: dict) -> dict:
+def remove_redundant_comm(doc) -> dict:
+    """Remove gather -> T -> scatter pairs with provably equal distributions
+     from a schema-v1 document in place — or from a
+    reference ``Sdfg`` in place; returns the report (pass name -> count)."""
+    if _is_reference_sdfg(doc):
+        d = as_doc(doc)
+        d.setdefault("dist_symbols", dict(getattr(doc, "_b2_dist_symbols", {}) or {}))
+        rep = remove_redundant_comm(d)
+        _write_back(doc, d)
+        return _Report(rep)
+    return _Report(_remove_redundant_comm(doc))
+
+
+class _Report(dict):
+    """A report dict that also reads like the reference's PassReport."""
+
+    @property
+    def applications(self):
+        return self
+
+
+def _remove_redundant_comm(doc: dict) -> dict:
     D = _Doc(doc)
     changed = True
     while changed:
@@ -604,23 +626,70 @@ def as_doc(g) -> dict:
     return copy.deepcopy(sdfg.as_graph(g).doc)
 
 
-def distribute(g, grid, blocks=None) -> tuple[dict, dict]:
+class PassResult(tuple):
+    """(document, report) — also the reference's PassReport shape:
+    ``.applications`` is the report (pass name -> count), ``.doc`` the
+    rewritten schema-v1 document."""
+
+    def __new__(cls, doc, report):
+        r = super().__new__(cls, (doc, report))
+        r.doc, r.applications = doc, report
+        return r
+
+
+def _canonical_ids(doc: dict) -> dict:
+    """Node ids renumbered 0..n-1 per state (the reference serializer indexes
+    nodes by position, serialize.py:229)."""
+    doc = copy.deepcopy(doc)
+    for st in doc["states"]:
+        remap = {n["id"]: i for i, n in enumerate(st["nodes"])}
+        for n in st["nodes"]:
+            n["id"] = remap[n["id"]]
+            if n.get("type") == "map_exit":
+                n["entry"] = remap[n["entry"]]
+        for e in st["edges"]:
+            e["src"], e["dst"] = remap[e["src"]], remap[e["dst"]]
+    return doc
+
+
+def _is_reference_sdfg(g) -> bool:
+    return (not isinstance(g, (dict, str, sdfg.Graph)) and hasattr(g, "states")
+            and type(g).__module__.split(".")[0] == "sdfgkit")
+
+
+def _write_back(g, doc: dict) -> None:
+    """Rewrite a reference ``Sdfg`` in place (the reference passes mutate
+    their argument): the document goes through the reference's own
+    serializer; the local-extent symbols ride along on the object."""
+    ser = importlib.import_module(type(g).__module__.split(".")[0] + ".serialize")
+    new = ser.from_dict(_canonical_ids(doc))
+    g.__dict__.clear()
+    g.__dict__.update(new.__dict__)
+    g._b2_dist_symbols = dict(doc.get("dist_symbols") or {})
+
+
+def distribute(g, grid, blocks=None) -> PassResult:
     """distribute_elementwise + expand_matmul_distributed; returns (new
-    document, report)."""
+    document, report).  A reference ``Sdfg`` argument is also rewritten in
+    place, like the reference pass."""
     doc = as_doc(g)
     rep = {}
     for k, v in expand_matmul_distributed(doc, grid).items():
         rep[k] = rep.get(k, 0) + v
     for k, v in distribute_elementwise(doc, grid, blocks).items():
         rep[k] = rep.get(k, 0) + v
-    return doc, rep
+    if _is_reference_sdfg(g):
+        _write_back(g, doc)
+    return PassResult(doc, rep)
 
 
-def distribution_pipeline(g, grid) -> tuple[dict, dict]:
-    doc, rep = distribute(g, grid)
+def distribution_pipeline(g, grid) -> PassResult:
+    doc, rep = distribute(as_doc(g), grid)
     for k, v in remove_redundant_comm(doc).items():
         rep[k] = rep.get(k, 0) + v
-    return doc, rep
+    if _is_reference_sdfg(g):
+        _write_back(g, doc)
+    return PassResult(doc, rep)
 
 
 def local_bindings(doc: dict, grid, bindings: dict, rank: int) -> dict:

@@ -485,5 +485,11 @@ def as_graph(g) -> Graph:
     if hasattr(g, "states") and hasattr(g, "containers") and hasattr(g, "transitions"):
         root = type(g).__module__.rsplit(".", 1)[0]
         ser = importlib.import_module(root + ".serialize")
-        return from_dict(ser.to_dict(g))
+        doc = ser.to_dict(g)
+        # local-extent symbols of a graph the distribution passes rewrote in
+        # place (distribution.py keeps them beside the reference object)
+        extra = getattr(g, "_b2_dist_symbols", None)
+        if extra:
+            doc["dist_symbols"] = dict(extra)
+        return from_dict(doc)
     raise TypeError(f"cannot interpret {type(g).__name__} as a program graph")

@@ -321,3 +321,40 @@ def test_reference_dist_import_surface():
     )
     d = Distribution(ProcessGrid((2, 2)), [2, 2], SCHEME_BLOCK_CYCLIC)
     assert d.attr() == {"grid": [2, 2], "block": ["2", "2"], "scheme": "block_cyclic"}
+
+
+def _ref_serializer():
+    import importlib
+    import pathlib
+    import sys
+
+    root = pathlib.Path(__file__).resolve().parent.parent
+    for p in (root / "baseline" / "_ref", pathlib.Path("/root/reference/pkg/src")):
+        if (p / "sdfgkit").exists() and str(p) not in sys.path:
+            sys.path.insert(0, str(p))
+    try:
+        return importlib.import_module("sdfgkit.serialize")
+    except ImportError:
+        pytest.skip("reference package not installed (baseline/_ref)")
+
+
+@pytest.mark.parametrize("gdims", [(2, 1), (2, 2)])
+def test_passes_rewrite_a_reference_sdfg_in_place(gdims):
+    """The reference's calling convention (test_dist.py:36-52, 216-262): the
+    passes mutate the reference Sdfg they are given and return a report with
+    .applications; the rewritten object validates in the reference and runs
+    distributed (rank-simulator oracle) to the shared-memory result."""
+    from oracle import dist_ref
+    from paper_2107_00555_b200 import distribution as D, sdfg
+
+    ser = _ref_serializer()
+    doc = _doc("gemm")
+    g = ser.from_dict(doc)
+    rep = D.distribution_pipeline(g, gdims)
+    assert rep.applications.get("expand_matmul_distributed", 0) == 1
+    assert not [d for d in g.validate() if d.severity == "error"]
+    syms = DIST_SYMBOLS["gemm"]
+    ins = _inputs(sdfg.from_dict(doc), syms)
+    out, _ = dist_ref.sim_run(g, gdims, syms, {k: np.array(v) for k, v in ins.items()})
+    ref = _shared("gemm", syms, ins)
+    assert max(rel_err(out[k], ref[k]) for k in ref) <= 1e-12
