@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_simrun.py -m gpu -q -x 2>&1 | tail -3
+for m in 2 4; do B2_ROWRED_EPI_MINB=$m timeout 300 python scripts/bench_suite.py --only softmax --reps 10 --out gpurun_out/sm.json 2>&1 | grep softmax | sed "s/^/prologue minb=$m /"; done
