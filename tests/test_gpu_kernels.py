@@ -147,7 +147,8 @@ def test_tc_sgemm_3xtf32_vs_numpy(M, K, N, acc):
 @pytest.mark.parametrize("N,H,SM", [(2, 3, 1), (2, 3, 33), (1, 2, 64), (3, 1, 100)])
 def test_softmax_fold_and_rowred_vs_numpy_port(N, H, SM):
     """softmax raw graph: the max loop runs as a warp fold (incl. zero-trip and
-    ragged-lane cases), the exp/sum map in row-reduction mode."""
+    ragged-lane cases), the exp/sum map in row-reduction mode with the divide
+    fused as its epilogue (ragged rows of 33 / 100: partial register rows)."""
     from oracle import kernels_np as K
 
     rng = np.random.default_rng(SM)
@@ -156,6 +157,22 @@ def test_softmax_fold_and_rowred_vs_numpy_port(N, H, SM):
     ref = np.empty_like(x)
     K.softmax(x.copy(), ref)
     assert rel_err(out["out"], ref) <= 1e-12
+
+
+def test_softmax_divide_runs_as_row_epilogue():
+    """The row-reduction epilogue fusion is what runs: the divide map is not
+    launched on its own and ex never gets a kernel store."""
+    from paper_2107_00555_b200 import sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    g = sdfg.load(GOLDEN / "graphs" / "softmax.raw.json")
+    ex = GpuExecutor(g, {"N": 2, "H": 3, "SM": 64})
+    try:
+        assert len(ex.epi_skip) == 1
+        fused = [sp for sp in ex.specs.values() if getattr(sp, "epilogue", None) is not None]
+        assert len(fused) == 1 and "c_ex[" not in fused[0].source
+    finally:
+        ex.close()
 
 
 def test_run_twice_bitwise_deterministic():
