@@ -17,6 +17,7 @@
 #define B2_NO_PDL
 #include "../../paper_2107_00555_b200/csrc/families/prelude.cuh"
 #include "gen_heat.cuh"
+#include "gen_heat_core.cuh"
 
 #define CK(x)                                                                  \
   do {                                                                         \
@@ -752,6 +753,7 @@ struct Var {
   int grid;
   KFn2 fn2 = nullptr;
   bool gen = false;
+  bool core = false;
 };
 static int *g_flag = nullptr;
 
@@ -804,7 +806,10 @@ static void launch(const Var &v, const double *a, double *b, cudaStream_t s, int
     ar.w[0] = (long long)a;
     ar.w[1] = (long long)b;
     ar.w[2] = (long long)g_flag;
-    CK(cudaLaunchKernelEx(&cfg, gen_heat, ar));
+    if (v.core)
+      CK(cudaLaunchKernelEx(&cfg, gen_heat_core, ar));
+    else
+      CK(cudaLaunchKernelEx(&cfg, gen_heat, ar));
   } else if (v.fn2)
     CK(cudaLaunchKernelEx(&cfg, v.fn2, a, b, odd));
   else
@@ -957,17 +962,14 @@ int main(int argc, char **argv) {
 
   Var gv{"generated", nullptr, dim3(64, 8), 8750};
   gv.gen = true;
+  Var gc{"generated_core_prefetch", nullptr, dim3(64, 8), 8750};
+  gc.gen = true;
+  gc.core = true;
   Var vars[] = {
       gv,
-      mk_zm<64, 8, 2, 0>("zm_64x8_s2"),
-      mk_zm<64, 8, 2, 4>("zm_64x8_s2_pf4"),
-      mk_zm<64, 8, 2, 8>("zm_64x8_s2_pf8"),
-      mk_zm<64, 8, 4, 4>("zm_64x8_s4_pf4"),
-      mk_zm<64, 4, 2, 4>("zm_64x4_s2_pf4"),
-      mk_zm<32, 8, 2, 4>("zm_32x8_s2_pf4"),
-      mk_zm<64, 8, 8, 4>("zm_64x8_s8_pf4"),
-      mk_zm<64, 8, 4, 8>("zm_64x8_s4_pf8"),
+      gc,
       gv,
+      gc,
   };
   const int nv = sizeof(vars) / sizeof(vars[0]);
   Sampler smp;

@@ -1,1 +1,2 @@
-timeout 600 python bench.py --steps 5 --warmup 3 2>&1 | grep "^{" | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d[\"value\"], d[\"roofline\"][\"step_share\"], d[\"roofline\"][\"sweep_share\"], d[\"roofline\"][\"sweep_kernels\"])"
+./scripts/heatlab/heatlab 40 2>&1 | grep generated
+./scripts/heatlab/heatlab 2500 2>&1 | grep generated
