@@ -184,6 +184,9 @@ class _Gen:
         mem = grp.members[0]
         kids = ([mem.tasklet] if mem.tasklet is not None else
                 list(P._scope_children(mem.state, mem.entry)))
+        nested = [k for k in kids if not isinstance(k, sdfg.MapExit)]
+        if len(nested) == 1 and isinstance(nested[0], sdfg.MapEntry):
+            return self._blocked_contraction_plan(mem, nested[0])
         if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet):
             return None
         t = kids[0]
@@ -257,6 +260,137 @@ class _Gen:
         return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
                 "M": M, "N": npar, "K": K, "ext": ext,
                 "rng": {q: self.const_ranges[params.index(q)] for q in params}}
+
+    def _blocked_contraction_plan(self, mem, inner):
+        """The reference's blocked MATMUL expansion (autoopt.py:707-813,
+        ``blocked_native``): a PARALLEL map over output tiles (ib, jb) around
+        one SEQUENTIAL map (i, j, k) whose i / j ranges are the tile's rows /
+        columns and k the whole reduction, one tasklet ``a * b`` with a WCR
+        add into O[i, j].  Per (i, j) that is the k-ascending sum of the
+        flat product, so it runs as the same DMMA implicit GEMM over the
+        flattened space (re-associated like every tensor-core product:
+        within the rel_err 1e-12 contract).  The tiles must partition the
+        output exactly (checked on the bound extents)."""
+        st = mem.state
+        grp = self.group
+        kids = [k for k in P._scope_children(st, inner) if not isinstance(k, sdfg.MapExit)]
+        if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet) or inner.schedule == "parallel":
+            return None
+        t = kids[0]
+        if len(t.code) != 1 or len(t.ins) != 2:
+            return None
+        code = t.code[0][1]
+        if code[0] != "bin" or code[1] != "*" or {code[2], code[3]} != \
+                {("ref", t.ins[0]), ("ref", t.ins[1])}:
+            return None
+        ins = {e.dst_conn: e.memlet for e in st.in_edges(t) if e.memlet is not None}
+        outs = [e.memlet for e in st.out_edges(t) if e.memlet is not None]
+        if len(outs) != 1 or outs[0].wcr != "add" or set(ins) != set(t.ins):
+            return None
+        env = dict(self.pl.fixed)
+        outer = [mp for mp, gp in mem.rename.items()]  # member's own outer parameter names
+        oranges = {mp: self.const_ranges[grp.params.index(gp)] for mp, gp in mem.rename.items()}
+        iparams = inner.param_names
+        # flattened extents: the union over the outer tiles of each inner range
+        flat = {}
+        for q, (b, e, s_) in inner.params:
+            if symexpr.free_symbols(s_) - set(env) or symexpr.evaluate(s_, env) != 1:
+                return None
+            deps = (symexpr.free_symbols(b) | symexpr.free_symbols(e)) & set(outer)
+            if len(deps) > 1:
+                return None
+            covered = []
+            vals = [None]
+            if deps:
+                d = next(iter(deps))
+                r0, r1, rn = oranges[d]
+                vals = [(d, r0 + r1 * x) for x in range(rn)]
+            for v in vals:
+                ev = dict(env)
+                if v is not None:
+                    ev[v[0]] = v[1]
+                try:
+                    lo, hi = symexpr.evaluate(b, ev), symexpr.evaluate(e, ev)
+                except KeyError:
+                    return None
+                if hi >= lo:
+                    covered.append((lo, hi))
+            covered.sort()
+            pos = 0
+            for lo, hi in covered:
+                if lo != pos:
+                    return None  # gaps or overlaps: not a partition
+                pos = hi + 1
+            if not covered or covered[0][0] != 0:
+                return None
+            flat[q] = (0, 1, pos)
+        # the tiles must vary independently (every (ib, jb) pair present)
+        if len({d for q, (b, e, s_) in inner.params
+                for d in (symexpr.free_symbols(b) | symexpr.free_symbols(e)) & set(outer)}) \
+                != len(outer):
+            return None
+
+        def pt_of(m):
+            out = []
+            for (b, e, s_) in m.subset:
+                if b != e:
+                    return None
+                a = symexpr.affine(b, tuple(iparams), env)
+                if a is None:
+                    return None
+                out.append((a[0], tuple(sorted(a[1].items()))))
+            return tuple(out)
+
+        def coeffs(cont, pt):
+            if pt is None or self.place(cont) != "memory" or self.g.containers[cont].dtype != "f64":
+                return None
+            st_ = _row_major(self.shapes[cont])
+            if len(pt) != len(st_):
+                return None
+            cst, co = 0, {}
+            for d, (c0, terms) in enumerate(pt):
+                cst += st_[d] * c0
+                for q, cq in terms:
+                    co[q] = co.get(q, 0) + st_[d] * cq
+            return cst, co
+
+        oc = outs[0].container
+        xs = [ins[c].container for c in t.ins]
+        if len(set(xs)) != 2 or oc in xs:
+            return None
+        opt = pt_of(outs[0])
+        ca = [coeffs(c, pt_of(ins[conn])) for c, conn in zip(xs, t.ins)]
+        co_ = coeffs(oc, opt)
+        if None in ca or co_ is None or opt is None:
+            return None
+        pout = []
+        for c0, terms in opt:
+            if len(terms) != 1 or terms[0][1] != 1:
+                return None
+            pout.append(terms[0][0])
+        if len(set(pout)) != len(pout):
+            return None
+        used = [set(q for q, v in c[1].items() if v) for c in ca]
+        outs_ = [set(pout) & u for u in used]
+        if outs_[0] & outs_[1] or (outs_[0] | outs_[1]) != set(pout):
+            return None
+        yi = 1 if len(outs_[1]) == 1 else (0 if len(outs_[0]) == 1 else None)
+        if yi is None:
+            return None
+        xi = 1 - yi
+        npar = next(iter(outs_[yi]))
+        M = [q for q in iparams if q in pout and q != npar]
+        K = [q for q in iparams if q not in pout]
+        if not M or not K or any(q in used[yi] for q in M):
+            return None
+        ext = {q: flat[q][2] for q in iparams}
+        fma = 1
+        for q in iparams:
+            fma *= ext[q]
+        if fma < CONTRACT_MIN_FMA:
+            return None
+        return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
+                "M": M, "N": npar, "K": K, "ext": ext, "rng": flat}
 
     def _contract_kernel(self, cp):
         """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 MF m x TN
@@ -434,9 +568,13 @@ class _Gen:
         # host-side bounds checks of the three memlets (as the generic body's)
         mem = self.group.members[0]
         menv = {mp: f"p_{gp}" for mp, gp in mem.rename.items()}
-        t = next(iter(P._scope_children(mem.state, mem.entry))) if mem.tasklet is None \
-            else mem.tasklet
-        for e in mem.state.in_edges(t) + mem.state.out_edges(t):
+        t = next(k for k in P._scope_children(mem.state, mem.entry)
+                 if not isinstance(k, sdfg.MapExit)) if mem.tasklet is None else mem.tasklet
+        if isinstance(t, sdfg.MapEntry):  # blocked form: the inner map's outer memlets
+            edges = mem.state.in_edges(t) + mem.state.out_edges(mem.state.exit_of(t))
+        else:
+            edges = mem.state.in_edges(t) + mem.state.out_edges(t)
+        for e in edges:
             if e.memlet is not None:
                 spec.checks.append((e.memlet.container, e.memlet.subset, menv))
         spec.source = "\n".join(L) + "\n"
