@@ -21,6 +21,7 @@ Thread mappings (chosen at plan time):
 
 from __future__ import annotations
 
+import math
 import os
 import struct
 
@@ -36,6 +37,8 @@ REDUCE_MODE = os.environ.get("B2_REDUCE", "1") == "1"  # register-accumulated WC
 # branch-free unrolled copy of the per-thread point loop for full tiles
 MARCH_FULL = os.environ.get("B2_FULL_TILES", "1") == "1"
 ROWRED_MODE = os.environ.get("B2_ROWRED", "1") == "1"  # warp-per-row WCR reductions
+ROWRED_CONTIG = os.environ.get("B2_ROWRED_CONTIG", "1") == "1"  # pure reductions over the contiguous dim: rowred over reduce
+ROWRED_CONTIG_MINROWS = 148 * 16  # ... when there are rows (warps) enough to fill the GPU
 # the next map of a row reduction fused as its epilogue (softmax: ex / sm)
 ROWRED_EPILOGUE = os.environ.get("B2_ROWRED_EPILOGUE", "1") == "1"
 ROWRED_EPI_MINB = int(os.environ.get("B2_ROWRED_EPI_MINB", "3"))  # softmax 1.231 ms (2: 1.391, 4: 1.314, 8: spills)
@@ -989,6 +992,26 @@ class _Gen:
         self.rowred_pointw = dict(pointw)
         return [last], list(grp.params[:-1]), targets
 
+    def _last_param_contiguous(self) -> bool:
+        """Some HBM read walks the map's last parameter along its contiguous
+        dimension with unit stride, and no read has it in another dimension."""
+        grp = self.group
+        last = grp.params[-1]
+        found = False
+        for mem in grp.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if w or self.place(c) != "memory":
+                    continue
+                if pt is None:
+                    return False
+                for d, key in enumerate(pt):
+                    co = dict(key[1])
+                    if last in co:
+                        if d != len(pt) - 1 or co[last] != 1:
+                            return False
+                        found = True
+        return found
+
     def _epilogue_plan(self, B):
         """Map group ``B`` (the next op) runs as the epilogue of this row
         reduction when it iterates the same space, reads this group's
@@ -1713,6 +1736,14 @@ class _Gen:
                 return self._contract_kernel(cp)
         if mode in ("flat", "tile2", "march") and REDUCE_MODE:
             rp = self._reduction_plan()
+            if (rp is not None and ROWRED_MODE and ROWRED_CONTIG and rp[0] == [grp.params[-1]]
+                    and math.prod(self.const_ranges[i][2] for i in range(k - 1)) >= ROWRED_CONTIG_MINROWS
+                    and self._last_param_contiguous() and self._rowred_plan() is not None):
+                # reducing over the contiguous dimension (the expanded GEMV
+                # row dot A[i, :] . x) with rows enough for a warp each: a
+                # thread per output reads rows strided by the row length, a
+                # warp per row reads them coalesced
+                rp = None
             if rp is not None:
                 R, pout, targets = rp
                 mode = "reduce"
