@@ -175,6 +175,16 @@ def run_one(name, reps):
                                     "replayed as one graph (median of 3)"
                                     if not ex.device_branching else
                                     "eager per-launch CUDA events (median of 3)")
+        top_ms = top[1][1]
+        if kern_ms > ms:
+            # the pairs break programmatic-dependent-launch overlap and add a
+            # gap per launch, so short kernels read long (jacobi_2d: 13.6 us
+            # per sweep under pairs, 7.8 us in the plain graph): the kernel's
+            # time is its event-pair share of the plain graph's run time
+            top_ms = ms * top[1][1] / kern_ms
+            res["kernel_time_basis"] += ("; the kernels' sum exceeded the plain run, so the "
+                                         "top kernel's time is its share of the plain run")
+        res["top_kernel_ms_basis"] = top_ms
         if bound == "hbm":
             # the kernel's share of the run's algorithmic bytes: explicit per
             # kernel where kernels of one run move different bytes per point
@@ -188,7 +198,7 @@ def run_one(name, reps):
                 tot_pts = sum(n * pp for (n, _, pp) in prof.values()) or npts
                 kb = work * npts / tot_pts
                 res["bytes_model"] = "run bytes x the kernel's share of points"
-            ach = kb / (top[1][1] / 1e3) / 1e9
+            ach = kb / (top_ms / 1e3) / 1e9
             l2 = name == "jacobi_2d"  # 2 x 32 MB stay in the 126 MB L2 across sweeps
             pk = extra.get("l2_read_gbs", 16190.1) if l2 else hbm
             res["roofline"] = {"bound": "l2" if l2 else "hbm", "achieved": ach, "peak": pk,
@@ -197,7 +207,7 @@ def run_one(name, reps):
         elif unit == "flop":
             # (the run's flops are the dominant kernel's: matmul / conv2d)
             pk = extra.get("dmma_f64_tflops", 37.13)
-            ach = work / (top[1][1] / 1e3) / 1e12
+            ach = work / (top_ms / 1e3) / 1e12
             res["roofline"] = {"bound": "fp64_tensor", "achieved": ach, "peak": pk,
                                "unit": "TFLOP/s", "frac": ach / pk, "peak_kind": "measured",
                                "kernel": top[0]}

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -q -x -k "atax or bicg or mvt or gesummv or gemver or azimint" 2>&1 | tail -3
-timeout 600 python scripts/variant_survey.py atax,bicg,mvt,gesummv,gemver 2>&1 | grep "^{"
+timeout 300 python scripts/probe_dgemm.py
+timeout 1200 python -m pytest tests -m gpu -q -x -k "gemm or matmul or summa or k2mm or k3mm or dgemm or doitgen or config" 2>&1 | tail -3
