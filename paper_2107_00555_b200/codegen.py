@@ -82,6 +82,12 @@ CONTRACT_MIN_FMA = 1 << 22
 # MF = 1, 0.705 at 2 (each B fragment feeds two DMMAs); BK = 32 is slower
 CONTRACT_MF = int(os.environ.get("B2_CONTRACT_MF", "2"))
 CONTRACT_BK = int(os.environ.get("B2_CONTRACT_BK", "16"))  # k chunk staged per barrier
+# contractions whose X operand slides along the fastest output parameter
+# (convolutions: X[n, i + ki, j + kj, ci]): stage one contiguous window of X
+# per (tile, k chunk) instead of gathering every (row, k) element
+CONTRACT_SLIDE = os.environ.get("B2_CONTRACT_SLIDE", "1") == "1"
+CONTRACT_SLIDE_MAXWIN = 4096  # doubles per window buffer
+CONTRACT_SLIDE_BK = int(os.environ.get("B2_CONTRACT_SLIDE_BK", "0"))  # 0: largest k chunk <= 64 dividing the run
 # 3-D stencil sweeps through a TMA plane ring (cp.async.bulk.tensor.3d into
 # shared memory, mbarrier-tracked, persistent balanced grid): the tma3 mode
 # (measured: heat_3d N=400 39.3 ms vs 37.3 for march at the best geometry
@@ -395,17 +401,201 @@ class _Gen:
         return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
                 "M": M, "N": npar, "K": K, "ext": ext, "rng": flat}
 
-    def _contract_kernel(self, cp):
-        """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 MF m x TN
-        n, 8 warps of 16 MF m rows; K in BK-wide chunks staged in (dynamic) shared memory
-        through affine gathers (address = row part + k part, both
-        precomputed), double-buffered through registers.  The accumulators
-        start from O's current value (the WCR add) and store once.  FP64
-        tensor ops fuse multiply and add: within 1e-12 of the sequential
-        reference sum, not bitwise."""
+    def _slide_plan(self, cp):
+        """X's address is R(outer M) + S * j + kx(k) with j the fastest M
+        parameter, and the fastest K parameters form a contiguous run of KR
+        addresses (conv2d_bias: kx = 768 ki + 3 kj + ci, KR = 60).  With k
+        chunks inside one run, the A tile of TM consecutive j's is the
+        contiguous window X[R + S j0 + kx(k0) .. + S (TM - 1) + BK)."""
+        Mp, Kp, ext, rng = cp["M"], cp["K"], cp["ext"], cp["rng"]
+        cx = cp["cx"][1]
+        jm = Mp[-1]
+        S = cx.get(jm, 0) * rng[jm][1]
+        if S <= 0:
+            return None
+        run = 1
+        for q in reversed(Kp):
+            c = cx.get(q, 0) * rng[q][1]
+            if c != run:
+                break
+            run *= ext[q]
+        order = (CONTRACT_SLIDE_BK,) if CONTRACT_SLIDE_BK else (64, 60, 56, 48, 40, 32, 24, 20, 16, 12, 8)
+        BK = next((b for b in order if run % b == 0), None)
+        if BK is None:
+            return None
+        TM = 128 * CONTRACT_MF
+        WS = S * (TM - 1) + BK
+        if WS > CONTRACT_SLIDE_MAXWIN:
+            return None
+        return {"S": S, "BK": BK, "KR": run, "WS": WS + (WS & 1), "jm": jm}
+
+    def _contract_slide_kernel(self, cp, sl):
+        """The contraction kernel with a sliding X window (see _slide_plan):
+        M tiles are TM consecutive values of the fastest M parameter j within
+        one outer point (rows past the last j compute garbage that is never
+        stored), each k chunk stages X[R + S j0 + kx(k0) ...] (one coalesced
+        contiguous range, register double-buffered) and the A fragments read
+        it at S * row + k.  Same DMMA order as _contract_kernel: within 1e-12
+        of the sequential reference sum, not bitwise."""
         spec = self.spec
         X, Y, O = cp["X"], cp["Y"], cp["O"]
         Mp, Kp, Np = cp["M"], cp["K"], cp["N"]
+        ext, rng = cp["ext"], cp["rng"]
+        decode = self._contract_decode(cp)
+        Mtot = math.prod(ext[q] for q in Mp)
+        Ktot = math.prod(ext[q] for q in Kp)
+        Ntot = ext[Np]
+        EJ = ext[sl["jm"]]
+        TN = 8 * min(4, -(-Ntot // 8))
+        NF = TN // 8
+        MF, BK, S, WS = CONTRACT_MF, sl["BK"], sl["S"], sl["WS"]
+        TM = 128 * MF
+        ax, ay, ao = (self.arg(("ptr", X)), self.arg(("ptr", Y)), self.arg(("ptr", O)))
+        for c in (X, Y, O):
+            self.cont(c)
+        cyn = cp["cy"][1].get(Np, 0)
+        con = cp["co"][1].get(Np, 0)
+        L = [f"// generated by paper_2107_00555_b200.codegen: sliding-window contraction "
+             f"(DMMA implicit GEMM) M={Mtot} N={Ntot} K={Ktot} S={S} KR={sl['KR']}",
+             "struct B2Args { long long w[%d]; };" % max(1, len(spec.args)),
+             "namespace {",
+             f"constexpr int MF = {MF}, TM = {TM}, BK = {BK}, TN = {TN}, NF = {NF}, BPAD = 4;",
+             f"constexpr int S = {S}, WS = {WS}, WR = (WS + 255) / 256;",
+             f"constexpr long long MT = {Mtot}LL, NT = {Ntot}LL, KT = {Ktot}LL, EJ = {EJ}LL;",
+             "constexpr long long NJB = (EJ + TM - 1) / TM, MO = MT / EJ;",
+             "__device__ __forceinline__ void b2c_dmma(double (&d)[4], double a0, double a1, "
+             "double b0) {",
+             '  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, '
+             '{%4,%5}, {%6}, {%0,%1,%2,%3};\\n" : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3]) '
+             ': "d"(a0), "d"(a1), "d"(b0));',
+             "}",
+             "__device__ __forceinline__ long long b2c_mx(unsigned m) { return "
+             + decode(Mp, cp["cx"], "m") + "; }",
+             "__device__ __forceinline__ long long b2c_kx(unsigned k) { return "
+             + decode(Kp, cp["cx"], "k") + "; }",
+             "__device__ __forceinline__ long long b2c_ky(unsigned k) { return "
+             + decode(Kp, cp["cy"], "k") + "; }",
+             "__device__ __forceinline__ long long b2c_mo(unsigned m) { return "
+             + decode(Mp, cp["co"], "m") + "; }",
+             "}  // namespace",
+             f'extern "C" __global__ void __launch_bounds__(256) {spec.name}'
+             f"(const __grid_constant__ B2Args a) {{",
+             "  B2_PDL_ENTRY();",
+             f"  const double *__restrict__ X = (const double *){ax} + {cp['cx'][0]}LL;",
+             f"  const double *__restrict__ Y = (const double *){ay} + {cp['cy'][0]}LL;",
+             f"  double *__restrict__ O = (double *){ao} + {cp['co'][0]}LL;",
+             "  extern __shared__ __align__(16) double b2c_smem[];",
+             "  double (*Win)[WS] = reinterpret_cast<double (*)[WS]>(b2c_smem);",
+             "  double (*Bs)[BK][TN + BPAD] = reinterpret_cast<double (*)[BK][TN + BPAD]>("
+             "b2c_smem + 2 * WS);",
+             "  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;",
+             "  const int g = lane >> 2, t = lane & 3;",
+             "  const long long ntiles = (NT + TN - 1) / TN;",
+             "  for (long long tile = blockIdx.x; tile < MO * NJB * ntiles; tile += gridDim.x) {",
+             "    const long long tm = tile / ntiles, n0 = (tile % ntiles) * TN;",
+             "    const long long j0 = (tm % NJB) * TM, mfirst = (tm / NJB) * EJ + j0;",
+             "    const long long rows = EJ - j0 < TM ? EJ - j0 : TM;",
+             "    const long long R = b2c_mx((unsigned)mfirst);",
+             "    const int wl = (int)(S * (rows - 1) + BK);",
+             "    double rw[WR], rb[(BK * TN + 255) / 256];",
+             "    auto load = [&](long long k0) {",
+             "      const double *src = X + R + b2c_kx((unsigned)k0);",
+             "#pragma unroll",
+             "      for (int r = 0; r < WR; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        rw[r] = e < wl ? src[e] : 0.0;",
+             "      }",
+             "#pragma unroll",
+             "      for (int r = 0; r < (BK * TN + 255) / 256; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        if (e < BK * TN) {",
+             "          const int row = e / TN, col = e % TN;",
+             "          const long long k = k0 + row, n = n0 + col;",
+             f"          rb[r] = n < NT ? Y[b2c_ky((unsigned)k) + {cyn}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             "        }",
+             "      }",
+             "    };",
+             "    auto store = [&](int buf) {",
+             "#pragma unroll",
+             "      for (int r = 0; r < WR; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        if (e < WS) Win[buf][e] = rw[r];",
+             "      }",
+             "#pragma unroll",
+             "      for (int r = 0; r < (BK * TN + 255) / 256; ++r) {",
+             "        const int e = tid + 256 * r;",
+             "        if (e < BK * TN) Bs[buf][e / TN][e % TN] = rb[r];",
+             "      }",
+             "    };",
+             "    double acc[MF][NF][4];",
+             "    const int wm = warp * 16 * MF;",
+             "#pragma unroll",
+             "    for (int mf = 0; mf < MF; ++mf)",
+             "#pragma unroll",
+             "    for (int f = 0; f < NF; ++f)",
+             "#pragma unroll",
+             "      for (int h = 0; h < 2; ++h)",
+             "#pragma unroll",
+             "        for (int e2 = 0; e2 < 2; ++e2) {",
+             "          const int row = wm + 16 * mf + g + 8 * h;",
+             "          const long long n = n0 + f * 8 + 2 * t + e2;",
+             f"          acc[mf][f][2 * h + e2] = (row < rows && n < NT) ? "
+             f"O[b2c_mo((unsigned)(mfirst + row)) + {con}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             "        }",
+             "    __syncthreads();",
+             "    load(0);",
+             "    store(0);",
+             "    __syncthreads();",
+             "    const long long nk = KT / BK;",
+             "    for (long long kc = 0; kc < nk; ++kc) {",
+             "      const int cur = (int)(kc & 1);",
+             "      if (kc + 1 < nk) load((kc + 1) * BK);",
+             "      const double *win = Win[cur];",
+             "#pragma unroll",
+             "      for (int k4 = 0; k4 < BK; k4 += 4) {",
+             "        double bf[NF];",
+             "#pragma unroll",
+             "        for (int f = 0; f < NF; ++f) bf[f] = Bs[cur][k4 + t][f * 8 + g];",
+             "#pragma unroll",
+             "        for (int mf = 0; mf < MF; ++mf) {",
+             "          if (wm + 16 * mf >= rows) break;  // m16 fragment past the row's last j",
+             "          const int r0 = wm + 16 * mf + g;",
+             "          const double a0 = win[S * r0 + k4 + t], a1 = win[S * (r0 + 8) + k4 + t];",
+             "#pragma unroll",
+             "          for (int f = 0; f < NF; ++f) b2c_dmma(acc[mf][f], a0, a1, bf[f]);",
+             "        }",
+             "      }",
+             "      if (kc + 1 < nk) store(cur ^ 1);",
+             "      __syncthreads();",
+             "    }",
+             "#pragma unroll",
+             "    for (int mf = 0; mf < MF; ++mf)",
+             "#pragma unroll",
+             "    for (int f = 0; f < NF; ++f)",
+             "#pragma unroll",
+             "      for (int h = 0; h < 2; ++h)",
+             "#pragma unroll",
+             "        for (int e2 = 0; e2 < 2; ++e2) {",
+             "          const int row = wm + 16 * mf + g + 8 * h;",
+             "          const long long n = n0 + f * 8 + 2 * t + e2;",
+             f"          if (row < rows && n < NT) O[b2c_mo((unsigned)(mfirst + row)) + {con}LL * "
+             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] = acc[mf][f][2 * h + e2];",
+             "        }",
+             "  }",
+             "}"]
+        self._contract_checks()
+        spec.source = "\n".join(L) + "\n"
+        spec.block = (256, 1, 1)
+        spec.vec = 1
+        spec.pdl = False
+        spec.contract = {"M": Mtot, "N": Ntot, "K": Ktot, "TN": TN, "TM": TM,
+                         "tiles_m": (Mtot // EJ) * (-(-EJ // TM)), "slide": dict(sl)}
+        spec.smem = 8 * (2 * WS + 2 * BK * (TN + 4))
+        return spec
+
+    def _contract_decode(self, cp):
         ext, rng = cp["ext"], cp["rng"]
 
         def decode(names, cst_co, idx):
@@ -423,6 +613,37 @@ class _Gen:
                 if c:
                     out.append(f"{c}LL * {val}")
             return " + ".join(out) if out else "0LL"
+        return decode
+
+    def _contract_checks(self):
+        """Host-side bounds checks of the three memlets (as the generic
+        body's)."""
+        spec = self.spec
+        mem = self.group.members[0]
+        menv = {mp: f"p_{gp}" for mp, gp in mem.rename.items()}
+        t = next(k for k in P._scope_children(mem.state, mem.entry)
+                 if not isinstance(k, sdfg.MapExit)) if mem.tasklet is None else mem.tasklet
+        if isinstance(t, sdfg.MapEntry):  # blocked form: the inner map's outer memlets
+            edges = mem.state.in_edges(t) + mem.state.out_edges(mem.state.exit_of(t))
+        else:
+            edges = mem.state.in_edges(t) + mem.state.out_edges(t)
+        for e in edges:
+            if e.memlet is not None:
+                spec.checks.append((e.memlet.container, e.memlet.subset, menv))
+
+    def _contract_kernel(self, cp):
+        """Implicit GEMM on DMMA (mma.sync.m16n8k4 f64): CTA tile 128 MF m x TN
+        n, 8 warps of 16 MF m rows; K in BK-wide chunks staged in (dynamic) shared memory
+        through affine gathers (address = row part + k part, both
+        precomputed), double-buffered through registers.  The accumulators
+        start from O's current value (the WCR add) and store once.  FP64
+        tensor ops fuse multiply and add: within 1e-12 of the sequential
+        reference sum, not bitwise."""
+        spec = self.spec
+        X, Y, O = cp["X"], cp["Y"], cp["O"]
+        Mp, Kp, Np = cp["M"], cp["K"], cp["N"]
+        ext, rng = cp["ext"], cp["rng"]
+        decode = self._contract_decode(cp)
 
         Mtot = 1
         for q in Mp:
@@ -483,7 +704,7 @@ class _Gen:
              "    if (tid < TM) sMX[tid] = (m0 + tid < MT) ? b2c_mx((unsigned)(m0 + tid)) : 0LL;",
              "    __syncthreads();",
              # staging: A element e = tid + 256 r: row e / BK, col e % BK
-             "    double ra[TM * BK / 256], rb[BK * TN / 256 > 0 ? BK * TN / 256 : 1];",
+             "    double ra[TM * BK / 256], rb[(BK * TN + 255) / 256];",
              "    auto load = [&](long long k0) {",
              "      // a thread stages one k column of A (8 rows) and one element of B",
              "      const int acol = tid % BK;",
@@ -568,18 +789,7 @@ class _Gen:
              "        }",
              "  }",
              "}"]
-        # host-side bounds checks of the three memlets (as the generic body's)
-        mem = self.group.members[0]
-        menv = {mp: f"p_{gp}" for mp, gp in mem.rename.items()}
-        t = next(k for k in P._scope_children(mem.state, mem.entry)
-                 if not isinstance(k, sdfg.MapExit)) if mem.tasklet is None else mem.tasklet
-        if isinstance(t, sdfg.MapEntry):  # blocked form: the inner map's outer memlets
-            edges = mem.state.in_edges(t) + mem.state.out_edges(mem.state.exit_of(t))
-        else:
-            edges = mem.state.in_edges(t) + mem.state.out_edges(t)
-        for e in edges:
-            if e.memlet is not None:
-                spec.checks.append((e.memlet.container, e.memlet.subset, menv))
+        self._contract_checks()
         spec.source = "\n".join(L) + "\n"
         spec.block = (256, 1, 1)
         spec.vec = 1
@@ -1733,7 +1943,8 @@ class _Gen:
             cp = self._contraction_plan()
             if cp is not None:
                 spec.mode = "contract"
-                return self._contract_kernel(cp)
+                sl = self._slide_plan(cp) if CONTRACT_SLIDE else None
+                return self._contract_slide_kernel(cp, sl) if sl else self._contract_kernel(cp)
         if mode in ("flat", "tile2", "march") and REDUCE_MODE:
             rp = self._reduction_plan()
             if (rp is not None and ROWRED_MODE and ROWRED_CONTIG and rp[0] == [grp.params[-1]]
@@ -2604,7 +2815,7 @@ def launch_geometry(spec: KernelSpec, rl: list[int]) -> tuple[tuple, tuple]:
         return (spec.grid_cap, 1, 1), spec.block
     if spec.mode == "contract":
         c = spec.contract
-        tiles = -(-c["M"] // c.get("TM", 128)) * -(-c["N"] // c["TN"])
+        tiles = c.get("tiles_m", -(-c["M"] // c.get("TM", 128))) * -(-c["N"] // c["TN"])
         return (max(1, min(tiles, 148 * 8)), 1, 1), (256, 1, 1)
     if spec.mode == "march2":
         rows = spec.block[1] * spec.vec

@@ -1,3 +1,2 @@
-timeout 300 python scripts/probe_dgemm.py > /dev/null 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:dgemm -s 4 -c 1 -o gpurun_out/dgemm_final python scripts/probe_dgemm.py > gpurun_out/ncu_dgf.log 2>&1
-tail -2 gpurun_out/ncu_dgf.log
+ncu --set full --clock-control none --import-source on -k regex:conv2d_bias_1 -c 1 -o gpurun_out/conv_slide60 python scripts/bench_suite.py --only conv2d_bias --reps 1 --out gpurun_out/s_conv_ncu.json > gpurun_out/ncu_conv.log 2>&1
+tail -1 gpurun_out/ncu_conv.log

@@ -175,10 +175,28 @@ def test_kernel_mode_selection():
     pl = P.Planner(g, syms).build()
     grp = [op for op in pl.all_ops if isinstance(op, P.MapGroup)][1]
     sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")
+    # inp[n, i + ki, j + kj, ci] slides along j (stride 3) and (kj, ci) is a
+    # contiguous run of 60 addresses: one 825-double window per (tile, ki)
+    assert sp.mode == "contract" and sp.contract == {
+        "M": 449352, "N": 16, "K": 1200, "TN": 16, "TM": 256, "tiles_m": 8 * 237,
+        "slide": {"S": 3, "BK": 60, "KR": 60, "WS": 826, "jm": "j"}}
+    assert "sliding-window contraction" in sp.source
+    assert "mma.sync.aligned.m16n8k4.row.col.f64" in sp.source
+    codegen.CONTRACT_SLIDE = False
+    try:
+        sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")
+    finally:
+        codegen.CONTRACT_SLIDE = True
     assert sp.mode == "contract" and sp.contract == {"M": 449352, "N": 16, "K": 1200, "TN": 16,
                                                      "TM": 256}
     assert sp.smem > 48 * 1024  # dynamic shared memory (two 256 x 20 A stages)
-    assert "mma.sync.aligned.m16n8k4.row.col.f64" in sp.source
+    # a plain GEMM has no sliding operand (A's row stride is K)
+    gm = sdfg.load(GOLDEN / "graphs" / "matmul.auto.json")
+    msy = {"M": 4096, "K": 4096, "N": 4096}
+    plm = P.Planner(gm, msy).build()
+    specs = [codegen.generate(plm, op, plm.shapes(msy), f"k{op.idx}") for op in plm.all_ops
+             if isinstance(op, P.MapGroup) and op.schedule == "parallel"]
+    assert any(x.mode == "contract" and "slide" not in x.contract for x in specs)
     codegen.CONTRACT_MODE = False
     try:
         sp = codegen.generate(pl, grp, pl.shapes(syms), "k1")

@@ -325,3 +325,39 @@ def test_blocked_matmul_expansion_runs_as_contraction(name, syms):
     for k in ref:
         assert rel_err(out[k], ref[k]) <= 1e-12, (k, rel_err(out[k], ref[k]))
     _ = interp_ref
+
+
+@pytest.mark.parametrize("NB,H,W,K,BK", [(2, 30, 40, 8, 24), (2, 24, 300, 20, 60),
+                                         (1, 40, 256, 20, 60), (2, 30, 60, 6, None)])
+def test_sliding_window_contraction(NB, H, W, K, BK):
+    """conv2d_bias's X operand slides along the output column (stride CI)
+    with (kj, ci) a contiguous run of K * CI addresses: the contraction
+    stages one window per (tile, k chunk) (BK = 24 for K = 8, 60 for K = 20;
+    W = 300 gives two column tiles per output row, the second with idle
+    m16 fragments; K = 6's run of 18 has no k-chunk divisor, so the generic
+    gather runs).  Equal to the closed form within the tensor-core
+    tolerance."""
+    from paper_2107_00555_b200 import ExecContext, interpret, sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    CI, CO = 3, 16
+    HO, WO = H - K + 1, W - K + 1
+    syms = dict(NB=NB, H=H, W=W, CI=CI, CO=CO, K=K, HO=HO, WO=WO)
+    g = sdfg.load(GOLDEN / "graphs" / "conv2d_bias.raw.json")
+    ex = GpuExecutor(g, syms)
+    try:
+        slides = [sp.contract.get("slide") for sp in ex.specs.values() if sp.mode == "contract"]
+    finally:
+        ex.close()
+    assert slides and (slides[0] or {}).get("BK") == BK
+    rng = np.random.default_rng(K * W)
+    inp = rng.uniform(-1, 1, (NB, H, W, CI))
+    w = rng.uniform(-1, 1, (K, K, CI, CO))
+    b = rng.uniform(-1, 1, CO)
+    out = interpret(g, ExecContext(bindings=syms).bind_inputs(
+        {"inp": inp, "w": w, "bias": b, "out": np.zeros((NB, HO, WO, CO))}))["out"]
+    ref = np.broadcast_to(b, (NB, HO, WO, CO)).copy()
+    for ki in range(K):
+        for kj in range(K):
+            ref += np.einsum("nijc,cd->nijd", inp[:, ki:ki + HO, kj:kj + WO, :], w[ki, kj])
+    assert rel_err(out, ref) <= 1e-12, rel_err(out, ref)
