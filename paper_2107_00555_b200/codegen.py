@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import math
 import os
+import re
 import struct
 
 from . import plan as P  # noqa: E402
@@ -51,6 +52,7 @@ MARCH_BX = int(os.environ.get("B2_MARCH_BX", "64"))  # tile columns (blockDim.x)
 # shift the innermost tile origin down to a 128-byte line so a warp's row
 # access covers whole lines (march / tile2 with a constant unit-stride range)
 RED_THREADS = int(os.environ.get("B2_RED_THREADS", str(148 * 8192)))  # chunked-reduction thread target (azimint 0.78 -> 0.51 ms vs 148 * 512)
+RED_OUT_BLOCK = int(os.environ.get("B2_RED_OUT_BLOCK", "4"))  # outputs per thread, broadcast-read chunked reductions
 SMALL_RED_CHUNK = int(os.environ.get("B2_SMALL_RED_CHUNK", "2"))  # terms per chunk, small reductions (0: off)
 RED_BLOCK = int(os.environ.get("B2_RED_BLOCK", "16"))  # max points of a register-blocked output dim
 MARCH_PREFETCH = os.environ.get("B2_MARCH_PF", "1") == "1"  # L2 bulk prefetch of march tiles
@@ -861,6 +863,9 @@ class _Gen:
             # consecutive outputs (coalesced / broadcast loads like the
             # thread-per-output layout) and the fold happens in-block
             return self._reduce_loop_inblock(R, pout, reg_decls, body, nout, nred, C)
+        ob = self._red_out_block(pout, nout) if not full else 1
+        if ob > 1:
+            return self._reduce_loop_ob(R, pout, reg_decls, body, nout, nred, C, ob)
         L = [f"  constexpr b2_ll NOUT = {nout}LL, NRED = {nred}LL, NCH = {C}LL;",
              "  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUT * NCH; "
              "f += (b2_ll)gridDim.x * blockDim.x) {",
@@ -924,6 +929,78 @@ class _Gen:
             else:
                 cond = "" if full else "if (lo < hi) "
                 L.append(f"    {cond}b2_atomic_{t['wcr']}(&{t['target']}, {a});")
+        L.append("  }")
+        return L
+
+    def _red_out_block(self, pout, nout) -> int:
+        """Outputs per thread for a chunked reduction whose every HBM read is
+        the same for all outputs (azimint: radius[k], data[k] per bin): each
+        loaded term then feeds RED_OUT_BLOCK accumulators (1: off)."""
+        if RED_OUT_BLOCK < 2 or len(pout) != 1 or nout % RED_OUT_BLOCK:
+            return 1
+        if any(t["ct"] != "double" for t in self.red.values()):
+            return 1
+        grp = self.group
+        for mem in grp.members:
+            for (c, w, wcr, depth, pt) in self.pl.member_accesses(mem, grp.params):
+                if w or self.place(c) != "memory":
+                    continue
+                if pt is None or any(p == pout[0] for key in pt for (p, _) in key[1]):
+                    return 1
+        return RED_OUT_BLOCK
+
+    def _reduce_loop_ob(self, R, pout, reg_decls, body, nout, nred, C, OB) -> list:
+        """The chunked reduction with OB consecutive outputs per thread: the
+        body runs OB times per term with the output parameter stepped and
+        its own accumulator (the loads are common subexpressions), partials
+        to the workspace as usual (same per-output term order: bitwise equal
+        to the one-output layout)."""
+        grp = self.group
+        idx = {p: i for i, p in enumerate(grp.params)}
+        i0 = idx[pout[0]]
+        names = [t["acc"] for t in self.red.values()]
+        pat = re.compile(r"\b(" + "|".join(map(re.escape, names)) + r")\b")
+        L = [f"  constexpr b2_ll NOUT = {nout}LL, NRED = {nred}LL, NCH = {C}LL;",
+             f"  constexpr int OB = {OB};",
+             "  constexpr b2_ll NOUTB = NOUT / OB;",
+             "  for (b2_ll f = (b2_ll)blockIdx.x * blockDim.x + threadIdx.x; f < NOUTB * NCH; "
+             "f += (b2_ll)gridDim.x * blockDim.x) {",
+             "    const b2_ll qb = (f % NOUTB) * OB;", "    const b2_ll ch = f / NOUTB;"]
+        for t in self.red.values():
+            ident = {"add": "0", "mul": "1", "min": "b2_inf()", "max": "(-b2_inf())"}[t["wcr"]]
+            L.append(f"    double {t['acc']}[OB];")
+            L.append(f"#pragma unroll")
+            L.append(f"    for (int ob_ = 0; ob_ < OB; ++ob_) {t['acc']}[ob_] = (double)({ident});")
+        L.append("    const b2_ll lo = ch * NRED / NCH, hi = (ch + 1) * NRED / NCH;")
+        it = "int" if nred < 2 ** 31 else "b2_ll"
+        L.append(f"    for ({it} rf = ({it})lo; rf < ({it})hi; ++rf) {{")
+        L.append("    b2_ll rr = rf;")
+        for p in reversed(R):
+            i = idx[p]
+            if len(R) == 1:
+                L.append(f"    const b2_ll j{i} = rr;")
+            else:
+                L.append(f"    const b2_ll j{i} = rr % rl{i}; rr /= rl{i};")
+            L.append(f"    const b2_ll p_{p} = rb{i} + rs{i} * j{i};")
+        L.append("#pragma unroll")
+        L.append("    for (int ob_ = 0; ob_ < OB; ++ob_) {")
+        L.append(f"    const b2_ll q{i0} = qb + ob_;")
+        L.append(f"    const b2_ll p_{pout[0]} = rb{i0} + rs{i0} * q{i0};")
+        L += reg_decls(4)
+        L += [pat.sub(lambda m: m.group(1) + "[ob_]", ln) for ln in body]
+        L.append("    }")
+        L.append("    }")
+        self.spec.red_fin = []
+        self.spec.red_nout, self.spec.red_nch = nout, C
+        self.spec.red_threads = (nout // OB) * C
+        self.red_decode = [f"    const b2_ll q{i0} = rem % rl{i0}; rem /= rl{i0};",
+                           f"    const b2_ll p_{pout[0]} = rb{i0} + rs{i0} * q{i0};"]
+        for k, t in enumerate(self.red.values()):
+            ws = self.arg(("ptr", f"{self.spec.name}#ws{k}"))
+            L.append("#pragma unroll")
+            L.append(f"    for (int ob_ = 0; ob_ < OB; ++ob_) "
+                     f"((double *){ws})[ch * NOUT + qb + ob_] = {t['acc']}[ob_];")
+            self.spec.red_fin.append((ws, t))
         L.append("  }")
         return L
 
