@@ -211,6 +211,16 @@ def run_one(name, reps):
             res["roofline"] = {"bound": "fp64_tensor", "achieved": ach, "peak": pk,
                                "unit": "TFLOP/s", "frac": ach / pk, "peak_kind": "measured",
                                "kernel": top[0]}
+        elif name == "azimint_naive":
+            # per (bin, sample) pair the program evaluates two f64 compares, a
+            # multiply and two adds (acc and cnt): 5 FP64 operations, one
+            # FP64-pipe instruction each; the pipe issues half the measured
+            # DFMA flop rate in instructions
+            pk = extra.get("dfma_f64_tflops", 35.96) / 2
+            ach = 5 * work / (top_ms / 1e3) / 1e12
+            res["roofline"] = {"bound": "fp64_pipe", "achieved": ach, "peak": pk,
+                               "unit": "Top/s", "frac": ach / pk, "peak_kind": "measured",
+                               "ops_per_pair": 5, "kernel": top[0]}
     # end to end through interpret(): pinned host inputs, H2D + D2H timed
     from paper_2107_00555_b200 import ExecContext, InterpOptions, interpret
 
