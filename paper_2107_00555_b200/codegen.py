@@ -2552,10 +2552,15 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         code, t = scalar.emit(c, types, lambda n: f"s_{n}")
         return scalar.cast(code, t, "b")
 
+    blockreg = bool(getattr(reg, "block", False))
+
     def emit_ops(h):
         for op in planner.ops[h]:
             if not isinstance(op, P.MapGroup):
                 raise P.PlanError("non-map op inside a device loop region")
+            if blockreg:
+                emit_block_group(op)
+                continue
             for mem in op.members:
                 if mem.tasklet is not None:
                     gen.tasklet(mem.state, mem.tasklet, {}, 1)
@@ -2575,6 +2580,50 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
                 for _ in heads:
                     gen.ind -= 2
                     gen.emit("}")
+
+    def emit_block_group(op):
+        """Block region: a top-level tasklet group runs on thread 0; a map
+        group's points are spread over the CTA's threads, each point running
+        every member in order (the fused members share its op-local
+        registers, as in the group's own kernel); a barrier orders the op
+        before the next (block-scope visibility of its global writes)."""
+        if op.schedule != "parallel":
+            gen.emit("if (threadIdx.x == 0) {")
+            gen.ind += 2
+            for mem in op.members:
+                gen.tasklet(mem.state, mem.tasklet, {}, 1)
+            gen.ind -= 2
+            gen.emit("}")
+            gen.emit("__syncthreads();")
+            return
+        ns = []
+        gen.emit("{")
+        gen.ind += 2
+        for p, (b, e, s_) in zip(op.params, op.ranges):
+            bb, ee, ss = (symexpr.to_c(x, gen.name_of({})) for x in (b, e, s_))
+            n, v0, st = gen.fresh(f"bn_{p}"), gen.fresh(f"bb_{p}"), gen.fresh(f"bs_{p}")
+            gen.emit(f"const b2_ll {v0} = {bb}, {st} = {ss};")
+            gen.emit(f"const b2_ll {n} = (({ee}) - {v0}) / {st} + 1;")
+            ns.append((p, n, v0, st))
+        tot = " * ".join(f"({n} > 0 ? {n} : 0)" for _, n, _, _ in ns) or "1"
+        bf = gen.fresh("bf")
+        gen.emit(f"for (b2_ll {bf} = threadIdx.x; {bf} < {tot}; {bf} += blockDim.x) {{")
+        gen.ind += 2
+        rem = gen.fresh("brem")
+        gen.emit(f"b2_ll {rem} = {bf}; (void){rem};")
+        gvar = {}
+        for p, n, v0, st in reversed(ns):
+            v = gen.fresh(f"p_{p}")
+            gen.emit(f"const b2_ll {v} = {v0} + {st} * ({rem} % {n}); {rem} /= {n};")
+            gvar[p] = v
+        for mem in op.members:
+            env = {mp: gvar[gp] for mp, gp in mem.rename.items()}
+            gen.scope(mem.state, mem.entry, env, 1)
+        gen.ind -= 2
+        gen.emit("}")
+        gen.ind -= 2
+        gen.emit("}")
+        gen.emit("__syncthreads();")
 
     def follow(t):
         for k, v in t.assignments.items():
@@ -2715,7 +2764,7 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         gen.emit("}")
 
     warp_mode = False
-    if reg.par and FOLD_MODE:
+    if reg.par and FOLD_MODE and not blockreg:
         for h in reg.heads:
             if h in loops_all and h != reg.loop.guard and loops_all[h] not in reg.par \
                     and fold_info(loops_all[h]) is not None:
@@ -2774,7 +2823,18 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         gen.emit("}")
     body = gen.lines
     spec = gen.spec
-    pro = [f'extern "C" __global__ void __launch_bounds__(256) {name}'
+    nthr = 256
+    if blockreg:
+        most = 1
+        for h in reg.heads:
+            for op in planner.ops[h]:
+                if isinstance(op, P.MapGroup) and op.schedule == "parallel":
+                    n = 1
+                    for r in op.ranges:
+                        n *= _const_range(planner, r)[2]
+                    most = max(most, n)
+        nthr = min(1024, max(64, -(-most // 32) * 32))
+    pro = [f'extern "C" __global__ void __launch_bounds__({nthr}) {name}'
            "(const __grid_constant__ B2Args a) {", "  B2_PDL_ENTRY();"]
     for cname in spec.containers:
         c = planner.g.containers[cname]
@@ -2795,7 +2855,9 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     for k, l in enumerate(reg.par):
         pro.append(f"  const b2_ll pb{k} = {gen.arg(('pb', k))}, ps{k} = {gen.arg(('ps', k))}, "
                    f"pn{k} = {gen.arg(('pn', k))};")
-    if warp_mode:  # one warp per parallel iteration
+    if blockreg:  # one CTA, every thread walks the whole nest
+        loop = ["  if (blockIdx.x != 0) return;", "  {", "    b2_ll rem = 0; (void)rem;"]
+    elif warp_mode:  # one warp per parallel iteration
         loop = ["  const int lane = threadIdx.x & 31;",
                 "  for (b2_ll f = ((b2_ll)blockIdx.x * blockDim.x + threadIdx.x) >> 5; f < NPAR; "
                 "f += ((b2_ll)gridDim.x * blockDim.x) >> 5) {", "    b2_ll rem = f; (void)rem;"]
@@ -2824,9 +2886,10 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
          f"'{reg.loop.guard}' ({len(reg.par)} parallel loop(s))",
          "struct B2Args { long long w[%d]; };" % max(1, len(spec.args))] + pro + loop + ["}"]) + "\n"
     spec.mode = "region"
-    spec.block = (256, 1, 1)
+    spec.block = (nthr, 1, 1)
     spec.params = []
     spec.warp = warp_mode
+    spec.block_region = blockreg
     return spec
 
 

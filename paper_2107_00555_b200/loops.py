@@ -46,6 +46,7 @@ class Region:
     heads: set  # every chain head executed inside the region (guard included)
     idx: int = -1
     spec: object = None
+    block: bool = False  # one CTA runs the whole nest, its maps spread over the threads
 
 
 def _trans_in(planner: P.Planner) -> dict:
@@ -110,7 +111,7 @@ def _reach(planner, start, stop, tail_of):
     return seen
 
 
-def _compilable(planner, loop: Loop, loops: dict) -> bool:
+def _compilable(planner, loop: Loop, loops: dict, maps: bool = False) -> bool:
     g = planner.g
     for h in loop.body:
         if h in loops:
@@ -120,9 +121,13 @@ def _compilable(planner, loop: Loop, loops: dict) -> bool:
             continue
         # inside some inner loop's body: checked through that loop as well.
         # Only scalar (top-level tasklet) ops: loops around real maps stay
-        # host-driven, each map a full-width kernel in the captured graph.
+        # host-driven, each map a full-width kernel in the captured graph —
+        # unless every map is small enough for one CTA (``maps``: block
+        # regions, below)
         for op in planner.ops[h]:
-            if not isinstance(op, P.MapGroup) or op.schedule != "scalar":
+            if not isinstance(op, P.MapGroup):
+                return False
+            if op.schedule != "scalar" and not (maps and _block_map_ok(planner, op)):
                 return False
         outs = g.out_transitions(planner.chain_end[h])
         if len(outs) != 1 or outs[0].condition is not None:
@@ -254,6 +259,48 @@ def _perfect_child(planner, loop: Loop, loops: dict) -> Loop | None:
     return inner
 
 
+def _block_map_ok(planner, op) -> bool:
+    """A parallel map one CTA can sweep per loop iteration: constant ranges
+    of at most BLOCK_MAX_POINTS points, no WCR writes (threads would race on
+    the targets) and no library nodes in its scope."""
+    from . import codegen
+
+    if op.schedule != "parallel":
+        return False
+    npts = 1
+    for r in op.ranges:
+        cr = codegen._const_range(planner, r)
+        if cr is None:
+            return False
+        npts *= cr[2]
+    if npts > BLOCK_MAX_POINTS:
+        return False
+    for m in op.members:
+        acc = _raw_accesses(planner, m)
+        if any(w and wcr is not None for (_, w, wcr, _) in acc):
+            return False
+        if any(planner.placement.get(c) == "private" for (c, _, _, _) in acc):
+            return False
+        if m.entry is not None and any(isinstance(n, sdfg.Library)
+                                       for n in P._scope_children(m.state, m.entry)):
+            return False
+    return True
+
+
+def _has_parallel_map(planner, loop: Loop) -> bool:
+    return any(isinstance(op, P.MapGroup) and op.schedule == "parallel"
+               for h in loop.body for op in planner.ops[h])
+
+
+def _nested_map_loop(planner, loop: Loop, loops: dict) -> bool:
+    """An inner loop of ``loop`` iterates maps: the launch count is the
+    product of trip counts (adi: TSTEPS x 4 x (N - 2)).  A single loop
+    around maps (a stencil's time loop) keeps one full-width kernel per map
+    in the captured graph."""
+    return any(h in loops and h != loop.guard and _has_parallel_map(planner, loops[h])
+               for h in loop.body)
+
+
 def find_regions(planner: P.Planner) -> list[Region]:
     if not LOOP_REGIONS:
         return []
@@ -274,7 +321,34 @@ def find_regions(planner: P.Planner) -> list[Region]:
         if _symbols_escape(planner, reg):
             continue
         regions.append(reg)
+    if BLOCK_REGIONS:
+        regions += _block_regions(planner, loops, regions)
     return regions
+
+
+def _block_regions(planner, loops: dict, regions: list) -> list:
+    """Host loops whose bodies hold small maps (adi's column / row sweeps:
+    one 398-point map per step of a 398-step j loop): the reference runs one
+    state transition per iteration (interp.py:240-263), a launch-per-map
+    backend one kernel per iteration.  Here the outermost such loop nest is
+    ONE single-CTA kernel: control flow and symbols uniform across the CTA,
+    every map's points spread over the threads, a barrier after every op
+    (program order, so results are bitwise those of the launch sequence)."""
+    taken = set()
+    for r in regions:
+        taken |= r.heads
+    cand = {h: l for h, l in loops.items()
+            if not (l.body | {h}) & taken and _compilable(planner, l, loops, maps=True)
+            and _nested_map_loop(planner, l, loops)}
+    out = []
+    for h, root in cand.items():
+        if any(h in other.body for oh, other in cand.items() if oh != h):
+            continue
+        reg = Region(root, [], root.body | {root.guard}, block=True)
+        if _symbols_escape(planner, reg):
+            continue
+        out.append(reg)
+    return out
 
 
 def region_transitions(planner, reg: Region) -> list:
@@ -327,6 +401,8 @@ def _symbols_escape(planner, reg: Region) -> bool:
 
 
 LOOP_REGIONS = True
+BLOCK_REGIONS = True
+BLOCK_MAX_POINTS = 4096  # points of one map inside a block region (one CTA sweeps them)
 
 
 def trip(loop: Loop, init: int, env: dict) -> list[int]:

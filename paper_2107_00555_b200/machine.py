@@ -944,11 +944,40 @@ class GpuExecutor:
                 else:
                     raise AssertionError(d)
             blob = struct.pack(f"<{len(vals)}q", *vals)
-            nthr = npar * (32 if getattr(spec, "warp", False) else 1)
-            grid = (max(1, min(-(-nthr // 256), codegen.MAX_BLOCKS * 8)), 1, 1)
-            rt.launch(spec.kernel, grid, (256, 1, 1), blob, self.stream)
+            if getattr(spec, "block_region", False):
+                rt.launch(spec.kernel, (1, 1, 1), spec.block, blob, self.stream)
+            else:
+                nthr = npar * (32 if getattr(spec, "warp", False) else 1)
+                grid = (max(1, min(-(-nthr // 256), codegen.MAX_BLOCKS * 8)), 1, 1)
+                rt.launch(spec.kernel, grid, (256, 1, 1), blob, self.stream)
             self.launches += 1
+            if counters is not None and getattr(reg, "block", False):
+                self._count_region(reg, dict(sym), counters)
         self._region_final(reg, sym)
+
+    def _count_region(self, reg, sym, counters):
+        """Counters of a block region's maps (interp.py:73-92): its control
+        flow walked on the host (conditions on symbols only), every map
+        counted at the ranges it runs with."""
+        g = self.g
+        cur = reg.loop.guard
+        steps = 0
+        while cur in reg.heads:
+            for op in self.planner.ops[cur]:
+                _count_map(self, op, codegen.range_values(op, sym), counters, sym)
+            nxt = None
+            for t in g.out_transitions(self.planner.chain_end[cur]):
+                if t.condition is None or self._eval_cond(t.condition, sym):
+                    for k, v in t.assignments.items():
+                        sym[k] = symexpr.evaluate(v, sym)
+                    nxt = t.dst
+                    break
+            if nxt is None:
+                raise InterpreterError(f"no transition taken out of state '{cur}'")
+            cur = nxt
+            steps += 1
+            if steps > self.opt.max_transitions:
+                raise InterpreterError("transition budget exceeded (infinite loop?)")
 
     def _eval_cond(self, cond, sym):
         env = {}

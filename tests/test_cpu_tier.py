@@ -401,3 +401,29 @@ def test_zero_skip_set_from_dry_run(name, syms, expect):
     ex._dead_on_entry()
     assert ex.zero_skip == expect
     assert "mx" not in ex.zero_skip
+
+
+def test_block_region_selection():
+    """Loop nests whose inner loops iterate small maps (adi: TSTEPS x 4 j
+    loops of one (N - 2)-point map each) become ONE single-CTA kernel; a
+    stencil's time loop around its full-width maps stays host-driven (one
+    kernel per map in the captured graph), and softmax's parallel row loops
+    keep their warp-fold region."""
+    from paper_2107_00555_b200 import codegen, plan as P, sdfg
+
+    def regions(name, syms):
+        g = sdfg.load(GOLDEN / "graphs" / f"{name}.json")
+        pl = P.Planner(g, syms).build()
+        return pl, [(r.loop.var, r.block, [l.var for l in r.par]) for r in pl.regions]
+
+    for v in ("raw", "pipe", "auto"):
+        pl, regs = regions(f"adi.{v}", {"N": 400, "TSTEPS": 5})
+        assert regs == [("t", True, [])], (v, regs)
+        spec = codegen.generate_region(pl, pl.regions[0], pl.shapes({"N": 400, "TSTEPS": 5}), "r")
+        assert spec.block_region and spec.block == (416, 1, 1)
+        assert "__syncthreads();" in spec.source and "if (blockIdx.x != 0) return;" in spec.source
+    assert regions("jacobi_2d.raw", {"N": 34, "TSTEPS": 5})[1] == []
+    assert regions("heat_3d.raw", {"N": 12, "TSTEPS": 3})[1] == []
+    assert regions("softmax.raw", {"N": 1, "H": 2, "SM": 40})[1] == [("i", False, ["i", "j", "k"])]
+    # maps larger than one CTA sweeps per step stay full-width kernels
+    assert regions("adi.pipe", {"N": 5000, "TSTEPS": 2})[1] == []
