@@ -2633,7 +2633,11 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
 
     def fold_info(L):
         """An inner loop that only folds ``C[idx] = max|min(C[idx], E(l))``
-        (idx independent of the loop variable, E reads anything but C)."""
+        or ``C[idx] = C[idx] + E(l)`` (idx independent of the loop variable,
+        E reads anything but C), optionally after tasklets that only set
+        op-local registers E reads (go_fast: ``e2 = exp(2 a[i, i])``).  The
+        add fold re-associates the sum (within the rel_err 1e-12 contract;
+        max / min folds are exact)."""
         if L.step <= 0 or L.body != {L.body_entry}:
             return None
         c = L.cond
@@ -2641,11 +2645,19 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
                 and c[2] == ("ref", L.var) and L.var not in scalar.free_names(c[3])):
             return None
         ops = planner.ops.get(L.body_entry, [])
-        if len(ops) != 1 or not isinstance(ops[0], P.MapGroup) or len(ops[0].members) != 1:
+        if len(ops) != 1 or not isinstance(ops[0], P.MapGroup):
             return None
-        mem = ops[0].members[0]
+        mems = ops[0].members
+        if any(m.tasklet is None for m in mems):
+            return None
+        pre, mem = mems[:-1], mems[-1]
+        for m in pre:  # helper tasklets: single statements into op-local registers
+            outs_ = [e for e in m.state.out_edges(m.tasklet) if e.memlet is not None]
+            if (len(m.tasklet.code) != 1 or len(outs_) != 1 or outs_[0].memlet.wcr is not None
+                    or gen.place(outs_[0].memlet.container) != "reg"):
+                return None
         t = mem.tasklet
-        if t is None or len(t.code) != 1:
+        if len(t.code) != 1:
             return None
         outs = planner.g.out_transitions(planner.chain_end[L.body_entry])
         if len(outs) != 1 or outs[0].dst != L.guard or set(outs[0].assignments) != {L.var}:
@@ -2657,17 +2669,21 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
             return None
         om = oe[0].memlet
         if (planner.g.containers[om.container].dtype != "f64"
+                or gen.place(om.container) == "reg"
                 or any(L.var in symexpr.free_symbols(x) for d in om.subset for x in d)):
             return None
         code = t.code[0][1]
-        if not (isinstance(code, tuple) and code[0] == "call" and code[1] in ("max", "min")
-                and len(code[2]) == 2):
+        if isinstance(code, tuple) and code[0] == "call" and code[1] in ("max", "min") \
+                and len(code[2]) == 2:
+            kind, (a0, a1) = code[1], code[2]
+        elif isinstance(code, tuple) and code[0] == "bin" and code[1] == "+":
+            kind, a0, a1 = "add", code[2], code[3]
+        else:
             return None
         accs = [e for e in ie if e.memlet.container == om.container]
         if len(accs) != 1 or accs[0].memlet.text != om.text:
             return None
         acc_conn = accs[0].dst_conn
-        a0, a1 = code[2]
         if a0 == ("ref", acc_conn):
             expr = a1
         elif a1 == ("ref", acc_conn):
@@ -2676,15 +2692,15 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
             return None
         if acc_conn in scalar.free_names(expr):
             return None
-        return {"op": code[1], "state": st, "t": t, "acc": accs[0], "out": oe[0],
+        return {"op": kind, "state": st, "t": t, "acc": accs[0], "out": oe[0], "pre": pre,
                 "others": [e for e in ie if e is not accs[0]], "expr": expr}
 
     def emit_fold(L, fi):
         """Warp-cooperative fold: lanes take every 32nd trip, combine with a
         fixed xor tree, lane 0 folds into C once (max/min are exact, so the
         result equals the sequential loop's for non-NaN data)."""
-        op = "b2_pymax" if fi["op"] == "max" else "b2_pymin"
-        ident = "(-b2_inf())" if fi["op"] == "max" else "b2_inf()"
+        op = {"max": "b2_pymax", "min": "b2_pymin", "add": "b2_op_add"}[fi["op"]]
+        ident = {"max": "(-b2_inf())", "min": "b2_inf()", "add": "0.0"}[fi["op"]]
         cond = cond_c(L.cond)
         fa, fl, ran = gen.fresh("fold"), gen.fresh("fl"), gen.fresh("ran")
         gen.emit("{")
@@ -2705,8 +2721,9 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         gen.emit(f"bool {ok} = true;")
         for e in fi["others"]:
             m = e.memlet
-            if any(symexpr.affine(b, tuple(symexpr.free_symbols(b)), {}) is None
-                   for b, _, _ in m.subset):
+            if gen.place(m.container) == "reg" or any(
+                    symexpr.affine(b, tuple(symexpr.free_symbols(b)), {}) is None
+                    for b, _, _ in m.subset):
                 continue
             fi["checked"][id(e)] = True
             for at in (f"{fbase}", f"{fbase} + ({trip} - 1) * {L.step}"):
@@ -2723,6 +2740,8 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         gen.emit(f"for (b2_ll {fl} = lane; {ok} && {fl} < {trip}; {fl} += 32) {{")
         gen.ind += 2
         gen.emit(f"const b2_ll s_{L.var} = {fbase} + {fl} * {L.step};")
+        for m in fi["pre"]:  # helper registers (lane-private)
+            gen.tasklet(m.state, m.tasklet, {}, 1)
         types, cname = {}, {}
         for e in fi["others"]:
             m = e.memlet
@@ -2769,6 +2788,11 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
             if h in loops_all and h != reg.loop.guard and loops_all[h] not in reg.par \
                     and fold_info(loops_all[h]) is not None:
                 warp_mode = True
+    root_fold = None
+    if not reg.par and FOLD_MODE and not blockreg:
+        # the whole region is one fold loop (go_fast raw's trace): one warp
+        root_fold = fold_info(reg.loop)
+        warp_mode = root_fold is not None
 
     def block(cur, stop):
         guard_budget = 0
@@ -2813,6 +2837,8 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
         inner = reg.par[-1]
         follow(inner.t_in)
         block(inner.body_entry, inner.guard)
+    elif root_fold is not None:
+        emit_fold(reg.loop, root_fold)
     else:
         root = reg.loop
         gen.emit(f"while ({cond_c(root.cond)}) {{")
