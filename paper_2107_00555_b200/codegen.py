@@ -2554,8 +2554,14 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
 
     blockreg = bool(getattr(reg, "block", False))
 
+    for c in getattr(reg, "private", ()):
+        gen.place_override[c] = "private"  # per-iteration local copy (loops._privatisable)
+
     def emit_ops(h):
         for op in planner.ops[h]:
+            if isinstance(op, P.LibOp) and op.node is not None and op.node.kind == "reduce":
+                gen.library_in_scope(op.state, op.node, {}, 1)  # sequential, in-thread
+                continue
             if not isinstance(op, P.MapGroup):
                 raise P.PlanError("non-map op inside a device loop region")
             if blockreg:
@@ -2905,6 +2911,10 @@ def generate_region(planner: P.Planner, reg, shapes: dict, name: str) -> KernelS
     for cname in spec.containers:
         if gen.place(cname) == "reg":
             loop.append(f"    {CT[planner.g.containers[cname].dtype]} r_{cname} = 0;")
+        elif gen.place(cname) == "private":
+            ct = CT[planner.g.containers[cname].dtype]
+            loop.append(f"    {ct} pva_{cname}[sz_{cname}];")
+            loop.append(f"    {ct} *__restrict__ pv_{cname} = pva_{cname};")
     loop += [ln[2:] for ln in body]
     loop.append("  }")
     spec.source = "\n".join(

@@ -47,6 +47,7 @@ class Region:
     idx: int = -1
     spec: object = None
     block: bool = False  # one CTA runs the whole nest, its maps spread over the threads
+    private: set = field(default_factory=set)  # transients privatised per parallel iteration
 
 
 def _trans_in(planner: P.Planner) -> dict:
@@ -125,6 +126,8 @@ def _compilable(planner, loop: Loop, loops: dict, maps: bool = False) -> bool:
         # unless every map is small enough for one CTA (``maps``: block
         # regions, below)
         for op in planner.ops[h]:
+            if maps == "par" and isinstance(op, P.LibOp) and _reduce_lib_ok(op):
+                continue
             if not isinstance(op, P.MapGroup):
                 return False
             if op.schedule != "scalar" and not (maps and _block_map_ok(planner, op)):
@@ -159,8 +162,13 @@ def _independent(planner, loop: Loop, par_vars: list) -> bool:
     allacc: dict[str, list] = {}
     for h in loop.body | {loop.guard}:
         for op in planner.ops[h]:
-            for m in op.members:
-                acc = _raw_accesses(planner, m)
+            if isinstance(op, P.LibOp):
+                st, n = op.state, op.node
+                accs = [[(e.memlet.container, e.dst is not n, e.memlet.wcr, e.memlet.subset)
+                         for e in st.in_edges(n) + st.out_edges(n) if e.memlet is not None]]
+            else:
+                accs = [_raw_accesses(planner, m) for m in op.members]
+            for acc in accs:
                 for (c, w, wcr, subset) in acc:
                     allacc.setdefault(c, []).append((w, wcr, subset))
                     if w:
@@ -287,6 +295,14 @@ def _block_map_ok(planner, op) -> bool:
     return True
 
 
+def _reduce_lib_ok(op) -> bool:
+    """A whole-array REDUCE library node (doitgen's sum over a transient row):
+    one sequential in-thread loop inside a region (codegen.library_in_scope)."""
+    n = op.node
+    return (n is not None and n.kind == "reduce" and n.attrs.get("axes") is None
+            and not op.fused and op.prologue is None and op.rowpass is None)
+
+
 def _has_parallel_map(planner, loop: Loop) -> bool:
     return any(isinstance(op, P.MapGroup) and op.schedule == "parallel"
                for h in loop.body for op in planner.ops[h])
@@ -323,7 +339,141 @@ def find_regions(planner: P.Planner) -> list[Region]:
         regions.append(reg)
     if BLOCK_REGIONS:
         regions += _block_regions(planner, loops, regions)
+    if MAP_REGIONS:
+        regions += _map_regions(planner, loops, regions)
     return regions
+
+
+def _op_containers(planner, op) -> set:
+    if isinstance(op, P.MapGroup):
+        names = set()
+        for m in op.members:
+            names |= {c for (c, _, _, _) in _raw_accesses(planner, m)}
+        return names
+    if isinstance(op, P.LibOp) and op.node is not None:
+        return {e.memlet.container for e in op.state.in_edges(op.node) + op.state.out_edges(op.node)
+                if e.memlet is not None}
+    return set(planner.g.containers)  # copies / nested graphs: treat as touching everything
+
+
+def _privatisable(planner, root: Loop, loops: dict) -> set:
+    """Transients only the body of ``root`` touches whose first access in
+    each iteration is a map writing the whole container point by point
+    (doitgen's tmp0[k] = A[r, q, k] * C4[k, p], k over all of tmp0): a
+    per-iteration private copy is then exact."""
+    from . import codegen
+
+    heads = root.body | {root.guard}
+    touched: dict = {}
+    for h, ops in planner.ops.items():
+        for op in ops:
+            for c in _op_containers(planner, op):
+                touched.setdefault(c, set()).add(h)
+    out = set()
+    for c, hs in touched.items():
+        cont = planner.g.containers.get(c)
+        if cont is None or not cont.transient or not hs <= heads or c in planner.host_read:
+            continue
+        if planner.placement.get(c) != "memory":
+            continue
+        shape = [symexpr.evaluate(d, planner.fixed) for d in cont.shape] if cont.shape else []
+        if not shape or any(not isinstance(x, int) for x in shape) or \
+                __import__("math").prod(shape) > PRIVATE_MAX_ELEMS:
+            continue
+        # the first op of the body (program order) touching c writes all of it
+        first = None
+        cur, seen = root.body_entry, set()
+        while cur in root.body and cur not in seen and first is None:
+            seen.add(cur)
+            for op in planner.ops[cur]:
+                if c in _op_containers(planner, op):
+                    first = op
+                    break
+            if cur in loops:  # into the nested loop's body
+                cur = loops[cur].body_entry
+                continue
+            outs = planner.g.out_transitions(planner.chain_end[cur])
+            cur = outs[0].dst if len(outs) == 1 else None
+        if not isinstance(first, P.MapGroup) or first.schedule != "parallel" \
+                or len(first.members) != 1:
+            continue
+        m = first.members[0]
+        acc = [a for a in _raw_accesses(planner, m) if a[0] == c]
+        if not acc or not acc[0][1] or acc[0][2] is not None:
+            continue
+        ranges = [codegen._const_range(planner, r) for r in first.ranges]
+        sub = acc[0][3]
+        full = len(sub) == len(shape)
+        for d, (b, e, _) in enumerate(sub if full else []):
+            names = symexpr.free_symbols(b)
+            if b != e or len(names) != 1:
+                full = False
+                break
+            q = next(iter(names))
+            gp = m.rename.get(q, q)
+            if gp not in first.params or b != ("s", q):
+                full = False
+                break
+            r = ranges[first.params.index(gp)]
+            if r is None or r != (0, 1, shape[d]):
+                full = False
+                break
+        if full:
+            out.add(c)
+    return out
+
+
+def _map_regions(planner, loops: dict, regions: list) -> list:
+    """Perfectly nested independent loops around small maps and whole-array
+    REDUCEs (doitgen.raw: r, q, p around a 256-point map into tmp0 and a
+    sum of tmp0): the reference runs NR x NQ x NP host iterations, a
+    launch-per-map backend two kernels per iteration.  Here one thread per
+    (r, q, p) runs the body sequentially with its own copy of each
+    privatisable transient.  Only when the parallel trip count fills the GPU
+    and the body has no sequential loops (counters: one body walk times the
+    trip count)."""
+    taken = set()
+    for r in regions:
+        taken |= r.heads
+    out = []
+    for h, root in loops.items():
+        if (root.body | {h}) & taken or any(h in o.body for oh, o in loops.items() if oh != h):
+            continue
+        if not _compilable(planner, root, loops, maps="par"):
+            continue
+        priv = _privatisable(planner, root, loops)
+        saved = {c: planner.placement[c] for c in priv}
+        for c in priv:
+            planner.placement[c] = "reg"  # private per thread: no cross-iteration effect
+        try:
+            par, cur = [], root
+            while cur is not None and _independent(planner, cur, [l.var for l in par]):
+                par.append(cur)
+                cur = _perfect_child(planner, cur, loops)
+        finally:
+            planner.placement.update(saved)
+        if not par:
+            continue
+        inner = par[-1]
+        if any(x in loops for x in inner.body):
+            continue  # sequential loops inside the body
+        env = dict(planner.fixed)
+        n = 1
+        try:
+            for L in par:
+                v0 = symexpr.evaluate(L.entry_edge.assignments[L.var], env)
+                vals = trip(L, v0, env)
+                env[L.var] = vals[0] if vals else v0
+                n *= len(vals)
+        except Exception:
+            continue
+        if n < MAP_REGION_MIN_PAR:
+            continue
+        reg = Region(root, par, root.body | {root.guard}, private=priv)
+        if _symbols_escape(planner, reg):
+            continue
+        out.append(reg)
+    return out
 
 
 def _block_regions(planner, loops: dict, regions: list) -> list:
@@ -403,6 +553,9 @@ def _symbols_escape(planner, reg: Region) -> bool:
 LOOP_REGIONS = True
 BLOCK_REGIONS = True
 BLOCK_MAX_POINTS = 4096  # points of one map inside a block region (one CTA sweeps them)
+MAP_REGIONS = True
+MAP_REGION_MIN_PAR = 148 * 64  # parallel iterations a thread-per-iteration region needs
+PRIVATE_MAX_ELEMS = 4096  # elements of a per-thread private transient (local memory)
 
 
 def trip(loop: Loop, init: int, env: dict) -> list[int]:

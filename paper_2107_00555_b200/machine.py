@@ -953,7 +953,41 @@ class GpuExecutor:
             self.launches += 1
             if counters is not None and getattr(reg, "block", False):
                 self._count_region(reg, dict(sym), counters)
+            elif counters is not None and reg.par and any(
+                    not (isinstance(op, P.MapGroup) and op.schedule == "scalar")
+                    for h in reg.heads for op in self.planner.ops[h]):
+                self._count_par_region(reg, trips, npar, dict(sym), counters)
         self._region_final(reg, sym)
+
+    def _count_par_region(self, reg, trips, npar, sym, counters):
+        """Counters of a thread-per-iteration region over maps / REDUCEs
+        (loops._map_regions: rectangular parallel nest, constant map ranges,
+        no sequential loops in the body): one body walk times the trip count."""
+        for L, (start, _, _) in zip(reg.par, trips):
+            sym[L.var] = start
+        inner = reg.par[-1]
+        one = Counters()
+        cur = inner.body_entry
+        steps = 0
+        while cur != inner.guard:
+            for op in self.planner.ops[cur]:
+                if isinstance(op, P.MapGroup):
+                    _count_map(self, op, codegen.range_values(op, sym), one, sym)
+                elif isinstance(op, P.LibOp):
+                    ins, outs = self._io(op)
+                    na = _volume(ins["a"].memlet, sym) or 1
+                    om = outs[0].memlet
+                    no = _volume(om, sym) or 1
+                    one.bytes_moved += na * 8 + no * 8
+                    if om.wcr is not None:
+                        one.wcr_commits += no
+            outs = self.g.out_transitions(self.planner.chain_end[cur])
+            cur = outs[0].dst
+            steps += 1
+            if steps > self.opt.max_transitions:
+                raise InterpreterError("transition budget exceeded (infinite loop?)")
+        for k in ("wcr_commits", "map_iterations", "bytes_moved"):
+            setattr(counters, k, getattr(counters, k) + npar * getattr(one, k))
 
     def _count_region(self, reg, sym, counters):
         """Counters of a block region's maps (interp.py:73-92): its control

@@ -361,3 +361,41 @@ def test_sliding_window_contraction(NB, H, W, K, BK):
         for kj in range(K):
             ref += np.einsum("nijc,cd->nijd", inp[:, ki:ki + HO, kj:kj + WO, :], w[ki, kj])
     assert rel_err(out, ref) <= 1e-12, rel_err(out, ref)
+
+
+def test_privatised_map_region_doitgen_raw(monkeypatch):
+    """doitgen.raw's loops r, q, p around a map into the transient tmp0 and
+    a REDUCE of tmp0 run as ONE thread-per-(r, q, p) region with tmp0
+    private per thread (loops._map_regions): the same counters as the
+    host-driven launch sequence, results within the f64 tolerance of it and
+    of the closed form (the in-thread REDUCE sums sequentially, the library
+    REDUCE in its own order)."""
+    from paper_2107_00555_b200 import ExecContext, interpret, loops, sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    syms = {"NR": 8, "NQ": 8, "NP": 160}
+    g = sdfg.load(GOLDEN / "graphs" / "doitgen.raw.json")
+    ex = GpuExecutor(g, syms)
+    try:
+        regs = [(r.block, [l.var for l in r.par], sorted(r.private)) for r in ex.planner.regions]
+    finally:
+        ex.close()
+    assert regs == [(False, ["r", "q", "p"], ["tmp0"])]
+    rng = np.random.default_rng(5)
+    A = rng.uniform(-1, 1, (8, 8, 160))
+    C4 = rng.uniform(-1, 1, (160, 160))
+
+    def run(graph):
+        ctx = ExecContext(bindings=dict(syms)).bind_inputs(
+            {"A": A.copy(), "C4": C4.copy(), "out": np.zeros((8, 8, 160))})
+        return interpret(graph, ctx), ctx.counters
+
+    out, cnt = run(g)
+    monkeypatch.setattr(loops, "MAP_REGIONS", False)
+    g2 = sdfg.load(GOLDEN / "graphs" / "doitgen.raw.json")
+    out2, cnt2 = run(g2)
+    ref = np.einsum("rqs,sp->rqp", A, C4)
+    assert rel_err(out["out"], ref) <= 1e-12
+    assert rel_err(out["out"], out2["out"]) <= 1e-12
+    assert (cnt.map_iterations, cnt.wcr_commits) == (cnt2.map_iterations, cnt2.wcr_commits)
+    assert cnt.map_iterations == 8 * 8 * 160 * 160
