@@ -198,6 +198,11 @@ class _Gen:
         nested = [k for k in kids if not isinstance(k, sdfg.MapExit)]
         if len(nested) == 1 and isinstance(nested[0], sdfg.MapEntry):
             return self._blocked_contraction_plan(mem, nested[0])
+        ents = [k for k in nested if isinstance(k, sdfg.MapEntry)]
+        libs = [k for k in nested if isinstance(k, sdfg.Library)]
+        if len(ents) == 1 and len(libs) == 1 and all(
+                isinstance(k, (sdfg.MapEntry, sdfg.Library, sdfg.Access)) for k in nested):
+            return self._mapreduce_contraction_plan(mem, ents[0], libs[0])
         if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet):
             return None
         t = kids[0]
@@ -271,6 +276,125 @@ class _Gen:
         return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
                 "M": M, "N": npar, "K": K, "ext": ext,
                 "rng": {q: self.const_ranges[params.index(q)] for q in params}}
+
+    def _mapreduce_contraction_plan(self, mem, inner, lib):
+        """``out[m, n] = sum(T)`` after ``T[k] = X[m, k] * Y[k, n]`` inside
+        one parallel map (doitgen's pipe / LoopToMap form: a map into a
+        transient row, then a whole-array REDUCE): per output point the sum
+        over k of the flat product, so the contraction kernel computes it
+        with its accumulators starting from zero (O is overwritten) and T is
+        never materialised.  Re-associated like every tensor-core product
+        (within the rel_err 1e-12 contract)."""
+        st = mem.state
+        grp = self.group
+        if lib.kind != "reduce" or lib.attrs.get("axes") is not None \
+                or lib.attrs.get("op", "add") != "add":
+            return None
+        lin = [e for e in st.in_edges(lib) if e.memlet is not None]
+        lout = [e for e in st.out_edges(lib) if e.memlet is not None]
+        if len(lin) != 1 or len(lout) != 1 or lout[0].memlet.wcr is not None:
+            return None
+        T = lin[0].memlet.container
+        tc = self.g.containers[T]
+        if not tc.transient or len(self.shapes[T]) != 1:
+            return None
+        if {s_.op for s_ in self.pl.sites.get(T, [])} != {grp.idx}:
+            return None  # T read elsewhere: it must be materialised
+        kids = [k for k in P._scope_children(st, inner) if not isinstance(k, sdfg.MapExit)]
+        if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet) or len(inner.params) != 1:
+            return None
+        t = kids[0]
+        if len(t.code) != 1 or len(t.ins) != 2:
+            return None
+        code = t.code[0][1]
+        if code[0] != "bin" or code[1] != "*" or {code[2], code[3]} != \
+                {("ref", t.ins[0]), ("ref", t.ins[1])}:
+            return None
+        ins = {e.dst_conn: e.memlet for e in st.in_edges(t) if e.memlet is not None}
+        touts = [e.memlet for e in st.out_edges(t) if e.memlet is not None]
+        kp, (kb, ke, ks) = inner.params[0]
+        if len(touts) != 1 or touts[0].container != T or touts[0].wcr is not None:
+            return None
+        if touts[0].subset != [(("s", kp), ("s", kp), ("c", 1))] and \
+                tuple(tuple(x) for x in touts[0].subset[0][:2]) != (("s", kp), ("s", kp)):
+            return None
+        kr = _const_range(self.pl, (kb, ke, ks))
+        if kr is None or kr != (0, 1, self.shapes[T][0]):
+            return None  # T[k] over the whole of T, k ascending
+        rin = lin[0].memlet.subset[0]
+        if _const_range(self.pl, rin) != (0, 1, self.shapes[T][0]):
+            return None
+        params = list(grp.params) + [kp]
+        if kp in grp.params:
+            return None
+        env = dict(self.pl.fixed)
+
+        def pt_of(m):
+            out = []
+            for (b, e, s_) in m.subset:
+                if b != e:
+                    return None
+                a = symexpr.affine(b, tuple(params), env)
+                if a is None:
+                    return None
+                out.append((a[0], tuple(sorted(a[1].items()))))
+            return tuple(out)
+
+        def coeffs(cont, pt):
+            if pt is None or self.place(cont) != "memory" or self.g.containers[cont].dtype != "f64":
+                return None
+            st_ = _row_major(self.shapes[cont])
+            if len(pt) != len(st_):
+                return None
+            cst, co = 0, {}
+            for d, (c0, terms) in enumerate(pt):
+                cst += st_[d] * c0
+                for q, cq in terms:
+                    co[q] = co.get(q, 0) + st_[d] * cq
+            return cst, co
+
+        oc = lout[0].memlet.container
+        xs = [ins[c].container for c in t.ins]
+        if len(set(xs)) != 2 or oc in xs or T in xs:
+            return None
+        opt = pt_of(lout[0].memlet)
+        ca = [coeffs(c, pt_of(ins[conn])) for c, conn in zip(xs, t.ins)]
+        co_ = coeffs(oc, opt)
+        if None in ca or co_ is None or opt is None:
+            return None
+        pout = []
+        for c0, terms in opt:
+            if len(terms) != 1 or terms[0][1] != 1:
+                return None
+            pout.append(terms[0][0])
+        if len(set(pout)) != len(pout) or set(pout) != set(grp.params):
+            return None
+        used = [set(q for q, v in c[1].items() if v) for c in ca]
+        outs_ = [set(pout) & u for u in used]
+        if outs_[0] & outs_[1] or (outs_[0] | outs_[1]) != set(pout):
+            return None
+        yi = 1 if len(outs_[1]) == 1 else (0 if len(outs_[0]) == 1 else None)
+        if yi is None:
+            return None
+        xi = 1 - yi
+        npar = next(iter(outs_[yi]))
+        M = [q for q in grp.params if q != npar]
+        K = [kp]
+        if not M or any(q in used[yi] for q in M):
+            return None
+        rng = {q: self.const_ranges[grp.params.index(q)] for q in grp.params}
+        rng[kp] = kr
+        if any(r is None for r in rng.values()):
+            return None
+        ext = {q: rng[q][2] for q in params}
+        fma = 1
+        for q in params:
+            fma *= ext[q]
+        if fma < CONTRACT_MIN_FMA:
+            return None
+        return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
+                "M": M, "N": npar, "K": K, "ext": ext, "rng": rng, "init_zero": True,
+                "checks": st.in_edges(inner) + lout}
 
     def _blocked_contraction_plan(self, mem, inner):
         """The reference's blocked MATMUL expansion (autoopt.py:707-813,
@@ -542,9 +666,10 @@ class _Gen:
              "        for (int e2 = 0; e2 < 2; ++e2) {",
              "          const int row = wm + 16 * mf + g + 8 * h;",
              "          const long long n = n0 + f * 8 + 2 * t + e2;",
-             f"          acc[mf][f][2 * h + e2] = (row < rows && n < NT) ? "
-             f"O[b2c_mo((unsigned)(mfirst + row)) + {con}LL * "
-             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             ("          acc[mf][f][2 * h + e2] = 0.0; (void)row; (void)n;" if cp.get("init_zero") else
+              f"          acc[mf][f][2 * h + e2] = (row < rows && n < NT) ? "
+              f"O[b2c_mo((unsigned)(mfirst + row)) + {con}LL * "
+              f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;"),
              "        }",
              "    __syncthreads();",
              "    load(0);",
@@ -587,7 +712,7 @@ class _Gen:
              "        }",
              "  }",
              "}"]
-        self._contract_checks()
+        self._contract_checks(cp)
         spec.source = "\n".join(L) + "\n"
         spec.block = (256, 1, 1)
         spec.vec = 1
@@ -617,12 +742,17 @@ class _Gen:
             return " + ".join(out) if out else "0LL"
         return decode
 
-    def _contract_checks(self):
+    def _contract_checks(self, cp=None):
         """Host-side bounds checks of the three memlets (as the generic
         body's)."""
         spec = self.spec
         mem = self.group.members[0]
         menv = {mp: f"p_{gp}" for mp, gp in mem.rename.items()}
+        if cp is not None and cp.get("checks") is not None:
+            for e in cp["checks"]:
+                if e.memlet is not None:
+                    spec.checks.append((e.memlet.container, e.memlet.subset, menv))
+            return
         t = next(k for k in P._scope_children(mem.state, mem.entry)
                  if not isinstance(k, sdfg.MapExit)) if mem.tasklet is None else mem.tasklet
         if isinstance(t, sdfg.MapEntry):  # blocked form: the inner map's outer memlets
@@ -751,8 +881,9 @@ class _Gen:
              "#pragma unroll",
              "        for (int e2 = 0; e2 < 2; ++e2) {",
              "          const long long m = m0 + wm + 16 * mf + g + 8 * h, n = n0 + f * 8 + 2 * t + e2;",
-             f"          acc[mf][f][2 * h + e2] = (m < MT && n < NT) ? O[b2c_mo((unsigned)m) + {con}LL * "
-             f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;",
+             (f"          acc[mf][f][2 * h + e2] = 0.0; (void)m; (void)n;" if cp.get("init_zero") else
+              f"          acc[mf][f][2 * h + e2] = (m < MT && n < NT) ? O[b2c_mo((unsigned)m) + {con}LL * "
+              f"({rng[Np][0]}LL + {rng[Np][1]}LL * n)] : 0.0;"),
              "        }",
              "    load(0);",
              "    store(0);",
@@ -791,7 +922,7 @@ class _Gen:
              "        }",
              "  }",
              "}"]
-        self._contract_checks()
+        self._contract_checks(cp)
         spec.source = "\n".join(L) + "\n"
         spec.block = (256, 1, 1)
         spec.vec = 1

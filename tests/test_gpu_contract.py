@@ -399,3 +399,29 @@ def test_privatised_map_region_doitgen_raw(monkeypatch):
     assert rel_err(out["out"], out2["out"]) <= 1e-12
     assert (cnt.map_iterations, cnt.wcr_commits) == (cnt2.map_iterations, cnt2.wcr_commits)
     assert cnt.map_iterations == 8 * 8 * 160 * 160
+
+
+@pytest.mark.parametrize("variant", ["pipe", "b2reg"])
+def test_map_reduce_contraction_doitgen(variant):
+    """doitgen's LoopToMap form — a map over (r, q, p) whose scope maps
+    T[k] = A[r, q, k] * C4[k, p] into a transient row and REDUCEs it into
+    out[r, q, p] — runs as the DMMA contraction with zero-initialised
+    accumulators (T never materialised): within the tensor-core tolerance
+    of the closed form."""
+    from paper_2107_00555_b200 import ExecContext, interpret, sdfg
+    from paper_2107_00555_b200.machine import GpuExecutor
+
+    syms = {"NR": 8, "NQ": 12, "NP": 256}
+    g = sdfg.load(GOLDEN / "graphs" / f"doitgen.{variant}.json")
+    ex = GpuExecutor(g, syms)
+    try:
+        assert any(sp.mode == "contract" for sp in ex.specs.values())
+    finally:
+        ex.close()
+    rng = np.random.default_rng(6)
+    A = rng.uniform(-1, 1, (8, 12, 256))
+    C4 = rng.uniform(-1, 1, (256, 256))
+    out = interpret(g, ExecContext(bindings=dict(syms)).bind_inputs(
+        {"A": A, "C4": C4, "out": np.full((8, 12, 256), np.nan)}))
+    ref = np.einsum("rqs,sp->rqp", A, C4)
+    assert rel_err(out["out"], ref) <= 1e-12
