@@ -1218,6 +1218,11 @@ def bench_slab(args, W):
 
     from .. import runtime as rt
 
+    if "RANK" not in os.environ and args.gpus == 1:
+        # one process without a launcher (B2_FORCE_SLAB=1 python bench.py)
+        os.environ.update({"RANK": "0", "WORLD_SIZE": "1", "LOCAL_RANK": "0",
+                           "MASTER_ADDR": "127.0.0.1"})
+        os.environ.setdefault("MASTER_PORT", "29533")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
