@@ -203,6 +203,12 @@ class _Gen:
         if len(ents) == 1 and len(libs) == 1 and all(
                 isinstance(k, (sdfg.MapEntry, sdfg.Library, sdfg.Access)) for k in nested):
             return self._mapreduce_contraction_plan(mem, ents[0], libs[0])
+        tks = [k for k in nested if isinstance(k, sdfg.Tasklet)]
+        if len(ents) == 2 and not libs and len(tks) == 1 and all(
+                isinstance(k, (sdfg.MapEntry, sdfg.Tasklet, sdfg.Access)) for k in nested):
+            tiled = self._tiled_sum_match(mem, ents, tks[0])
+            if tiled is not None:
+                return self._mapreduce_contraction_plan(mem, tiled["producer"], None, tiled)
         if len(kids) != 1 or not isinstance(kids[0], sdfg.Tasklet):
             return None
         t = kids[0]
@@ -277,7 +283,90 @@ class _Gen:
                 "M": M, "N": npar, "K": K, "ext": ext,
                 "rng": {q: self.const_ranges[params.index(q)] for q in params}}
 
-    def _mapreduce_contraction_plan(self, mem, inner, lib):
+    def _tiled_sum_match(self, mem, ents, zero):
+        """auto_optimize's tiled REDUCE expansion inside a map (tile_wcr,
+        autoopt.py:480-595; doitgen.auto): ``O = 0``, then per tile
+        ``acc = 0; acc += T[k]`` over the tile's k (sequential), ``O += acc``
+        (WCR add), the tiles partitioning T's range.  Returns the producer
+        map of T and the O edges, or None."""
+        st = mem.state
+
+        def kids(e):
+            return [k for k in P._scope_children(st, e) if not isinstance(k, sdfg.MapExit)]
+
+        def only_code(t):
+            return t.code[0][1] if len(t.code) == 1 else None
+
+        zo = [e for e in st.out_edges(zero) if e.memlet is not None]
+        if zero.ins or len(zo) != 1 or zo[0].memlet.wcr is not None or \
+                only_code(zero) not in (("num", 0.0), ("num", 0)):
+            return None
+        O = zo[0].memlet
+        for prod, tile in (ents, ents[::-1]):
+            pk = [k for k in kids(prod)]
+            tk = kids(tile)
+            if len(pk) != 1 or not isinstance(pk[0], sdfg.Tasklet) or len(tile.params) != 1:
+                continue
+            pouts = [e for e in st.out_edges(pk[0]) if e.memlet is not None]
+            if len(pouts) != 1:
+                continue
+            T = pouts[0].memlet.container
+            inner = [k for k in tk if isinstance(k, sdfg.MapEntry)]
+            tts = [k for k in tk if isinstance(k, sdfg.Tasklet)]
+            if len(inner) != 1 or len(tts) != 2 or len(inner[0].params) != 1 \
+                    or any(not isinstance(k, (sdfg.MapEntry, sdfg.Tasklet, sdfg.Access)) for k in tk):
+                continue
+            red = kids(inner[0])
+            if len(red) != 1 or not isinstance(red[0], sdfg.Tasklet):
+                continue
+            rt_ = red[0]
+            rin = {e.dst_conn: e.memlet for e in st.in_edges(rt_) if e.memlet is not None}
+            rout = [e.memlet for e in st.out_edges(rt_) if e.memlet is not None]
+            code = only_code(rt_)
+            if not (len(rin) == 2 and len(rout) == 1 and code is not None and code[0] == "bin"
+                    and code[1] == "+"):
+                continue
+            accn = rout[0].container
+            tin = [c for c, m in rin.items() if m.container == T]
+            ain = [c for c, m in rin.items() if m.container == accn]
+            if len(tin) != 1 or len(ain) != 1 or \
+                    {code[2], code[3]} != {("ref", tin[0]), ("ref", ain[0])}:
+                continue
+            kq = inner[0].params[0][0]
+            if rin[tin[0]].subset[0][:2] != (("s", kq), ("s", kq)) and \
+                    tuple(rin[tin[0]].subset[0][:2]) != (("s", kq), ("s", kq)):
+                continue
+            init = [t for t in tts if t is not rt_ and not t.ins]
+            fin = [t for t in tts if t is not rt_ and t.ins]
+            if len(init) != 1 or len(fin) != 1 or only_code(init[0]) not in (("num", 0.0), ("num", 0)):
+                continue
+            io = [e for e in st.out_edges(init[0]) if e.memlet is not None]
+            fo = [e for e in st.out_edges(fin[0]) if e.memlet is not None]
+            fi = [e for e in st.in_edges(fin[0]) if e.memlet is not None]
+            if len(io) != 1 or io[0].memlet.container != accn or len(fo) != 1 or len(fi) != 1 \
+                    or fi[0].memlet.container != accn or fo[0].memlet.wcr != "add" \
+                    or fo[0].memlet.text != O.text or only_code(fin[0]) != ("ref", fin[0].ins[0]):
+                continue
+            # the tiles' k ranges partition T (numerically, at the bound sizes)
+            env = dict(self.pl.fixed)
+            tp, (tb, te, ts) = tile.params[0]
+            try:
+                tvals = range(symexpr.evaluate(tb, env), symexpr.evaluate(te, env) + 1,
+                              symexpr.evaluate(ts, env))
+                seen = []
+                for v in tvals:
+                    e2 = dict(env)
+                    e2[tp] = v
+                    b, e, s_ = (symexpr.evaluate(x, e2) for x in inner[0].params[0][1])
+                    seen.extend(range(b, e + 1, s_))
+            except Exception:
+                continue
+            if seen != list(range(self.shapes[T][0])):
+                continue
+            return {"producer": prod, "T": T, "o_edge": fo[0], "zero_edge": zo[0]}
+        return None
+
+    def _mapreduce_contraction_plan(self, mem, inner, lib, tiled=None):
         """``out[m, n] = sum(T)`` after ``T[k] = X[m, k] * Y[k, n]`` inside
         one parallel map (doitgen's pipe / LoopToMap form: a map into a
         transient row, then a whole-array REDUCE): per output point the sum
@@ -287,14 +376,19 @@ class _Gen:
         (within the rel_err 1e-12 contract)."""
         st = mem.state
         grp = self.group
-        if lib.kind != "reduce" or lib.attrs.get("axes") is not None \
-                or lib.attrs.get("op", "add") != "add":
-            return None
-        lin = [e for e in st.in_edges(lib) if e.memlet is not None]
-        lout = [e for e in st.out_edges(lib) if e.memlet is not None]
-        if len(lin) != 1 or len(lout) != 1 or lout[0].memlet.wcr is not None:
-            return None
-        T = lin[0].memlet.container
+        if tiled is not None:
+            T = tiled["T"]
+            lout = [tiled["o_edge"]]
+            lin = None
+        else:
+            if lib.kind != "reduce" or lib.attrs.get("axes") is not None \
+                    or lib.attrs.get("op", "add") != "add":
+                return None
+            lin = [e for e in st.in_edges(lib) if e.memlet is not None]
+            lout = [e for e in st.out_edges(lib) if e.memlet is not None]
+            if len(lin) != 1 or len(lout) != 1 or lout[0].memlet.wcr is not None:
+                return None
+            T = lin[0].memlet.container
         tc = self.g.containers[T]
         if not tc.transient or len(self.shapes[T]) != 1:
             return None
@@ -321,8 +415,8 @@ class _Gen:
         kr = _const_range(self.pl, (kb, ke, ks))
         if kr is None or kr != (0, 1, self.shapes[T][0]):
             return None  # T[k] over the whole of T, k ascending
-        rin = lin[0].memlet.subset[0]
-        if _const_range(self.pl, rin) != (0, 1, self.shapes[T][0]):
+        if lin is not None and _const_range(self.pl, lin[0].memlet.subset[0]) != \
+                (0, 1, self.shapes[T][0]):
             return None
         params = list(grp.params) + [kp]
         if kp in grp.params:
@@ -394,7 +488,7 @@ class _Gen:
             return None
         return {"X": xs[xi], "Y": xs[yi], "O": oc, "cx": ca[xi], "cy": ca[yi], "co": co_,
                 "M": M, "N": npar, "K": K, "ext": ext, "rng": rng, "init_zero": True,
-                "checks": st.in_edges(inner) + lout}
+                "checks": st.in_edges(inner) + lout + ([tiled["zero_edge"]] if tiled else [])}
 
     def _blocked_contraction_plan(self, mem, inner):
         """The reference's blocked MATMUL expansion (autoopt.py:707-813,

@@ -401,17 +401,19 @@ def test_privatised_map_region_doitgen_raw(monkeypatch):
     assert cnt.map_iterations == 8 * 8 * 160 * 160
 
 
-@pytest.mark.parametrize("variant", ["pipe", "b2reg"])
-def test_map_reduce_contraction_doitgen(variant):
+@pytest.mark.parametrize("variant,NP", [("pipe", 256), ("b2reg", 256), ("auto", 256), ("auto", 250)])
+def test_map_reduce_contraction_doitgen(variant, NP):
     """doitgen's LoopToMap form — a map over (r, q, p) whose scope maps
     T[k] = A[r, q, k] * C4[k, p] into a transient row and REDUCEs it into
     out[r, q, p] — runs as the DMMA contraction with zero-initialised
     accumulators (T never materialised): within the tensor-core tolerance
-    of the closed form."""
+    of the closed form.  The auto form (auto_optimize's tiled REDUCE: O = 0,
+    per 16-wide tile acc += T[k], O += acc) is the same sum; NP = 250 leaves
+    a partial last tile."""
     from paper_2107_00555_b200 import ExecContext, interpret, sdfg
     from paper_2107_00555_b200.machine import GpuExecutor
 
-    syms = {"NR": 8, "NQ": 12, "NP": 256}
+    syms = {"NR": 8, "NQ": 12, "NP": NP}
     g = sdfg.load(GOLDEN / "graphs" / f"doitgen.{variant}.json")
     ex = GpuExecutor(g, syms)
     try:
@@ -419,9 +421,9 @@ def test_map_reduce_contraction_doitgen(variant):
     finally:
         ex.close()
     rng = np.random.default_rng(6)
-    A = rng.uniform(-1, 1, (8, 12, 256))
-    C4 = rng.uniform(-1, 1, (256, 256))
+    A = rng.uniform(-1, 1, (8, 12, NP))
+    C4 = rng.uniform(-1, 1, (NP, NP))
     out = interpret(g, ExecContext(bindings=dict(syms)).bind_inputs(
-        {"A": A, "C4": C4, "out": np.full((8, 12, 256), np.nan)}))
+        {"A": A, "C4": C4, "out": np.full((8, 12, NP), np.nan)}))
     ref = np.einsum("rqs,sp->rqp", A, C4)
     assert rel_err(out["out"], ref) <= 1e-12
