@@ -427,3 +427,21 @@ def test_block_region_selection():
     assert regions("softmax.raw", {"N": 1, "H": 2, "SM": 40})[1] == [("i", False, ["i", "j", "k"])]
     # maps larger than one CTA sweeps per step stay full-width kernels
     assert regions("adi.pipe", {"N": 5000, "TSTEPS": 2})[1] == []
+
+
+def test_rowred_prefetches_next_row():
+    """softmax's exp+sum row reduction: lane 0 L2-prefetches the warp's next
+    row of x (the only read-only input walked along the row); the per-row
+    maximum mx is not prefetched (no row-parameter dimension)."""
+    from paper_2107_00555_b200 import codegen as CG, plan as P_, sdfg as S_
+
+    syms = {"N": 2, "H": 2, "SM": 512}
+    g = S_.load(GOLDEN / "graphs" / "softmax.raw.json")
+    pl = P_.Planner(g, syms).build()
+    specs = [CG.generate(pl, o, pl.shapes(syms), f"s{o.idx}") for o in pl.all_ops
+             if isinstance(o, P_.MapGroup)]
+    rr = [sp for sp in specs if sp.mode == "rowred"]
+    assert rr and CG.ROWRED_PF
+    src = rr[0].source
+    assert "const b2_ll rown = row + " in src
+    assert src.count("b2_prefetch_l2(") == 1 and "c_x + e0" in src.replace("(const char *)", "")
