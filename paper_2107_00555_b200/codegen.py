@@ -77,8 +77,7 @@ ROWRED_UNROLL = int(os.environ.get("B2_ROWRED_UNROLL", "1"))  # unroll of the wa
 ROWRED_MINB = int(os.environ.get("B2_ROWRED_MINB", "8"))  # min CTAs/SM for rowred kernels (softmax 1.11 -> 1.06 ms)
 # row reductions: lane 0 L2-prefetches the warp's NEXT row of each read-only
 # input while the current row is reduced (cp.async.bulk.prefetch.L2):
-# softmax's row kernel 876 -> 836 us, run 1.223 -> 1.183 ms; GEMV row dots
-# unchanged
+# softmax's row kernel 876 -> 836 us; GEMV row dots unchanged
 ROWRED_PF = os.environ.get("B2_ROWRED_PF", "1") == "1"
 SLAB_VEC = int(os.environ.get("B2_SLAB_VEC", "8"))  # planes per thread, runtime dim-0 range
 # out[m, n] += X[m, k] * Y[k, n] maps (affine gathers, e.g. conv2d's 7-D WCR
